@@ -1,0 +1,102 @@
+/*
+ * cfp_oracle.h -- plain, slow, obviously-correct CPU oracle for the CFP
+ * plan-search hot path (arXiv 2504.00598).
+ *
+ * TEST INFRASTRUCTURE ONLY.  Only tests/, __graft_entry__.smoke() and
+ * bench.py's cpu_baseline / --impl reference legs may load this library.
+ * It shares no code, header, table or helper with the CUDA path
+ * (paper_2504_00598_b200/, include/cfp.h).
+ *
+ * Citations: P:n = PAPER.md line n, S:n = SPEC.md line n, SURVEY = SURVEY.md.
+ *
+ * Definitions implemented (the normative reading):
+ *  - cost of combination s of a segment instance under input state u
+ *      C(u,s) = sum_j (p_j[s_j] + c_j[s_j])               (Eq. 3 p_n + c_n)
+ *             + sum_{intra edges (a,b,R)} R[s_a][s_b]     (reshard between PBs)
+ *             + sum_{cross edges (j,Q)}  Q[u][s_j]        (Eq. 3 r_n)
+ *    computed exactly in uint64; any INF (0xFFFFFFFF) term makes C = INF.
+ *  - combination index: big-endian mixed radix, block 0 most significant
+ *    (S = prod_i D_i; order = SURVEY Q5).
+ *  - A[u][v] = min_{s: s_o = v} C(u,s); I[u][v] = least index attaining it
+ *    (NOIDX if the bucket is all-INF).
+ *  - chain (textbook backward DP, P:625-627 with the state of S:501):
+ *      G_N = terminal (0); G_{n-1}(u) = min_v A_n[u][v] + G_n(v); OPT = G_0(0).
+ *  - reconstruction: forward greedy choosing, among optimal successors, the
+ *    least combination index (lexicographically smallest plan tuple).
+ */
+#ifndef CFP_ORACLE_H
+#define CFP_ORACLE_H
+#include <stdint.h>
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define ORC_INF32 0xFFFFFFFFu
+#define ORC_INF64 0xFFFFFFFFFFFFFFFFull
+#define ORC_NOIDX 0xFFFFFFFFFFFFFFFFull
+
+enum { ORC_OK = 0, ORC_EINVAL = 1, ORC_EINFEASIBLE = 3, ORC_ETOOBIG = 4, ORC_ENOMEM = 7 };
+
+typedef struct {
+  int32_t K;
+  const int32_t* radix;     /* [K] */
+  const uint32_t* comp;     /* [sum D] p_j[s] */
+  const uint32_t* comm;     /* [sum D] c_j[s], nullable = 0 */
+  int32_t E;
+  const int32_t* esrc;      /* [E] */
+  const int32_t* edst;      /* [E] */
+  const uint32_t* etab;     /* concat row-major [D_src][D_dst] */
+  int32_t out_block;
+} orc_type;
+
+typedef struct {
+  int32_t pred;             /* -1 = chain start, D_in = 1 */
+  int32_t type;
+  int32_t X;
+  const int32_t* xdst;      /* [X] consumer block */
+  const uint32_t* xtab;     /* concat row-major [D_in][D_dst] */
+} orc_trans;
+
+typedef struct {
+  int32_t ntypes;
+  const orc_type* types;
+  int32_t ntrans;
+  const orc_trans* trans;
+  int32_t N;
+  const int32_t* inst;      /* [N] transition id per instance */
+} orc_problem;
+
+/* C(u, s) for digit vector s (length K of the transition's type). */
+uint64_t orc_cost(const orc_problem* p, int32_t tr, int32_t u, const int32_t* s);
+/* C(u, s) for s given as big-endian index. */
+uint64_t orc_cost_index(const orc_problem* p, int32_t tr, int32_t u, uint64_t idx);
+/* Full A/I table of one transition: A, I are [D_in][D_o]. */
+int orc_segment_table(const orc_problem* p, int32_t tr, uint64_t* A, uint64_t* I, int nthreads);
+/* One bucket (u, v): enumerates every s with s_o = v in index order. */
+int orc_bucket(const orc_problem* p, int32_t tr, int32_t u, int32_t v,
+               uint64_t* a, uint64_t* i, int nthreads);
+/* Backward DP over N instance matrices (rows[n] x cols[n], row-major).
+ * G receives (N+1) ragged vectors: G_0 (rows[0]) then G_n (cols[n-1]).
+ * terminal: cols[N-1] values or NULL (= 0). */
+int orc_chain(int32_t N, const int32_t* rows, const int32_t* cols,
+              const uint64_t* const* A, const uint64_t* terminal, uint64_t* G);
+/* Forward greedy reconstruction from u_1 = 0. Outputs per instance the chosen
+ * column v_n, index I_n[u][v_n] and cost A_n[u][v_n]. Returns EINFEASIBLE if
+ * G_0(0) is INF. */
+int orc_reconstruct(int32_t N, const int32_t* rows, const int32_t* cols,
+                    const uint64_t* const* A, const uint64_t* const* I,
+                    const uint64_t* G, int32_t* v_out, uint64_t* idx_out, uint64_t* cost_out);
+/* Full search: tables for every transition used, chain, reconstruction.
+ * digits: [N * kmax] padded with -1. */
+int orc_search_plan(const orc_problem* p, int nthreads, uint64_t* total,
+                    uint64_t* seg_index, int32_t* digits, int32_t kmax, uint64_t* seg_ns);
+/* (A (x) B)[i][j] = min_k A[i][k] + B[k][j]; argk = least k (NOIDX if INF). */
+int orc_minplus(int32_t m, int32_t k, int32_t n, const uint64_t* A, const uint64_t* B,
+                uint64_t* C, uint64_t* argk);
+/* Big-endian mixed-radix decode. */
+void orc_decode(int32_t K, const int32_t* radix, uint64_t idx, int32_t* digits);
+
+#ifdef __cplusplus
+}
+#endif
+#endif
