@@ -1,0 +1,205 @@
+/*
+ * cfp.h -- C-ABI of the B200-native CFP plan-search hot path (arXiv 2504.00598).
+ *
+ * Citations: P:n = /root/reference/PAPER.md line n; S:n = SPEC.md line n;
+ * SURVEY = /root/repo/SURVEY.md (its §8 is the scope contract).
+ *
+ * What is computed (the data-parallel hot path of "ComposeSearch"):
+ *   (1) cfp_segment_costs -- for one distinct segment type and one
+ *       incoming transition, evaluate EVERY strategy combination of its
+ *       ParallelBlocks (S = prod_i D_i; "combines all ParallelBlocks'
+ *       strategies") under every input layout u of the predecessor's
+ *       output block, with the Eq. 3 cost terms:
+ *          C(u,s) = sum_j (p_j[s_j] + c_j[s_j])
+ *                 + sum_{intra edges a->b} R_ab[s_a][s_b]
+ *                 + sum_{cross edges ->j}  Q_j[u][s_j]
+ *       and reduce to A[u][v] = min_{s: s_o = v} C(u,s) with the least
+ *       big-endian combination index I[u][v] attaining it.
+ *   (2) cfp_minplus_chain -- the segment DP as tropical (min,+)
+ *       products: G_N = terminal, G_{n-1} = A_n (x) G_n, using repeated squaring
+ *       for runs of identical transitions.
+ *   (3) cfp_search_plan -- (1) for every distinct segment type + (2) + the
+ *       forward-greedy backtrack that emits the canonical optimal plan tuple
+ *       (i_1..i_N), lexicographically smallest among optimal.
+ *
+ * Conventions:
+ *  - Costs are integer nanoseconds.  Table entries are uint32; CFP_INF32 marks
+ *    an infeasible strategy / pair and is absorbing.  Results are exact uint64;
+ *    CFP_INF64 = unreachable.  CFP_NOIDX = argmin of an all-infeasible bucket.
+ *  - Combination index: big-endian mixed radix, block 0 most significant:
+ *    idx(s) = ((s_0*D_1 + s_1)*D_2 + ...)*D_{K-1} + s_{K-1}.
+ *  - Ownership: every input pointer is caller-owned HOST memory, read only
+ *    during the call and never retained.  Outputs are caller-allocated HOST
+ *    memory; their contents are unspecified when the call fails.  Device
+ *    scratch belongs to the ctx.
+ *  - Errors: every function returns cfp_status (0 = CFP_OK) and never throws
+ *    across the ABI; cfp_last_error() gives a thread-local message.
+ *      CFP_EINVAL      structural problem (K<1, D<1, bad block id, self edge,
+ *                      D_in mismatch with the predecessor's output radix, N<1,
+ *                      chain not starting with pred_type=-1, ...)
+ *      CFP_EOVERFLOW   a finite sum could reach 2^63
+ *      CFP_EINFEASIBLE OPT = infinity (message names the first instance with
+ *                      no finite completion)
+ *      CFP_ETOOBIG     prod D > 2^48, K > 32, or device scratch too large
+ *      CFP_ECUDA / CFP_ENCCL  wrapped runtime failures
+ *      CFP_EVERSION    abi_version != CFP_ABI_VERSION
+ *    There is no CPU fallback: without a usable CUDA device cfp_ctx_create
+ *    fails with CFP_ECUDA.
+ *  - Determinism: identical inputs give byte-identical outputs,
+ *    independent of the world size.
+ *  - Threading: a ctx is not thread-safe.  With world > 1 every rank must make
+ *    the same calls with identical inputs (SPMD / NCCL semantics).
+ */
+#ifndef CFP_H
+#define CFP_H
+#include <stddef.h>
+#include <stdint.h>
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CFP_ABI_VERSION 1
+#define CFP_INF32 0xFFFFFFFFu
+#define CFP_INF64 0xFFFFFFFFFFFFFFFFull
+#define CFP_NOIDX 0xFFFFFFFFFFFFFFFFull
+#define CFP_MAX_BLOCKS 32
+
+typedef enum {
+  CFP_OK = 0, CFP_EINVAL = 1, CFP_EOVERFLOW = 2, CFP_EINFEASIBLE = 3, CFP_ETOOBIG = 4,
+  CFP_ECUDA = 5, CFP_ENCCL = 6, CFP_ENOMEM = 7, CFP_EVERSION = 8
+} cfp_status;
+
+/* TARGET training mesh being planned for.  Metadata only: it
+ * determined the strategy counts D_j upstream; the search never reads it. */
+typedef struct { int32_t ndim; const int32_t* axes; } cfp_mesh;
+
+/* One distinct segment type (fingerprint class). */
+typedef struct {
+  int32_t num_blocks;          /* K, 1..CFP_MAX_BLOCKS ParallelBlocks */
+  const int32_t* radix;        /* [K] D_j >= 1 strategies per block */
+  const uint32_t* comp_ns;     /* [sum D_j] profiled compute time p_j[s] */
+  const uint32_t* comm_ns;     /* [sum D_j] profiled comm time c_j[s]; NULL = 0 */
+  int32_t num_edges;           /* intra-segment PB->PB dependencies */
+  const int32_t* edge_src;     /* [E] producer block */
+  const int32_t* edge_dst;     /* [E] consumer block, != src */
+  const uint32_t* edge_ns;     /* concat of row-major [D_src][D_dst] reshard tables */
+  int32_t out_block;           /* o: its strategy is the segment's output layout */
+} cfp_segment_type;
+
+/* Transition type tau = (pred_type -> type) with its cross-segment reshard
+ * tables from the predecessor's output block. */
+typedef struct {
+  int32_t pred_type;           /* -1 = chain start (D_in = 1) */
+  int32_t type;
+  int32_t num_in_edges;
+  const int32_t* in_dst;       /* [X] consumer blocks of `type` */
+  const uint32_t* in_ns;       /* concat of row-major [D_in][D_dst] tables */
+} cfp_transition;
+
+typedef struct {
+  int32_t abi_version;         /* must equal CFP_ABI_VERSION */
+  cfp_mesh mesh;
+  int32_t num_types;        const cfp_segment_type* types;
+  int32_t num_transitions;  const cfp_transition* transitions;
+  int32_t num_instances;    const int32_t* inst_transition;  /* [N] */
+} cfp_problem;
+
+typedef struct {               /* caller-allocated outputs */
+  uint64_t total_ns;           /* OPT = Eq. 3 of the emitted plan */
+  uint64_t* seg_index;         /* [N] big-endian combination index i_n */
+  int32_t* digits;             /* [N * kmax] per-block strategy, rows padded with -1 */
+  int32_t kmax;                /* row stride of digits (>= max K of used types) */
+  uint64_t* seg_ns;            /* [N] C_n(u_n, s_n) incl. incoming cross terms */
+} cfp_plan;
+
+typedef struct {
+  int32_t device;              /* CUDA device ordinal */
+  void* cuda_stream;           /* cudaStream_t; NULL = a stream owned by the ctx */
+  int32_t world, rank;         /* world > 1: enumeration sharded over ranks */
+  const void* nccl_unique_id;  /* world > 1: 128-byte ncclUniqueId (same on all ranks) */
+} cfp_ctx_opts;
+
+typedef struct cfp_ctx cfp_ctx;
+typedef struct cfp_prepared cfp_prepared;
+
+cfp_status  cfp_ctx_create(cfp_ctx** ctx, const cfp_ctx_opts* opts);
+void        cfp_ctx_destroy(cfp_ctx* ctx);
+const char* cfp_last_error(void);
+/* Writes a fresh 128-byte ncclUniqueId (call on one rank, broadcast it). */
+cfp_status  cfp_nccl_unique_id(void* out128);
+
+/* (1) One transition: cost_out/index_out are [d_in][D_o] row-major.
+ * tr == NULL: no cross edges and d_in must be 1.  Collective if world > 1. */
+cfp_status cfp_segment_costs(cfp_ctx* ctx, const cfp_segment_type* t, const cfp_transition* tr,
+                             int32_t d_in, uint64_t* cost_out, uint64_t* index_out);
+
+/* (2) Chain over run-length-encoded matrices.  mats[m] is rows[m] x cols[m]
+ * row-major uint64 (CFP_INF64 = no edge).  Instance sequence = run r repeats
+ * matrix run_mat[r] run_len[r] times (square when run_len > 1); consecutive
+ * matrices must chain (cols of one = rows of the next); rows of the first = 1
+ * is NOT required: G_0 has rows of the first matrix.
+ * terminal: [cols of the last matrix] or NULL (= 0).
+ * opt_out: G_0[0].  suffix_out (nullable): G_0, G_1, ..., G_N concatenated
+ * (G_0 has rows(first) entries, G_n has cols(matrix of instance n) entries). */
+cfp_status cfp_minplus_chain(cfp_ctx* ctx, int32_t num_mats, const int32_t* rows,
+                             const int32_t* cols, const uint64_t* const* mats,
+                             int32_t num_runs, const int32_t* run_mat, const int64_t* run_len,
+                             const uint64_t* terminal, uint64_t* opt_out, uint64_t* suffix_out);
+
+/* (3) Full search: identical result on every rank. */
+cfp_status cfp_search_plan(cfp_ctx* ctx, const cfp_problem* p, cfp_plan* out);
+
+/* One (min,+) product C = A (x) B with the least k attaining each entry
+ * (CFP_NOIDX if the row/column pair is all-infinite).  argk nullable. */
+cfp_status cfp_minplus_product(cfp_ctx* ctx, int32_t m, int32_t k, int32_t n,
+                               const uint64_t* A, const uint64_t* B,
+                               uint64_t* C, uint64_t* argk);
+
+/* ---- device-resident execution (used by the bench to time the hot path
+ * with inputs already in HBM) ---------------------------------------------
+ * cfp_prepare validates, prunes and stages the problem on the device (H2D);
+ * cfp_execute runs the whole hot path (enumeration, merge, chain, backtrack)
+ * on the ctx stream WITHOUT host synchronisation or copies; cfp_fetch_plan
+ * synchronises and copies the plan to host memory. */
+cfp_status cfp_prepare(cfp_ctx* ctx, const cfp_problem* p, cfp_prepared** out);
+cfp_status cfp_execute(cfp_ctx* ctx, cfp_prepared* prep);
+cfp_status cfp_fetch_plan(cfp_ctx* ctx, cfp_prepared* prep, cfp_plan* out);
+void       cfp_prepared_free(cfp_prepared* prep);
+
+typedef struct {
+  double combos;               /* sum over distinct used types of prod_j feasible D_j */
+  double combos_local;         /* this rank's share */
+  double evals;                /* combos x (#incoming transitions folded) */
+  int32_t num_types, num_transitions, wide_types;  /* wide = 64-bit path */
+  int32_t kernel_launches;     /* kernels launched by one cfp_execute */
+  int32_t prefix_len[CFP_MAX_BLOCKS];   /* per type: enumeration schedule summary */
+  int32_t nb[CFP_MAX_BLOCKS], na[CFP_MAX_BLOCKS];
+} cfp_prepared_info;
+cfp_status cfp_prepared_query(const cfp_prepared* prep, cfp_prepared_info* info);
+/* Record CUDA events around the enumeration kernel of the given type's next
+ * cfp_execute (ms via cfp_prepared_enum_ms after the stream completes).
+ * Used for the bench's per-kernel roofline; 0 = off. */
+cfp_status cfp_prepared_time_kernels(cfp_prepared* prep, int32_t on);
+cfp_status cfp_prepared_kernel_ms(cfp_prepared* prep, double* enum_ms, double* total_ms);
+
+/* ---- host-only helpers (no device work; callable without a GPU) ---------- */
+/* Contiguous, balanced share [lo, hi) of `units` items for `rank` of `world`
+ * in multiples of `align`. */
+cfp_status cfp_shard_range(int64_t units, int64_t align, int32_t world, int32_t rank,
+                           int64_t* lo, int64_t* hi);
+/* Packed merge key (cost << idx_bits) | idx, CFP_INF64 for (INF, NOIDX). */
+cfp_status cfp_pack_keys(int64_t n, const uint64_t* cost, const uint64_t* idx, int32_t idx_bits,
+                         uint64_t* keys);
+cfp_status cfp_unpack_keys(int64_t n, const uint64_t* keys, int32_t idx_bits,
+                           uint64_t* cost, uint64_t* idx);
+
+/* ---- N5 integer-pipe microbenchmark (roofline denominator) --------------
+ * op 0: VIADDMNMX.U32 (fused add+min), op 1: IADD3, op 2: 64-bit add+min.
+ * Reports lane-ops/s and the elapsed ms of one launch. */
+cfp_status cfp_intpipe_bench(cfp_ctx* ctx, int32_t op, int32_t iters, double* ops_per_s,
+                             double* ms);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -105,13 +105,17 @@ static int nthreads_or_default(int n) {
   return n < 1 ? 1 : n;
 }
 
-int orc_segment_table(const orc_problem* p, int32_t tr, uint64_t* A, uint64_t* I, int nthreads) {
+int orc_segment_table_range(const orc_problem* p, int32_t tr, uint64_t lo_idx, uint64_t hi_idx,
+                            uint64_t* A, uint64_t* I, int nthreads) {
   if (tr < 0 || tr >= p->ntrans) return ORC_EINVAL;
   const orc_type* t = &p->types[p->trans[tr].type];
   if (t->K > 64) return ORC_ETOOBIG;
   const int32_t din = d_in_of(p, tr);
   const int32_t dout = t->radix[t->out_block];
-  const uint64_t S = space_size(t);
+  const uint64_t S0 = space_size(t);
+  if (hi_idx > S0) hi_idx = S0;
+  if (lo_idx > hi_idx) lo_idx = hi_idx;
+  const uint64_t S = hi_idx - lo_idx;
   const int nt = nthreads_or_default(nthreads);
   const size_t cells = (size_t)din * dout;
   uint64_t* LA = (uint64_t*)malloc(sizeof(uint64_t) * cells * nt);
@@ -120,7 +124,7 @@ int orc_segment_table(const orc_problem* p, int32_t tr, uint64_t* A, uint64_t* I
   for (size_t c = 0; c < cells * nt; ++c) { LA[c] = ORC_INF64; LI[c] = ORC_NOIDX; }
 #pragma omp parallel for schedule(static, 1) num_threads(nt)
   for (int ch = 0; ch < nt; ++ch) {
-    uint64_t lo = S * (uint64_t)ch / nt, hi = S * (uint64_t)(ch + 1) / nt;
+    uint64_t lo = lo_idx + S * (uint64_t)ch / nt, hi = lo_idx + S * (uint64_t)(ch + 1) / nt;
     uint64_t* a = LA + cells * ch;
     uint64_t* ix = LI + cells * ch;
     int32_t s[64];
@@ -139,6 +143,11 @@ int orc_segment_table(const orc_problem* p, int32_t tr, uint64_t* A, uint64_t* I
       if (LA[cells * ch + c] < A[c]) { A[c] = LA[cells * ch + c]; I[c] = LI[cells * ch + c]; }
   free(LA); free(LI);
   return ORC_OK;
+}
+
+int orc_segment_table(const orc_problem* p, int32_t tr, uint64_t* A, uint64_t* I, int nthreads) {
+  if (tr < 0 || tr >= p->ntrans) return ORC_EINVAL;
+  return orc_segment_table_range(p, tr, 0, space_size(&p->types[p->trans[tr].type]), A, I, nthreads);
 }
 
 int orc_bucket(const orc_problem* p, int32_t tr, int32_t u, int32_t v,

@@ -72,6 +72,9 @@ uint64_t orc_cost(const orc_problem* p, int32_t tr, int32_t u, const int32_t* s)
 uint64_t orc_cost_index(const orc_problem* p, int32_t tr, int32_t u, uint64_t idx);
 /* Full A/I table of one transition: A, I are [D_in][D_o]. */
 int orc_segment_table(const orc_problem* p, int32_t tr, uint64_t* A, uint64_t* I, int nthreads);
+/* Same over the index sub-range [lo, hi) only (bounded CPU-baseline samples). */
+int orc_segment_table_range(const orc_problem* p, int32_t tr, uint64_t lo, uint64_t hi,
+                            uint64_t* A, uint64_t* I, int nthreads);
 /* One bucket (u, v): enumerates every s with s_o = v in index order. */
 int orc_bucket(const orc_problem* p, int32_t tr, int32_t u, int32_t v,
                uint64_t* a, uint64_t* i, int nthreads);

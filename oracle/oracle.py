@@ -65,6 +65,8 @@ def lib():
         L.orc_cost_index.restype = C.c_uint64
         L.orc_cost_index.argtypes = [P(_Problem), C.c_int32, C.c_int32, C.c_uint64]
         L.orc_segment_table.argtypes = [P(_Problem), C.c_int32, P(C.c_uint64), P(C.c_uint64), C.c_int]
+        L.orc_segment_table_range.argtypes = [P(_Problem), C.c_int32, C.c_uint64, C.c_uint64,
+                                              P(C.c_uint64), P(C.c_uint64), C.c_int]
         L.orc_bucket.argtypes = [P(_Problem), C.c_int32, C.c_int32, C.c_int32,
                                  P(C.c_uint64), P(C.c_uint64), C.c_int]
         L.orc_chain.argtypes = [C.c_int32, P(C.c_int32), P(C.c_int32), P(P(C.c_uint64)),
@@ -150,6 +152,18 @@ def segment_table(prob: Problem, tr: int, nthreads: int = 0,
     I = np.empty((din, dout), dtype=np.uint64)
     _check(lib().orc_segment_table(m.ref, tr, _ptr(A, C.c_uint64), _ptr(I, C.c_uint64), nthreads),
            "segment_table")
+    return A, I
+
+
+def segment_table_range(prob: Problem, tr: int, lo: int, hi: int, nthreads: int = 0,
+                        m: Optional[Marshalled] = None) -> Tuple[np.ndarray, np.ndarray]:
+    """A/I restricted to combination indices [lo, hi) (all input states u)."""
+    m = m or Marshalled(prob)
+    din, dout = prob.d_in(tr), prob.d_out(tr)
+    A = np.empty((din, dout), dtype=np.uint64)
+    I = np.empty((din, dout), dtype=np.uint64)
+    _check(lib().orc_segment_table_range(m.ref, tr, lo, hi, _ptr(A, C.c_uint64), _ptr(I, C.c_uint64),
+                                         nthreads), "segment_table_range")
     return A, I
 
 

@@ -1,0 +1,390 @@
+"""Thin ctypes binding of include/cfp.h (argument marshalling only).
+
+Every step of the search runs in libcfp.so's sm_100a kernels; this module
+only converts numpy arrays / problem objects to the C structs and back.  There
+is no CPU fallback: if the library or a CUDA device is missing, the calls
+raise CfpError.
+
+Problem objects are duck-typed: anything with `.types` (radix, comp_ns,
+comm_ns, edges[(src, dst, table)], out_block), `.transitions` (pred_type,
+type, in_edges[(dst, table)]), `.instances` and `.mesh` -- e.g.
+`synth.Problem`.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass
+from typing import List, Optional, Sequence, Tuple
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libcfp.so")
+
+CFP_ABI_VERSION = 1
+INF64 = (1 << 64) - 1
+NOIDX = INF64
+STATUS = {0: "CFP_OK", 1: "CFP_EINVAL", 2: "CFP_EOVERFLOW", 3: "CFP_EINFEASIBLE",
+          4: "CFP_ETOOBIG", 5: "CFP_ECUDA", 6: "CFP_ENCCL", 7: "CFP_ENOMEM", 8: "CFP_EVERSION"}
+CFP_OK, CFP_EINVAL, CFP_EOVERFLOW, CFP_EINFEASIBLE, CFP_ETOOBIG = 0, 1, 2, 3, 4
+CFP_ECUDA, CFP_ENCCL, CFP_ENOMEM, CFP_EVERSION = 5, 6, 7, 8
+
+
+class CfpError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"{STATUS.get(status, status)}: {msg}")
+        self.status = status
+
+
+P = C.POINTER
+
+
+class cfp_mesh(C.Structure):
+    _fields_ = [("ndim", C.c_int32), ("axes", P(C.c_int32))]
+
+
+class cfp_segment_type(C.Structure):
+    _fields_ = [("num_blocks", C.c_int32), ("radix", P(C.c_int32)), ("comp_ns", P(C.c_uint32)),
+                ("comm_ns", P(C.c_uint32)), ("num_edges", C.c_int32), ("edge_src", P(C.c_int32)),
+                ("edge_dst", P(C.c_int32)), ("edge_ns", P(C.c_uint32)), ("out_block", C.c_int32)]
+
+
+class cfp_transition(C.Structure):
+    _fields_ = [("pred_type", C.c_int32), ("type", C.c_int32), ("num_in_edges", C.c_int32),
+                ("in_dst", P(C.c_int32)), ("in_ns", P(C.c_uint32))]
+
+
+class cfp_problem(C.Structure):
+    _fields_ = [("abi_version", C.c_int32), ("mesh", cfp_mesh), ("num_types", C.c_int32),
+                ("types", P(cfp_segment_type)), ("num_transitions", C.c_int32),
+                ("transitions", P(cfp_transition)), ("num_instances", C.c_int32),
+                ("inst_transition", P(C.c_int32))]
+
+
+class cfp_plan(C.Structure):
+    _fields_ = [("total_ns", C.c_uint64), ("seg_index", P(C.c_uint64)), ("digits", P(C.c_int32)),
+                ("kmax", C.c_int32), ("seg_ns", P(C.c_uint64))]
+
+
+class cfp_ctx_opts(C.Structure):
+    _fields_ = [("device", C.c_int32), ("cuda_stream", C.c_void_p), ("world", C.c_int32),
+                ("rank", C.c_int32), ("nccl_unique_id", C.c_void_p)]
+
+
+class cfp_prepared_info(C.Structure):
+    _fields_ = [("combos", C.c_double), ("combos_local", C.c_double), ("evals", C.c_double),
+                ("num_types", C.c_int32), ("num_transitions", C.c_int32), ("wide_types", C.c_int32),
+                ("kernel_launches", C.c_int32), ("prefix_len", C.c_int32 * 32),
+                ("nb", C.c_int32 * 32), ("na", C.c_int32 * 32)]
+
+
+EXPORTS = ["cfp_ctx_create", "cfp_ctx_destroy", "cfp_last_error", "cfp_nccl_unique_id",
+           "cfp_segment_costs", "cfp_minplus_chain", "cfp_search_plan", "cfp_minplus_product",
+           "cfp_prepare", "cfp_execute", "cfp_fetch_plan", "cfp_prepared_free",
+           "cfp_prepared_query", "cfp_prepared_time_kernels", "cfp_prepared_kernel_ms",
+           "cfp_shard_range", "cfp_pack_keys", "cfp_unpack_keys", "cfp_intpipe_bench"]
+
+_lib = None
+
+
+def lib() -> C.CDLL:
+    """Load libcfp.so (built in-tree by paper_2504_00598_b200/build.py)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise CfpError(CFP_ECUDA, f"{LIB_PATH} is missing: run `python -c 'import __graft_entry__ as g; "
+                                  f"g.build()'` (no CPU fallback exists)")
+    L = C.CDLL(LIB_PATH)
+    vp = C.c_void_p
+    L.cfp_ctx_create.argtypes = [P(vp), P(cfp_ctx_opts)]
+    L.cfp_ctx_destroy.argtypes = [vp]
+    L.cfp_ctx_destroy.restype = None
+    L.cfp_last_error.restype = C.c_char_p
+    L.cfp_nccl_unique_id.argtypes = [vp]
+    L.cfp_segment_costs.argtypes = [vp, P(cfp_segment_type), P(cfp_transition), C.c_int32,
+                                    P(C.c_uint64), P(C.c_uint64)]
+    L.cfp_minplus_chain.argtypes = [vp, C.c_int32, P(C.c_int32), P(C.c_int32), P(P(C.c_uint64)),
+                                    C.c_int32, P(C.c_int32), P(C.c_int64), P(C.c_uint64),
+                                    P(C.c_uint64), P(C.c_uint64)]
+    L.cfp_search_plan.argtypes = [vp, P(cfp_problem), P(cfp_plan)]
+    L.cfp_minplus_product.argtypes = [vp, C.c_int32, C.c_int32, C.c_int32, P(C.c_uint64),
+                                      P(C.c_uint64), P(C.c_uint64), P(C.c_uint64)]
+    L.cfp_prepare.argtypes = [vp, P(cfp_problem), P(vp)]
+    L.cfp_execute.argtypes = [vp, vp]
+    L.cfp_fetch_plan.argtypes = [vp, vp, P(cfp_plan)]
+    L.cfp_prepared_free.argtypes = [vp]
+    L.cfp_prepared_free.restype = None
+    L.cfp_prepared_query.argtypes = [vp, P(cfp_prepared_info)]
+    L.cfp_prepared_time_kernels.argtypes = [vp, C.c_int32]
+    L.cfp_prepared_kernel_ms.argtypes = [vp, P(C.c_double), P(C.c_double)]
+    L.cfp_shard_range.argtypes = [C.c_int64, C.c_int64, C.c_int32, C.c_int32, P(C.c_int64), P(C.c_int64)]
+    L.cfp_pack_keys.argtypes = [C.c_int64, P(C.c_uint64), P(C.c_uint64), C.c_int32, P(C.c_uint64)]
+    L.cfp_unpack_keys.argtypes = [C.c_int64, P(C.c_uint64), C.c_int32, P(C.c_uint64), P(C.c_uint64)]
+    L.cfp_intpipe_bench.argtypes = [vp, C.c_int32, C.c_int32, P(C.c_double), P(C.c_double)]
+    _lib = L
+    return L
+
+
+def _check(status: int):
+    if status != CFP_OK:
+        raise CfpError(status, lib().cfp_last_error().decode(errors="replace"))
+
+
+def _p(a: Optional[np.ndarray], ct):
+    return None if a is None else a.ctypes.data_as(P(ct))
+
+
+# ---------------------------------------------------------------- marshalling
+class _Marshal:
+    def __init__(self):
+        self.keep = []
+
+    def arr(self, a, dtype):
+        a = np.ascontiguousarray(a, dtype=dtype)
+        self.keep.append(a)
+        return a
+
+    def segment_type(self, ty) -> cfp_segment_type:
+        radix = self.arr(ty.radix, np.int32)
+        comp = self.arr(ty.comp_ns, np.uint32)
+        comm = None if ty.comm_ns is None else self.arr(ty.comm_ns, np.uint32)
+        edges = list(ty.edges)
+        src = self.arr([_e(e)[0] for e in edges] or [0], np.int32)
+        dst = self.arr([_e(e)[1] for e in edges] or [0], np.int32)
+        tab = self.arr(np.concatenate([np.asarray(_e(e)[2], np.uint32).ravel() for e in edges])
+                       if edges else np.zeros(1, np.uint32), np.uint32)
+        return cfp_segment_type(len(radix), _p(radix, C.c_int32), _p(comp, C.c_uint32),
+                                _p(comm, C.c_uint32), len(edges), _p(src, C.c_int32),
+                                _p(dst, C.c_int32), _p(tab, C.c_uint32), int(ty.out_block))
+
+    def transition(self, tr) -> cfp_transition:
+        xs = list(tr.in_edges)
+        dst = self.arr([_x(x)[0] for x in xs] or [0], np.int32)
+        tab = self.arr(np.concatenate([np.asarray(_x(x)[1], np.uint32).ravel() for x in xs])
+                       if xs else np.zeros(1, np.uint32), np.uint32)
+        return cfp_transition(int(tr.pred_type), int(tr.type), len(xs), _p(dst, C.c_int32),
+                              _p(tab, C.c_uint32))
+
+    def problem(self, prob) -> cfp_problem:
+        types = (cfp_segment_type * len(prob.types))(*[self.segment_type(t) for t in prob.types])
+        trans = (cfp_transition * len(prob.transitions))(*[self.transition(t) for t in prob.transitions])
+        self.keep += [types, trans]
+        mesh = self.arr(list(prob.mesh) or [1], np.int32)
+        inst = self.arr(prob.instances, np.int32)
+        return cfp_problem(CFP_ABI_VERSION, cfp_mesh(len(prob.mesh), _p(mesh, C.c_int32)),
+                           len(prob.types), types, len(prob.transitions), trans, len(inst),
+                           _p(inst, C.c_int32))
+
+
+def _e(e):
+    return (e.src, e.dst, e.table) if hasattr(e, "src") else e
+
+
+def _x(x):
+    return (x.dst, x.table) if hasattr(x, "dst") else x
+
+
+@dataclass
+class Plan:
+    total_ns: int
+    seg_index: np.ndarray      # uint64 [N]
+    digits: np.ndarray         # int32 [N, kmax]
+    seg_ns: np.ndarray         # uint64 [N]
+
+
+@dataclass
+class PreparedInfo:
+    combos: float
+    combos_local: float
+    evals: float
+    num_types: int
+    num_transitions: int
+    wide_types: int
+    kernel_launches: int
+    schedule: List[Tuple[int, int, int, int]]   # per type (prefix_len, NB, VG, na)
+
+
+class Context:
+    """cfp_ctx wrapper: one per process / GPU."""
+
+    def __init__(self, device: int = 0, stream: Optional[int] = None, world: int = 1, rank: int = 0,
+                 nccl_unique_id: Optional[bytes] = None):
+        L = lib()
+        self._h = C.c_void_p()
+        uid = None
+        if world > 1:
+            if nccl_unique_id is None or len(nccl_unique_id) != 128:
+                raise CfpError(CFP_EINVAL, "world > 1 needs a 128-byte nccl unique id")
+            uid = C.create_string_buffer(bytes(nccl_unique_id), 128)
+        opts = cfp_ctx_opts(device, stream, world, rank, C.cast(uid, C.c_void_p) if uid else None)
+        _check(L.cfp_ctx_create(C.byref(self._h), C.byref(opts)))
+        self.world, self.rank, self.device = world, rank, device
+
+    def close(self):
+        if self._h:
+            lib().cfp_ctx_destroy(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # -- (1)
+    def segment_costs(self, seg_type, transition=None, d_in: int = 1) -> Tuple[np.ndarray, np.ndarray]:
+        m = _Marshal()
+        t = m.segment_type(seg_type)
+        tr = m.transition(transition) if transition is not None else None
+        do = int(np.asarray(seg_type.radix)[int(seg_type.out_block)])
+        A = np.empty((d_in, do), np.uint64)
+        I = np.empty((d_in, do), np.uint64)
+        _check(lib().cfp_segment_costs(self._h, C.byref(t), C.byref(tr) if tr is not None else None,
+                                       d_in, _p(A, C.c_uint64), _p(I, C.c_uint64)))
+        return A, I
+
+    # -- (2)
+    def minplus_chain(self, mats: Sequence[np.ndarray], runs: Sequence[Tuple[int, int]],
+                      terminal: Optional[np.ndarray] = None, suffix: bool = True):
+        mats = [np.ascontiguousarray(M, dtype=np.uint64) for M in mats]
+        rows = np.array([M.shape[0] for M in mats], np.int32)
+        cols = np.array([M.shape[1] for M in mats], np.int32)
+        ptrs = (P(C.c_uint64) * len(mats))(*[_p(M, C.c_uint64) for M in mats])
+        run_mat = np.array([r[0] for r in runs], np.int32)
+        run_len = np.array([r[1] for r in runs], np.int64)
+        N = int(run_len.sum())
+        term = None if terminal is None else np.ascontiguousarray(terminal, dtype=np.uint64)
+        opt = np.zeros(1, np.uint64)
+        total = int(rows[run_mat[0]]) + int(sum(int(cols[run_mat[r]]) * int(run_len[r])
+                                                 for r in range(len(runs))))
+        suf = np.empty(total, np.uint64) if suffix else None
+        _check(lib().cfp_minplus_chain(self._h, len(mats), _p(rows, C.c_int32), _p(cols, C.c_int32),
+                                       ptrs, len(runs), _p(run_mat, C.c_int32), _p(run_len, C.c_int64),
+                                       _p(term, C.c_uint64), _p(opt, C.c_uint64), _p(suf, C.c_uint64)))
+        if not suffix:
+            return int(opt[0]), None
+        out, off = [suf[:rows[run_mat[0]]]], int(rows[run_mat[0]])
+        for r in range(len(runs)):
+            c = int(cols[run_mat[r]])
+            for _ in range(int(run_len[r])):
+                out.append(suf[off:off + c])
+                off += c
+        assert len(out) == N + 1
+        return int(opt[0]), out
+
+    # -- (3)
+    def search_plan(self, prob) -> Plan:
+        m = _Marshal()
+        p = m.problem(prob)
+        N = len(prob.instances)
+        kmax = max(int(len(t.radix)) for t in prob.types)
+        idx = np.empty(N, np.uint64)
+        dig = np.empty(N * kmax, np.int32)
+        seg = np.empty(N, np.uint64)
+        plan = cfp_plan(0, _p(idx, C.c_uint64), _p(dig, C.c_int32), kmax, _p(seg, C.c_uint64))
+        _check(lib().cfp_search_plan(self._h, C.byref(p), C.byref(plan)))
+        return Plan(int(plan.total_ns), idx, dig.reshape(N, kmax), seg)
+
+    def minplus_product(self, A: np.ndarray, B: np.ndarray) -> Tuple[np.ndarray, np.ndarray]:
+        A = np.ascontiguousarray(A, dtype=np.uint64)
+        B = np.ascontiguousarray(B, dtype=np.uint64)
+        m, k = A.shape
+        k2, n = B.shape
+        if k != k2:
+            raise CfpError(CFP_EINVAL, "inner dimensions differ")
+        Cm = np.empty((m, n), np.uint64)
+        arg = np.empty((m, n), np.uint64)
+        _check(lib().cfp_minplus_product(self._h, m, k, n, _p(A, C.c_uint64), _p(B, C.c_uint64),
+                                         _p(Cm, C.c_uint64), _p(arg, C.c_uint64)))
+        return Cm, arg
+
+    def prepare(self, prob) -> "Prepared":
+        return Prepared(self, prob)
+
+    def intpipe_bench(self, op: int = 0, iters: int = 20000) -> Tuple[float, float]:
+        ops, ms = C.c_double(), C.c_double()
+        _check(lib().cfp_intpipe_bench(self._h, op, iters, C.byref(ops), C.byref(ms)))
+        return ops.value, ms.value
+
+
+class Prepared:
+    """Device-resident problem: prepare once, execute many times."""
+
+    def __init__(self, ctx: Context, prob):
+        self.ctx = ctx
+        self._m = _Marshal()
+        p = self._m.problem(prob)
+        self._h = C.c_void_p()
+        _check(lib().cfp_prepare(ctx._h, C.byref(p), C.byref(self._h)))
+        self.N = len(prob.instances)
+        self.kmax = max(int(len(t.radix)) for t in prob.types)
+
+    def execute(self):
+        _check(lib().cfp_execute(self.ctx._h, self._h))
+
+    def fetch(self) -> Plan:
+        idx = np.empty(self.N, np.uint64)
+        dig = np.empty(self.N * self.kmax, np.int32)
+        seg = np.empty(self.N, np.uint64)
+        plan = cfp_plan(0, _p(idx, C.c_uint64), _p(dig, C.c_int32), self.kmax, _p(seg, C.c_uint64))
+        _check(lib().cfp_fetch_plan(self.ctx._h, self._h, C.byref(plan)))
+        return Plan(int(plan.total_ns), idx, dig.reshape(self.N, self.kmax), seg)
+
+    def info(self) -> PreparedInfo:
+        i = cfp_prepared_info()
+        _check(lib().cfp_prepared_query(self._h, C.byref(i)))
+        sched = [(i.prefix_len[t], i.nb[t] // 100, i.nb[t] % 100, i.na[t]) for t in range(i.num_types)]
+        return PreparedInfo(i.combos, i.combos_local, i.evals, i.num_types, i.num_transitions,
+                            i.wide_types, i.kernel_launches, sched)
+
+    def time_kernels(self, on: bool = True):
+        _check(lib().cfp_prepared_time_kernels(self._h, 1 if on else 0))
+
+    def kernel_ms(self) -> Tuple[float, float]:
+        a, b = C.c_double(), C.c_double()
+        _check(lib().cfp_prepared_kernel_ms(self._h, C.byref(a), C.byref(b)))
+        return a.value, b.value
+
+    def close(self):
+        if self._h:
+            lib().cfp_prepared_free(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+# ---------------------------------------------------------------- host-only helpers
+def shard_range(units: int, align: int, world: int, rank: int) -> Tuple[int, int]:
+    lo, hi = C.c_int64(), C.c_int64()
+    _check(lib().cfp_shard_range(units, align, world, rank, C.byref(lo), C.byref(hi)))
+    return lo.value, hi.value
+
+
+def pack_keys(cost: np.ndarray, idx: np.ndarray, idx_bits: int) -> np.ndarray:
+    cost = np.ascontiguousarray(cost, np.uint64)
+    idx = np.ascontiguousarray(idx, np.uint64)
+    keys = np.empty_like(cost)
+    _check(lib().cfp_pack_keys(cost.size, _p(cost, C.c_uint64), _p(idx, C.c_uint64), idx_bits,
+                               _p(keys, C.c_uint64)))
+    return keys
+
+
+def unpack_keys(keys: np.ndarray, idx_bits: int) -> Tuple[np.ndarray, np.ndarray]:
+    keys = np.ascontiguousarray(keys, np.uint64)
+    cost = np.empty_like(keys)
+    idx = np.empty_like(keys)
+    _check(lib().cfp_unpack_keys(keys.size, _p(keys, C.c_uint64), idx_bits, _p(cost, C.c_uint64),
+                                 _p(idx, C.c_uint64)))
+    return cost, idx
+
+
+def nccl_unique_id() -> bytes:
+    buf = C.create_string_buffer(128)
+    _check(lib().cfp_nccl_unique_id(buf))
+    return buf.raw

@@ -1,0 +1,166 @@
+// cfp_internal.h -- structures shared by the host runtime (cfp_host.cu) and the
+// sm_100a kernels (cfp_kernels.cu).  Not part of the ABI.
+//
+// Vocabulary: a segment type has K blocks ("digits"); a
+// combination s is a mixed-radix number, block 0 most significant.  After
+// pruning strategies whose own p+c is infeasible (monotone remap),
+// every block j has D'_j >= 1 "compact" strategies.
+//
+// Enumeration schedule of one type (chosen by the host planner):
+//   digits [0, P)  = prefix: one GPU thread (or VG threads) per prefix value;
+//                    every fold digit (consumer block of a cross edge) is here.
+//   suffix digits  = M (loop) | A (broadcast operand) | B (register operand),
+//                    no intra edge between an A digit and a B digit.
+// For a prefix p and an M value m, every combination (p, m, a, b) costs
+//      C = K0[p] + Z[ctxZ] + X[ctxA][a] + Y[ctxB][b]
+// (each cost term of Eq. 3 is assigned to exactly one of the four tables), so
+// one fused add+min (VIADDMNMX) per combination evaluates and reduces it.
+#pragma once
+#include <cstdint>
+
+namespace cfp {
+
+constexpr int kMaxDigits = 32;
+constexpr int kMaxTerms = 96;
+constexpr int kBlock = 256;          // threads per CTA of the enumeration kernel
+constexpr uint32_t kCap32 = 0x7FFFFFFFu;            // narrow "infinity" (>= CAP => INF)
+constexpr uint64_t kCap64 = 0x7FFFFFFFFFFFFFFFull;  // wide "infinity"
+constexpr uint64_t kInf64 = 0xFFFFFFFFFFFFFFFFull;
+
+// A cost term over the digits of a table's index space.
+//   kind 0: unary   W[off + s_a]
+//   kind 1: pair    R[off + s_a * db + s_b]
+//   kind 2: cross   Q[off + u * db + s_b]      (fold only; u = input state)
+struct Term {
+  int32_t kind;
+  int32_t a, b;      // positions in the owning index space (or block ids)
+  int32_t db;        // row length of the pair table
+  int64_t off;       // element offset into the value blob
+};
+
+// A table T[e] over the mixed-radix space of `ndig` digits (last fastest),
+// entry = saturated sum of `nterm` terms.  Rows may be padded: the last digit
+// group spans `row` entries of which `row_valid` are real (the rest = CAP).
+struct TableSpec {
+  int32_t ndig;
+  int32_t radix[kMaxDigits];
+  int32_t nterm;
+  Term term[kMaxTerms];
+  int64_t rows;        // product of radices of the leading (row) digits
+  int32_t row_digits;  // number of trailing digits forming one row
+  int64_t row_valid;   // product of radices of the row digits
+  int64_t row;         // padded row length
+  int64_t out_off;     // element offset of T in the derived blob
+};
+
+struct EnumParams {
+  // prefix mapping: p = h * W + l, thread t -> (l, vg) = t / Gpad, h = h0 + t % Gpad
+  int32_t P;                    // prefix length
+  int32_t pre_radix[kMaxDigits];
+  int64_t W;                    // size of the low prefix part (canonical last digits)
+  int64_t G, Gpad, h0;          // high values handled, padded to a multiple of kBlock
+  int32_t VG;                   // register groups per prefix (B split)
+  int64_t pre_sx[kMaxDigits], pre_sy[kMaxDigits], pre_sz[kMaxDigits];  // ctx strides
+  int64_t nM;                   // |M space| (mtab rows)
+  int32_t na, na_pad;           // |A space| (XT row length), padded
+  int32_t nb;                   // |B space|
+  int32_t nb_pad;               // YT row length = VG * NB
+  int32_t o_mode;               // 0: o in B, 1: o in M, 2: o in prefix
+  int32_t o_pre;                // o's prefix position (mode 2)
+  int32_t o_bstride, o_bradix;  // v(j) = (j / o_bstride) % o_bradix (mode 0)
+  int32_t Do;                   // compact output radix
+  int32_t staged;               // 1: tables sliced into shared memory per CTA
+  int32_t init_row;             // 1: B_p row must be pre-filled with CAP
+  int64_t xspan, yspan, zspan;  // slice lengths (staged)
+  // device pointers (element type = the path's value type)
+  const void* XT; const void* YT; const void* ZT; const void* K0;
+  const int4* mtab;             // [nM] (x, y, z, v_o)
+  void* Bp;                     // [G*W][Do] local canonical prefixes
+};
+
+struct FoldParams {
+  int32_t P;
+  int32_t pre_radix[kMaxDigits];
+  int64_t p_lo;                 // global canonical prefix of local row 0
+  int64_t nPl;                  // local prefixes
+  int32_t Din, Do;
+  int32_t nq;                   // cross terms: a = prefix position of consumer, db, off
+  Term q[kMaxTerms];
+  int32_t CH;                   // prefixes per chunk
+  int64_t nchunks;
+  const void* Bp;
+  const void* vals;             // value blob (compact Q tables)
+  void* chunkmin;               // [nchunks][Din][Do]
+};
+
+// Generic evaluation of all intra terms of a compact combination (argmin
+// recovery) -- terms reference block ids directly.
+struct EvalSpec {
+  int32_t K;
+  int32_t radix[kMaxDigits];    // compact
+  int32_t P;                    // prefix length
+  int32_t o;                    // output block
+  int32_t nterm;
+  Term term[kMaxTerms];         // kind 0/1 over block ids
+  int64_t nsuffix;              // prod of suffix radices
+};
+
+struct ArgminParams {
+  FoldParams f;
+  EvalSpec e;
+  const void* K0;               // unused (full evaluation)
+  int32_t map_off[kMaxDigits];  // compact -> original strategy maps (int32 blob)
+  int32_t orig_radix[kMaxDigits];
+  int32_t Do_orig;
+  const int32_t* maps;
+  const int32_t* vmap;          // compact v -> original v of the output block
+  uint64_t* A_out;              // [Din][Do_orig] uint64
+  uint64_t* I_out;
+  uint64_t* key_out;            // [Din][Do_orig] local (cost, idx) for merge (nullable)
+  int64_t* pstar;               // scratch [Din*Do]
+};
+
+struct ChainInst {
+  const uint64_t* A;            // [rows][cols]
+  const uint64_t* I;            // nullable
+  int32_t rows, cols;
+  int32_t K;                    // digits of the instance's type (plan decode)
+  int32_t radix_off;            // offset into radix blob
+};
+
+struct ChainRun {
+  int32_t first;                // first instance (0-based)
+  int32_t len;                  // instances in the run (same matrix)
+};
+
+struct CompactJob {
+  int32_t kind;          // 0 unary, 1 pair (rows & cols remapped), 2 cross (cols remapped)
+  int32_t rows, cols;    // compact shape (unary: rows = 1)
+  int32_t raw_cols;      // raw row length
+  int64_t raw_off, raw_off2;   // comp / comm (unary), table (pair/cross); raw_off2 < 0: no comm
+  int32_t map_r, map_c;  // offsets into the map blob (-1 = identity)
+  int64_t out_off;
+};
+
+struct ChainParams {
+  int32_t N;
+  int32_t nruns;
+  const ChainInst* inst;        // [N]
+  const ChainRun* runs;         // [nruns], in instance order
+  const uint64_t* terminal;     // nullable
+  uint64_t* G;                  // ragged (N+1) vectors
+  const int64_t* goff;          // [N+2] offsets of G_0..G_N (+end)
+  uint64_t* powers;             // scratch
+  int64_t powers_cap;           // elements available
+  int32_t backtrack;
+  // plan outputs (backtrack)
+  uint64_t* total;
+  uint64_t* seg_index;
+  uint64_t* seg_ns;
+  int32_t* digits;
+  int32_t kmax;
+  const int32_t* radix_blob;
+  int32_t* status;              // 0 ok, 3 infeasible, 4 scratch too small
+};
+
+}  // namespace cfp

@@ -1,0 +1,796 @@
+// cfp_kernels.cu -- sm_100a kernels of the CFP plan-search hot path.
+//
+// Hot path and where each step lives:
+//   a0 stage:       compact_kernel (prune + p+c), build_table_kernel (X/Y/Z/K0)
+//   a1 enumerate:   enum_kernel  -- one VIADDMNMX per strategy combination
+//   a1 fold:        fold_kernel  -- cross-segment terms Q_j[u][s_j] folded per
+//                                   prefix: A[u][v] = min_p X_p[u] + B_p[v]
+//   a1 argmin:      fold_reduce_kernel + suffix_argmin_kernel -- least index
+//   a2 merge:       NCCL min-allreduce on packed keys (host side, world > 1)
+//   a3 chain:       chain_kernel -- (min,+) powers by repeated squaring,
+//                                   suffix vectors by doubling
+//   a4 backtrack:   chain_kernel (forward greedy) + plan decode
+// Everything is exact integer arithmetic; the narrow path keeps values in
+// [0, CAP32] with CAP32 = 2^31-1 meaning "infeasible" (any sum >= CAP is
+// infeasible, guaranteed by the host's bound check), so the fused
+// add+min never wraps.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "cfp_internal.h"
+
+namespace cfp {
+
+template <typename V> struct VT;
+template <> struct VT<uint32_t> {
+  static constexpr uint32_t CAP = kCap32;
+  static __device__ __forceinline__ uint32_t addmin(uint32_t a, uint32_t b, uint32_t c) {
+    return __viaddmin_u32(a, b, c);          // VIADDMNMX.U32: min(a + b, c)
+  }
+  static __device__ __forceinline__ uint32_t sat(uint32_t a, uint32_t b) {
+    return __viaddmin_u32(a, b, CAP);
+  }
+  static __device__ __forceinline__ uint32_t mn(uint32_t a, uint32_t b) { return a < b ? a : b; }
+};
+template <> struct VT<uint64_t> {
+  static constexpr uint64_t CAP = kCap64;
+  static __device__ __forceinline__ uint64_t addmin(uint64_t a, uint64_t b, uint64_t c) {
+    uint64_t s = a + b;
+    return s < c ? s : c;
+  }
+  static __device__ __forceinline__ uint64_t sat(uint64_t a, uint64_t b) {
+    uint64_t s = a + b;
+    return s < CAP ? s : CAP;
+  }
+  static __device__ __forceinline__ uint64_t mn(uint64_t a, uint64_t b) { return a < b ? a : b; }
+};
+
+// --------------------------------------------------------------------------
+// a0: compaction.  Each job gathers one table of the pruned problem from the
+// raw uint32 inputs: unary w = p + c (INF absorbing), pair / cross
+// tables with rows/cols remapped to the surviving strategies.  INF -> CAP.
+// --------------------------------------------------------------------------
+
+
+template <typename V>
+__global__ void compact_kernel(const CompactJob* __restrict__ jobs, const uint32_t* __restrict__ raw,
+                               const int32_t* __restrict__ maps, V* __restrict__ out) {
+  const CompactJob j = jobs[blockIdx.x];
+  const int64_t n = (int64_t)j.rows * j.cols;
+  for (int64_t e = threadIdx.x; e < n; e += blockDim.x) {
+    const int32_t r = (int32_t)(e / j.cols), c = (int32_t)(e % j.cols);
+    const int32_t rc = j.map_c >= 0 ? maps[j.map_c + c] : c;
+    V v;
+    if (j.kind == 0) {
+      const uint32_t pc = raw[j.raw_off + rc];
+      const uint32_t cc = j.raw_off2 >= 0 ? raw[j.raw_off2 + rc] : 0u;
+      if (pc == 0xFFFFFFFFu || cc == 0xFFFFFFFFu) v = VT<V>::CAP;
+      else {
+        const uint64_t s = (uint64_t)pc + cc;
+        v = s >= (uint64_t)VT<V>::CAP ? VT<V>::CAP : (V)s;
+      }
+    } else {
+      const int32_t rr = (j.kind == 1 && j.map_r >= 0) ? maps[j.map_r + r] : r;
+      const uint32_t x = raw[j.raw_off + (int64_t)rr * j.raw_cols + rc];
+      v = (x == 0xFFFFFFFFu || (uint64_t)x >= (uint64_t)VT<V>::CAP) ? VT<V>::CAP : (V)x;
+    }
+    out[j.out_off + e] = v;
+  }
+}
+
+// --------------------------------------------------------------------------
+// a0: derived tables X / Y / Z / K0 -- saturated sums of the cost terms the
+// host assigned to each table, over the table's mixed-radix index space.
+// --------------------------------------------------------------------------
+template <typename V>
+__global__ void build_table_kernel(const TableSpec* __restrict__ specs, const V* __restrict__ vals,
+                                   V* __restrict__ out) {
+  const TableSpec& s = specs[blockIdx.y];
+  const int64_t total = s.rows * s.row;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = e / s.row, c = e % s.row;
+    V acc = 0;
+    if (c >= s.row_valid) {
+      acc = VT<V>::CAP;
+    } else {
+      int32_t dig[kMaxDigits];
+      int64_t q = r * s.row_valid + c;
+      for (int d = s.ndig - 1; d >= 0; --d) {
+        dig[d] = (int32_t)(q % s.radix[d]);
+        q /= s.radix[d];
+      }
+      for (int t = 0; t < s.nterm; ++t) {
+        const Term& tm = s.term[t];
+        const V v = tm.kind == 0 ? vals[tm.off + dig[tm.a]]
+                                 : vals[tm.off + (int64_t)dig[tm.a] * tm.db + dig[tm.b]];
+        acc = VT<V>::sat(acc, v);
+      }
+    }
+    out[s.out_off + e] = acc;
+  }
+}
+
+template <typename V>
+__global__ void fill_kernel(V* __restrict__ p, int64_t n, V v) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    p[i] = v;
+}
+
+// --------------------------------------------------------------------------
+// a1: exhaustive enumeration.  Thread = (prefix p, register group vg).  For
+// each M value: Y[j] = YT[..][j] + K0[p] + Z (NB registers), then for every A
+// value x = XT[..][a] (a warp-uniform shared-memory broadcast) and every
+// register slot j:  acc[j] = min(x + Y[j], acc[j])  -- one VIADDMNMX per
+// combination (p, m, a, b_j).  acc[j] ends as min over the combination's
+// bucket; the per-prefix bucket minima B_p[v] go to global memory.
+// --------------------------------------------------------------------------
+template <typename V> struct Vec4;
+template <> struct Vec4<uint32_t> { using T = uint4; static constexpr int N = 4; };
+template <> struct Vec4<uint64_t> { using T = ulonglong2; static constexpr int N = 2; };
+
+template <typename V>
+__device__ __forceinline__ void load_vec(const V* p, V* out);
+template <>
+__device__ __forceinline__ void load_vec<uint32_t>(const uint32_t* p, uint32_t* out) {
+  const uint4 v = *reinterpret_cast<const uint4*>(p);
+  out[0] = v.x; out[1] = v.y; out[2] = v.z; out[3] = v.w;
+}
+template <>
+__device__ __forceinline__ void load_vec<uint64_t>(const uint64_t* p, uint64_t* out) {
+  const ulonglong2 v = *reinterpret_cast<const ulonglong2*>(p);
+  out[0] = v.x; out[1] = v.y;
+}
+
+template <typename V, int NB, bool STAGED>
+__global__ void __launch_bounds__(kBlock) enum_kernel(const EnumParams p) {
+  using T = VT<V>;
+  constexpr int VN = Vec4<V>::N;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int64_t t = (int64_t)blockIdx.x * kBlock + threadIdx.x;
+  const int64_t grp = t / p.Gpad;                 // (l, vg): CTA-uniform
+  const int64_t hh = t - grp * p.Gpad;
+  const int64_t l = grp / p.VG;
+  const int vg = (int)(grp - l * p.VG);
+  const bool live = hh < p.G && l < p.W;
+  const int64_t pg = (p.h0 + hh) * p.W + l;       // global canonical prefix
+  const int64_t row = hh * p.W + l;               // local canonical prefix
+
+  // prefix digits -> table offsets (ctx digits live in the low part, so the
+  // offsets are CTA-uniform whenever STAGED)
+  int64_t sx = 0, sy = 0, sz = 0;
+  int od = 0;
+  {
+    int64_t q = pg;
+    for (int d = p.P - 1; d >= 0; --d) {
+      const int dig = (int)(q % p.pre_radix[d]);
+      q /= p.pre_radix[d];
+      sx += dig * p.pre_sx[d];
+      sy += dig * p.pre_sy[d];
+      sz += dig * p.pre_sz[d];
+      if (d == p.o_pre) od = dig;
+    }
+  }
+  const V* XT = static_cast<const V*>(p.XT);
+  const V* YT = static_cast<const V*>(p.YT);
+  const V* ZT = static_cast<const V*>(p.ZT);
+  const int4* MT = p.mtab;
+  if constexpr (STAGED) {
+    V* xs = reinterpret_cast<V*>(smem_raw);
+    V* ys = xs + p.xspan;
+    V* zs = ys + p.yspan;
+    int4* ms = reinterpret_cast<int4*>(zs + ((p.zspan + 3) & ~3LL));
+    for (int64_t i = threadIdx.x * VN; i < p.xspan; i += kBlock * VN)
+      *reinterpret_cast<typename Vec4<V>::T*>(xs + i) =
+          *reinterpret_cast<const typename Vec4<V>::T*>(XT + sx + i);
+    for (int64_t i = threadIdx.x * VN; i < p.yspan; i += kBlock * VN)
+      *reinterpret_cast<typename Vec4<V>::T*>(ys + i) =
+          *reinterpret_cast<const typename Vec4<V>::T*>(YT + sy + i);
+    for (int64_t i = threadIdx.x; i < p.zspan; i += kBlock) zs[i] = ZT[sz + i];
+    for (int64_t i = threadIdx.x; i < p.nM; i += kBlock) ms[i] = MT[i];
+    __syncthreads();
+    XT = xs; YT = ys; ZT = zs; MT = ms;
+    sx = sy = sz = 0;
+  }
+  if (!live) return;
+
+  V* Bp = static_cast<V*>(p.Bp) + row * p.Do;
+  const V k0 = static_cast<const V*>(p.K0)[pg];
+  if (p.init_row) {
+    for (int v = 0; v < p.Do; ++v) Bp[v] = T::CAP;
+  }
+  V acc[NB];
+#pragma unroll
+  for (int j = 0; j < NB; ++j) acc[j] = T::CAP;
+  const int ybase = vg * NB;
+
+  for (int64_t m = 0; m < p.nM; ++m) {
+    const int4 mt = MT[m];
+    const V km = T::sat(k0, ZT[sz + mt.z]);
+    const V* yr = YT + sy + mt.y + ybase;
+    V y[NB];
+#pragma unroll
+    for (int j = 0; j < NB; j += VN) load_vec<V>(yr + j, y + j);
+#pragma unroll
+    for (int j = 0; j < NB; ++j) y[j] = T::sat(y[j], km);
+    const V* xr = XT + sx + mt.x;
+#pragma unroll 2
+    for (int a = 0; a < p.na_pad; a += VN) {
+      V x[VN];
+      load_vec<V>(xr + a, x);
+#pragma unroll
+      for (int q = 0; q < VN; ++q)
+#pragma unroll
+        for (int j = 0; j < NB; ++j) acc[j] = T::addmin(x[q], y[j], acc[j]);
+    }
+    if (p.o_mode == 1) {                        // bucket digit in M: flush per m
+      V r = acc[0];
+#pragma unroll
+      for (int j = 1; j < NB; ++j) r = T::mn(r, acc[j]);
+      Bp[mt.w] = T::mn(Bp[mt.w], r);
+#pragma unroll
+      for (int j = 0; j < NB; ++j) acc[j] = T::CAP;
+    }
+  }
+  if (p.o_mode == 0) {
+    if (p.o_bstride == 1 && p.o_bradix == p.nb) {       // B = {o}: slot j <-> v
+#pragma unroll
+      for (int j = 0; j < NB; ++j)
+        if (ybase + j < p.nb) Bp[ybase + j] = acc[j];
+    } else {
+#pragma unroll
+      for (int j = 0; j < NB; ++j)
+        if (ybase + j < p.nb) {
+          const int v = ((ybase + j) / p.o_bstride) % p.o_bradix;
+          Bp[v] = T::mn(Bp[v], acc[j]);
+        }
+    }
+  } else if (p.o_mode == 2) {
+    V r = acc[0];
+#pragma unroll
+    for (int j = 1; j < NB; ++j) r = T::mn(r, acc[j]);
+    Bp[od] = r;
+  }
+}
+
+// --------------------------------------------------------------------------
+// a1 fold: chunk c of local prefixes; chunkmin[c][u][v] = min_p X_p[u] + B_p[v]
+// with X_p[u] = sum_{cross (j, Q)} Q[u][s_j(p)]   (Eq. 3 r_n).
+// --------------------------------------------------------------------------
+template <typename V>
+__device__ __forceinline__ V cross_sum(const FoldParams& f, const V* vals, int64_t pg, int u) {
+  V x = 0;
+  for (int i = 0; i < f.nq; ++i) {
+    const Term& q = f.q[i];
+    int64_t pp = pg;
+    int dig = 0;
+    for (int d = f.P - 1; d >= q.a; --d) {
+      dig = (int)(pp % f.pre_radix[d]);
+      pp /= f.pre_radix[d];
+    }
+    x = VT<V>::sat(x, vals[q.off + (int64_t)u * q.db + dig]);
+  }
+  return x;
+}
+
+template <typename V>
+__global__ void __launch_bounds__(256) fold_kernel(const FoldParams f) {
+  using T = VT<V>;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  V* bs = reinterpret_cast<V*>(smem_raw);          // [CH][Do]
+  V* xs = bs + (int64_t)f.CH * f.Do;                // [CH][Din]
+  int32_t* dg = reinterpret_cast<int32_t*>(xs + (int64_t)f.CH * f.Din);   // [CH][nq]
+  const int64_t c = blockIdx.x;
+  const int64_t p0 = c * f.CH;
+  const int n = (int)min((int64_t)f.CH, f.nPl - p0);
+  const V* Bp = static_cast<const V*>(f.Bp);
+  const V* vals = static_cast<const V*>(f.vals);
+  for (int e = threadIdx.x; e < n * f.Do; e += blockDim.x) bs[e] = Bp[p0 * f.Do + e];
+  for (int e = threadIdx.x; e < n * f.nq; e += blockDim.x) {
+    const int pi = e / f.nq, i = e % f.nq;
+    int64_t pp = f.p_lo + p0 + pi;
+    int dig = 0;
+    for (int d = f.P - 1; d >= f.q[i].a; --d) {
+      dig = (int)(pp % f.pre_radix[d]);
+      pp /= f.pre_radix[d];
+    }
+    dg[e] = dig;
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < n * f.Din; e += blockDim.x) {
+    const int pi = e / f.Din, u = e % f.Din;
+    V x = 0;
+    for (int i = 0; i < f.nq; ++i)
+      x = T::sat(x, vals[f.q[i].off + (int64_t)u * f.q[i].db + dg[pi * f.nq + i]]);
+    xs[e] = x;
+  }
+  __syncthreads();
+  V* out = static_cast<V*>(f.chunkmin) + c * (int64_t)f.Din * f.Do;
+  // register-blocked: each thread owns a 2x2 (u, v) block
+  const int ub = (f.Din + 1) / 2, vb = (f.Do + 1) / 2;
+  for (int blk = threadIdx.x; blk < ub * vb; blk += blockDim.x) {
+    const int u0 = (blk / vb) * 2, v0 = (blk % vb) * 2;
+    const int u1 = min(u0 + 1, f.Din - 1), v1 = min(v0 + 1, f.Do - 1);
+    V m00 = T::CAP, m01 = T::CAP, m10 = T::CAP, m11 = T::CAP;
+    for (int pi = 0; pi < n; ++pi) {
+      const V x0 = xs[pi * f.Din + u0], x1 = xs[pi * f.Din + u1];
+      const V b0 = bs[pi * f.Do + v0], b1 = bs[pi * f.Do + v1];
+      m00 = T::addmin(x0, b0, m00);
+      m01 = T::addmin(x0, b1, m01);
+      m10 = T::addmin(x1, b0, m10);
+      m11 = T::addmin(x1, b1, m11);
+    }
+    out[u0 * f.Do + v0] = m00;
+    if (v0 + 1 < f.Do) out[u0 * f.Do + v0 + 1] = m01;
+    if (u0 + 1 < f.Din) {
+      out[(u0 + 1) * f.Do + v0] = m10;
+      if (v0 + 1 < f.Do) out[(u0 + 1) * f.Do + v0 + 1] = m11;
+    }
+  }
+}
+
+// --------------------------------------------------------------------------
+// argmin phase 1: per (u, v): A = min over chunks; the first chunk attaining
+// it, then the least local prefix in that chunk with X_p[u] + B_p[v] == A.
+// One warp per (u, v).
+// --------------------------------------------------------------------------
+template <typename V>
+__global__ void fold_reduce_kernel(const FoldParams f, V* __restrict__ Aval, int64_t* __restrict__ pstar) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (warp >= f.Din * f.Do) return;
+  const int u = warp / f.Do, v = warp % f.Do;
+  const V* cm = static_cast<const V*>(f.chunkmin);
+  V best = VT<V>::CAP;
+  int64_t bc = INT64_MAX;
+  for (int64_t c = lane; c < f.nchunks; c += 32) {
+    const V x = cm[c * f.Din * f.Do + u * f.Do + v];
+    if (x < best) { best = x; bc = c; }       // c increasing per lane: first wins
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    const V ob = __shfl_xor_sync(0xffffffffu, best, o);
+    const int64_t oc = __shfl_xor_sync(0xffffffffu, bc, o);
+    if (ob < best || (ob == best && oc < bc)) { best = ob; bc = oc; }
+  }
+  if (best >= VT<V>::CAP) {
+    if (lane == 0) { Aval[warp] = VT<V>::CAP; pstar[warp] = -1; }
+    return;
+  }
+  const V* Bp = static_cast<const V*>(f.Bp);
+  const V* vals = static_cast<const V*>(f.vals);
+  const int64_t p0 = bc * f.CH;
+  const int n = (int)min((int64_t)f.CH, f.nPl - p0);
+  int64_t first = INT64_MAX;
+  for (int pi = lane; pi < n; pi += 32) {
+    const int64_t pl = p0 + pi;
+    const V x = cross_sum<V>(f, vals, f.p_lo + pl, u);
+    if (VT<V>::sat(x, Bp[pl * f.Do + v]) == best) { first = pl; break; }
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    const int64_t of = __shfl_xor_sync(0xffffffffu, first, o);
+    first = of < first ? of : first;
+  }
+  if (lane == 0) { Aval[warp] = best; pstar[warp] = first; }
+}
+
+// --------------------------------------------------------------------------
+// argmin phase 2: least suffix (in canonical order, restricted to s_o = v when
+// o is a suffix digit) whose intra cost equals B_p*[v]; then the original
+// combination index and the outputs in the caller's (unpruned) layout.
+// --------------------------------------------------------------------------
+template <typename V>
+__global__ void __launch_bounds__(256) suffix_argmin_kernel(const ArgminParams ap,
+                                                            const V* __restrict__ Aval,
+                                                            const V* __restrict__ vals) {
+  const FoldParams& f = ap.f;
+  const EvalSpec& e = ap.e;
+  const int pair = blockIdx.x;
+  const int u = pair / f.Do, v = pair % f.Do;
+  const int vo = ap.vmap[v];
+  const int64_t outi = (int64_t)u * ap.Do_orig + vo;
+  const int64_t pl = ap.pstar[pair];
+  __shared__ unsigned long long s_first;
+  if (pl < 0) {
+    if (threadIdx.x == 0) {
+      ap.A_out[outi] = kInf64;
+      ap.I_out[outi] = kInf64;
+    }
+    return;
+  }
+  const V* Bp = static_cast<const V*>(f.Bp);
+  const uint64_t target = (uint64_t)Bp[pl * f.Do + v];
+  const int64_t pg = f.p_lo + pl;
+  int32_t pre[kMaxDigits];
+  {
+    int64_t q = pg;
+    for (int d = e.P - 1; d >= 0; --d) { pre[d] = (int)(q % e.radix[d]); q /= e.radix[d]; }
+  }
+  const bool o_suffix = e.o >= e.P;
+  const int64_t nrest = o_suffix ? e.nsuffix / e.radix[e.o] : e.nsuffix;
+  if (threadIdx.x == 0) s_first = ~0ull;
+  __syncthreads();
+  const int64_t per = (nrest + blockDim.x - 1) / blockDim.x;
+  const int64_t lo = (int64_t)threadIdx.x * per;
+  const int64_t hi = min(nrest, lo + per);
+  for (int64_t r = lo; r < hi; ++r) {
+    int32_t s[kMaxDigits];
+    for (int d = 0; d < e.P; ++d) s[d] = pre[d];
+    int64_t q = r;
+    for (int d = e.K - 1; d >= e.P; --d) {
+      if (o_suffix && d == e.o) { s[d] = v; continue; }
+      s[d] = (int)(q % e.radix[d]);
+      q /= e.radix[d];
+    }
+    uint64_t c = 0;
+    bool inf = false;
+    for (int i = 0; i < e.nterm && !inf; ++i) {
+      const Term& tm = e.term[i];
+      const V x = tm.kind == 0 ? vals[tm.off + s[tm.a]]
+                               : vals[tm.off + (int64_t)s[tm.a] * tm.db + s[tm.b]];
+      if (x >= VT<V>::CAP) inf = true;
+      c += (uint64_t)x;
+    }
+    if (!inf && c == target) {
+      // suffix index in canonical order (o digit included)
+      int64_t sfx = 0;
+      for (int d = e.P; d < e.K; ++d) sfx = sfx * e.radix[d] + s[d];
+      atomicMin(&s_first, (unsigned long long)sfx);
+      break;
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const uint64_t sfx = s_first;
+    // compact digits of the winner -> original index
+    int32_t s[kMaxDigits];
+    for (int d = 0; d < e.P; ++d) s[d] = pre[d];
+    uint64_t q = sfx;
+    for (int d = e.K - 1; d >= e.P; --d) { s[d] = (int)(q % e.radix[d]); q /= e.radix[d]; }
+    uint64_t idx = 0;
+    for (int d = 0; d < e.K; ++d) idx = idx * ap.orig_radix[d] + ap.maps[ap.map_off[d] + s[d]];
+    ap.A_out[outi] = (uint64_t)Aval[pair];
+    ap.I_out[outi] = sfx == ~0ull ? kInf64 : idx;     // ~0: cannot happen (exact arithmetic)
+  }
+}
+
+// --------------------------------------------------------------------------
+// a3 + a4: chain (single CTA).  G_N = terminal; runs processed last to first;
+// a run of L identical square matrices uses powers P_j = M^(2^j) (repeated
+// squaring) and fills its suffix vectors by doubling:
+//    G_{e-k} = P_j (x) G_{e-k+2^j}   for k in [2^j, 2^(j+1))
+// then (optionally) the forward greedy backtrack picks, at each instance, the
+// optimal successor with the least combination index.
+// --------------------------------------------------------------------------
+__device__ __forceinline__ uint64_t sat64(uint64_t a, uint64_t b) {
+  return (a == kInf64 || b == kInf64) ? kInf64 : a + b;
+}
+
+
+
+__device__ void matvec(const uint64_t* M, int rows, int cols, const uint64_t* g, uint64_t* out,
+                       int tid, int nth) {
+  for (int u = tid; u < rows; u += nth) {
+    uint64_t best = kInf64;
+    for (int v = 0; v < cols; ++v) {
+      const uint64_t c = sat64(M[(int64_t)u * cols + v], g[v]);
+      best = c < best ? c : best;
+    }
+    out[u] = best;
+  }
+}
+
+__global__ void __launch_bounds__(1024) chain_kernel(const ChainParams cp) {
+  const int tid = threadIdx.x, nth = blockDim.x;
+  const int N = cp.N;
+  uint64_t* GN = cp.G + cp.goff[N];
+  const int lastc = cp.inst[N - 1].cols;
+  for (int v = tid; v < lastc; v += nth) GN[v] = cp.terminal ? cp.terminal[v] : 0;
+  __syncthreads();
+  for (int r = cp.nruns - 1; r >= 0; --r) {
+    const ChainRun run = cp.runs[r];
+    const ChainInst in = cp.inst[run.first];
+    const int e = run.first + run.len;             // G_e known (1-based instance e)
+    if (run.len == 1) {
+      matvec(in.A, in.rows, in.cols, cp.G + cp.goff[e], cp.G + cp.goff[e - 1], tid, nth);
+      __syncthreads();
+      continue;
+    }
+    const int S = in.rows;                          // square
+    int levels = 0;
+    while ((1 << (levels + 1)) <= run.len) ++levels;   // P_0 .. P_levels
+    if ((int64_t)S * S * levels > cp.powers_cap) {
+      if (tid == 0) *cp.status = 4;
+      return;
+    }
+    // P_0 = M (read in place); P_j in scratch
+    for (int j = 1; j <= levels; ++j) {
+      const uint64_t* Pa = j == 1 ? in.A : cp.powers + (int64_t)(j - 2) * S * S;
+      uint64_t* Pc = cp.powers + (int64_t)(j - 1) * S * S;
+      for (int64_t c = tid; c < (int64_t)S * S; c += nth) {
+        const int i = (int)(c / S), k2 = (int)(c % S);
+        uint64_t best = kInf64;
+        for (int k = 0; k < S; ++k) {
+          const uint64_t x = sat64(Pa[(int64_t)i * S + k], Pa[(int64_t)k * S + k2]);
+          best = x < best ? x : best;
+        }
+        Pc[c] = best;
+      }
+      __syncthreads();
+    }
+    for (int j = 0; j <= levels; ++j) {
+      const uint64_t* Pj = j == 0 ? in.A : cp.powers + (int64_t)(j - 1) * S * S;
+      const int k_lo = 1 << j, k_hi = min(1 << (j + 1), run.len + 1);
+      const int64_t work = (int64_t)(k_hi - k_lo) * S;
+      for (int64_t w = tid; w < work; w += nth) {
+        const int k = k_lo + (int)(w / S), u = (int)(w % S);
+        const uint64_t* g = cp.G + cp.goff[e - k + (1 << j)];
+        uint64_t best = kInf64;
+        for (int v = 0; v < S; ++v) {
+          const uint64_t x = sat64(Pj[(int64_t)u * S + v], g[v]);
+          best = x < best ? x : best;
+        }
+        cp.G[cp.goff[e - k] + u] = best;
+      }
+      __syncthreads();
+    }
+  }
+  if (!cp.backtrack) return;
+  // forward greedy (warp 0)
+  if (tid < 32) {
+    const int lane = tid;
+    int u = 0;
+    if (cp.G[0] == kInf64) {
+      if (lane == 0) { *cp.status = 3; *cp.total = kInf64; }
+      return;
+    }
+    if (lane == 0) *cp.total = cp.G[0];
+    for (int n = 1; n <= N; ++n) {
+      const ChainInst in = cp.inst[n - 1];
+      const uint64_t target = cp.G[cp.goff[n - 1] + u];
+      const uint64_t* Gn = cp.G + cp.goff[n];
+      uint64_t bi = kInf64;
+      int bv = -1;
+      for (int v = lane; v < in.cols; v += 32) {
+        const uint64_t a = in.A[(int64_t)u * in.cols + v];
+        if (a == kInf64 || Gn[v] == kInf64 || a + Gn[v] != target) continue;
+        const uint64_t ix = in.I[(int64_t)u * in.cols + v];
+        if (ix < bi) { bi = ix; bv = v; }
+      }
+      for (int o = 16; o > 0; o >>= 1) {
+        const uint64_t ob = __shfl_xor_sync(0xffffffffu, bi, o);
+        const int ov = __shfl_xor_sync(0xffffffffu, bv, o);
+        if (ob < bi || (ob == bi && ov >= 0 && (bv < 0 || ov < bv))) { bi = ob; bv = ov; }
+      }
+      if (bv < 0) {
+        if (lane == 0) *cp.status = 3;
+        return;
+      }
+      if (lane == 0) {
+        cp.seg_index[n - 1] = bi;
+        cp.seg_ns[n - 1] = in.A[(int64_t)u * in.cols + bv];
+      }
+      u = bv;
+    }
+  }
+  __syncthreads();
+  if (*cp.status != 0) return;
+  for (int64_t w = tid; w < (int64_t)N * cp.kmax; w += nth) {
+    const int n = (int)(w / cp.kmax), j = (int)(w % cp.kmax);
+    const ChainInst in = cp.inst[n];
+    int32_t dval = -1;
+    if (j < in.K) {
+      uint64_t q = cp.seg_index[n];
+      for (int d = in.K - 1; d > j; --d) q /= (uint64_t)cp.radix_blob[in.radix_off + d];
+      dval = (int32_t)(q % (uint64_t)cp.radix_blob[in.radix_off + j]);
+    }
+    cp.digits[w] = dval;
+  }
+}
+
+// --------------------------------------------------------------------------
+// (min,+) product with least-k argmin (cfp_minplus_product; also the large-S
+// chain path).  16x16 output tile per CTA, K staged through shared memory.
+// --------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) minplus_kernel(int m, int k, int n, const uint64_t* __restrict__ A,
+                                                      const uint64_t* __restrict__ B, uint64_t* __restrict__ C,
+                                                      uint64_t* __restrict__ argk) {
+  __shared__ uint64_t As[16][17], Bs[16][17];
+  const int ty = threadIdx.x / 16, tx = threadIdx.x % 16;
+  const int i = blockIdx.y * 16 + ty, j = blockIdx.x * 16 + tx;
+  uint64_t best = kInf64, bk = kInf64;
+  for (int k0 = 0; k0 < k; k0 += 16) {
+    As[ty][tx] = (i < m && k0 + tx < k) ? A[(int64_t)i * k + k0 + tx] : kInf64;
+    Bs[ty][tx] = (k0 + ty < k && j < n) ? B[(int64_t)(k0 + ty) * n + j] : kInf64;
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < 16; ++q) {
+      const uint64_t x = sat64(As[ty][q], Bs[q][tx]);
+      if (x < best) { best = x; bk = (uint64_t)(k0 + q); }
+    }
+    __syncthreads();
+  }
+  if (i < m && j < n) {
+    C[(int64_t)i * n + j] = best;
+    if (argk) argk[(int64_t)i * n + j] = best == kInf64 ? kInf64 : bk;
+  }
+}
+
+__global__ void matvec_kernel(const uint64_t* __restrict__ M, int rows, int cols,
+                              const uint64_t* __restrict__ g, uint64_t* __restrict__ out) {
+  const int u = blockIdx.x * blockDim.x + threadIdx.x;
+  if (u >= rows) return;
+  uint64_t best = kInf64;
+  for (int v = 0; v < cols; ++v) {
+    const uint64_t c = sat64(M[(int64_t)u * cols + v], g[v]);
+    best = c < best ? c : best;
+  }
+  out[u] = best;
+}
+
+// --------------------------------------------------------------------------
+// N5: integer-pipe microbenchmark (roofline denominator).
+// --------------------------------------------------------------------------
+template <int OP>
+__global__ void __launch_bounds__(1024) intpipe_kernel(uint32_t* out, int iters, uint32_t seed) {
+  uint32_t a[8], y[8];
+  uint64_t a64[8], y64[8];
+  uint32_t x = seed ^ (threadIdx.x * 2654435761u) ^ (uint32_t)clock64();
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    a[i] = 0xFFFFFFFFu - i * x; y[i] = x * (i + 3);
+    a64[i] = ~0ull - i * (uint64_t)x; y64[i] = (uint64_t)x * (i + 5);
+  }
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        if (OP == 0) a[i] = __viaddmin_u32(x, y[i], a[i]);
+        else if (OP == 1) a[i] = a[i] + y[i] + x;
+        else { const uint64_t s = (uint64_t)x + y64[i]; a64[i] = s < a64[i] ? s : a64[i]; }
+      }
+      x += 0x9E3779B9u;
+      if (OP == 1) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) y[i] ^= a[i];
+      }
+    }
+  }
+  uint32_t s = 0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) s ^= a[i] ^ (uint32_t)a64[i];
+  if (s == 0x12345678u) out[threadIdx.x] = s;
+}
+
+// ===================== launchers (called from cfp_host.cu) =================
+#define CFP_LAUNCH_CHECK() do { cudaError_t e_ = cudaGetLastError(); if (e_ != cudaSuccess) return e_; } while (0)
+
+template <typename V>
+cudaError_t launch_compact(const CompactJob* jobs, int njobs, const uint32_t* raw, const int32_t* maps,
+                           V* out, cudaStream_t st) {
+  if (njobs == 0) return cudaSuccess;
+  compact_kernel<V><<<njobs, 256, 0, st>>>(jobs, raw, maps, out);
+  CFP_LAUNCH_CHECK();
+  return cudaSuccess;
+}
+
+template <typename V>
+cudaError_t launch_build_tables(const TableSpec* specs, int nspecs, int64_t max_entries, const V* vals,
+                                V* out, cudaStream_t st) {
+  if (nspecs == 0) return cudaSuccess;
+  int64_t blocks = (max_entries + 255) / 256;
+  if (blocks > 4096) blocks = 4096;
+  if (blocks < 1) blocks = 1;
+  build_table_kernel<V><<<dim3((unsigned)blocks, nspecs), 256, 0, st>>>(specs, vals, out);
+  CFP_LAUNCH_CHECK();
+  return cudaSuccess;
+}
+
+template <typename V>
+cudaError_t launch_fill(V* p, int64_t n, V v, cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  int64_t blocks = (n + 255) / 256;
+  if (blocks > 8192) blocks = 8192;
+  fill_kernel<V><<<(unsigned)blocks, 256, 0, st>>>(p, n, v);
+  CFP_LAUNCH_CHECK();
+  return cudaSuccess;
+}
+
+template <typename V, int NB>
+cudaError_t launch_enum_nb(const EnumParams& p, int64_t nthreads, size_t smem, cudaStream_t st) {
+  const int64_t blocks = nthreads / kBlock;
+  if (p.staged) {
+    auto k = enum_kernel<V, NB, true>;
+    if (smem > 48 * 1024) {
+      cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (e != cudaSuccess) return e;
+    }
+    k<<<(unsigned)blocks, kBlock, smem, st>>>(p);
+  } else {
+    enum_kernel<V, NB, false><<<(unsigned)blocks, kBlock, 0, st>>>(p);
+  }
+  CFP_LAUNCH_CHECK();
+  return cudaSuccess;
+}
+
+template <typename V>
+cudaError_t launch_enum(const EnumParams& p, int NB, int64_t nthreads, size_t smem, cudaStream_t st) {
+  switch (NB) {
+    case 4: return launch_enum_nb<V, 4>(p, nthreads, smem, st);
+    case 8: return launch_enum_nb<V, 8>(p, nthreads, smem, st);
+    case 12: return launch_enum_nb<V, 12>(p, nthreads, smem, st);
+    case 16: return launch_enum_nb<V, 16>(p, nthreads, smem, st);
+    case 24: return launch_enum_nb<V, 24>(p, nthreads, smem, st);
+    case 32: return launch_enum_nb<V, 32>(p, nthreads, smem, st);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+template <typename V>
+cudaError_t launch_fold(const FoldParams& f, cudaStream_t st) {
+  const size_t smem = (size_t)f.CH * (f.Do + f.Din) * sizeof(V) + (size_t)f.CH * f.nq * 4 + 16;
+  auto k = fold_kernel<V>;
+  if (smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+  }
+  k<<<(unsigned)f.nchunks, 256, smem, st>>>(f);
+  CFP_LAUNCH_CHECK();
+  return cudaSuccess;
+}
+
+template <typename V>
+cudaError_t launch_argmin(const ArgminParams& ap, V* Aval, const V* vals, cudaStream_t st) {
+  const int pairs = ap.f.Din * ap.f.Do;
+  fold_reduce_kernel<V><<<(pairs * 32 + 255) / 256, 256, 0, st>>>(ap.f, Aval, ap.pstar);
+  CFP_LAUNCH_CHECK();
+  suffix_argmin_kernel<V><<<pairs, 256, 0, st>>>(ap, Aval, vals);
+  CFP_LAUNCH_CHECK();
+  return cudaSuccess;
+}
+
+cudaError_t launch_chain(const ChainParams& cp, cudaStream_t st) {
+  chain_kernel<<<1, 1024, 0, st>>>(cp);
+  CFP_LAUNCH_CHECK();
+  return cudaSuccess;
+}
+
+cudaError_t launch_minplus(int m, int k, int n, const uint64_t* A, const uint64_t* B, uint64_t* C,
+                           uint64_t* argk, cudaStream_t st) {
+  dim3 grid((n + 15) / 16, (m + 15) / 16);
+  minplus_kernel<<<grid, 256, 0, st>>>(m, k, n, A, B, C, argk);
+  CFP_LAUNCH_CHECK();
+  return cudaSuccess;
+}
+
+cudaError_t launch_matvec(const uint64_t* M, int rows, int cols, const uint64_t* g, uint64_t* out,
+                          cudaStream_t st) {
+  matvec_kernel<<<(rows + 255) / 256, 256, 0, st>>>(M, rows, cols, g, out);
+  CFP_LAUNCH_CHECK();
+  return cudaSuccess;
+}
+
+cudaError_t launch_intpipe(int op, int blocks, int iters, uint32_t* out, cudaStream_t st) {
+  if (op == 0) intpipe_kernel<0><<<blocks, 1024, 0, st>>>(out, iters, 7u);
+  else if (op == 1) intpipe_kernel<1><<<blocks, 1024, 0, st>>>(out, iters, 7u);
+  else intpipe_kernel<2><<<blocks, 1024, 0, st>>>(out, iters, 7u);
+  CFP_LAUNCH_CHECK();
+  return cudaSuccess;
+}
+
+template cudaError_t launch_compact<uint32_t>(const CompactJob*, int, const uint32_t*, const int32_t*, uint32_t*, cudaStream_t);
+template cudaError_t launch_compact<uint64_t>(const CompactJob*, int, const uint32_t*, const int32_t*, uint64_t*, cudaStream_t);
+template cudaError_t launch_build_tables<uint32_t>(const TableSpec*, int, int64_t, const uint32_t*, uint32_t*, cudaStream_t);
+template cudaError_t launch_build_tables<uint64_t>(const TableSpec*, int, int64_t, const uint64_t*, uint64_t*, cudaStream_t);
+template cudaError_t launch_fill<uint32_t>(uint32_t*, int64_t, uint32_t, cudaStream_t);
+template cudaError_t launch_fill<uint64_t>(uint64_t*, int64_t, uint64_t, cudaStream_t);
+template cudaError_t launch_enum<uint32_t>(const EnumParams&, int, int64_t, size_t, cudaStream_t);
+template cudaError_t launch_enum<uint64_t>(const EnumParams&, int, int64_t, size_t, cudaStream_t);
+template cudaError_t launch_fold<uint32_t>(const FoldParams&, cudaStream_t);
+template cudaError_t launch_fold<uint64_t>(const FoldParams&, cudaStream_t);
+template cudaError_t launch_argmin<uint32_t>(const ArgminParams&, uint32_t*, const uint32_t*, cudaStream_t);
+template cudaError_t launch_argmin<uint64_t>(const ArgminParams&, uint64_t*, const uint64_t*, cudaStream_t);
+
+}  // namespace cfp

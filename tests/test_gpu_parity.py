@@ -1,0 +1,280 @@
+"""GPU parity: the CUDA path (through the C-ABI) vs the CPU oracle, bit-exact.
+
+Costs are integer ns, so every comparison is exact equality (north_star:
+"GPU and oracle plans and costs must be bit-exact with lowest-index
+tie-break").
+"""
+import numpy as np
+import pytest
+
+from golden_util import load, problem_from
+from synth import generators as G
+from synth.problem import INF32, CrossEdge, Problem, SegmentType, Transition
+
+pytestmark = pytest.mark.gpu
+INF64 = (1 << 64) - 1
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    from paper_2504_00598_b200 import build as B
+    B.build()
+    from paper_2504_00598_b200 import cfp
+    c = cfp.Context(device=0)
+    yield c
+    c.close()
+
+
+def _cfp():
+    from paper_2504_00598_b200 import cfp
+    return cfp
+
+
+def _assert_plan(got, want, name=""):
+    assert got.total_ns == want["total"], (name, got.total_ns, want["total"])
+    assert got.seg_index.tolist() == want["seg_index"].tolist(), name
+    assert got.seg_ns.tolist() == want["seg_ns"].tolist(), name
+    k = min(got.digits.shape[1], want["digits"].shape[1])
+    assert np.array_equal(got.digits[:, :k], want["digits"][:, :k]), name
+
+
+def _search_or_infeasible(ctx, oracle_lib, prob):
+    O = oracle_lib
+    cfp = _cfp()
+    try:
+        want = O.search_plan(prob)
+    except O.OracleError as e:
+        assert e.rc == O.ORC_EINFEASIBLE
+        with pytest.raises(cfp.CfpError) as ei:
+            ctx.search_plan(prob)
+        assert ei.value.status == cfp.CFP_EINFEASIBLE
+        return None
+    got = ctx.search_plan(prob)
+    _assert_plan(got, want, prob.name)
+    return got
+
+
+# ---------------------------------------------------------------- golden
+@pytest.mark.parametrize("name", ["h1", "h2", "h2p", "h3"])
+def test_golden_plans(ctx, name):
+    g = load(name)
+    p = problem_from(g["problem"])
+    got = ctx.search_plan(p)
+    assert got.total_ns == g["expect"]["total"]
+    assert got.seg_index.tolist() == g["expect"]["seg_index"]
+    assert got.seg_ns.tolist() == g["expect"]["seg_ns"]
+
+
+def test_golden_h1_tables(ctx):
+    g = load("h1")
+    p = problem_from(g["problem"])
+    A, I = ctx.segment_costs(p.types[0], None, 1)
+    assert A.tolist() == g["expect"]["A"]["0"] and I.tolist() == g["expect"]["I"]["0"]
+    A, I = ctx.segment_costs(p.types[0], p.transitions[1], 3)
+    assert A.tolist() == g["expect"]["A"]["1"] and I.tolist() == g["expect"]["I"]["1"]
+
+
+def test_golden_cx_chain(ctx):
+    g = load("cx")
+    mats = [np.array(M, np.uint64) for M in g["chain"]["mats"]]
+    opt, Gs = ctx.minplus_chain(mats, [(0, 1), (1, 1)])
+    assert opt == g["expect"]["total"]
+    assert [x.tolist() for x in Gs] == g["expect"]["G"]
+
+
+# ---------------------------------------------------------------- corpus
+MODES = ("ties", "random", "nearmax")
+
+
+@pytest.mark.parametrize("mode", MODES)
+@pytest.mark.parametrize("block", range(4))
+def test_random_corpus_search(ctx, oracle_lib, mode, block):
+    for seed in range(block * 25, block * 25 + 25):
+        p = G.tiny_random(seed * 7 + MODES.index(mode), mode=mode, max_plans=None, max_n=6)
+        _search_or_infeasible(ctx, oracle_lib, p)
+
+
+@pytest.mark.parametrize("seed", range(40))
+def test_random_segment_tables(ctx, oracle_lib, seed):
+    O = oracle_lib
+    p = G.tiny_random(5000 + seed, mode=MODES[seed % 3], max_plans=None, max_n=4, max_k=4)
+    for tr_id, tr in enumerate(p.transitions):
+        A0, I0 = O.segment_table(p, tr_id)
+        ty = p.types[tr.type]
+        A, I = ctx.segment_costs(ty, tr, p.d_in(tr_id))
+        assert np.array_equal(A, A0), (seed, tr_id)
+        assert np.array_equal(I, I0), (seed, tr_id)
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_larger_random_segment_tables(ctx, oracle_lib, seed):
+    """K up to 6, D up to 6 -- exercises the M/A/B schedules and multi-CTA
+    grids (several tiles, ragged tails)."""
+    O = oracle_lib
+    p = G.tiny_random(7000 + seed, mode=("ties", "random")[seed % 2], max_plans=None, max_n=3,
+                      max_k=6, max_d=6, max_edges=6, p_inf=0.03)
+    for tr_id, tr in enumerate(p.transitions):
+        A0, I0 = O.segment_table(p, tr_id)
+        ty = p.types[tr.type]
+        A, I = ctx.segment_costs(ty, tr, p.d_in(tr_id))
+        assert np.array_equal(A, A0), (seed, tr_id)
+        assert np.array_equal(I, I0), (seed, tr_id)
+
+
+@pytest.mark.parametrize("seed", range(10))
+def test_long_runs_repeated_squaring(ctx, oracle_lib, seed):
+    """Chains with long runs of one transition (repeated squaring + doubling)."""
+    p = G.tiny_random(8000 + seed, mode=MODES[seed % 3], max_plans=None, max_n=40, max_types=2,
+                      max_run=37)
+    _search_or_infeasible(ctx, oracle_lib, p)
+
+
+# ---------------------------------------------------------------- chain / product
+@pytest.mark.parametrize("seed", range(10))
+def test_minplus_product(ctx, oracle_lib, seed):
+    rng = np.random.default_rng(seed)
+    m, k, n = (int(x) for x in rng.integers(1, 40, 3))
+    A = rng.integers(0, 1000, (m, k)).astype(np.uint64)
+    B = rng.integers(0, 1000, (k, n)).astype(np.uint64)
+    A[rng.random(A.shape) < 0.2] = np.uint64(INF64)
+    B[rng.random(B.shape) < 0.2] = np.uint64(INF64)
+    C0, a0 = oracle_lib.minplus(A, B)
+    C1, a1 = ctx.minplus_product(A, B)
+    assert np.array_equal(C0, C1) and np.array_equal(a0, a1)
+
+
+@pytest.mark.parametrize("seed", range(10))
+def test_minplus_chain_runs(ctx, oracle_lib, seed):
+    rng = np.random.default_rng(100 + seed)
+    S = int(rng.integers(1, 30))
+    M0 = rng.integers(0, 1 << 20, (1, S)).astype(np.uint64)
+    M1 = rng.integers(0, 1 << 20, (S, S)).astype(np.uint64)
+    M1[rng.random(M1.shape) < 0.3] = np.uint64(INF64)
+    L = int(rng.integers(1, 100))
+    term = rng.integers(0, 1000, S).astype(np.uint64)
+    opt, Gs = ctx.minplus_chain([M0, M1], [(0, 1), (1, L)], terminal=term)
+    want = oracle_lib.chain([M0] + [M1] * L, terminal=term)
+    assert opt == int(want[0][0])
+    for a, b in zip(Gs, want):
+        assert np.array_equal(a, b)
+
+
+# ---------------------------------------------------------------- configs
+@pytest.mark.parametrize("cfg", ["C1", "C2"])
+@pytest.mark.parametrize("dist", ["shaped", "random", "ties"])
+@pytest.mark.parametrize("seed", [0, 1])
+def test_small_configs_full_parity(ctx, oracle_lib, cfg, dist, seed):
+    p = G.make_config(cfg, seed=seed, dist=dist)
+    got = _search_or_infeasible(ctx, oracle_lib, p)
+    assert got is not None
+
+
+def _check_table_properties(O, p, tr_id, A, I, m, samples):
+    """Full-size A/I: every entry's index decodes to its bucket and re-evaluates
+    (oracle, Eq. 3 terms) to exactly A; sampled buckets are recomputed by the
+    oracle's exhaustive enumeration (value and least index)."""
+    ty = p.types[p.transitions[tr_id].type]
+    din, dout = A.shape
+    for u in range(din):
+        for v in range(dout):
+            if int(A[u, v]) == INF64:
+                assert int(I[u, v]) == INF64
+                continue
+            s = O._digits(ty.radix, int(I[u, v]))
+            assert s[ty.out_block] == v
+            assert O.cost_index(p, tr_id, u, int(I[u, v]), m) == int(A[u, v])
+    for (u, v) in samples:
+        a, i = O.bucket(p, tr_id, u, v, m=m)
+        assert (int(A[u, v]), int(I[u, v])) == (a, i), (tr_id, u, v)
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("cfg", ["C3", "C5"])
+def test_large_config_tables_sampled(ctx, oracle_lib, cfg):
+    O = oracle_lib
+    p = G.make_config(cfg, seed=0, dist="shaped")
+    m = O.Marshalled(p)
+    rng = np.random.default_rng(1)
+    tr_id = 3                                    # L -> L
+    tr = p.transitions[tr_id]
+    A, I = ctx.segment_costs(p.types[tr.type], tr, p.d_in(tr_id))
+    samples = [(int(rng.integers(0, A.shape[0])), int(rng.integers(0, A.shape[1]))) for _ in range(2)]
+    _check_table_properties(O, p, tr_id, A, I, m, samples)
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("cfg", ["C3", "C4", "C5"])
+def test_large_config_plan(ctx, oracle_lib, cfg):
+    """Full-size plan: Eq. 3 recomputation of the GPU tuple equals its total,
+    and the oracle's chain DP + reconstruction over the GPU's per-transition
+    tables gives the same OPT and plan."""
+    O = oracle_lib
+    p = G.make_config(cfg, seed=0, dist="shaped")
+    got = ctx.search_plan(p)
+    m = O.Marshalled(p)
+    u, tot = 0, 0
+    for n, t in enumerate(p.instances):
+        ty = p.types[p.transitions[int(t)].type]
+        c = O.cost_index(p, int(t), u, int(got.seg_index[n]), m)
+        assert c == int(got.seg_ns[n])
+        tot += c
+        u = O._digits(ty.radix, int(got.seg_index[n]))[ty.out_block]
+    assert tot == got.total_ns
+    tabs = {}
+    for tr_id, tr in enumerate(p.transitions):
+        tabs[tr_id] = ctx.segment_costs(p.types[tr.type], tr,
+                                        p.d_in(tr_id))
+    mats = [tabs[int(t)][0] for t in p.instances]
+    idxs = [tabs[int(t)][1] for t in p.instances]
+    Gs = O.chain(mats)
+    assert int(Gs[0][0]) == got.total_ns
+    v, ix, cost = O.reconstruct(mats, idxs, Gs)
+    assert ix.tolist() == got.seg_index.tolist()
+
+
+# ---------------------------------------------------------------- errors
+def test_errors(ctx):
+    cfp = _cfp()
+    p = problem_from(load("h1")["problem"])
+    bad = problem_from(load("h1")["problem"])
+    bad.instances = np.array([1, 1], np.int32)            # chain must start with pred -1
+    with pytest.raises(cfp.CfpError) as ei:
+        ctx.search_plan(bad)
+    assert ei.value.status == cfp.CFP_EINVAL
+    bad = problem_from(load("h1")["problem"])
+    bad.types[0].out_block = 5
+    with pytest.raises(cfp.CfpError) as ei:
+        ctx.search_plan(bad)
+    assert ei.value.status == cfp.CFP_EINVAL
+    bad = problem_from(load("h1")["problem"])
+    bad.types[0].edges[0].dst = 0                          # self edge
+    with pytest.raises(cfp.CfpError) as ei:
+        ctx.search_plan(bad)
+    assert ei.value.status == cfp.CFP_EINVAL
+    inf = problem_from(load("h1")["problem"])
+    inf.types[0].comp_ns[3:6] = INF32                      # block 1 all infeasible
+    with pytest.raises(cfp.CfpError) as ei:
+        ctx.search_plan(inf)
+    assert ei.value.status == cfp.CFP_EINFEASIBLE
+    assert ctx.search_plan(p).total_ns == 6
+
+
+def test_determinism(ctx):
+    p = G.make_config("C2", seed=2, dist="ties")
+    a = ctx.search_plan(p)
+    b = ctx.search_plan(p)
+    assert a.total_ns == b.total_ns
+    assert np.array_equal(a.seg_index, b.seg_index) and np.array_equal(a.digits, b.digits)
+
+
+def test_prepared_execute_matches(ctx, oracle_lib):
+    p = G.make_config("C2", seed=0, dist="shaped")
+    prep = ctx.prepare(p)
+    for _ in range(3):
+        prep.execute()
+    got = prep.fetch()
+    want = oracle_lib.search_plan(p)
+    _assert_plan(got, want)
+    info = prep.info()
+    assert info.combos == 3 + 81 + 81 + 3
+    prep.close()
