@@ -46,58 +46,55 @@ def alu_peak_gops(sm_mhz: float) -> float:
 
 # ---------------------------------------------------------------- clocks
 class ClockSampler:
-    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
-              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-              "clocks_event_reasons.sw_power_cap")
+    """NVML sampling (every 2 ms) of SM clock and throttle reasons while the
+    timed region runs (B200_PROFILING.md clocks line)."""
+    REASONS = {0x4: "sw_power_cap", 0x8: "hw_slowdown", 0x20: "sw_thermal_slowdown",
+               0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown"}
 
     def __init__(self, device: int):
         self.device = device
-        self.proc = None
-        self.lines = []
+        self.samples = []
+        self.reasons = 0
+        self.max_mhz = None
+        self._stop = threading.Event()
 
     def __enter__(self):
         try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
-                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.t = threading.Thread(target=self._read, daemon=True)
+            import pynvml as N
+            N.nvmlInit()
+            self.N = N
+            self.h = N.nvmlDeviceGetHandleByIndex(self.device)
+            self.max_mhz = float(N.nvmlDeviceGetMaxClockInfo(self.h, N.NVML_CLOCK_SM))
+            self.t = threading.Thread(target=self._run, daemon=True)
             self.t.start()
-        except Exception:
-            self.proc = None
+        except Exception as e:  # no NVML: report nothing rather than guess
+            self.N = None
+            self.err = str(e)
         return self
 
-    def _read(self):
-        for line in self.proc.stdout:
-            self.lines.append(line.strip())
+    def _run(self):
+        N = self.N
+        while not self._stop.is_set():
+            try:
+                self.samples.append(float(N.nvmlDeviceGetClockInfo(self.h, N.NVML_CLOCK_SM)))
+                try:
+                    r = N.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                except AttributeError:
+                    r = N.nvmlDeviceGetCurrentClocksThrottleReasons(self.h)
+                self.reasons |= int(r)
+            except Exception:
+                pass
+            time.sleep(0.002)
 
     def __exit__(self, *a):
-        if self.proc:
-            self.proc.terminate()
-            try:
-                self.proc.wait(timeout=2)
-            except Exception:
-                self.proc.kill()
+        self._stop.set()
+        if self.N is not None:
+            self.t.join(timeout=1)
 
     def summary(self):
-        sm, mx, reasons = [], None, set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
-            parts = [x.strip() for x in ln.split(",")]
-            if len(parts) < 7:
-                continue
-            try:
-                sm.append(float(parts[0]))
-                mx = float(parts[1])
-            except ValueError:
-                continue
-            for n, v in zip(names, parts[3:7]):
-                if v.lower().startswith("active"):
-                    reasons.add(n)
-        if not sm:
-            return {"sm_mhz": None, "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": 0}
-        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons),
-                "samples": len(sm)}
+        reasons = sorted(v for k, v in self.REASONS.items() if self.reasons & k)
+        return {"sm_mhz": statistics.median(self.samples) if self.samples else None,
+                "sm_max_mhz": self.max_mhz, "reasons": reasons, "samples": len(self.samples)}
 
 
 # ---------------------------------------------------------------- helpers
@@ -123,31 +120,43 @@ def combos_of(prob) -> float:
     return float(sum(prob.feasible_combinations(t) for t in prob.used_types()))
 
 
-def cpu_baseline(prob, budget_s: float = 12.0):
-    """The oracle (as it stands) on the host cores: a bounded index sub-range of
-    the largest segment type, evaluated for every incoming transition and every
-    input state -- exactly the oracle's work per combination of a full step."""
+def _oracle_step_sample(prob, frac, m, cores):
+    """Run the oracle over the first `frac` of every used transition's
+    combination space (all input states): `frac` of a full step's oracle work."""
     from oracle import oracle as O
-    cores = len(os.sched_getaffinity(0))
-    types = prob.used_types()
-    big = max(types, key=lambda t: prob.num_combinations(t))
-    trs = [i for i, tr in enumerate(prob.transitions)
-           if tr.type == big and i in set(int(x) for x in prob.instances)]
-    m = O.Marshalled(prob)
-    n = 1 << 16
-    spent = 0.0
+    used = sorted(set(int(x) for x in prob.instances))
+    t0 = time.perf_counter()
+    for tr in used:
+        S = prob.num_combinations(prob.transitions[tr].type)
+        n = max(1, min(S, int(round(S * frac))))
+        O.segment_table_range(prob, tr, 0, n, nthreads=cores, m=m)
+    return time.perf_counter() - t0
+
+
+def _calibrate(prob, budget_s, m, cores):
+    frac = 1e-7
     while True:
-        t0 = time.perf_counter()
-        for tr in trs:
-            O.segment_table_range(prob, tr, 0, n, nthreads=cores, m=m)
-        dt = time.perf_counter() - t0
-        if dt > budget_s / 3 or n >= prob.num_combinations(big):
+        dt = _oracle_step_sample(prob, frac, m, cores)
+        if dt > budget_s / 8 or frac >= 1.0:
             break
-        spent += dt
-        n = min(prob.num_combinations(big), int(n * max(2.0, (budget_s / 3) / max(dt, 1e-3))))
-    return {"value": n / dt, "unit": UNIT, "cores": cores, "kind": "oracle",
-            "sample": f"combination indices [0, {n}) of type {big} ({prob.types[big].name}) for all "
-                      f"{len(trs)} incoming transitions x all input states, {dt:.2f} s"}
+        frac = min(1.0, frac * max(2.0, (budget_s / 8) / max(dt, 1e-4)))
+    return min(1.0, frac * budget_s / 2 / max(dt, 1e-4))
+
+
+def cpu_baseline(prob, budget_s: float = 12.0):
+    """The oracle (as it stands) timed on this host's cores: a bounded sample
+    (the same fraction of every used transition's combination space, all input
+    states) scaled to the metric's unit."""
+    from oracle import oracle as O
+    O.build()
+    cores = len(os.sched_getaffinity(0))
+    m = O.Marshalled(prob)
+    frac = _calibrate(prob, budget_s, m, cores)
+    dt = _oracle_step_sample(prob, frac, m, cores)
+    combos = combos_of(prob)
+    return {"value": combos * frac / dt, "unit": UNIT, "cores": cores, "kind": "oracle",
+            "sample": f"first {frac:.3g} of every used transition's combination space (all input "
+                      f"states), {dt:.2f} s; value = combos/step x fraction / time"}
 
 
 def flush_l2(torch, buf):
@@ -161,33 +170,25 @@ def run_reference(args, prob, rank, world):
     from oracle import oracle as O
     O.build()
     cores = len(os.sched_getaffinity(0))
-    base = cpu_baseline(prob, budget_s=6.0)
-    # each step: the same bounded sample
-    n = int(base["sample"].split("[0, ")[1].split(")")[0])
-    big = max(prob.used_types(), key=lambda t: prob.num_combinations(t))
-    trs = [i for i, tr in enumerate(prob.transitions)
-           if tr.type == big and i in set(int(x) for x in prob.instances)]
     m = O.Marshalled(prob)
+    # each step: the same bounded sample, sized so that the whole run stays short
+    frac = _calibrate(prob, 150.0 / max(1, args.steps + args.warmup), m, cores)
     for _ in range(args.warmup):
-        for tr in trs:
-            O.segment_table_range(prob, tr, 0, n, nthreads=cores, m=m)
-    times = []
-    for _ in range(args.steps):
-        t0 = time.perf_counter()
-        for tr in trs:
-            O.segment_table_range(prob, tr, 0, n, nthreads=cores, m=m)
-        times.append(time.perf_counter() - t0)
+        _oracle_step_sample(prob, frac, m, cores)
+    times = [_oracle_step_sample(prob, frac, m, cores) for _ in range(args.steps)]
     tot = sum(times)
-    value = n * args.steps / tot
+    combos = combos_of(prob)
+    value = combos * frac * args.steps / tot
+    sample = (f"per step: first {frac:.3g} of every used transition's combination space "
+              f"(all input states); value = combos/step x fraction / time")
     return {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": tot / args.steps * 1e3, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
             "impl": "reference",
             "config": {"workload": f"{args.config} ({prob.name}) {args.dist} seed {args.seed}",
-                       "l2": "n/a (CPU)"},
+                       "combos_per_step": combos, "l2": "n/a (CPU oracle)"},
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle",
-                             "sample": f"per step: combination indices [0, {n}) of type {big} for all "
-                                       f"incoming transitions and input states"},
+                             "sample": sample},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
 
 

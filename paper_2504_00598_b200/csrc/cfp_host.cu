@@ -16,6 +16,7 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -114,6 +115,12 @@ extern "C" cfp_status cfp_ctx_create(cfp_ctx** out, const cfp_ctx_opts* opts) {
     CUDA_TRY(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
     c->own_stream = true;
   }
+  {
+    cudaMemPool_t pool;
+    CUDA_TRY(cudaDeviceGetDefaultMemPool(&pool, c->device));
+    uint64_t thr = ~0ull;
+    CUDA_TRY(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+  }
   if (c->world > 1) {
     if (!opts->nccl_unique_id) return fail(CFP_EINVAL, "world > 1 needs nccl_unique_id");
     ncclUniqueId id;
@@ -170,14 +177,24 @@ extern "C" cfp_status cfp_unpack_keys(int64_t n, const uint64_t* keys, int32_t i
 }
 
 // ---------------------------------------------------------------- device buffer
+// Stream-ordered allocations from the device's default memory pool (release
+// threshold raised at ctx creation), so repeated prepare/search calls reuse
+// memory instead of paying cudaMalloc/cudaFree.
+static thread_local cudaStream_t g_alloc_stream = nullptr;
 struct DevBuf {
   void* p = nullptr;
   size_t n = 0;
-  ~DevBuf() { if (p) cudaFree(p); }
+  cudaStream_t st = nullptr;
+  ~DevBuf() { release(); }
+  void release() {
+    if (p) cudaFreeAsync(p, st);
+    p = nullptr;
+  }
   cudaError_t alloc(size_t bytes) {
-    if (p) { cudaFree(p); p = nullptr; }
+    release();
     n = bytes;
-    return cudaMalloc(&p, bytes ? bytes : 16);
+    st = g_alloc_stream;
+    return cudaMallocAsync(&p, bytes ? bytes : 16, st);
   }
   template <typename T> T* as() const { return static_cast<T*>(p); }
 };
@@ -256,7 +273,7 @@ struct cfp_prepared {
   std::vector<int> inst;
   // device memory
   DevBuf raw, maps, vals32, vals64, jobs32, jobs64, specs32, specs64, mtab, bp, scratch,
-      outAI, chain_inst, chain_runs, chain_G, chain_goff, chain_pow, plan, radix_blob, status,
+      outAI, chain_inst, chain_runs, chain_mats, chain_moff, chain_G, chain_goff, chain_pow, plan, radix_blob, status,
       merge_keys;
   int njobs32 = 0, njobs64 = 0, nspecs32 = 0, nspecs64 = 0;
   int64_t spec_max32 = 0, spec_max64 = 0;
@@ -605,9 +622,38 @@ static int64_t stride_in(const TableSpec& s, int pos) {
   return st;
 }
 
+// Distinct matrices + shared-memory budget of the single-CTA chain kernel.
+static cfp_status setup_chain_staging(ChainParams& cp, const std::vector<ChainInst>& mats, int64_t g_elems,
+                                      int levels_max, int smax, DevBuf& dmats, DevBuf& dmoff,
+                                      cudaStream_t st) {
+  std::vector<int64_t> moff(mats.size());
+  int64_t tot = 0;
+  for (size_t m = 0; m < mats.size(); ++m) {
+    moff[m] = tot;
+    tot += (int64_t)mats[m].rows * mats[m].cols;
+  }
+  CUDA_TRY(dmats.alloc(std::max<size_t>(1, mats.size()) * sizeof(ChainInst)));
+  CUDA_TRY(dmoff.alloc(std::max<size_t>(1, mats.size()) * sizeof(int64_t)));
+  if (!mats.empty()) {
+    CUDA_TRY(cudaMemcpyAsync(dmats.p, mats.data(), mats.size() * sizeof(ChainInst), cudaMemcpyHostToDevice, st));
+    CUDA_TRY(cudaMemcpyAsync(dmoff.p, moff.data(), moff.size() * sizeof(int64_t), cudaMemcpyHostToDevice, st));
+  }
+  cp.nmat = (int)mats.size();
+  cp.mats = dmats.as<ChainInst>();
+  cp.moff = dmoff.as<int64_t>();
+  cp.mat_elems = tot;
+  cp.levels_max = levels_max;
+  cp.smax = smax;
+  const int64_t need = (tot * (cp.backtrack ? 2 : 1) + g_elems + (int64_t)levels_max * smax * smax) * 8 +
+                       (int64_t)(cp.N + 2) * 8 + (int64_t)cp.N * 16 + 128;
+  cp.smem_bytes = need <= 200 * 1024 ? need : 0;
+  return CFP_OK;
+}
+
 static cfp_status prepare_impl(cfp_ctx* ctx, const cfp_problem* p, bool do_chain,
                                cfp_prepared** out) {
   *out = nullptr;
+  g_alloc_stream = ctx->stream;
   std::vector<HostType> T;
   std::vector<HostTrans> X;
   Builder b;
@@ -906,6 +952,19 @@ static cfp_status prepare_impl(cfp_ctx* ctx, const cfp_problem* p, bool do_chain
     es.P = Pp;
     es.o = t.o;
     es.nsuffix = prod(r, Pp, K);
+    {
+      int64_t lo = INT64_MAX, hi = 0;
+      for (int j = 0; j < K; ++j) { lo = std::min<int64_t>(lo, te.w_off[j]); hi = std::max<int64_t>(hi, te.w_off[j] + r[j]); }
+      for (int e2 = 0; e2 < t.E; ++e2) {
+        lo = std::min<int64_t>(lo, te.e_off[e2]);
+        hi = std::max<int64_t>(hi, te.e_off[e2] + (int64_t)r[t.esrc[e2]] * r[t.edst[e2]]);
+      }
+      if ((hi - lo) * (int64_t)vbytes > 160 * 1024) return fail(CFP_ETOOBIG, "segment tables too large");
+      es.tab_lo = lo;
+      es.tab_n = (int32_t)(hi - lo);
+    }
+    for (int d = 0; d < K; ++d)
+      if (r[d] > 65535) return fail(CFP_ETOOBIG, "more than 65535 feasible strategies for one block");
     for (auto& tm : terms) {
       if (es.nterm >= kMaxTerms) return fail(CFP_ETOOBIG, "too many terms");
       Term x{};
@@ -928,8 +987,23 @@ static cfp_status prepare_impl(cfp_ctx* ctx, const cfp_problem* p, bool do_chain
         tq.kind = 2; tq.a = X[x].xdst[q]; tq.db = r[X[x].xdst[q]]; tq.off = tx.q_off[q];
         f.q[f.nq++] = tq;
       }
-      f.CH = 256;
-      while ((size_t)f.CH * ((f.Do + f.Din) * vbytes + f.nq * 4) > 96 * 1024 && f.CH > 8) f.CH /= 2;
+      {
+        const int64_t DinP = (f.Din + 3) & ~3, DoP = (f.Do + 3) & ~3;
+        const int64_t nblk = (DinP / 4) * (DoP / 4);
+        const int64_t groups = std::max<int64_t>(1, std::min<int64_t>(256 / nblk, 8));
+        const int64_t red = groups * DinP * DoP * (int64_t)vbytes;
+        if (red > 150 * 1024)
+          return fail(CFP_ETOOBIG, "D_in x D_o too large for the fold kernel");
+        f.qelems = 0;
+        for (int q = 0; q < f.nq; ++q) f.qelems += f.Din * f.q[q].db;
+        const int64_t qbytes = (int64_t)f.qelems * vbytes;
+        if (red + qbytes > 170 * 1024)
+          return fail(CFP_ETOOBIG, "cross tables too large for the fold kernel");
+        f.CH = 256;
+        while (f.CH > 8 && (size_t)f.CH * ((DoP + DinP) * vbytes + f.nq * 4) + red + qbytes > 190 * 1024)
+          f.CH /= 2;
+        f.tma = ((int64_t)f.Do * (int64_t)vbytes) % 16 == 0 ? 1 : 0;
+      }
       f.nchunks = std::max<int64_t>(1, (f.nPl + f.CH - 1) / f.CH);
       tx.chunk_off = scratch_bytes;
       scratch_bytes += ((f.nchunks * f.Din * f.Do * vbytes) + 255) & ~255LL;
@@ -1036,6 +1110,7 @@ static cfp_status prepare_impl(cfp_ctx* ctx, const cfp_problem* p, bool do_chain
       const HostType& t = T[tx.type];
       ci[n].A = outA + tx.out_off;
       ci[n].I = outI + tx.out_off;
+      ci[n].mat = trans_slot[P->inst[n]];
       ci[n].rows = tx.Din;
       ci[n].cols = tx.Do_orig;
       ci[n].K = t.K;
@@ -1074,7 +1149,7 @@ static cfp_status prepare_impl(cfp_ctx* ctx, const cfp_problem* p, bool do_chain
     CUDA_TRY(cudaMemcpyAsync(P->radix_blob.p, radix_blob.data(), radix_blob.size() * 4, cudaMemcpyHostToDevice, st));
     // plan: total, seg_index[N], seg_ns[N], digits[N*kmax], status
     CUDA_TRY(P->plan.alloc(8 + (size_t)N * 16 + (size_t)N * kmax * 4 + 16));
-    CUDA_TRY(P->status.alloc(16));
+    CUDA_TRY(P->status.alloc(16 + 64 * 8));
     ChainParams& cp = P->cp;
     cp.N = N;
     cp.nruns = P->nruns;
@@ -1094,6 +1169,22 @@ static cfp_status prepare_impl(cfp_ctx* ctx, const cfp_problem* p, bool do_chain
     cp.kmax = kmax;
     cp.radix_blob = P->radix_blob.as<int32_t>();
     cp.status = P->status.as<int32_t>();
+    cp.dbg = getenv("CFP_DEBUG_CHAIN") ? reinterpret_cast<uint64_t*>(P->status.as<char>() + 16) : nullptr;
+    {
+      std::vector<ChainInst> mats(P->trans.size());
+      int lv = 0, smax = 1;
+      for (size_t q = 0; q < P->trans.size(); ++q) {
+        const TransExec& tx = P->trans[q];
+        mats[q] = ChainInst{outA + tx.out_off, outI + tx.out_off, (int)q, tx.Din, tx.Do_orig, 0, 0};
+        smax = std::max(smax, std::max(tx.Din, tx.Do_orig));
+      }
+      for (auto& r : runs) {
+        int levels = 0;
+        while ((1 << (levels + 1)) <= r.len) ++levels;
+        if (r.len > 1) lv = std::max(lv, levels);
+      }
+      TRY(setup_chain_staging(cp, mats, goff[N + 1], lv, smax, P->chain_mats, P->chain_moff, st));
+    }
   }
   CUDA_TRY(cudaStreamSynchronize(st));
   *out = P.release();
@@ -1101,11 +1192,17 @@ static cfp_status prepare_impl(cfp_ctx* ctx, const cfp_problem* p, bool do_chain
 }
 
 // ---------------------------------------------------------------- execute
+template <typename V> constexpr V VTcap();
+template <> constexpr uint32_t VTcap<uint32_t>() { return kCap32; }
+template <> constexpr uint64_t VTcap<uint64_t>() { return kCap64; }
+
 template <typename V>
 static cfp_status run_type_kernels(cfp_prepared* P, TypeExec& te, cudaStream_t st, bool first_of_prec) {
   (void)first_of_prec;
+  // B_p pre-filled with CAP: (g, hb) groups cut between CTAs merge by atomicMin
+  CUDA_TRY(launch_fill<V>(static_cast<V*>(te.ep.Bp), te.nPl * te.ep.Do, (V)VTcap<V>(), st));
   CUDA_TRY(launch_enum<V>(te.ep, te.NB, te.nthreads, te.smem, st));
-  P->launches++;
+  P->launches += 2;
   return CFP_OK;
 }
 
@@ -1248,6 +1345,13 @@ static cfp_status fetch_impl(cfp_ctx* ctx, cfp_prepared* P, cfp_plan* out) {
   std::vector<char> buf(8 + (size_t)N * 16 + (size_t)N * P->kmax * 4);
   CUDA_TRY(cudaMemcpyAsync(buf.data(), P->plan.p, buf.size(), cudaMemcpyDeviceToHost, st));
   CUDA_TRY(cudaStreamSynchronize(st));
+  if (P->cp.dbg) {
+    uint64_t t[64];
+    CUDA_TRY(cudaMemcpy(t, P->cp.dbg, sizeof(t), cudaMemcpyDeviceToHost));
+    fprintf(stderr, "chain phases (us):");
+    for (uint64_t i = 1; i < t[63] && i < 63; ++i) fprintf(stderr, " %.2f", (t[i] - t[i - 1]) * 1e-3);
+    fprintf(stderr, "\n");
+  }
   if (status == 4) return fail(CFP_ETOOBIG, "chain scratch too small");
   if (status == 3) {
     // diagnostic: forward reachability over finite entries of A_n
@@ -1425,6 +1529,7 @@ extern "C" cfp_status cfp_minplus_chain(cfp_ctx* ctx, int32_t num_mats, const in
         if (terminal[v] != CFP_INF64) tot += terminal[v];
     if (tot >= 9.2e18L) return fail(CFP_EOVERFLOW, "a finite chain cost could reach 2^63");
   }
+  g_alloc_stream = ctx->stream;
   CUDA_TRY(cudaSetDevice(ctx->device));
   cudaStream_t st = ctx->stream;
   DevBuf dm, dinst, druns, dgoff, dG, dpow, dterm, dstatus;
@@ -1442,7 +1547,7 @@ extern "C" cfp_status cfp_minplus_chain(cfp_ctx* ctx, int32_t num_mats, const in
     const int m = run_mat[r];
     runs.push_back({(int)ci.size(), (int)run_len[r]});
     for (int64_t k = 0; k < run_len[r]; ++k)
-      ci.push_back({dm.as<uint64_t>() + moff[m], nullptr, rows[m], cols[m], 0, 0});
+      ci.push_back({dm.as<uint64_t>() + moff[m], nullptr, m, rows[m], cols[m], 0, 0});
     if (run_len[r] > 1) {
       int levels = 0;
       while ((1ll << (levels + 1)) <= run_len[r]) ++levels;
@@ -1480,6 +1585,19 @@ extern "C" cfp_status cfp_minplus_chain(cfp_ctx* ctx, int32_t num_mats, const in
   cp.powers_cap = pow_need;
   cp.backtrack = 0;
   cp.status = dstatus.as<int32_t>();
+  DevBuf dmats, dmoff;
+  {
+    std::vector<ChainInst> umats(num_mats);
+    int lv = 0;
+    for (int m = 0; m < num_mats; ++m)
+      umats[m] = ChainInst{dm.as<uint64_t>() + moff[m], nullptr, m, rows[m], cols[m], 0, 0};
+    for (int r = 0; r < num_runs; ++r) {
+      int levels = 0;
+      while ((1ll << (levels + 1)) <= run_len[r]) ++levels;
+      if (run_len[r] > 1) lv = std::max(lv, levels);
+    }
+    TRY(setup_chain_staging(cp, umats, goff[N + 1], lv, maxS, dmats, dmoff, st));
+  }
   CUDA_TRY(launch_chain(cp, st));
   int32_t status = 0;
   CUDA_TRY(cudaMemcpyAsync(&status, dstatus.p, 4, cudaMemcpyDeviceToHost, st));
@@ -1488,7 +1606,6 @@ extern "C" cfp_status cfp_minplus_chain(cfp_ctx* ctx, int32_t num_mats, const in
     CUDA_TRY(cudaMemcpyAsync(suffix_out, dG.p, goff[N + 1] * 8, cudaMemcpyDeviceToHost, st));
   CUDA_TRY(cudaStreamSynchronize(st));
   if (status == 4) return fail(CFP_ETOOBIG, "chain scratch too small");
-  (void)maxS;
   return CFP_OK;
 }
 
@@ -1499,6 +1616,7 @@ extern "C" cfp_status cfp_minplus_product(cfp_ctx* ctx, int32_t m, int32_t k, in
   for (int64_t i = 0; i < (int64_t)m * k; ++i) if (A[i] != CFP_INF64) ma = std::max(ma, A[i]);
   for (int64_t i = 0; i < (int64_t)k * n; ++i) if (B[i] != CFP_INF64) mb = std::max(mb, B[i]);
   if ((long double)ma + mb >= 18446744073709551615.0L) return fail(CFP_EOVERFLOW, "finite sum overflows");
+  g_alloc_stream = ctx->stream;
   CUDA_TRY(cudaSetDevice(ctx->device));
   cudaStream_t st = ctx->stream;
   DevBuf dA, dB, dC, dK;
@@ -1518,6 +1636,7 @@ extern "C" cfp_status cfp_minplus_product(cfp_ctx* ctx, int32_t m, int32_t k, in
 
 extern "C" cfp_status cfp_intpipe_bench(cfp_ctx* ctx, int32_t op, int32_t iters, double* ops_per_s, double* ms) {
   if (!ctx || op < 0 || op > 2 || iters < 1) return fail(CFP_EINVAL, "bad intpipe arguments");
+  g_alloc_stream = ctx->stream;
   CUDA_TRY(cudaSetDevice(ctx->device));
   cudaStream_t st = ctx->stream;
   DevBuf out;

@@ -88,6 +88,8 @@ struct FoldParams {
   Term q[kMaxTerms];
   int32_t CH;                   // prefixes per chunk
   int64_t nchunks;
+  int32_t tma;                  // 1: B_p chunk rows are 16-byte multiples (bulk copy)
+  int32_t qelems;               // sum of D_in * D_j over cross terms (smem copy)
   const void* Bp;
   const void* vals;             // value blob (compact Q tables)
   void* chunkmin;               // [nchunks][Din][Do]
@@ -103,6 +105,8 @@ struct EvalSpec {
   int32_t nterm;
   Term term[kMaxTerms];         // kind 0/1 over block ids
   int64_t nsuffix;              // prod of suffix radices
+  int64_t tab_lo;               // the type's compact W/R tables: [tab_lo, tab_lo + tab_n)
+  int32_t tab_n;
 };
 
 struct ArgminParams {
@@ -123,6 +127,7 @@ struct ArgminParams {
 struct ChainInst {
   const uint64_t* A;            // [rows][cols]
   const uint64_t* I;            // nullable
+  int32_t mat;                  // distinct matrix id (staging)
   int32_t rows, cols;
   int32_t K;                    // digits of the instance's type (plan decode)
   int32_t radix_off;            // offset into radix blob
@@ -161,6 +166,14 @@ struct ChainParams {
   int32_t kmax;
   const int32_t* radix_blob;
   int32_t* status;              // 0 ok, 3 infeasible, 4 scratch too small
+  // shared-memory staging (all distinct matrices, G and powers fit)
+  int32_t nmat;
+  const ChainInst* mats;        // [nmat] distinct matrices (A, I, rows, cols)
+  const int64_t* moff;          // [nmat] element offsets in the staged area
+  int64_t mat_elems;            // sum rows*cols
+  int64_t smem_bytes;           // 0 = global mode
+  int32_t levels_max, smax;
+  uint64_t* dbg;                // nullable: %globaltimer at phase boundaries
 };
 
 }  // namespace cfp

@@ -16,6 +16,7 @@
 // add+min never wraps.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdint>
 
 #include "cfp_internal.h"
@@ -45,6 +46,58 @@ template <> struct VT<uint64_t> {
   }
   static __device__ __forceinline__ uint64_t mn(uint64_t a, uint64_t b) { return a < b ? a : b; }
 };
+
+// --------------------------------------------------------------------------
+// TMA 1-D bulk copies (cp.async.bulk, SASS UBLKCP) with mbarrier completion.
+// --------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void tma_bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+  asm volatile(
+      "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+      "r"(phase)
+      : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+// digit at canonical position `pos` of prefix value pg (block 0 most significant)
+__device__ __forceinline__ int prefix_digit(int64_t pg, int pos, int P, const int32_t* radix) {
+  if (pg < 0x7FFFFFFF) {
+    uint32_t q = (uint32_t)pg;
+    uint32_t dig = 0;
+    for (int d = P - 1; d >= pos; --d) {
+      const uint32_t r = (uint32_t)radix[d];
+      dig = q % r;
+      q /= r;
+    }
+    return (int)dig;
+  }
+  int64_t q = pg;
+  int dig = 0;
+  for (int d = P - 1; d >= pos; --d) {
+    dig = (int)(q % radix[d]);
+    q /= radix[d];
+  }
+  return dig;
+}
 
 // --------------------------------------------------------------------------
 // a0: compaction.  Each job gathers one table of the pruned problem from the
@@ -144,114 +197,146 @@ __device__ __forceinline__ void load_vec<uint64_t>(const uint64_t* p, uint64_t* 
   out[0] = v.x; out[1] = v.y;
 }
 
+template <typename V>
+__device__ __forceinline__ void atomic_min_v(V* p, V v);
+template <>
+__device__ __forceinline__ void atomic_min_v<uint32_t>(uint32_t* p, uint32_t v) { atomicMin(p, v); }
+template <>
+__device__ __forceinline__ void atomic_min_v<uint64_t>(uint64_t* p, uint64_t v) {
+  atomicMin(reinterpret_cast<unsigned long long*>(p), (unsigned long long)v);
+}
+
+// Persistent, statically balanced: the work items (group g = (l, vg), h-block
+// hb of kBlock prefixes, m) are linearised g-major and split into gridDim.x
+// contiguous equal ranges.  A CTA keeps its accumulators in registers while
+// (g, hb) stays the same; a (g, hb) pair cut by a range boundary is merged
+// with atomicMin into B_p (pre-filled with CAP), all others are stored.
 template <typename V, int NB, bool STAGED>
 __global__ void __launch_bounds__(kBlock) enum_kernel(const EnumParams p) {
   using T = VT<V>;
   constexpr int VN = Vec4<V>::N;
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  const int64_t t = (int64_t)blockIdx.x * kBlock + threadIdx.x;
-  const int64_t grp = t / p.Gpad;                 // (l, vg): CTA-uniform
-  const int64_t hh = t - grp * p.Gpad;
-  const int64_t l = grp / p.VG;
-  const int vg = (int)(grp - l * p.VG);
-  const bool live = hh < p.G && l < p.W;
-  const int64_t pg = (p.h0 + hh) * p.W + l;       // global canonical prefix
-  const int64_t row = hh * p.W + l;               // local canonical prefix
-
-  // prefix digits -> table offsets (ctx digits live in the low part, so the
-  // offsets are CTA-uniform whenever STAGED)
-  int64_t sx = 0, sy = 0, sz = 0;
-  int od = 0;
-  {
-    int64_t q = pg;
-    for (int d = p.P - 1; d >= 0; --d) {
-      const int dig = (int)(q % p.pre_radix[d]);
-      q /= p.pre_radix[d];
-      sx += dig * p.pre_sx[d];
-      sy += dig * p.pre_sy[d];
-      sz += dig * p.pre_sz[d];
-      if (d == p.o_pre) od = dig;
+  const int64_t nhb = p.Gpad / kBlock;
+  const int64_t per_g = nhb * p.nM;
+  const int64_t total = p.W * p.VG * per_g;
+  const int64_t i_end = (int64_t)(blockIdx.x + 1) * total / gridDim.x;
+  int64_t i = (int64_t)blockIdx.x * total / gridDim.x;
+  int64_t staged_g = -1;
+  V* xs = reinterpret_cast<V*>(smem_raw);
+  V* ys = xs + p.xspan;
+  V* zs = ys + p.yspan;
+  int4* ms = reinterpret_cast<int4*>(zs + ((p.zspan + 3) & ~3LL));
+  while (i < i_end) {
+    const int64_t g = i / per_g;
+    const int64_t rem = i - g * per_g;
+    const int64_t hb = rem / p.nM;
+    const int64_t m0 = rem - hb * p.nM;
+    const int64_t m1 = min(p.nM, m0 + (i_end - i));
+    const bool partial = m0 > 0 || m1 < p.nM;
+    i += m1 - m0;
+    const int64_t l = g / p.VG;
+    const int vg = (int)(g - l * p.VG);
+    const int64_t hh = hb * kBlock + threadIdx.x;
+    const bool live = hh < p.G;
+    const int64_t pg = (p.h0 + hh) * p.W + l;       // global canonical prefix
+    const int64_t row = hh * p.W + l;               // local canonical prefix
+    // prefix digits -> table offsets (ctx digits live in the low part l, so
+    // sx/sy/sz are uniform over the CTA)
+    int64_t sx = 0, sy = 0, sz = 0;
+    int od = 0;
+    {
+      int64_t q = pg;
+      for (int d = p.P - 1; d >= 0; --d) {
+        const int dig = (int)(q % p.pre_radix[d]);
+        q /= p.pre_radix[d];
+        sx += dig * p.pre_sx[d];
+        sy += dig * p.pre_sy[d];
+        sz += dig * p.pre_sz[d];
+        if (d == p.o_pre) od = dig;
+      }
     }
-  }
-  const V* XT = static_cast<const V*>(p.XT);
-  const V* YT = static_cast<const V*>(p.YT);
-  const V* ZT = static_cast<const V*>(p.ZT);
-  const int4* MT = p.mtab;
-  if constexpr (STAGED) {
-    V* xs = reinterpret_cast<V*>(smem_raw);
-    V* ys = xs + p.xspan;
-    V* zs = ys + p.yspan;
-    int4* ms = reinterpret_cast<int4*>(zs + ((p.zspan + 3) & ~3LL));
-    for (int64_t i = threadIdx.x * VN; i < p.xspan; i += kBlock * VN)
-      *reinterpret_cast<typename Vec4<V>::T*>(xs + i) =
-          *reinterpret_cast<const typename Vec4<V>::T*>(XT + sx + i);
-    for (int64_t i = threadIdx.x * VN; i < p.yspan; i += kBlock * VN)
-      *reinterpret_cast<typename Vec4<V>::T*>(ys + i) =
-          *reinterpret_cast<const typename Vec4<V>::T*>(YT + sy + i);
-    for (int64_t i = threadIdx.x; i < p.zspan; i += kBlock) zs[i] = ZT[sz + i];
-    for (int64_t i = threadIdx.x; i < p.nM; i += kBlock) ms[i] = MT[i];
-    __syncthreads();
-    XT = xs; YT = ys; ZT = zs; MT = ms;
-    sx = sy = sz = 0;
-  }
-  if (!live) return;
-
-  V* Bp = static_cast<V*>(p.Bp) + row * p.Do;
-  const V k0 = static_cast<const V*>(p.K0)[pg];
-  if (p.init_row) {
-    for (int v = 0; v < p.Do; ++v) Bp[v] = T::CAP;
-  }
-  V acc[NB];
+    const V* XT = static_cast<const V*>(p.XT);
+    const V* YT = static_cast<const V*>(p.YT);
+    const V* ZT = static_cast<const V*>(p.ZT);
+    const int4* MT = p.mtab;
+    if constexpr (STAGED) {
+      if (g != staged_g) {
+        __syncthreads();
+        for (int64_t e = threadIdx.x * VN; e < p.xspan; e += kBlock * VN)
+          *reinterpret_cast<typename Vec4<V>::T*>(xs + e) =
+              *reinterpret_cast<const typename Vec4<V>::T*>(XT + sx + e);
+        for (int64_t e = threadIdx.x * VN; e < p.yspan; e += kBlock * VN)
+          *reinterpret_cast<typename Vec4<V>::T*>(ys + e) =
+              *reinterpret_cast<const typename Vec4<V>::T*>(YT + sy + e);
+        for (int64_t e = threadIdx.x; e < p.zspan; e += kBlock) zs[e] = ZT[sz + e];
+        if (staged_g < 0)
+          for (int64_t e = threadIdx.x; e < p.nM; e += kBlock) ms[e] = MT[e];
+        __syncthreads();
+        staged_g = g;
+      }
+      XT = xs; YT = ys; ZT = zs; MT = ms;
+      sx = sy = sz = 0;
+    }
+    if (!live) continue;
+    V* Bp = static_cast<V*>(p.Bp) + row * p.Do;
+    const V k0 = static_cast<const V*>(p.K0)[pg];
+    V acc[NB];
 #pragma unroll
-  for (int j = 0; j < NB; ++j) acc[j] = T::CAP;
-  const int ybase = vg * NB;
-
-  for (int64_t m = 0; m < p.nM; ++m) {
-    const int4 mt = MT[m];
-    const V km = T::sat(k0, ZT[sz + mt.z]);
-    const V* yr = YT + sy + mt.y + ybase;
-    V y[NB];
+    for (int j = 0; j < NB; ++j) acc[j] = T::CAP;
+    const int ybase = vg * NB;
+    for (int64_t m = m0; m < m1; ++m) {
+      const int4 mt = MT[m];
+      const V km = T::sat(k0, ZT[sz + mt.z]);
+      const V* yr = YT + sy + mt.y + ybase;
+      V y[NB];
 #pragma unroll
-    for (int j = 0; j < NB; j += VN) load_vec<V>(yr + j, y + j);
+      for (int j = 0; j < NB; j += VN) load_vec<V>(yr + j, y + j);
 #pragma unroll
-    for (int j = 0; j < NB; ++j) y[j] = T::sat(y[j], km);
-    const V* xr = XT + sx + mt.x;
+      for (int j = 0; j < NB; ++j) y[j] = T::sat(y[j], km);
+      const V* xr = XT + sx + mt.x;
 #pragma unroll 2
-    for (int a = 0; a < p.na_pad; a += VN) {
-      V x[VN];
-      load_vec<V>(xr + a, x);
+      for (int a = 0; a < p.na_pad; a += VN) {
+        V x[VN];
+        load_vec<V>(xr + a, x);
 #pragma unroll
-      for (int q = 0; q < VN; ++q)
+        for (int q = 0; q < VN; ++q)
 #pragma unroll
-        for (int j = 0; j < NB; ++j) acc[j] = T::addmin(x[q], y[j], acc[j]);
+          for (int j = 0; j < NB; ++j) acc[j] = T::addmin(x[q], y[j], acc[j]);
+      }
+      if (p.o_mode == 1) {                        // bucket digit in M: flush per m
+        V r = acc[0];
+#pragma unroll
+        for (int j = 1; j < NB; ++j) r = T::mn(r, acc[j]);
+        if (partial) atomic_min_v<V>(Bp + mt.w, r);
+        else Bp[mt.w] = T::mn(Bp[mt.w], r);
+#pragma unroll
+        for (int j = 0; j < NB; ++j) acc[j] = T::CAP;
+      }
     }
-    if (p.o_mode == 1) {                        // bucket digit in M: flush per m
+    if (p.o_mode == 0) {
+      if (p.o_bstride == 1 && p.o_bradix == p.nb) {       // B = {o}: slot j <-> v
+#pragma unroll
+        for (int j = 0; j < NB; ++j)
+          if (ybase + j < p.nb) {
+            if (partial) atomic_min_v<V>(Bp + ybase + j, acc[j]);
+            else Bp[ybase + j] = acc[j];
+          }
+      } else {
+#pragma unroll
+        for (int j = 0; j < NB; ++j)
+          if (ybase + j < p.nb) {
+            const int v = ((ybase + j) / p.o_bstride) % p.o_bradix;
+            if (partial) atomic_min_v<V>(Bp + v, acc[j]);
+            else Bp[v] = T::mn(Bp[v], acc[j]);
+          }
+      }
+    } else if (p.o_mode == 2) {
       V r = acc[0];
 #pragma unroll
       for (int j = 1; j < NB; ++j) r = T::mn(r, acc[j]);
-      Bp[mt.w] = T::mn(Bp[mt.w], r);
-#pragma unroll
-      for (int j = 0; j < NB; ++j) acc[j] = T::CAP;
+      if (partial) atomic_min_v<V>(Bp + od, r);
+      else Bp[od] = T::mn(Bp[od], r);
     }
-  }
-  if (p.o_mode == 0) {
-    if (p.o_bstride == 1 && p.o_bradix == p.nb) {       // B = {o}: slot j <-> v
-#pragma unroll
-      for (int j = 0; j < NB; ++j)
-        if (ybase + j < p.nb) Bp[ybase + j] = acc[j];
-    } else {
-#pragma unroll
-      for (int j = 0; j < NB; ++j)
-        if (ybase + j < p.nb) {
-          const int v = ((ybase + j) / p.o_bstride) % p.o_bradix;
-          Bp[v] = T::mn(Bp[v], acc[j]);
-        }
-    }
-  } else if (p.o_mode == 2) {
-    V r = acc[0];
-#pragma unroll
-    for (int j = 1; j < NB; ++j) r = T::mn(r, acc[j]);
-    Bp[od] = r;
   }
 }
 
@@ -264,77 +349,129 @@ __device__ __forceinline__ V cross_sum(const FoldParams& f, const V* vals, int64
   V x = 0;
   for (int i = 0; i < f.nq; ++i) {
     const Term& q = f.q[i];
-    int64_t pp = pg;
-    int dig = 0;
-    for (int d = f.P - 1; d >= q.a; --d) {
-      dig = (int)(pp % f.pre_radix[d]);
-      pp /= f.pre_radix[d];
-    }
+    const int dig = prefix_digit(pg, q.a, f.P, f.pre_radix);
     x = VT<V>::sat(x, vals[q.off + (int64_t)u * q.db + dig]);
   }
   return x;
 }
 
 template <typename V>
+__device__ __forceinline__ void load4(const V* p, V* out) {
+  if constexpr (sizeof(V) == 4) {
+    load_vec<V>(p, out);
+  } else {
+    load_vec<V>(p, out);
+    load_vec<V>(p + 2, out + 2);
+  }
+}
+
+// Chunk c = CH consecutive local canonical prefixes.  Each thread owns a 4x4
+// (u, v) block over a subset of the chunk's prefixes (two 4-wide shared loads
+// per 16 fused add+mins), partial minima are reduced over the subsets.
+// Output layout: chunkmin[(u * Do + v) * nchunks + c] (coalesced for the
+// per-pair reduction that follows).
+template <typename V>
 __global__ void __launch_bounds__(256) fold_kernel(const FoldParams f) {
   using T = VT<V>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  V* bs = reinterpret_cast<V*>(smem_raw);          // [CH][Do]
-  V* xs = bs + (int64_t)f.CH * f.Do;                // [CH][Din]
-  int32_t* dg = reinterpret_cast<int32_t*>(xs + (int64_t)f.CH * f.Din);   // [CH][nq]
+  const int DinP = (f.Din + 3) & ~3, DoP = (f.Do + 3) & ~3;
+  V* bs = reinterpret_cast<V*>(smem_raw);          // [CH][DoP]
+  V* xs = bs + (int64_t)f.CH * DoP;                 // [CH][DinP]
+  V* red = xs + (int64_t)f.CH * DinP;               // [groups][DinP*DoP]
+  const int nblk = (DinP / 4) * (DoP / 4);
+  const int groups = max(1, min((int)(blockDim.x / nblk), 8));
+  int32_t* dg = reinterpret_cast<int32_t*>(red + (int64_t)groups * DinP * DoP);   // [CH][nq]
+  V* qs = reinterpret_cast<V*>(dg + ((f.CH * f.nq + 3) & ~3));                   // cross tables
+  __shared__ __align__(8) uint64_t mbar;
   const int64_t c = blockIdx.x;
   const int64_t p0 = c * f.CH;
   const int n = (int)min((int64_t)f.CH, f.nPl - p0);
   const V* Bp = static_cast<const V*>(f.Bp);
   const V* vals = static_cast<const V*>(f.vals);
-  for (int e = threadIdx.x; e < n * f.Do; e += blockDim.x) bs[e] = Bp[p0 * f.Do + e];
+  const bool tma = f.tma && DoP == f.Do;
+  if (tma) {
+    if (threadIdx.x == 0) mbar_init(&mbar, 1);
+    __syncthreads();
+    if (threadIdx.x == 0) {                  // one bulk copy of the chunk's B_p rows
+      const uint32_t bytes = (uint32_t)((int64_t)n * f.Do * sizeof(V));
+      mbar_expect_tx(&mbar, bytes);
+      tma_bulk_g2s(bs, Bp + p0 * f.Do, bytes, &mbar);
+    }
+  } else {
+    for (int e = threadIdx.x; e < n * DoP; e += blockDim.x) {
+      const int pi = e / DoP, v = e % DoP;
+      bs[e] = v < f.Do ? Bp[(p0 + pi) * f.Do + v] : T::CAP;
+    }
+  }
   for (int e = threadIdx.x; e < n * f.nq; e += blockDim.x) {
     const int pi = e / f.nq, i = e % f.nq;
-    int64_t pp = f.p_lo + p0 + pi;
-    int dig = 0;
-    for (int d = f.P - 1; d >= f.q[i].a; --d) {
-      dig = (int)(pp % f.pre_radix[d]);
-      pp /= f.pre_radix[d];
+    dg[e] = prefix_digit(f.p_lo + p0 + pi, f.q[i].a, f.P, f.pre_radix);
+  }
+  {
+    int qo = 0;
+    for (int i = 0; i < f.nq; ++i) {
+      const int ne = f.Din * f.q[i].db;
+      for (int e = threadIdx.x; e < ne; e += blockDim.x) qs[qo + e] = vals[f.q[i].off + e];
+      qo += ne;
     }
-    dg[e] = dig;
   }
   __syncthreads();
-  for (int e = threadIdx.x; e < n * f.Din; e += blockDim.x) {
-    const int pi = e / f.Din, u = e % f.Din;
-    V x = 0;
-    for (int i = 0; i < f.nq; ++i)
-      x = T::sat(x, vals[f.q[i].off + (int64_t)u * f.q[i].db + dg[pi * f.nq + i]]);
+  for (int e = threadIdx.x; e < n * DinP; e += blockDim.x) {
+    const int pi = e / DinP, u = e % DinP;
+    V x = T::CAP;
+    if (u < f.Din) {
+      x = 0;
+      int qo = 0;
+      for (int i = 0; i < f.nq; ++i) {
+        x = T::sat(x, qs[qo + u * f.q[i].db + dg[pi * f.nq + i]]);
+        qo += f.Din * f.q[i].db;
+      }
+    }
     xs[e] = x;
   }
+  if (tma) mbar_wait(&mbar, 0);
   __syncthreads();
-  V* out = static_cast<V*>(f.chunkmin) + c * (int64_t)f.Din * f.Do;
-  // register-blocked: each thread owns a 2x2 (u, v) block
-  const int ub = (f.Din + 1) / 2, vb = (f.Do + 1) / 2;
-  for (int blk = threadIdx.x; blk < ub * vb; blk += blockDim.x) {
-    const int u0 = (blk / vb) * 2, v0 = (blk % vb) * 2;
-    const int u1 = min(u0 + 1, f.Din - 1), v1 = min(v0 + 1, f.Do - 1);
-    V m00 = T::CAP, m01 = T::CAP, m10 = T::CAP, m11 = T::CAP;
-    for (int pi = 0; pi < n; ++pi) {
-      const V x0 = xs[pi * f.Din + u0], x1 = xs[pi * f.Din + u1];
-      const V b0 = bs[pi * f.Do + v0], b1 = bs[pi * f.Do + v1];
-      m00 = T::addmin(x0, b0, m00);
-      m01 = T::addmin(x0, b1, m01);
-      m10 = T::addmin(x1, b0, m10);
-      m11 = T::addmin(x1, b1, m11);
+  auto do_block = [&](int blk, int pstart, int pstep, V* r) {
+    const int u0 = (blk / (DoP / 4)) * 4, v0 = (blk % (DoP / 4)) * 4;
+    V acc[4][4];
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int b = 0; b < 4; ++b) acc[a][b] = T::CAP;
+    for (int pi = pstart; pi < n; pi += pstep) {
+      V x[4], y[4];
+      load4<V>(xs + pi * DinP + u0, x);
+      load4<V>(bs + pi * DoP + v0, y);
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) acc[a][b] = T::addmin(x[a], y[b], acc[a][b]);
     }
-    out[u0 * f.Do + v0] = m00;
-    if (v0 + 1 < f.Do) out[u0 * f.Do + v0 + 1] = m01;
-    if (u0 + 1 < f.Din) {
-      out[(u0 + 1) * f.Do + v0] = m10;
-      if (v0 + 1 < f.Do) out[(u0 + 1) * f.Do + v0 + 1] = m11;
-    }
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int b = 0; b < 4; ++b) r[(u0 + a) * DoP + v0 + b] = acc[a][b];
+  };
+  if (groups > 1) {
+    const int gi = threadIdx.x / nblk;
+    if (gi < groups) do_block(threadIdx.x % nblk, gi, groups, red + (int64_t)gi * DinP * DoP);
+  } else {
+    for (int blk = threadIdx.x; blk < nblk; blk += blockDim.x) do_block(blk, 0, 1, red);
+  }
+  __syncthreads();
+  V* out = static_cast<V*>(f.chunkmin);
+  for (int e = threadIdx.x; e < f.Din * f.Do; e += blockDim.x) {
+    const int u = e / f.Do, v = e % f.Do;
+    V m = red[u * DoP + v];
+    for (int g2 = 1; g2 < groups; ++g2) m = T::mn(m, red[(int64_t)g2 * DinP * DoP + u * DoP + v]);
+    out[(int64_t)e * f.nchunks + c] = m;
   }
 }
 
 // --------------------------------------------------------------------------
 // argmin phase 1: per (u, v): A = min over chunks; the first chunk attaining
 // it, then the least local prefix in that chunk with X_p[u] + B_p[v] == A.
-// One warp per (u, v).
+// One warp per (u, v); chunk minima are contiguous per pair.
 // --------------------------------------------------------------------------
 template <typename V>
 __global__ void fold_reduce_kernel(const FoldParams f, V* __restrict__ Aval, int64_t* __restrict__ pstar) {
@@ -342,11 +479,11 @@ __global__ void fold_reduce_kernel(const FoldParams f, V* __restrict__ Aval, int
   const int lane = threadIdx.x & 31;
   if (warp >= f.Din * f.Do) return;
   const int u = warp / f.Do, v = warp % f.Do;
-  const V* cm = static_cast<const V*>(f.chunkmin);
+  const V* cm = static_cast<const V*>(f.chunkmin) + (int64_t)warp * f.nchunks;
   V best = VT<V>::CAP;
   int64_t bc = INT64_MAX;
   for (int64_t c = lane; c < f.nchunks; c += 32) {
-    const V x = cm[c * f.Din * f.Do + u * f.Do + v];
+    const V x = cm[c];
     if (x < best) { best = x; bc = c; }       // c increasing per lane: first wins
   }
   for (int o = 16; o > 0; o >>= 1) {
@@ -386,6 +523,9 @@ __global__ void __launch_bounds__(256) suffix_argmin_kernel(const ArgminParams a
                                                             const V* __restrict__ vals) {
   const FoldParams& f = ap.f;
   const EvalSpec& e = ap.e;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  V* tabs = reinterpret_cast<V*>(smem_raw);                                   // W/R tables
+  uint16_t* sd = reinterpret_cast<uint16_t*>(tabs + ((e.tab_n + 1) & ~1));    // [K][blockDim]
   const int pair = blockIdx.x;
   const int u = pair / f.Do, v = pair % f.Do;
   const int vo = ap.vmap[v];
@@ -399,57 +539,61 @@ __global__ void __launch_bounds__(256) suffix_argmin_kernel(const ArgminParams a
     }
     return;
   }
+  for (int i = threadIdx.x; i < e.tab_n; i += blockDim.x) tabs[i] = vals[e.tab_lo + i];
   const V* Bp = static_cast<const V*>(f.Bp);
   const uint64_t target = (uint64_t)Bp[pl * f.Do + v];
   const int64_t pg = f.p_lo + pl;
-  int32_t pre[kMaxDigits];
+  const int tid = threadIdx.x, nth = blockDim.x;
+  auto S = [&](int d) -> uint16_t& { return sd[d * nth + tid]; };
   {
     int64_t q = pg;
-    for (int d = e.P - 1; d >= 0; --d) { pre[d] = (int)(q % e.radix[d]); q /= e.radix[d]; }
+    for (int d = e.P - 1; d >= 0; --d) { S(d) = (uint16_t)(q % e.radix[d]); q /= e.radix[d]; }
   }
   const bool o_suffix = e.o >= e.P;
   const int64_t nrest = o_suffix ? e.nsuffix / e.radix[e.o] : e.nsuffix;
-  if (threadIdx.x == 0) s_first = ~0ull;
+  if (tid == 0) s_first = ~0ull;
   __syncthreads();
-  const int64_t per = (nrest + blockDim.x - 1) / blockDim.x;
-  const int64_t lo = (int64_t)threadIdx.x * per;
+  const int64_t per = (nrest + nth - 1) / nth;
+  const int64_t lo = (int64_t)tid * per;
   const int64_t hi = min(nrest, lo + per);
-  for (int64_t r = lo; r < hi; ++r) {
-    int32_t s[kMaxDigits];
-    for (int d = 0; d < e.P; ++d) s[d] = pre[d];
-    int64_t q = r;
+  if (lo < hi) {
+    // decode lo over the free suffix digits (canonical order, o fixed to v)
+    int64_t q = lo;
     for (int d = e.K - 1; d >= e.P; --d) {
-      if (o_suffix && d == e.o) { s[d] = v; continue; }
-      s[d] = (int)(q % e.radix[d]);
+      if (o_suffix && d == e.o) { S(d) = (uint16_t)v; continue; }
+      S(d) = (uint16_t)(q % e.radix[d]);
       q /= e.radix[d];
     }
-    uint64_t c = 0;
-    bool inf = false;
-    for (int i = 0; i < e.nterm && !inf; ++i) {
-      const Term& tm = e.term[i];
-      const V x = tm.kind == 0 ? vals[tm.off + s[tm.a]]
-                               : vals[tm.off + (int64_t)s[tm.a] * tm.db + s[tm.b]];
-      if (x >= VT<V>::CAP) inf = true;
-      c += (uint64_t)x;
-    }
-    if (!inf && c == target) {
-      // suffix index in canonical order (o digit included)
-      int64_t sfx = 0;
-      for (int d = e.P; d < e.K; ++d) sfx = sfx * e.radix[d] + s[d];
-      atomicMin(&s_first, (unsigned long long)sfx);
-      break;
+    for (int64_t r = lo; r < hi; ++r) {
+      uint64_t c = 0;
+      bool inf = false;
+      for (int i = 0; i < e.nterm; ++i) {
+        const Term& tm = e.term[i];
+        const int64_t o = tm.off - e.tab_lo;
+        const V x = tm.kind == 0 ? tabs[o + S(tm.a)] : tabs[o + (int)S(tm.a) * tm.db + S(tm.b)];
+        inf |= x >= VT<V>::CAP;
+        c += (uint64_t)x;
+      }
+      if (!inf && c == target) {
+        int64_t sfx = 0;                       // suffix index in canonical order
+        for (int d = e.P; d < e.K; ++d) sfx = sfx * e.radix[d] + S(d);
+        atomicMin(&s_first, (unsigned long long)sfx);
+        break;
+      }
+      for (int d = e.K - 1; d >= e.P; --d) {   // odometer step
+        if (o_suffix && d == e.o) continue;
+        if (++S(d) < e.radix[d]) break;
+        S(d) = 0;
+      }
     }
   }
   __syncthreads();
-  if (threadIdx.x == 0) {
+  if (tid == 0) {
     const uint64_t sfx = s_first;
-    // compact digits of the winner -> original index
-    int32_t s[kMaxDigits];
-    for (int d = 0; d < e.P; ++d) s[d] = pre[d];
     uint64_t q = sfx;
-    for (int d = e.K - 1; d >= e.P; --d) { s[d] = (int)(q % e.radix[d]); q /= e.radix[d]; }
+    for (int d = e.K - 1; d >= e.P; --d) { S(d) = (uint16_t)(q % e.radix[d]); q /= e.radix[d]; }
     uint64_t idx = 0;
-    for (int d = 0; d < e.K; ++d) idx = idx * ap.orig_radix[d] + ap.maps[ap.map_off[d] + s[d]];
+    for (int d = 0; d < e.K; ++d) idx = idx * ap.orig_radix[d] + ap.maps[ap.map_off[d] + S(d)];
     ap.A_out[outi] = (uint64_t)Aval[pair];
     ap.I_out[outi] = sfx == ~0ull ? kInf64 : idx;     // ~0: cannot happen (exact arithmetic)
   }
@@ -481,33 +625,84 @@ __device__ void matvec(const uint64_t* M, int rows, int cols, const uint64_t* g,
   }
 }
 
+// Single-CTA chain.  SM = true: every distinct matrix (A and, for the
+// backtrack, I), every suffix vector G_n, the powers of the current run and the
+// instance metadata live in shared memory; G is copied out at the end.
+// SM = false: same algorithm on global memory (large S).
+__device__ __forceinline__ uint64_t gtimer() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+template <bool SM>
 __global__ void __launch_bounds__(1024) chain_kernel(const ChainParams cp) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  int dbg_i = 0;
+  auto mark = [&]() { if (cp.dbg && threadIdx.x == 0 && dbg_i < 64) cp.dbg[dbg_i++] = gtimer(); };
+  mark();
   const int tid = threadIdx.x, nth = blockDim.x;
   const int N = cp.N;
-  uint64_t* GN = cp.G + cp.goff[N];
-  const int lastc = cp.inst[N - 1].cols;
-  for (int v = tid; v < lastc; v += nth) GN[v] = cp.terminal ? cp.terminal[v] : 0;
+  uint64_t* sA = reinterpret_cast<uint64_t*>(smem_raw);
+  uint64_t* sI = sA + cp.mat_elems;
+  uint64_t* sG = sI + (cp.backtrack ? cp.mat_elems : 0);
+  uint64_t* sP = sG + cp.goff[N + 1];
+  int64_t* sgoff = reinterpret_cast<int64_t*>(sP + (int64_t)cp.levels_max * cp.smax * cp.smax);
+  int4* sinst = reinterpret_cast<int4*>((reinterpret_cast<uintptr_t>(sgoff + N + 2) + 15) & ~uintptr_t(15));
+  uint64_t* G = SM ? sG : cp.G;
+  uint64_t* Pw = SM ? sP : cp.powers;
+  const int64_t* goff = SM ? sgoff : cp.goff;
+  if constexpr (SM) {
+    for (int m = 0; m < cp.nmat; ++m) {
+      const ChainInst mi = cp.mats[m];
+      const int64_t n = (int64_t)mi.rows * mi.cols;
+      for (int64_t e = tid; e < n; e += nth) {
+        sA[cp.moff[m] + e] = mi.A[e];
+        if (cp.backtrack) sI[cp.moff[m] + e] = mi.I[e];
+      }
+    }
+    for (int i = tid; i < N + 2; i += nth) sgoff[i] = cp.goff[i];
+    for (int i = tid; i < N; i += nth) sinst[i] = make_int4(cp.inst[i].mat, cp.inst[i].rows, cp.inst[i].cols, 0);
+    __syncthreads();
+  }
+  mark();
+  auto rows_of = [&](int n) { return SM ? sinst[n].y : cp.inst[n].rows; };
+  auto cols_of = [&](int n) { return SM ? sinst[n].z : cp.inst[n].cols; };
+  auto matA = [&](int n) -> const uint64_t* { return SM ? sA + cp.moff[sinst[n].x] : cp.inst[n].A; };
+  auto matI = [&](int n) -> const uint64_t* { return SM ? sI + cp.moff[sinst[n].x] : cp.inst[n].I; };
+  const int lastc = cols_of(N - 1);
+  for (int v = tid; v < lastc; v += nth) G[goff[N] + v] = cp.terminal ? cp.terminal[v] : 0;
   __syncthreads();
   for (int r = cp.nruns - 1; r >= 0; --r) {
     const ChainRun run = cp.runs[r];
-    const ChainInst in = cp.inst[run.first];
+    const uint64_t* M = matA(run.first);
+    const int R = rows_of(run.first), Cc = cols_of(run.first);
     const int e = run.first + run.len;             // G_e known (1-based instance e)
     if (run.len == 1) {
-      matvec(in.A, in.rows, in.cols, cp.G + cp.goff[e], cp.G + cp.goff[e - 1], tid, nth);
+      const uint64_t* g = G + goff[e];
+      for (int u = tid; u < R; u += nth) {
+        uint64_t best = kInf64;
+        for (int v = 0; v < Cc; ++v) {
+          const uint64_t c = sat64(M[(int64_t)u * Cc + v], g[v]);
+          best = c < best ? c : best;
+        }
+        G[goff[e - 1] + u] = best;
+      }
       __syncthreads();
+      mark();
       continue;
     }
-    const int S = in.rows;                          // square
+    const int S = R;                                // square
     int levels = 0;
     while ((1 << (levels + 1)) <= run.len) ++levels;   // P_0 .. P_levels
-    if ((int64_t)S * S * levels > cp.powers_cap) {
+    if (!SM && (int64_t)S * S * levels > cp.powers_cap) {
       if (tid == 0) *cp.status = 4;
       return;
     }
-    // P_0 = M (read in place); P_j in scratch
+    // repeated squaring: P_j = P_{j-1} (x) P_{j-1}
     for (int j = 1; j <= levels; ++j) {
-      const uint64_t* Pa = j == 1 ? in.A : cp.powers + (int64_t)(j - 2) * S * S;
-      uint64_t* Pc = cp.powers + (int64_t)(j - 1) * S * S;
+      const uint64_t* Pa = j == 1 ? M : Pw + (int64_t)(j - 2) * S * S;
+      uint64_t* Pc = Pw + (int64_t)(j - 1) * S * S;
       for (int64_t c = tid; c < (int64_t)S * S; c += nth) {
         const int i = (int)(c / S), k2 = (int)(c % S);
         uint64_t best = kInf64;
@@ -518,64 +713,76 @@ __global__ void __launch_bounds__(1024) chain_kernel(const ChainParams cp) {
         Pc[c] = best;
       }
       __syncthreads();
+      mark();
     }
+    // doubling: G_{e-k} = P_j (x) G_{e-k+2^j}, k in [2^j, 2^(j+1))
     for (int j = 0; j <= levels; ++j) {
-      const uint64_t* Pj = j == 0 ? in.A : cp.powers + (int64_t)(j - 1) * S * S;
+      const uint64_t* Pj = j == 0 ? M : Pw + (int64_t)(j - 1) * S * S;
       const int k_lo = 1 << j, k_hi = min(1 << (j + 1), run.len + 1);
       const int64_t work = (int64_t)(k_hi - k_lo) * S;
       for (int64_t w = tid; w < work; w += nth) {
         const int k = k_lo + (int)(w / S), u = (int)(w % S);
-        const uint64_t* g = cp.G + cp.goff[e - k + (1 << j)];
+        const uint64_t* g = G + goff[e - k + (1 << j)];
         uint64_t best = kInf64;
         for (int v = 0; v < S; ++v) {
           const uint64_t x = sat64(Pj[(int64_t)u * S + v], g[v]);
           best = x < best ? x : best;
         }
-        cp.G[cp.goff[e - k] + u] = best;
+        G[goff[e - k] + u] = best;
       }
       __syncthreads();
+      mark();
     }
   }
+  if constexpr (SM)
+    for (int64_t e2 = tid; e2 < goff[N + 1]; e2 += nth) cp.G[e2] = G[e2];
   if (!cp.backtrack) return;
-  // forward greedy (warp 0)
+  // forward greedy (warp 0): among optimal successors the least index
+  __shared__ int s_status;
+  if (tid == 0) s_status = 0;
+  __syncthreads();
   if (tid < 32) {
     const int lane = tid;
     int u = 0;
-    if (cp.G[0] == kInf64) {
-      if (lane == 0) { *cp.status = 3; *cp.total = kInf64; }
-      return;
-    }
-    if (lane == 0) *cp.total = cp.G[0];
-    for (int n = 1; n <= N; ++n) {
-      const ChainInst in = cp.inst[n - 1];
-      const uint64_t target = cp.G[cp.goff[n - 1] + u];
-      const uint64_t* Gn = cp.G + cp.goff[n];
-      uint64_t bi = kInf64;
-      int bv = -1;
-      for (int v = lane; v < in.cols; v += 32) {
-        const uint64_t a = in.A[(int64_t)u * in.cols + v];
-        if (a == kInf64 || Gn[v] == kInf64 || a + Gn[v] != target) continue;
-        const uint64_t ix = in.I[(int64_t)u * in.cols + v];
-        if (ix < bi) { bi = ix; bv = v; }
+    if (G[0] == kInf64) {
+      if (lane == 0) { s_status = 3; *cp.total = kInf64; }
+    } else {
+      if (lane == 0) *cp.total = G[0];
+      for (int n = 1; n <= N; ++n) {
+        const uint64_t* A = matA(n - 1);
+        const uint64_t* I = matI(n - 1);
+        const int cols = cols_of(n - 1);
+        const uint64_t target = G[goff[n - 1] + u];
+        const uint64_t* Gn = G + goff[n];
+        uint64_t bi = kInf64;
+        int bv = -1;
+        for (int v = lane; v < cols; v += 32) {
+          const uint64_t a = A[(int64_t)u * cols + v];
+          if (a == kInf64 || Gn[v] == kInf64 || a + Gn[v] != target) continue;
+          const uint64_t ix = I[(int64_t)u * cols + v];
+          if (ix < bi) { bi = ix; bv = v; }
+        }
+        for (int o = 16; o > 0; o >>= 1) {
+          const uint64_t ob = __shfl_xor_sync(0xffffffffu, bi, o);
+          const int ov = __shfl_xor_sync(0xffffffffu, bv, o);
+          if (ob < bi || (ob == bi && ov >= 0 && (bv < 0 || ov < bv))) { bi = ob; bv = ov; }
+        }
+        if (bv < 0) {
+          if (lane == 0) s_status = 3;
+          break;
+        }
+        if (lane == 0) {
+          cp.seg_index[n - 1] = bi;
+          cp.seg_ns[n - 1] = A[(int64_t)u * cols + bv];
+        }
+        u = bv;
       }
-      for (int o = 16; o > 0; o >>= 1) {
-        const uint64_t ob = __shfl_xor_sync(0xffffffffu, bi, o);
-        const int ov = __shfl_xor_sync(0xffffffffu, bv, o);
-        if (ob < bi || (ob == bi && ov >= 0 && (bv < 0 || ov < bv))) { bi = ob; bv = ov; }
-      }
-      if (bv < 0) {
-        if (lane == 0) *cp.status = 3;
-        return;
-      }
-      if (lane == 0) {
-        cp.seg_index[n - 1] = bi;
-        cp.seg_ns[n - 1] = in.A[(int64_t)u * in.cols + bv];
-      }
-      u = bv;
     }
   }
   __syncthreads();
-  if (*cp.status != 0) return;
+  mark();
+  if (tid == 0) *cp.status = s_status;
+  if (s_status != 0) return;
   for (int64_t w = tid; w < (int64_t)N * cp.kmax; w += nth) {
     const int n = (int)(w / cp.kmax), j = (int)(w % cp.kmax);
     const ChainInst in = cp.inst[n];
@@ -587,6 +794,9 @@ __global__ void __launch_bounds__(1024) chain_kernel(const ChainParams cp) {
     }
     cp.digits[w] = dval;
   }
+  __syncthreads();
+  mark();
+  if (cp.dbg && tid == 0) cp.dbg[63] = dbg_i;
 }
 
 // --------------------------------------------------------------------------
@@ -700,19 +910,26 @@ cudaError_t launch_fill(V* p, int64_t n, V v, cudaStream_t st) {
 
 template <typename V, int NB>
 cudaError_t launch_enum_nb(const EnumParams& p, int64_t nthreads, size_t smem, cudaStream_t st) {
-  const int64_t blocks = nthreads / kBlock;
-  if (p.staged) {
-    auto k = enum_kernel<V, NB, true>;
+  (void)nthreads;
+  const int64_t total = p.W * p.VG * (p.Gpad / kBlock) * p.nM;
+  if (total <= 0) return cudaSuccess;
+  auto launch = [&](auto kern) -> cudaError_t {
     if (smem > 48 * 1024) {
-      cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       if (e != cudaSuccess) return e;
     }
-    k<<<(unsigned)blocks, kBlock, smem, st>>>(p);
-  } else {
-    enum_kernel<V, NB, false><<<(unsigned)blocks, kBlock, 0, st>>>(p);
-  }
-  CFP_LAUNCH_CHECK();
-  return cudaSuccess;
+    int dev = 0, sms = 148, occ = 1;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kBlock, smem);
+    if (occ < 1) occ = 1;
+    int64_t grid = (int64_t)sms * occ;
+    if (grid > total) grid = total;
+    kern<<<(unsigned)grid, kBlock, smem, st>>>(p);
+    return cudaGetLastError();
+  };
+  if (p.staged) return launch(enum_kernel<V, NB, true>);
+  return launch(enum_kernel<V, NB, false>);
 }
 
 template <typename V>
@@ -730,7 +947,11 @@ cudaError_t launch_enum(const EnumParams& p, int NB, int64_t nthreads, size_t sm
 
 template <typename V>
 cudaError_t launch_fold(const FoldParams& f, cudaStream_t st) {
-  const size_t smem = (size_t)f.CH * (f.Do + f.Din) * sizeof(V) + (size_t)f.CH * f.nq * 4 + 16;
+  const int DinP = (f.Din + 3) & ~3, DoP = (f.Do + 3) & ~3;
+  const int nblk = (DinP / 4) * (DoP / 4);
+  const int groups = std::max(1, std::min(256 / nblk, 8));
+  const size_t smem = (size_t)f.CH * (DoP + DinP) * sizeof(V) + (size_t)groups * DinP * DoP * sizeof(V) +
+                      (size_t)((f.CH * f.nq + 3) & ~3) * 4 + (size_t)f.qelems * sizeof(V) + 16;
   auto k = fold_kernel<V>;
   if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -746,13 +967,28 @@ cudaError_t launch_argmin(const ArgminParams& ap, V* Aval, const V* vals, cudaSt
   const int pairs = ap.f.Din * ap.f.Do;
   fold_reduce_kernel<V><<<(pairs * 32 + 255) / 256, 256, 0, st>>>(ap.f, Aval, ap.pstar);
   CFP_LAUNCH_CHECK();
-  suffix_argmin_kernel<V><<<pairs, 256, 0, st>>>(ap, Aval, vals);
+  const size_t smem = (size_t)((ap.e.tab_n + 1) & ~1) * sizeof(V) + (size_t)ap.e.K * 256 * 2 + 16;
+  if (smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(suffix_argmin_kernel<V>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem);
+    if (e != cudaSuccess) return e;
+  }
+  suffix_argmin_kernel<V><<<pairs, 256, smem, st>>>(ap, Aval, vals);
   CFP_LAUNCH_CHECK();
   return cudaSuccess;
 }
 
 cudaError_t launch_chain(const ChainParams& cp, cudaStream_t st) {
-  chain_kernel<<<1, 1024, 0, st>>>(cp);
+  if (cp.smem_bytes > 0) {
+    if (cp.smem_bytes > 48 * 1024) {
+      cudaError_t e = cudaFuncSetAttribute(chain_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           (int)cp.smem_bytes);
+      if (e != cudaSuccess) return e;
+    }
+    chain_kernel<true><<<1, 1024, (size_t)cp.smem_bytes, st>>>(cp);
+  } else {
+    chain_kernel<false><<<1, 1024, 0, st>>>(cp);
+  }
   CFP_LAUNCH_CHECK();
   return cudaSuccess;
 }

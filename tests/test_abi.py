@@ -1,0 +1,81 @@
+"""C-ABI surface checks that need no GPU: the library builds, loads and exports
+every function include/cfp.h declares; host-only helpers behave; without a
+GPU the context refuses loudly (no CPU fallback)."""
+import ctypes as C
+import os
+import re
+
+import numpy as np
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def cfp():
+    from paper_2504_00598_b200 import build as B
+    B.build()
+    from paper_2504_00598_b200 import cfp as m
+    return m
+
+
+def declared_functions():
+    src = open(os.path.join(ROOT, "include", "cfp.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(cfp_[a-z0-9_]+)\s*\(", src)))
+
+
+def test_header_declares_the_north_star_entry_points():
+    fns = declared_functions()
+    for name in ("cfp_segment_costs", "cfp_minplus_chain", "cfp_search_plan"):
+        assert name in fns
+
+
+def test_library_exports_every_declared_symbol(cfp):
+    L = C.CDLL(cfp.LIB_PATH)
+    missing = [f for f in declared_functions() if not hasattr(L, f)]
+    assert not missing, missing
+    assert sorted(cfp.EXPORTS) == sorted(declared_functions())
+
+
+def test_no_cpu_fallback(cfp):
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    with pytest.raises(cfp.CfpError) as ei:
+        cfp.Context(device=0)
+    assert ei.value.status == cfp.CFP_ECUDA
+
+
+@pytest.mark.parametrize("units,align,world", [(100, 1, 3), (100, 8, 3), (7, 4, 8), (0, 1, 2),
+                                               (23 ** 4, 23, 8), (5, 1, 8)])
+def test_shard_range_partitions(cfp, units, align, world):
+    prev = 0
+    for r in range(world):
+        lo, hi = cfp.shard_range(units, align, world, r)
+        assert lo == prev and lo <= hi
+        assert lo % align == 0 or lo == units
+        prev = hi
+    assert prev == units
+
+
+def test_pack_unpack_roundtrip_and_order(cfp):
+    rng = np.random.default_rng(0)
+    cost = rng.integers(0, 1 << 30, 1000).astype(np.uint64)
+    idx = rng.integers(0, 1 << 33, 1000).astype(np.uint64)
+    cost[::17] = np.uint64((1 << 64) - 1)
+    keys = cfp.pack_keys(cost, idx, 33)
+    c2, i2 = cfp.unpack_keys(keys, 33)
+    fin = cost != np.uint64((1 << 64) - 1)
+    assert np.array_equal(c2[fin], cost[fin]) and np.array_equal(i2[fin], idx[fin])
+    assert np.all(i2[~fin] == np.uint64((1 << 64) - 1))
+    # unsigned key order == lexicographic (cost, idx) order
+    order = np.argsort(keys, kind="stable")
+    lex = sorted(range(1000), key=lambda i: (int(cost[i]), int(idx[i])))
+    assert [int(keys[i]) for i in order] == [int(keys[i]) for i in lex]
+
+
+def test_pack_rejects_overflow(cfp):
+    with pytest.raises(cfp.CfpError) as ei:
+        cfp.pack_keys(np.array([1 << 40], np.uint64), np.array([0], np.uint64), 33)
+    assert ei.value.status == cfp.CFP_EOVERFLOW
