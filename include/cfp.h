@@ -150,10 +150,20 @@ cfp_status cfp_minplus_chain(cfp_ctx* ctx, int32_t num_mats, const int32_t* rows
 cfp_status cfp_search_plan(cfp_ctx* ctx, const cfp_problem* p, cfp_plan* out);
 
 /* One (min,+) product C = A (x) B with the least k attaining each entry
- * (CFP_NOIDX if the row/column pair is all-infinite).  argk nullable. */
+ * (CFP_NOIDX if the row/column pair is all-infinite).  argk nullable.
+ * Finite entries must satisfy max(A) + max(B) < 2^63 - 1 (else
+ * CFP_EOVERFLOW); when max(A) + max(B) < 2^31 - 1 the uint32 fused add+min
+ * path runs, else uint64 -- identical results. */
 cfp_status cfp_minplus_product(cfp_ctx* ctx, int32_t m, int32_t k, int32_t n,
                                const uint64_t* A, const uint64_t* B,
                                uint64_t* C, uint64_t* argk);
+
+/* (min,+) product microbenchmark: S x S x S on device-resident synthetic
+ * operands (values < 2^20); wide = 0 -> uint32 VIADDMNMX path, 1 -> uint64;
+ * with_argk = 1 also tracks the least k.  Reports ms per launch and
+ * add+min operations per second (S^3 / time). */
+cfp_status cfp_minplus_bench(cfp_ctx* ctx, int32_t S, int32_t wide, int32_t with_argk, int32_t iters,
+                             double* ms_per_launch, double* addmins_per_s);
 
 /* ---- device-resident execution (used by the bench to time the hot path
  * with inputs already in HBM) ---------------------------------------------

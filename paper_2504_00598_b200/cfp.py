@@ -83,7 +83,8 @@ EXPORTS = ["cfp_ctx_create", "cfp_ctx_destroy", "cfp_last_error", "cfp_nccl_uniq
            "cfp_segment_costs", "cfp_minplus_chain", "cfp_search_plan", "cfp_minplus_product",
            "cfp_prepare", "cfp_execute", "cfp_fetch_plan", "cfp_prepared_free",
            "cfp_prepared_query", "cfp_prepared_time_kernels", "cfp_prepared_kernel_ms",
-           "cfp_shard_range", "cfp_pack_keys", "cfp_unpack_keys", "cfp_intpipe_bench"]
+           "cfp_shard_range", "cfp_pack_keys", "cfp_unpack_keys", "cfp_intpipe_bench",
+           "cfp_minplus_bench"]
 
 _lib = None
 
@@ -123,6 +124,8 @@ def lib() -> C.CDLL:
     L.cfp_pack_keys.argtypes = [C.c_int64, P(C.c_uint64), P(C.c_uint64), C.c_int32, P(C.c_uint64)]
     L.cfp_unpack_keys.argtypes = [C.c_int64, P(C.c_uint64), C.c_int32, P(C.c_uint64), P(C.c_uint64)]
     L.cfp_intpipe_bench.argtypes = [vp, C.c_int32, C.c_int32, P(C.c_double), P(C.c_double)]
+    L.cfp_minplus_bench.argtypes = [vp, C.c_int32, C.c_int32, C.c_int32, C.c_int32, P(C.c_double),
+                                    P(C.c_double)]
     _lib = L
     return L
 
@@ -302,6 +305,12 @@ class Context:
 
     def prepare(self, prob) -> "Prepared":
         return Prepared(self, prob)
+
+    def minplus_bench(self, S: int, wide: bool = False, argk: bool = False, iters: int = 5):
+        """(ms per launch, add+min ops per second) of an S^3 (min,+) product."""
+        ms, ops = C.c_double(), C.c_double()
+        _check(lib().cfp_minplus_bench(self._h, S, int(wide), int(argk), iters, C.byref(ms), C.byref(ops)))
+        return ms.value, ops.value
 
     def intpipe_bench(self, op: int = 0, iters: int = 20000) -> Tuple[float, float]:
         ops, ms = C.c_double(), C.c_double()

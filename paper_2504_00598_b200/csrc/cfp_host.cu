@@ -31,12 +31,17 @@ template <typename V> cudaError_t launch_compact(const CompactJob*, int, const u
 template <typename V> cudaError_t launch_build_tables(const TableSpec*, int, int64_t, const V*, V*, cudaStream_t);
 template <typename V> cudaError_t launch_fill(V*, int64_t, V, cudaStream_t);
 template <typename V> cudaError_t launch_enum(const EnumParams&, int, int64_t, size_t, cudaStream_t);
-template <typename V> cudaError_t launch_fold(const FoldParams&, cudaStream_t);
 template <typename V> cudaError_t launch_argmin(const ArgminParams&, V*, const V*, cudaStream_t);
 cudaError_t launch_chain(const ChainParams&, cudaStream_t);
 cudaError_t launch_minplus(int, int, int, const uint64_t*, const uint64_t*, uint64_t*, uint64_t*, cudaStream_t);
 cudaError_t launch_matvec(const uint64_t*, int, int, const uint64_t*, uint64_t*, cudaStream_t);
 cudaError_t launch_intpipe(int, int, int, uint32_t*, cudaStream_t);
+template <typename V> cudaError_t launch_minplus_tiled(int, int, int, const V*, const V*, V*, uint32_t*, cudaStream_t);
+template <typename V> cudaError_t launch_to_path(const uint64_t*, V*, int64_t, cudaStream_t);
+template <typename V> cudaError_t launch_from_path(const V*, const uint32_t*, uint64_t*, uint64_t*, int64_t, cudaStream_t);
+template <typename V> cudaError_t launch_fill_random(V*, int64_t, uint64_t, cudaStream_t);
+cudaError_t launch_matvec_batch(const uint64_t*, int, int, const uint64_t*, const int64_t*, const int64_t*, uint64_t*,
+                                int, cudaStream_t);
 }  // namespace cfp
 
 using namespace cfp;
@@ -251,6 +256,7 @@ struct TypeExec {
   std::vector<int> w_off, e_off;            // value blob offsets (elements)
   int64_t xt_off = 0, yt_off = 0, zt_off = 0, k0_off = 0, mtab_off = 0, bp_off = 0;
   std::vector<int> trans;                   // incoming transitions (used)
+  int epi_off = 0;                          // first EpiTau of this type
   EvalSpec es{};
   double combos = 0, combos_local = 0;
 };
@@ -278,6 +284,8 @@ struct cfp_prepared {
   int njobs32 = 0, njobs64 = 0, nspecs32 = 0, nspecs64 = 0;
   int64_t spec_max32 = 0, spec_max64 = 0;
   std::vector<CompactJob> hjobs32, hjobs64;
+  std::vector<EpiTau> epi_host;
+  DevBuf epi;
   std::vector<TableSpec> hspecs32, hspecs64;
   ChainParams cp{};
   int nruns = 0;
@@ -640,12 +648,14 @@ static cfp_status setup_chain_staging(ChainParams& cp, const std::vector<ChainIn
   }
   cp.nmat = (int)mats.size();
   cp.mats = dmats.as<ChainInst>();
+  cp.baseA = mats.empty() ? nullptr : mats[0].A;     // matrices are contiguous in moff order
+  cp.baseI = mats.empty() ? nullptr : mats[0].I;
   cp.moff = dmoff.as<int64_t>();
   cp.mat_elems = tot;
   cp.levels_max = levels_max;
   cp.smax = smax;
   const int64_t need = (tot * (cp.backtrack ? 2 : 1) + g_elems + (int64_t)levels_max * smax * smax) * 8 +
-                       (int64_t)(cp.N + 2) * 8 + (int64_t)cp.N * 16 + 128;
+                       (int64_t)(cp.N + 2) * 8 + (int64_t)cp.N * 16 + 128 + g_elems * 2 + 16;
   cp.smem_bytes = need <= 200 * 1024 ? need : 0;
   return CFP_OK;
 }
@@ -945,6 +955,8 @@ static cfp_status prepare_impl(cfp_ctx* ctx, const cfp_problem* p, bool do_chain
     if (te.nthreads / kBlock > 0x7FFFFFFF) return fail(CFP_ETOOBIG, "grid too large");
     te.bp_off = bp_bytes;
     bp_bytes += ((te.nPl * ep.Do * vbytes) + 255) & ~255LL;
+    for (int i = 0; i < Pp; ++i) ep.pre_stride[i] = prod(r, i + 1, Pp);
+    ep.nchunks = ep.W * (ep.Gpad / kBlock);
     // eval spec for argmin recovery
     EvalSpec& es = te.es;
     es.K = K;
@@ -976,43 +988,58 @@ static cfp_status prepare_impl(cfp_ctx* ctx, const cfp_problem* p, bool do_chain
       TransExec& tx = P->trans[trans_slot[x]];
       FoldParams& f = tx.fp;
       f.P = Pp;
-      for (int i = 0; i < Pp; ++i) f.pre_radix[i] = r[i];
+      for (int i = 0; i < Pp; ++i) {
+        f.pre_radix[i] = r[i];
+        f.pre_stride[i] = prod(r, i + 1, Pp);
+      }
       f.p_lo = ep.h0 * ep.W;
       f.nPl = te.nPl;
       f.Din = tx.Din;
       f.Do = ep.Do;
       for (int q = 0; q < X[x].X; ++q) {
-        if (f.nq >= kMaxTerms) return fail(CFP_ETOOBIG, "too many cross terms");
+        if (f.nq >= kMaxCross) return fail(CFP_ETOOBIG, "more than 16 cross edges in one transition");
         Term tq{};
         tq.kind = 2; tq.a = X[x].xdst[q]; tq.db = r[X[x].xdst[q]]; tq.off = tx.q_off[q];
         f.q[f.nq++] = tq;
       }
-      {
-        const int64_t DinP = (f.Din + 3) & ~3, DoP = (f.Do + 3) & ~3;
-        const int64_t nblk = (DinP / 4) * (DoP / 4);
-        const int64_t groups = std::max<int64_t>(1, std::min<int64_t>(256 / nblk, 8));
-        const int64_t red = groups * DinP * DoP * (int64_t)vbytes;
-        if (red > 150 * 1024)
-          return fail(CFP_ETOOBIG, "D_in x D_o too large for the fold kernel");
-        f.qelems = 0;
-        for (int q = 0; q < f.nq; ++q) f.qelems += f.Din * f.q[q].db;
-        const int64_t qbytes = (int64_t)f.qelems * vbytes;
-        if (red + qbytes > 170 * 1024)
-          return fail(CFP_ETOOBIG, "cross tables too large for the fold kernel");
-        f.CH = 256;
-        while (f.CH > 8 && (size_t)f.CH * ((DoP + DinP) * vbytes + f.nq * 4) + red + qbytes > 190 * 1024)
-          f.CH /= 2;
-        f.tma = ((int64_t)f.Do * (int64_t)vbytes) % 16 == 0 ? 1 : 0;
-      }
-      f.nchunks = std::max<int64_t>(1, (f.nPl + f.CH - 1) / f.CH);
-      tx.chunk_off = scratch_bytes;
-      scratch_bytes += ((f.nchunks * f.Din * f.Do * vbytes) + 255) & ~255LL;
-      tx.aval_off = scratch_bytes;
-      scratch_bytes += ((int64_t)f.Din * f.Do * 8 + 255) & ~255LL;
-      tx.pstar_off = scratch_bytes;
-      scratch_bytes += ((int64_t)f.Din * f.Do * 8 + 255) & ~255LL;
+      f.qelems = 0;
+      for (int q = 0; q < f.nq; ++q) f.qelems += f.Din * f.q[q].db;
+      f.tma = ((int64_t)f.Do * (int64_t)vbytes) % 16 == 0 ? 1 : 0;
       tx.ap.e = es;
       tx.ap.Do_orig = tx.Do_orig;
+    }
+    // cross-term fold in the enumeration epilogue: one chunk = one CTA
+    {
+      const bool simple = ep.o_mode == 0 && ep.o_bstride == 1 && ep.o_bradix == ep.nb;
+      const int64_t VP = simple ? te.NB : ((ep.Do + 3) & ~3);
+      int64_t dinp_max = 4;
+      for (int x : te.trans) dinp_max = std::max<int64_t>(dinp_max, (P->trans[trans_slot[x]].Din + 3) & ~3);
+      int64_t epi = kBlock * VP + kBlock * dinp_max;
+      if (8 * VP > kBlock) epi += 8 * dinp_max * VP;
+      ep.smem_epi = (int32_t)(te.trans.empty() ? 0 : epi * (int64_t)vbytes);
+      if (ep.smem_epi > 200 * 1024) return fail(CFP_ETOOBIG, "D_in x D_o too large for the fold epilogue");
+      ep.ntau = (int)te.trans.size();
+      te.epi_off = (int)P->epi_host.size();
+      for (int x : te.trans) {
+        TransExec& tx = P->trans[trans_slot[x]];
+        EpiTau et{};
+        et.Din = tx.Din;
+        et.nq = tx.fp.nq;
+        for (int q = 0; q < tx.fp.nq; ++q) et.q[q] = tx.fp.q[q];
+        P->epi_host.push_back(et);
+        tx.fp.CH = kBlock;
+        tx.fp.nchunks = ep.nchunks;
+        tx.fp.W = ep.W;
+        tx.fp.G = ep.G;
+        tx.fp.h0 = ep.h0;
+        tx.fp.nhb = ep.Gpad / kBlock;
+        tx.chunk_off = scratch_bytes;
+        scratch_bytes += ((ep.nchunks * tx.fp.Din * tx.fp.Do * vbytes) + 255) & ~255LL;
+        tx.aval_off = scratch_bytes;
+        scratch_bytes += ((int64_t)tx.fp.Din * tx.fp.Do * 8 + 255) & ~255LL;
+        tx.pstar_off = scratch_bytes;
+        scratch_bytes += ((int64_t)tx.fp.Din * tx.fp.Do * 8 + 255) & ~255LL;
+      }
     }
   }
   // ---- device allocation + H2D
@@ -1034,6 +1061,8 @@ static cfp_status prepare_impl(cfp_ctx* ctx, const cfp_problem* p, bool do_chain
   CUDA_TRY(P->vals64.alloc((size_t)(v64 + b.der64) * 8));
   for (auto& s : P->hspecs32) { s.out_off += v32; P->spec_max32 = std::max(P->spec_max32, s.rows * s.row); }
   for (auto& s : P->hspecs64) { s.out_off += v64; P->spec_max64 = std::max(P->spec_max64, s.rows * s.row); }
+  // epilogue transition descriptors (chunkmin pointers patched below)
+  CUDA_TRY(P->epi.alloc(std::max<size_t>(1, P->epi_host.size()) * sizeof(EpiTau)));
   P->njobs32 = (int)P->hjobs32.size();
   P->njobs64 = (int)P->hjobs64.size();
   P->nspecs32 = (int)P->hspecs32.size();
@@ -1087,7 +1116,14 @@ static cfp_status prepare_impl(cfp_ctx* ctx, const cfp_problem* p, bool do_chain
       tx.ap.I_out = outI + tx.out_off;
       tx.ap.pstar = reinterpret_cast<int64_t*>((char*)P->scratch.p + tx.pstar_off);
     }
+    for (size_t q = 0; q < te.trans.size(); ++q)
+      P->epi_host[te.epi_off + q].chunkmin = P->trans[trans_slot[te.trans[q]]].fp.chunkmin;
+    ep.taus = P->epi.as<EpiTau>() + te.epi_off;
+    ep.vals = vals;
   }
+  if (!P->epi_host.empty())
+    CUDA_TRY(cudaMemcpyAsync(P->epi.p, P->epi_host.data(), P->epi_host.size() * sizeof(EpiTau),
+                             cudaMemcpyHostToDevice, st));
   for (TransExec& tx : P->trans) {
     const TypeExec& te = P->types[type_slot[tx.type]];
     P->evals += te.combos;
@@ -1199,19 +1235,16 @@ template <> constexpr uint64_t VTcap<uint64_t>() { return kCap64; }
 template <typename V>
 static cfp_status run_type_kernels(cfp_prepared* P, TypeExec& te, cudaStream_t st, bool first_of_prec) {
   (void)first_of_prec;
-  // B_p pre-filled with CAP: (g, hb) groups cut between CTAs merge by atomicMin
-  CUDA_TRY(launch_fill<V>(static_cast<V*>(te.ep.Bp), te.nPl * te.ep.Do, (V)VTcap<V>(), st));
   CUDA_TRY(launch_enum<V>(te.ep, te.NB, te.nthreads, te.smem, st));
-  P->launches += 2;
+  P->launches += 1;
   return CFP_OK;
 }
 
 template <typename V>
 static cfp_status run_trans_kernels(cfp_prepared* P, TransExec& tx, cudaStream_t st) {
-  CUDA_TRY(launch_fold<V>(tx.fp, st));
   CUDA_TRY(launch_argmin<V>(tx.ap, reinterpret_cast<V*>((char*)P->scratch.p + tx.aval_off),
                             static_cast<const V*>(tx.fp.vals), st));
-  P->launches += 3;
+  P->launches += 1;
   return CFP_OK;
 }
 
@@ -1495,6 +1528,69 @@ extern "C" cfp_status cfp_segment_costs(cfp_ctx* ctx, const cfp_segment_type* t,
 }
 
 // ---------------------------------------------------------------- chain API
+// Large-S chain (shared-memory staging impossible): repeated squaring with the
+// tiled (min,+) kernel, doubling stages as batched matrix-vector launches.
+static cfp_status chain_large(const std::vector<ChainInst>& ci, const std::vector<ChainRun>& runs,
+                              const std::vector<int64_t>& goff, uint64_t* G, bool narrow, cudaStream_t st) {
+  int64_t maxS2 = 1, maxL = 1;
+  for (const ChainRun& r : runs) {
+    maxS2 = std::max<int64_t>(maxS2, (int64_t)ci[r.first].rows * ci[r.first].cols);
+    maxL = std::max<int64_t>(maxL, r.len);
+  }
+  int levels_max = 0;
+  while ((1ll << (levels_max + 1)) <= maxL) ++levels_max;
+  DevBuf pw, pa, pc, offs;
+  CUDA_TRY(pw.alloc((size_t)std::max(1, levels_max) * maxS2 * 8));
+  CUDA_TRY(pa.alloc((size_t)maxS2 * 8));
+  CUDA_TRY(pc.alloc((size_t)maxS2 * 8));
+  CUDA_TRY(offs.alloc((size_t)(2 * maxL + 2) * 8));
+  std::vector<int64_t> ho(2 * maxL + 2);
+  auto batch = [&](const uint64_t* P, int R, int C, const std::vector<std::pair<int64_t, int64_t>>& sd) -> cfp_status {
+    const int nv = (int)sd.size();
+    for (int i = 0; i < nv; ++i) { ho[i] = sd[i].first; ho[maxL + 1 + i] = sd[i].second; }
+    CUDA_TRY(cudaMemcpyAsync(offs.p, ho.data(), ho.size() * 8, cudaMemcpyHostToDevice, st));
+    CUDA_TRY(cudaStreamSynchronize(st));     // host vector is reused by the next batch
+    CUDA_TRY(launch_matvec_batch(P, R, C, G, offs.as<int64_t>(), offs.as<int64_t>() + maxL + 1, G, nv, st));
+    return CFP_OK;
+  };
+  for (int r = (int)runs.size() - 1; r >= 0; --r) {
+    const ChainRun run = runs[r];
+    const ChainInst& in = ci[run.first];
+    const int e = run.first + run.len;
+    if (run.len == 1) {
+      TRY(batch(in.A, in.rows, in.cols, {{goff[e], goff[e - 1]}}));
+      continue;
+    }
+    const int S = in.rows;
+    int levels = 0;
+    while ((1 << (levels + 1)) <= run.len) ++levels;
+    const int64_t S2 = (int64_t)S * S;
+    for (int j = 1; j <= levels; ++j) {
+      const uint64_t* src = j == 1 ? in.A : pw.as<uint64_t>() + (j - 2) * S2;
+      uint64_t* dst = pw.as<uint64_t>() + (j - 1) * S2;
+      if (narrow) {
+        CUDA_TRY(launch_to_path<uint32_t>(src, pa.as<uint32_t>(), S2, st));
+        CUDA_TRY(launch_minplus_tiled<uint32_t>(S, S, S, pa.as<uint32_t>(), pa.as<uint32_t>(), pc.as<uint32_t>(),
+                                                nullptr, st));
+        CUDA_TRY(launch_from_path<uint32_t>(pc.as<uint32_t>(), nullptr, dst, nullptr, S2, st));
+      } else {
+        CUDA_TRY(launch_to_path<uint64_t>(src, pa.as<uint64_t>(), S2, st));
+        CUDA_TRY(launch_minplus_tiled<uint64_t>(S, S, S, pa.as<uint64_t>(), pa.as<uint64_t>(), pc.as<uint64_t>(),
+                                                nullptr, st));
+        CUDA_TRY(launch_from_path<uint64_t>(pc.as<uint64_t>(), nullptr, dst, nullptr, S2, st));
+      }
+    }
+    for (int j = 0; j <= levels; ++j) {
+      const uint64_t* Pj = j == 0 ? in.A : pw.as<uint64_t>() + (j - 1) * S2;
+      const int k_lo = 1 << j, k_hi = std::min(1 << (j + 1), run.len + 1);
+      std::vector<std::pair<int64_t, int64_t>> sd;
+      for (int k = k_lo; k < k_hi; ++k) sd.push_back({goff[e - k + (1 << j)], goff[e - k]});
+      TRY(batch(Pj, S, S, sd));
+    }
+  }
+  return CFP_OK;
+}
+
 extern "C" cfp_status cfp_minplus_chain(cfp_ctx* ctx, int32_t num_mats, const int32_t* rows,
                                         const int32_t* cols, const uint64_t* const* mats,
                                         int32_t num_runs, const int32_t* run_mat, const int64_t* run_len,
@@ -1514,6 +1610,7 @@ extern "C" cfp_status cfp_minplus_chain(cfp_ctx* ctx, int32_t num_mats, const in
     N += run_len[r];
   }
   if (N > (1 << 26)) return fail(CFP_ETOOBIG, "chain too long");
+  long double chain_bound = 0;
   // overflow guard: sum of per-instance maximum finite entries < 2^63
   {
     long double tot = 0;
@@ -1528,6 +1625,7 @@ extern "C" cfp_status cfp_minplus_chain(cfp_ctx* ctx, int32_t num_mats, const in
       for (int v = 0; v < cols[run_mat[num_runs - 1]]; ++v)
         if (terminal[v] != CFP_INF64) tot += terminal[v];
     if (tot >= 9.2e18L) return fail(CFP_EOVERFLOW, "a finite chain cost could reach 2^63");
+    chain_bound = tot;
   }
   g_alloc_stream = ctx->stream;
   CUDA_TRY(cudaSetDevice(ctx->device));
@@ -1598,7 +1696,16 @@ extern "C" cfp_status cfp_minplus_chain(cfp_ctx* ctx, int32_t num_mats, const in
     }
     TRY(setup_chain_staging(cp, umats, goff[N + 1], lv, maxS, dmats, dmoff, st));
   }
-  CUDA_TRY(launch_chain(cp, st));
+  if (cp.smem_bytes == 0 && maxS > 64) {
+    if (terminal)
+      CUDA_TRY(cudaMemcpyAsync(dG.as<uint64_t>() + goff[N], terminal, (size_t)ci.back().cols * 8,
+                               cudaMemcpyHostToDevice, st));
+    else
+      CUDA_TRY(cudaMemsetAsync(dG.as<uint64_t>() + goff[N], 0, (size_t)ci.back().cols * 8, st));
+    TRY(chain_large(ci, runs, goff, dG.as<uint64_t>(), chain_bound < (long double)kCap32, st));
+  } else {
+    CUDA_TRY(launch_chain(cp, st));
+  }
   int32_t status = 0;
   CUDA_TRY(cudaMemcpyAsync(&status, dstatus.p, 4, cudaMemcpyDeviceToHost, st));
   CUDA_TRY(cudaMemcpyAsync(opt_out, dG.p, 8, cudaMemcpyDeviceToHost, st));
@@ -1609,28 +1716,92 @@ extern "C" cfp_status cfp_minplus_chain(cfp_ctx* ctx, int32_t num_mats, const in
   return CFP_OK;
 }
 
+// Narrow (uint32, VIADDMNMX) when every finite a + b < 2^31 - 1, else uint64.
 extern "C" cfp_status cfp_minplus_product(cfp_ctx* ctx, int32_t m, int32_t k, int32_t n, const uint64_t* A,
                                           const uint64_t* B, uint64_t* C, uint64_t* argk) {
   if (!ctx || m < 1 || k < 1 || n < 1 || !A || !B || !C) return fail(CFP_EINVAL, "bad product arguments");
   uint64_t ma = 0, mb = 0;
   for (int64_t i = 0; i < (int64_t)m * k; ++i) if (A[i] != CFP_INF64) ma = std::max(ma, A[i]);
   for (int64_t i = 0; i < (int64_t)k * n; ++i) if (B[i] != CFP_INF64) mb = std::max(mb, B[i]);
-  if ((long double)ma + mb >= 18446744073709551615.0L) return fail(CFP_EOVERFLOW, "finite sum overflows");
+  if ((long double)ma + mb >= (long double)kCap64) return fail(CFP_EOVERFLOW, "a finite sum could reach 2^63");
+  const bool narrow = (long double)ma + mb < (long double)kCap32;
   g_alloc_stream = ctx->stream;
   CUDA_TRY(cudaSetDevice(ctx->device));
   cudaStream_t st = ctx->stream;
-  DevBuf dA, dB, dC, dK;
-  CUDA_TRY(dA.alloc((size_t)m * k * 8));
-  CUDA_TRY(dB.alloc((size_t)k * n * 8));
-  CUDA_TRY(dC.alloc((size_t)m * n * 8));
-  CUDA_TRY(dK.alloc((size_t)m * n * 8));
-  CUDA_TRY(cudaMemcpyAsync(dA.p, A, (size_t)m * k * 8, cudaMemcpyHostToDevice, st));
-  CUDA_TRY(cudaMemcpyAsync(dB.p, B, (size_t)k * n * 8, cudaMemcpyHostToDevice, st));
-  CUDA_TRY(launch_minplus(m, k, n, dA.as<uint64_t>(), dB.as<uint64_t>(), dC.as<uint64_t>(),
-                          dK.as<uint64_t>(), st));
-  CUDA_TRY(cudaMemcpyAsync(C, dC.p, (size_t)m * n * 8, cudaMemcpyDeviceToHost, st));
-  if (argk) CUDA_TRY(cudaMemcpyAsync(argk, dK.p, (size_t)m * n * 8, cudaMemcpyDeviceToHost, st));
+  const size_t vb = narrow ? 4 : 8;
+  DevBuf dA, dB, dC, dK, dA8, dB8, dC8, dK8;
+  CUDA_TRY(dA8.alloc((size_t)m * k * 8));
+  CUDA_TRY(dB8.alloc((size_t)k * n * 8));
+  CUDA_TRY(dC8.alloc((size_t)m * n * 8));
+  CUDA_TRY(dK8.alloc((size_t)m * n * 8));
+  CUDA_TRY(dA.alloc((size_t)m * k * vb));
+  CUDA_TRY(dB.alloc((size_t)k * n * vb));
+  CUDA_TRY(dC.alloc((size_t)m * n * vb));
+  CUDA_TRY(dK.alloc((size_t)m * n * 4));
+  CUDA_TRY(cudaMemcpyAsync(dA8.p, A, (size_t)m * k * 8, cudaMemcpyHostToDevice, st));
+  CUDA_TRY(cudaMemcpyAsync(dB8.p, B, (size_t)k * n * 8, cudaMemcpyHostToDevice, st));
+  uint32_t* kp = argk ? dK.as<uint32_t>() : nullptr;
+  if (narrow) {
+    CUDA_TRY(launch_to_path<uint32_t>(dA8.as<uint64_t>(), dA.as<uint32_t>(), (int64_t)m * k, st));
+    CUDA_TRY(launch_to_path<uint32_t>(dB8.as<uint64_t>(), dB.as<uint32_t>(), (int64_t)k * n, st));
+    CUDA_TRY(launch_minplus_tiled<uint32_t>(m, k, n, dA.as<uint32_t>(), dB.as<uint32_t>(), dC.as<uint32_t>(), kp, st));
+    CUDA_TRY(launch_from_path<uint32_t>(dC.as<uint32_t>(), kp, dC8.as<uint64_t>(), argk ? dK8.as<uint64_t>() : nullptr,
+                                        (int64_t)m * n, st));
+  } else {
+    CUDA_TRY(launch_to_path<uint64_t>(dA8.as<uint64_t>(), dA.as<uint64_t>(), (int64_t)m * k, st));
+    CUDA_TRY(launch_to_path<uint64_t>(dB8.as<uint64_t>(), dB.as<uint64_t>(), (int64_t)k * n, st));
+    CUDA_TRY(launch_minplus_tiled<uint64_t>(m, k, n, dA.as<uint64_t>(), dB.as<uint64_t>(), dC.as<uint64_t>(), kp, st));
+    CUDA_TRY(launch_from_path<uint64_t>(dC.as<uint64_t>(), kp, dC8.as<uint64_t>(), argk ? dK8.as<uint64_t>() : nullptr,
+                                        (int64_t)m * n, st));
+  }
+  CUDA_TRY(cudaMemcpyAsync(C, dC8.p, (size_t)m * n * 8, cudaMemcpyDeviceToHost, st));
+  if (argk) CUDA_TRY(cudaMemcpyAsync(argk, dK8.p, (size_t)m * n * 8, cudaMemcpyDeviceToHost, st));
   CUDA_TRY(cudaStreamSynchronize(st));
+  return CFP_OK;
+}
+
+// Device-resident (min,+) product microbenchmark: S x S x S,
+// hash-generated operands < 2^20, `iters` timed launches after one warm-up.
+extern "C" cfp_status cfp_minplus_bench(cfp_ctx* ctx, int32_t S, int32_t wide, int32_t with_argk, int32_t iters,
+                                        double* ms_per_launch, double* addmins_per_s) {
+  if (!ctx || S < 1 || S > 65536 || iters < 1) return fail(CFP_EINVAL, "bad minplus bench arguments");
+  g_alloc_stream = ctx->stream;
+  CUDA_TRY(cudaSetDevice(ctx->device));
+  cudaStream_t st = ctx->stream;
+  const size_t vb = wide ? 8 : 4;
+  const int64_t n2 = (int64_t)S * S;
+  DevBuf dA, dB, dC, dK;
+  CUDA_TRY(dA.alloc(n2 * vb));
+  CUDA_TRY(dB.alloc(n2 * vb));
+  CUDA_TRY(dC.alloc(n2 * vb));
+  CUDA_TRY(dK.alloc(with_argk ? n2 * 4 : 16));
+  cudaEvent_t e0, e1;
+  CUDA_TRY(cudaEventCreate(&e0));
+  CUDA_TRY(cudaEventCreate(&e1));
+  uint32_t* kp = with_argk ? dK.as<uint32_t>() : nullptr;
+  auto run = [&]() -> cudaError_t {
+    if (wide) return launch_minplus_tiled<uint64_t>(S, S, S, dA.as<uint64_t>(), dB.as<uint64_t>(), dC.as<uint64_t>(), kp, st);
+    return launch_minplus_tiled<uint32_t>(S, S, S, dA.as<uint32_t>(), dB.as<uint32_t>(), dC.as<uint32_t>(), kp, st);
+  };
+  if (wide) {
+    CUDA_TRY(launch_fill_random<uint64_t>(dA.as<uint64_t>(), n2, 1, st));
+    CUDA_TRY(launch_fill_random<uint64_t>(dB.as<uint64_t>(), n2, 2, st));
+  } else {
+    CUDA_TRY(launch_fill_random<uint32_t>(dA.as<uint32_t>(), n2, 1, st));
+    CUDA_TRY(launch_fill_random<uint32_t>(dB.as<uint32_t>(), n2, 2, st));
+  }
+  CUDA_TRY(run());
+  CUDA_TRY(cudaEventRecord(e0, st));
+  for (int i = 0; i < iters; ++i) CUDA_TRY(run());
+  CUDA_TRY(cudaEventRecord(e1, st));
+  CUDA_TRY(cudaEventSynchronize(e1));
+  float t = 0;
+  CUDA_TRY(cudaEventElapsedTime(&t, e0, e1));
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  const double per = t / iters;
+  if (ms_per_launch) *ms_per_launch = per;
+  if (addmins_per_s) *addmins_per_s = (double)S * S * S / (per * 1e-3);
   return CFP_OK;
 }
 

@@ -17,11 +17,14 @@
 // one fused add+min (VIADDMNMX) per combination evaluates and reduces it.
 #pragma once
 #include <cstdint>
+#include <cuda_runtime.h>
 
 namespace cfp {
 
 constexpr int kMaxDigits = 32;
 constexpr int kMaxTerms = 96;
+constexpr int kMaxCross = 16;    // cross edges per transition
+constexpr int kMaxFoldTau = 4;   // transitions folded by one launch
 constexpr int kBlock = 256;          // threads per CTA of the enumeration kernel
 constexpr uint32_t kCap32 = 0x7FFFFFFFu;            // narrow "infinity" (>= CAP => INF)
 constexpr uint64_t kCap64 = 0x7FFFFFFFFFFFFFFFull;  // wide "infinity"
@@ -53,6 +56,14 @@ struct TableSpec {
   int64_t out_off;     // element offset of T in the derived blob
 };
 
+// A transition folded in the enumeration epilogue (cross terms into this type).
+struct EpiTau {
+  int32_t Din;
+  int32_t nq;
+  Term q[kMaxCross];            // kind 2: a = prefix position of the consumer, db, off
+  void* chunkmin;               // [Din * Do][nchunks]
+};
+
 struct EnumParams {
   // prefix mapping: p = h * W + l, thread t -> (l, vg) = t / Gpad, h = h0 + t % Gpad
   int32_t P;                    // prefix length
@@ -76,24 +87,76 @@ struct EnumParams {
   const void* XT; const void* YT; const void* ZT; const void* K0;
   const int4* mtab;             // [nM] (x, y, z, v_o)
   void* Bp;                     // [G*W][Do] local canonical prefixes
+  // epilogue fold of the cross-segment terms (one chunk = one CTA's prefixes)
+  int64_t pre_stride[kMaxDigits];
+  int32_t ntau;
+  const EpiTau* taus;           // device [ntau]
+  const void* vals;             // value blob (compact Q tables)
+  int64_t nchunks;              // W * (Gpad / kBlock)
+  int32_t smem_epi;             // bytes of the epilogue region
 };
 
 struct FoldParams {
   int32_t P;
   int32_t pre_radix[kMaxDigits];
+  int64_t pre_stride[kMaxDigits];   // prod of the radices after each prefix digit
   int64_t p_lo;                 // global canonical prefix of local row 0
   int64_t nPl;                  // local prefixes
   int32_t Din, Do;
   int32_t nq;                   // cross terms: a = prefix position of consumer, db, off
-  Term q[kMaxTerms];
+  Term q[kMaxCross];
   int32_t CH;                   // prefixes per chunk
   int64_t nchunks;
   int32_t tma;                  // 1: B_p chunk rows are 16-byte multiples (bulk copy)
   int32_t qelems;               // sum of D_in * D_j over cross terms (smem copy)
   const void* Bp;
   const void* vals;             // value blob (compact Q tables)
-  void* chunkmin;               // [nchunks][Din][Do]
+  void* chunkmin;               // [Din * Do][nchunks]
+  // chunk -> rows: chunk = l * nhb + hb holds local rows (hb*kBlock + i) * W + l
+  int64_t W, G, h0, nhb;
 };
+
+struct FoldMulti {              // all transitions into one type (share B_p)
+  int32_t ntau;
+  FoldParams f[kMaxFoldTau];
+};
+
+// Shared-memory layout of the fold kernel (host sizes it, device uses it).
+struct FoldSmem {
+  int DoP, CH, Dl, ngrp, DinP[4], nblk[4], blk0[4], nblk_all, groups;
+  int64_t bs, xs[4], red[4], xh[4], qs[4], ql[4], rows, gdig, total;
+};
+
+__host__ __device__ inline FoldSmem fold_layout(const FoldMulti& fm, int vbytes) {
+  FoldSmem L{};
+  const FoldParams& f0 = fm.f[0];
+  L.DoP = (f0.Do + 3) & ~3;
+  L.CH = f0.CH;
+  L.Dl = f0.P > 0 ? f0.pre_radix[f0.P - 1] : 1;   // rows sharing all but the last prefix digit
+  L.ngrp = L.CH / L.Dl + 2;
+  int64_t off = 0;
+  auto take = [&](int64_t bytes) { const int64_t o = off; off += (bytes + 15) & ~15LL; return o; };
+  L.bs = take(2LL * L.CH * L.DoP * vbytes);
+  L.nblk_all = 0;
+  for (int t = 0; t < fm.ntau; ++t) {
+    L.DinP[t] = (fm.f[t].Din + 3) & ~3;
+    L.nblk[t] = (L.DinP[t] / 4) * (L.DoP / 4);
+    L.blk0[t] = L.nblk_all;
+    L.nblk_all += L.nblk[t];
+  }
+  L.groups = L.nblk_all >= 256 ? 1 : (256 / L.nblk_all < 8 ? 256 / L.nblk_all : 8);
+  for (int t = 0; t < fm.ntau; ++t) {
+    L.xs[t] = take((int64_t)L.CH * L.DinP[t] * vbytes);
+    L.red[t] = take((int64_t)L.groups * L.DinP[t] * L.DoP * vbytes);
+    L.xh[t] = take((int64_t)L.ngrp * L.DinP[t] * vbytes);
+    L.qs[t] = take((int64_t)fm.f[t].qelems * vbytes);
+    L.ql[t] = take((int64_t)L.DinP[t] * L.Dl * vbytes);
+  }
+  L.rows = take((int64_t)L.CH * 2 * 4);             // (group, last digit) per chunk row
+  L.gdig = take((int64_t)L.ngrp * kMaxFoldTau * kMaxCross * 4);
+  L.total = off;
+  return L;
+}
 
 // Generic evaluation of all intra terms of a compact combination (argmin
 // recovery) -- terms reference block ids directly.
@@ -174,6 +237,8 @@ struct ChainParams {
   int64_t smem_bytes;           // 0 = global mode
   int32_t levels_max, smax;
   uint64_t* dbg;                // nullable: %globaltimer at phase boundaries
+  const uint64_t* baseA;        // all distinct A matrices, contiguous (moff offsets)
+  const uint64_t* baseI;        // same for I (backtrack)
 };
 
 }  // namespace cfp

@@ -206,85 +206,85 @@ __device__ __forceinline__ void atomic_min_v<uint64_t>(uint64_t* p, uint64_t v) 
   atomicMin(reinterpret_cast<unsigned long long*>(p), (unsigned long long)v);
 }
 
-// Persistent, statically balanced: the work items (group g = (l, vg), h-block
-// hb of kBlock prefixes, m) are linearised g-major and split into gridDim.x
-// contiguous equal ranges.  A CTA keeps its accumulators in registers while
-// (g, hb) stays the same; a (g, hb) pair cut by a range boundary is merged
-// with atomicMin into B_p (pre-filled with CAP), all others are stored.
+// CTA = (group g = (low prefix part l, register group vg), h-block hb of
+// kBlock prefixes); thread = one prefix.  After the enumeration the CTA holds
+// the complete B_p[v] of its prefixes and folds the cross-segment terms of
+// every incoming transition into this chunk's minima (epilogue):
+//    chunkmin_t[u][v][chunk] = min_{p in chunk} X^t_p[u] + B_p[v],
+//    X^t_p[u] = sum_{cross (j, Q)} Q[u][s_j(p)]          (Eq. 3 r_n)
+// with 4x4 register-blocked fused add+mins over the chunk's rows.
 template <typename V, int NB, bool STAGED>
 __global__ void __launch_bounds__(kBlock) enum_kernel(const EnumParams p) {
   using T = VT<V>;
   constexpr int VN = Vec4<V>::N;
   extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int tid = threadIdx.x;
   const int64_t nhb = p.Gpad / kBlock;
-  const int64_t per_g = nhb * p.nM;
-  const int64_t total = p.W * p.VG * per_g;
-  const int64_t i_end = (int64_t)(blockIdx.x + 1) * total / gridDim.x;
-  int64_t i = (int64_t)blockIdx.x * total / gridDim.x;
-  int64_t staged_g = -1;
-  V* xs = reinterpret_cast<V*>(smem_raw);
-  V* ys = xs + p.xspan;
-  V* zs = ys + p.yspan;
-  int4* ms = reinterpret_cast<int4*>(zs + ((p.zspan + 3) & ~3LL));
-  while (i < i_end) {
-    const int64_t g = i / per_g;
-    const int64_t rem = i - g * per_g;
-    const int64_t hb = rem / p.nM;
-    const int64_t m0 = rem - hb * p.nM;
-    const int64_t m1 = min(p.nM, m0 + (i_end - i));
-    const bool partial = m0 > 0 || m1 < p.nM;
-    i += m1 - m0;
-    const int64_t l = g / p.VG;
-    const int vg = (int)(g - l * p.VG);
-    const int64_t hh = hb * kBlock + threadIdx.x;
-    const bool live = hh < p.G;
-    const int64_t pg = (p.h0 + hh) * p.W + l;       // global canonical prefix
-    const int64_t row = hh * p.W + l;               // local canonical prefix
-    // prefix digits -> table offsets (ctx digits live in the low part l, so
-    // sx/sy/sz are uniform over the CTA)
-    int64_t sx = 0, sy = 0, sz = 0;
-    int od = 0;
-    {
-      int64_t q = pg;
-      for (int d = p.P - 1; d >= 0; --d) {
-        const int dig = (int)(q % p.pre_radix[d]);
-        q /= p.pre_radix[d];
-        sx += dig * p.pre_sx[d];
-        sy += dig * p.pre_sy[d];
-        sz += dig * p.pre_sz[d];
-        if (d == p.o_pre) od = dig;
-      }
+  const int64_t g = blockIdx.x / nhb;
+  const int64_t hb = blockIdx.x - g * nhb;
+  const int64_t l = g / p.VG;
+  const int vg = (int)(g - l * p.VG);
+  const int64_t hh = hb * kBlock + tid;
+  const bool live = hh < p.G;
+  const int64_t pg = (p.h0 + hh) * p.W + l;       // global canonical prefix
+  const int64_t row = hh * p.W + l;               // local canonical prefix
+  // prefix digits -> table offsets (ctx digits live in the low part l, so
+  // sx/sy/sz are uniform over the CTA)
+  int64_t sx = 0, sy = 0, sz = 0;
+  int od = 0;
+  if (pg < 0x7FFFFFFF) {
+    uint32_t q = (uint32_t)pg;
+    for (int d = p.P - 1; d >= 0; --d) {
+      const uint32_t r = (uint32_t)p.pre_radix[d];
+      const int dig = (int)(q % r);
+      q /= r;
+      sx += dig * p.pre_sx[d];
+      sy += dig * p.pre_sy[d];
+      sz += dig * p.pre_sz[d];
+      if (d == p.o_pre) od = dig;
     }
-    const V* XT = static_cast<const V*>(p.XT);
-    const V* YT = static_cast<const V*>(p.YT);
-    const V* ZT = static_cast<const V*>(p.ZT);
-    const int4* MT = p.mtab;
-    if constexpr (STAGED) {
-      if (g != staged_g) {
-        __syncthreads();
-        for (int64_t e = threadIdx.x * VN; e < p.xspan; e += kBlock * VN)
-          *reinterpret_cast<typename Vec4<V>::T*>(xs + e) =
-              *reinterpret_cast<const typename Vec4<V>::T*>(XT + sx + e);
-        for (int64_t e = threadIdx.x * VN; e < p.yspan; e += kBlock * VN)
-          *reinterpret_cast<typename Vec4<V>::T*>(ys + e) =
-              *reinterpret_cast<const typename Vec4<V>::T*>(YT + sy + e);
-        for (int64_t e = threadIdx.x; e < p.zspan; e += kBlock) zs[e] = ZT[sz + e];
-        if (staged_g < 0)
-          for (int64_t e = threadIdx.x; e < p.nM; e += kBlock) ms[e] = MT[e];
-        __syncthreads();
-        staged_g = g;
-      }
-      XT = xs; YT = ys; ZT = zs; MT = ms;
-      sx = sy = sz = 0;
+  } else {
+    int64_t q = pg;
+    for (int d = p.P - 1; d >= 0; --d) {
+      const int dig = (int)(q % p.pre_radix[d]);
+      q /= p.pre_radix[d];
+      sx += dig * p.pre_sx[d];
+      sy += dig * p.pre_sy[d];
+      sz += dig * p.pre_sz[d];
+      if (d == p.o_pre) od = dig;
     }
-    if (!live) continue;
-    V* Bp = static_cast<V*>(p.Bp) + row * p.Do;
-    const V k0 = static_cast<const V*>(p.K0)[pg];
-    V acc[NB];
+  }
+  const V* XT = static_cast<const V*>(p.XT);
+  const V* YT = static_cast<const V*>(p.YT);
+  const V* ZT = static_cast<const V*>(p.ZT);
+  const int4* MT = p.mtab;
+  if constexpr (STAGED) {
+    V* xs = reinterpret_cast<V*>(smem_raw);
+    V* ys = xs + p.xspan;
+    V* zs = ys + p.yspan;
+    int4* ms = reinterpret_cast<int4*>(zs + ((p.zspan + 3) & ~3LL));
+    for (int64_t e = tid * VN; e < p.xspan; e += kBlock * VN)
+      *reinterpret_cast<typename Vec4<V>::T*>(xs + e) =
+          *reinterpret_cast<const typename Vec4<V>::T*>(XT + sx + e);
+    for (int64_t e = tid * VN; e < p.yspan; e += kBlock * VN)
+      *reinterpret_cast<typename Vec4<V>::T*>(ys + e) =
+          *reinterpret_cast<const typename Vec4<V>::T*>(YT + sy + e);
+    for (int64_t e = tid; e < p.zspan; e += kBlock) zs[e] = ZT[sz + e];
+    for (int64_t e = tid; e < p.nM; e += kBlock) ms[e] = MT[e];
+    __syncthreads();
+    XT = xs; YT = ys; ZT = zs; MT = ms;
+    sx = sy = sz = 0;
+  }
+  V* Bp = static_cast<V*>(p.Bp) + row * p.Do;
+  V acc[NB];
 #pragma unroll
-    for (int j = 0; j < NB; ++j) acc[j] = T::CAP;
-    const int ybase = vg * NB;
-    for (int64_t m = m0; m < m1; ++m) {
+  for (int j = 0; j < NB; ++j) acc[j] = T::CAP;
+  const int ybase = vg * NB;
+  if (live) {
+    if (p.init_row)
+      for (int v = 0; v < p.Do; ++v) Bp[v] = T::CAP;
+    const V k0 = static_cast<const V*>(p.K0)[pg];
+    for (int64_t m = 0; m < p.nM; ++m) {
       const int4 mt = MT[m];
       const V km = T::sat(k0, ZT[sz + mt.z]);
       const V* yr = YT + sy + mt.y + ybase;
@@ -307,8 +307,7 @@ __global__ void __launch_bounds__(kBlock) enum_kernel(const EnumParams p) {
         V r = acc[0];
 #pragma unroll
         for (int j = 1; j < NB; ++j) r = T::mn(r, acc[j]);
-        if (partial) atomic_min_v<V>(Bp + mt.w, r);
-        else Bp[mt.w] = T::mn(Bp[mt.w], r);
+        Bp[mt.w] = T::mn(Bp[mt.w], r);
 #pragma unroll
         for (int j = 0; j < NB; ++j) acc[j] = T::CAP;
       }
@@ -317,25 +316,114 @@ __global__ void __launch_bounds__(kBlock) enum_kernel(const EnumParams p) {
       if (p.o_bstride == 1 && p.o_bradix == p.nb) {       // B = {o}: slot j <-> v
 #pragma unroll
         for (int j = 0; j < NB; ++j)
-          if (ybase + j < p.nb) {
-            if (partial) atomic_min_v<V>(Bp + ybase + j, acc[j]);
-            else Bp[ybase + j] = acc[j];
-          }
+          if (ybase + j < p.nb) Bp[ybase + j] = acc[j];
       } else {
 #pragma unroll
         for (int j = 0; j < NB; ++j)
           if (ybase + j < p.nb) {
             const int v = ((ybase + j) / p.o_bstride) % p.o_bradix;
-            if (partial) atomic_min_v<V>(Bp + v, acc[j]);
-            else Bp[v] = T::mn(Bp[v], acc[j]);
+            Bp[v] = T::mn(Bp[v], acc[j]);
           }
       }
     } else if (p.o_mode == 2) {
       V r = acc[0];
 #pragma unroll
       for (int j = 1; j < NB; ++j) r = T::mn(r, acc[j]);
-      if (partial) atomic_min_v<V>(Bp + od, r);
-      else Bp[od] = T::mn(Bp[od], r);
+      Bp[od] = r;
+    }
+  }
+  if (p.ntau == 0) return;
+  // ---- epilogue: fold the cross-segment terms of every incoming transition
+  __syncthreads();                                // staged tables no longer needed
+  const bool simple = p.o_mode == 0 && p.o_bstride == 1 && p.o_bradix == p.nb;
+  const int v_lo = simple ? ybase : 0;
+  const int v_cnt = simple ? min(NB, p.nb - ybase) : p.Do;
+  const int VP = (v_cnt + 3) & ~3;
+  V* Bs = reinterpret_cast<V*>(smem_raw);                     // [kBlock][VP]
+  V* Xs = Bs + kBlock * VP;                                   // [kBlock][DinP] (red afterwards)
+  if (simple) {
+#pragma unroll
+    for (int j = 0; j < NB; ++j)
+      if (j < VP) Bs[tid * VP + j] = (live && j < v_cnt) ? acc[j] : T::CAP;
+  } else {
+    for (int j = 0; j < VP; ++j) Bs[tid * VP + j] = (live && j < v_cnt) ? Bp[j] : T::CAP;
+  }
+  const V* vals = static_cast<const V*>(p.vals);
+  const int64_t chunk = l * nhb + hb;
+  int dinp_max = 4;
+  for (int t = 0; t < p.ntau; ++t) dinp_max = max(dinp_max, (p.taus[t].Din + 3) & ~3);
+  for (int t = 0; t < p.ntau; ++t) {
+    const EpiTau& et = p.taus[t];
+    const int Din = et.Din, DinP = (Din + 3) & ~3;
+    for (int u = 0; u < DinP; ++u) Xs[tid * DinP + u] = T::CAP;
+    if (live) {
+      for (int u = 0; u < Din; ++u) Xs[tid * DinP + u] = 0;
+      for (int i = 0; i < et.nq; ++i) {
+        const Term& q = et.q[i];
+        const int dig = pg < 0x7FFFFFFF
+                            ? (int)(((uint32_t)pg / (uint32_t)p.pre_stride[q.a]) % (uint32_t)p.pre_radix[q.a])
+                            : (int)((pg / p.pre_stride[q.a]) % p.pre_radix[q.a]);
+        const V* Q = vals + q.off + dig;
+        for (int u = 0; u < Din; ++u) Xs[tid * DinP + u] = T::sat(Xs[tid * DinP + u], Q[(int64_t)u * q.db]);
+      }
+    }
+    __syncthreads();
+    const int nblk = (DinP / 4) * (VP / 4);
+    const int stripes = nblk >= kBlock ? 1 : min(8, kBlock / nblk);
+    V res[4][4];
+    int u0 = 0, v0 = 0;
+    const int gi = tid / nblk;
+    const bool active = nblk >= kBlock ? tid < nblk : gi < stripes;
+    // (nblk > kBlock handled by the loop below)
+    for (int blk = (nblk >= kBlock ? tid : tid - gi * nblk); active && blk < nblk;
+         blk += (nblk >= kBlock ? kBlock : nblk)) {
+      u0 = (blk / (VP / 4)) * 4;
+      v0 = (blk % (VP / 4)) * 4;
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) res[i][j] = T::CAP;
+      const int rs = stripes > 1 ? gi : 0;
+      for (int r = rs; r < kBlock; r += stripes) {
+        V x[4], y[4];
+        load_vec<V>(Xs + r * DinP + u0, x);
+        if (VN == 2) load_vec<V>(Xs + r * DinP + u0 + 2, x + 2);
+        load_vec<V>(Bs + r * VP + v0, y);
+        if (VN == 2) load_vec<V>(Bs + r * VP + v0 + 2, y + 2);
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) res[i][j] = T::addmin(x[i], y[j], res[i][j]);
+      }
+      if (nblk >= kBlock) {                         // one stripe: write straight out
+        V* out = static_cast<V*>(et.chunkmin);
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int j = 0; j < 4; ++j)
+            if (u0 + i < Din && v0 + j < v_cnt)
+              out[((int64_t)(u0 + i) * p.Do + v_lo + v0 + j) * p.nchunks + chunk] = res[i][j];
+      }
+      if (stripes > 1) break;
+    }
+    __syncthreads();                                 // Xs free -> stripe partials
+    if (nblk < kBlock) {
+      V* red = stripes * VP <= kBlock ? Xs : Xs + kBlock * dinp_max;   // [stripes][DinP][VP]
+      if (active) {
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) red[(gi * DinP + u0 + i) * VP + v0 + j] = res[i][j];
+      }
+      __syncthreads();
+      V* out = static_cast<V*>(et.chunkmin);
+      for (int e = tid; e < Din * v_cnt; e += kBlock) {
+        const int u = e / v_cnt, vv = e - u * v_cnt;
+        V m = red[u * VP + vv];
+        for (int s = 1; s < stripes; ++s) m = T::mn(m, red[(s * DinP + u) * VP + vv]);
+        out[((int64_t)u * p.Do + v_lo + vv) * p.nchunks + chunk] = m;
+      }
+      __syncthreads();
     }
   }
 }
@@ -365,106 +453,197 @@ __device__ __forceinline__ void load4(const V* p, V* out) {
   }
 }
 
-// Chunk c = CH consecutive local canonical prefixes.  Each thread owns a 4x4
-// (u, v) block over a subset of the chunk's prefixes (two 4-wide shared loads
-// per 16 fused add+mins), partial minima are reduced over the subsets.
-// Output layout: chunkmin[(u * Do + v) * nchunks + c] (coalesced for the
-// per-pair reduction that follows).
+// Persistent fold over all transitions into one segment type (they share
+// B_p).  The local prefixes are cut into chunks of CH rows; CTA c owns a
+// contiguous run of chunks.  Per chunk: B_p rows arrive by double-buffered
+// TMA bulk copies; X_p[u] is built from the prefix's digit structure -- rows
+// sharing all but the last prefix digit ("group") share Xhi[u] = the cross
+// terms on the other digits, so X_p[u] = Xhi[u] + sum of the last-digit terms
+// (1-2 shared loads per entry); then each thread folds a 4x4 (u, v) block
+// over a stripe of the rows (two 4-wide shared loads per 16 fused add+mins)
+// and the stripes are reduced into chunkmin_t[(u * Do + v) * nchunks + chunk].
 template <typename V>
-__global__ void __launch_bounds__(256) fold_kernel(const FoldParams f) {
+__global__ void __launch_bounds__(256) fold_kernel(const FoldMulti fm) {
   using T = VT<V>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  const int DinP = (f.Din + 3) & ~3, DoP = (f.Do + 3) & ~3;
-  V* bs = reinterpret_cast<V*>(smem_raw);          // [CH][DoP]
-  V* xs = bs + (int64_t)f.CH * DoP;                 // [CH][DinP]
-  V* red = xs + (int64_t)f.CH * DinP;               // [groups][DinP*DoP]
-  const int nblk = (DinP / 4) * (DoP / 4);
-  const int groups = max(1, min((int)(blockDim.x / nblk), 8));
-  int32_t* dg = reinterpret_cast<int32_t*>(red + (int64_t)groups * DinP * DoP);   // [CH][nq]
-  V* qs = reinterpret_cast<V*>(dg + ((f.CH * f.nq + 3) & ~3));                   // cross tables
-  __shared__ __align__(8) uint64_t mbar;
-  const int64_t c = blockIdx.x;
-  const int64_t p0 = c * f.CH;
-  const int n = (int)min((int64_t)f.CH, f.nPl - p0);
-  const V* Bp = static_cast<const V*>(f.Bp);
-  const V* vals = static_cast<const V*>(f.vals);
-  const bool tma = f.tma && DoP == f.Do;
-  if (tma) {
-    if (threadIdx.x == 0) mbar_init(&mbar, 1);
-    __syncthreads();
-    if (threadIdx.x == 0) {                  // one bulk copy of the chunk's B_p rows
-      const uint32_t bytes = (uint32_t)((int64_t)n * f.Do * sizeof(V));
-      mbar_expect_tx(&mbar, bytes);
-      tma_bulk_g2s(bs, Bp + p0 * f.Do, bytes, &mbar);
-    }
-  } else {
-    for (int e = threadIdx.x; e < n * DoP; e += blockDim.x) {
-      const int pi = e / DoP, v = e % DoP;
-      bs[e] = v < f.Do ? Bp[(p0 + pi) * f.Do + v] : T::CAP;
-    }
-  }
-  for (int e = threadIdx.x; e < n * f.nq; e += blockDim.x) {
-    const int pi = e / f.nq, i = e % f.nq;
-    dg[e] = prefix_digit(f.p_lo + p0 + pi, f.q[i].a, f.P, f.pre_radix);
-  }
-  {
+  const FoldSmem L = fold_layout(fm, (int)sizeof(V));
+  const FoldParams& f0 = fm.f[0];
+  const int Do = f0.Do, DoP = L.DoP, CH = L.CH, Dl = L.Dl, P = f0.P;
+  V* bs = reinterpret_cast<V*>(smem_raw + L.bs);
+  __shared__ __align__(8) uint64_t mbar[2];
+  const int tid = threadIdx.x;
+  const int64_t nch = f0.nchunks;
+  const int64_t c_lo = blockIdx.x * nch / gridDim.x, c_hi = (blockIdx.x + 1) * nch / gridDim.x;
+  const V* Bp = static_cast<const V*>(f0.Bp);
+  const V* vals = static_cast<const V*>(f0.vals);
+  const bool tma = f0.tma && DoP == Do;
+  for (int t = 0; t < fm.ntau; ++t) {                 // Q tables -> smem
+    const FoldParams& f = fm.f[t];
+    V* qs = reinterpret_cast<V*>(smem_raw + L.qs[t]);
     int qo = 0;
     for (int i = 0; i < f.nq; ++i) {
       const int ne = f.Din * f.q[i].db;
-      for (int e = threadIdx.x; e < ne; e += blockDim.x) qs[qo + e] = vals[f.q[i].off + e];
+      for (int e = tid; e < ne; e += 256) qs[qo + e] = vals[f.q[i].off + e];
       qo += ne;
     }
   }
+  if (tma && tid == 0) { mbar_init(&mbar[0], 1); mbar_init(&mbar[1], 1); }
   __syncthreads();
-  for (int e = threadIdx.x; e < n * DinP; e += blockDim.x) {
-    const int pi = e / DinP, u = e % DinP;
-    V x = T::CAP;
-    if (u < f.Din) {
-      x = 0;
-      int qo = 0;
-      for (int i = 0; i < f.nq; ++i) {
-        x = T::sat(x, qs[qo + u * f.q[i].db + dg[pi * f.nq + i]]);
-        qo += f.Din * f.q[i].db;
+  for (int t = 0; t < fm.ntau; ++t) {                 // QL[u][s]: cross terms on the last digit
+    const FoldParams& f = fm.f[t];
+    const V* qs = reinterpret_cast<const V*>(smem_raw + L.qs[t]);
+    V* ql = reinterpret_cast<V*>(smem_raw + L.ql[t]);      // [s][u] (u contiguous)
+    for (int e = tid; e < L.DinP[t] * Dl; e += 256) {
+      const int s = e / L.DinP[t], u = e - s * L.DinP[t];
+      V x = u < f.Din ? (V)0 : T::CAP;
+      if (u < f.Din) {
+        int qo = 0;
+        for (int i = 0; i < f.nq; ++i) {
+          if (f.q[i].a == P - 1) x = T::sat(x, qs[qo + u * f.q[i].db + s]);
+          qo += f.Din * f.q[i].db;
+        }
+      }
+      ql[e] = x;
+    }
+  }
+  int32_t* rg = reinterpret_cast<int32_t*>(smem_raw + L.rows);
+  int32_t* rs = rg + CH;
+  int32_t* gdig = reinterpret_cast<int32_t*>(smem_raw + L.gdig);
+  auto rows_of = [&](int64_t ch) { return (int)min((int64_t)CH, f0.nPl - ch * CH); };
+  auto issue = [&](int64_t ch, int buf) {             // B_p rows of chunk ch -> bs[buf]
+    const int64_t p0 = ch * CH;
+    const int n = rows_of(ch);
+    V* dst = bs + (int64_t)buf * CH * DoP;
+    if (tma) {
+      if (tid == 0) {
+        const uint32_t bytes = (uint32_t)((int64_t)n * Do * sizeof(V));
+        mbar_expect_tx(&mbar[buf], bytes);
+        tma_bulk_g2s(dst, Bp + p0 * Do, bytes, &mbar[buf]);
+      }
+    } else {
+      for (int e = tid; e < n * DoP; e += 256) {
+        const int pi = e / DoP, v = e - pi * DoP;
+        dst[e] = v < Do ? Bp[(p0 + pi) * Do + v] : T::CAP;
       }
     }
-    xs[e] = x;
-  }
-  if (tma) mbar_wait(&mbar, 0);
-  __syncthreads();
-  auto do_block = [&](int blk, int pstart, int pstep, V* r) {
-    const int u0 = (blk / (DoP / 4)) * 4, v0 = (blk % (DoP / 4)) * 4;
-    V acc[4][4];
-#pragma unroll
-    for (int a = 0; a < 4; ++a)
-#pragma unroll
-      for (int b = 0; b < 4; ++b) acc[a][b] = T::CAP;
-    for (int pi = pstart; pi < n; pi += pstep) {
-      V x[4], y[4];
-      load4<V>(xs + pi * DinP + u0, x);
-      load4<V>(bs + pi * DoP + v0, y);
-#pragma unroll
-      for (int a = 0; a < 4; ++a)
-#pragma unroll
-        for (int b = 0; b < 4; ++b) acc[a][b] = T::addmin(x[a], y[b], acc[a][b]);
-    }
-#pragma unroll
-    for (int a = 0; a < 4; ++a)
-#pragma unroll
-      for (int b = 0; b < 4; ++b) r[(u0 + a) * DoP + v0 + b] = acc[a][b];
   };
-  if (groups > 1) {
-    const int gi = threadIdx.x / nblk;
-    if (gi < groups) do_block(threadIdx.x % nblk, gi, groups, red + (int64_t)gi * DinP * DoP);
-  } else {
-    for (int blk = threadIdx.x; blk < nblk; blk += blockDim.x) do_block(blk, 0, 1, red);
-  }
-  __syncthreads();
-  V* out = static_cast<V*>(f.chunkmin);
-  for (int e = threadIdx.x; e < f.Din * f.Do; e += blockDim.x) {
-    const int u = e / f.Do, v = e % f.Do;
-    V m = red[u * DoP + v];
-    for (int g2 = 1; g2 < groups; ++g2) m = T::mn(m, red[(int64_t)g2 * DinP * DoP + u * DoP + v]);
-    out[(int64_t)e * f.nchunks + c] = m;
+  if (c_lo < c_hi) issue(c_lo, 0);
+  uint32_t phases = 0;                               // bit b = parity of mbar[b]
+  const int gi = tid / L.nblk_all;
+  for (int64_t ch = c_lo; ch < c_hi; ++ch) {
+    const int buf = (int)((ch - c_lo) & 1);
+    const int64_t p0 = ch * CH;
+    const int n = rows_of(ch);
+    if (ch + 1 < c_hi) issue(ch + 1, buf ^ 1);         // buffer freed by the previous chunk's last sync
+    const int64_t pg0 = f0.p_lo + p0;
+    const int64_t grp0 = pg0 / Dl;
+    const int ng = (int)((pg0 + n - 1) / Dl - grp0 + 1);
+    // per row: (group, last digit); per group: the digits the other cross terms read
+    const int s0 = (int)(pg0 - grp0 * Dl);          // last digit of the chunk's first row
+    for (int pi = tid; pi < n; pi += 256) {
+      const int g = (s0 + pi) / Dl;
+      rg[pi] = g;
+      rs[pi] = s0 + pi - g * Dl;
+    }
+    for (int t = 0, col = 0; t < fm.ntau; ++t)
+      for (int i = 0; i < fm.f[t].nq; ++i, ++col) {
+        const int a = fm.f[t].q[i].a;
+        if (a >= P - 1) continue;
+        const int64_t st = f0.pre_stride[a] / Dl;
+        for (int g = tid; g < ng; g += 256) {
+          const int64_t ghi = grp0 + g;             // prefix value without its last digit
+          gdig[g * kMaxFoldTau * kMaxCross + col] =
+              (ghi < 0x7FFFFFFF && st < 0x7FFFFFFF)
+                  ? (int)(((uint32_t)ghi / (uint32_t)st) % (uint32_t)f0.pre_radix[a])
+                  : (int)((ghi / st) % f0.pre_radix[a]);
+        }
+      }
+    __syncthreads();
+    for (int t = 0, col0 = 0; t < fm.ntau; ++t) {     // Xhi[g][u]
+      const FoldParams& f = fm.f[t];
+      V* xh = reinterpret_cast<V*>(smem_raw + L.xh[t]);
+      const V* qs = reinterpret_cast<const V*>(smem_raw + L.qs[t]);
+      for (int g = tid >> 5; g < ng; g += 8)
+        for (int u = tid & 31; u < L.DinP[t]; u += 32) {
+          V x = u < f.Din ? (V)0 : T::CAP;
+          if (u < f.Din) {
+            int qo = 0;
+            for (int i = 0; i < f.nq; ++i) {
+              if (f.q[i].a < P - 1)
+                x = T::sat(x, qs[qo + u * f.q[i].db + gdig[g * kMaxFoldTau * kMaxCross + col0 + i]]);
+              qo += f.Din * f.q[i].db;
+            }
+          }
+          xh[g * L.DinP[t] + u] = x;
+        }
+      col0 += f.nq;
+    }
+    __syncthreads();
+    for (int t = 0; t < fm.ntau; ++t) {                // X_p[u] = Xhi[g][u] + QL[s][u], 4 u at a time
+      V* xs = reinterpret_cast<V*>(smem_raw + L.xs[t]);
+      const V* xh = reinterpret_cast<const V*>(smem_raw + L.xh[t]);
+      const V* ql = reinterpret_cast<const V*>(smem_raw + L.ql[t]);
+      const int DinP = L.DinP[t], nq4 = DinP / 4;
+      for (int e = tid; e < n * nq4; e += 256) {
+        const int pi = e / nq4, u0 = (e - pi * nq4) * 4;
+        V a[4], b[4];
+        load4<V>(xh + rg[pi] * DinP + u0, a);
+        load4<V>(ql + rs[pi] * DinP + u0, b);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) xs[pi * DinP + u0 + i] = T::sat(a[i], b[i]);
+      }
+    }
+    if (tma) { mbar_wait(&mbar[buf], (phases >> buf) & 1u); phases ^= 1u << buf; }
+    __syncthreads();
+    const V* b = bs + (int64_t)buf * CH * DoP;
+    auto fold_block = [&](int gblk, int pstart, int pstep, int grp) {
+      int t = 0;
+      while (t + 1 < fm.ntau && gblk >= L.blk0[t + 1]) ++t;
+      const int blk = gblk - L.blk0[t];
+      const int DinP = L.DinP[t];
+      const V* xs = reinterpret_cast<const V*>(smem_raw + L.xs[t]);
+      V* red = reinterpret_cast<V*>(smem_raw + L.red[t]) + (int64_t)grp * DinP * DoP;
+      const int u0 = (blk / (DoP / 4)) * 4, v0 = (blk % (DoP / 4)) * 4;
+      V acc[4][4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = T::CAP;
+      const V* xp = xs + pstart * DinP + u0;
+      const V* bp = b + pstart * DoP + v0;
+      for (int pi = pstart; pi < n; pi += pstep, xp += pstep * DinP, bp += pstep * DoP) {
+        V x[4], y[4];
+        load4<V>(xp, x);
+        load4<V>(bp, y);
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) acc[i][j] = T::addmin(x[i], y[j], acc[i][j]);
+      }
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) red[(u0 + i) * DoP + v0 + j] = acc[i][j];
+    };
+    if (L.groups > 1) {
+      if (gi < L.groups) fold_block(tid - gi * L.nblk_all, gi, L.groups, gi);
+    } else {
+      for (int gb = tid; gb < L.nblk_all; gb += 256) fold_block(gb, 0, 1, 0);
+    }
+    __syncthreads();
+    for (int t = 0; t < fm.ntau; ++t) {              // stripes -> this chunk's minima
+      const FoldParams& f = fm.f[t];
+      const V* red = reinterpret_cast<const V*>(smem_raw + L.red[t]);
+      V* out = static_cast<V*>(f.chunkmin);
+      const int DinP = L.DinP[t];
+      for (int u = tid >> 5; u < f.Din; u += 8)
+        for (int v = tid & 31; v < Do; v += 32) {
+          V m = red[u * DoP + v];
+          for (int g2 = 1; g2 < L.groups; ++g2) m = T::mn(m, red[(int64_t)g2 * DinP * DoP + u * DoP + v]);
+          out[(int64_t)(u * Do + v) * nch + ch] = m;
+        }
+    }
+    __syncthreads();
   }
 }
 
@@ -600,6 +779,138 @@ __global__ void __launch_bounds__(256) suffix_argmin_kernel(const ArgminParams a
 }
 
 // --------------------------------------------------------------------------
+// Fused least-index argmin, one CTA (128 threads) per bucket (u, v):
+//  1. A = min over the chunk minima and the first chunk c* attaining it;
+//  2. the least prefix p* in chunk c* with X_p[u] + B_p[v] == A;
+//  3. the least suffix (canonical order; s_o = v when o is a suffix digit)
+//     whose intra cost equals B_p*[v];
+//  4. outputs in the caller's (unpruned) layout: A[u][v_orig], I[u][v_orig].
+// --------------------------------------------------------------------------
+template <typename V>
+__global__ void __launch_bounds__(128) argmin_kernel(const ArgminParams ap, const V* __restrict__ vals) {
+  const FoldParams& f = ap.f;
+  const EvalSpec& e = ap.e;
+  constexpr int NT = 128;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  uint16_t* sd = reinterpret_cast<uint16_t*>(smem_raw);        // [K][NT] digits
+  __shared__ V s_best[4];
+  __shared__ int64_t s_bc[4];
+  __shared__ unsigned long long s_first;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int pair = blockIdx.x;
+  const int u = pair / f.Do, v = pair - (pair / f.Do) * f.Do;
+  const int64_t outi = (int64_t)u * ap.Do_orig + ap.vmap[v];
+  // 1. chunk minima of this pair are contiguous
+  const V* cm = static_cast<const V*>(f.chunkmin) + (int64_t)pair * f.nchunks;
+  V best = VT<V>::CAP;
+  int64_t bc = INT64_MAX;
+  for (int64_t c = tid; c < f.nchunks; c += NT) {
+    const V x = cm[c];
+    if (x < best) { best = x; bc = c; }
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    const V ob = __shfl_xor_sync(0xffffffffu, best, o);
+    const int64_t oc = __shfl_xor_sync(0xffffffffu, bc, o);
+    if (ob < best || (ob == best && oc < bc)) { best = ob; bc = oc; }
+  }
+  if (lane == 0) { s_best[warp] = best; s_bc[warp] = bc; }
+  if (tid == 0) s_first = ~0ull;
+  __syncthreads();
+  best = s_best[0];
+  bc = s_bc[0];
+  for (int w = 1; w < NT / 32; ++w)
+    if (s_best[w] < best || (s_best[w] == best && s_bc[w] < bc)) { best = s_best[w]; bc = s_bc[w]; }
+  if (best >= VT<V>::CAP) {
+    if (tid == 0) { ap.A_out[outi] = kInf64; ap.I_out[outi] = kInf64; }
+    return;
+  }
+  // 2. least canonical prefix over every chunk attaining the minimum
+  //    (chunk c = (l, hb) holds local rows (hb * kBlock + i) * W + l)
+  const V* Bp = static_cast<const V*>(f.Bp);
+  __shared__ int64_t s_list[NT];
+  __shared__ int s_cnt;
+  for (int64_t base = 0; base < f.nchunks; base += NT) {
+    if (tid == 0) s_cnt = 0;
+    __syncthreads();
+    const int64_t c = base + tid;
+    if (c < f.nchunks && cm[c] == best) s_list[atomicAdd(&s_cnt, 1)] = c;
+    __syncthreads();
+    const int cnt = s_cnt;
+    for (int li = 0; li < cnt; ++li) {
+      const int64_t cc = s_list[li];
+      const int64_t l = cc / f.nhb, hb = cc - l * f.nhb;
+      for (int i = tid; i < kBlock; i += NT) {
+        const int64_t hh = hb * kBlock + i;
+        if (hh >= f.G) break;
+        const int64_t plr = hh * f.W + l;
+        const V x = cross_sum<V>(f, vals, f.p_lo + plr, u);
+        if (VT<V>::sat(x, Bp[plr * f.Do + v]) == best) {
+          atomicMin(&s_first, (unsigned long long)plr);   // local order == canonical order
+          break;
+        }
+      }
+    }
+    __syncthreads();
+  }
+  const int64_t pl = (int64_t)s_first;
+  __syncthreads();
+  if (tid == 0) s_first = ~0ull;
+  const uint64_t target = (uint64_t)Bp[pl * f.Do + v];
+  const int64_t pg = f.p_lo + pl;
+  auto S = [&](int d) -> uint16_t& { return sd[d * NT + tid]; };
+  {
+    int64_t q = pg;
+    for (int d = e.P - 1; d >= 0; --d) { S(d) = (uint16_t)(q % e.radix[d]); q /= e.radix[d]; }
+  }
+  const bool o_suffix = e.o >= e.P;
+  const int64_t nrest = o_suffix ? e.nsuffix / e.radix[e.o] : e.nsuffix;
+  __syncthreads();
+  // 3. least suffix with intra cost == B_p*[v]
+  const int64_t per = (nrest + NT - 1) / NT;
+  const int64_t lo = (int64_t)tid * per;
+  const int64_t hi = min(nrest, lo + per);
+  if (lo < hi) {
+    int64_t q = lo;
+    for (int d = e.K - 1; d >= e.P; --d) {
+      if (o_suffix && d == e.o) { S(d) = (uint16_t)v; continue; }
+      S(d) = (uint16_t)(q % e.radix[d]);
+      q /= e.radix[d];
+    }
+    for (int64_t r = lo; r < hi; ++r) {
+      uint64_t c = 0;
+      bool inf = false;
+      for (int i = 0; i < e.nterm; ++i) {
+        const Term& tm = e.term[i];
+        const V x = tm.kind == 0 ? vals[tm.off + S(tm.a)] : vals[tm.off + (int)S(tm.a) * tm.db + S(tm.b)];
+        inf |= x >= VT<V>::CAP;
+        c += (uint64_t)x;
+      }
+      if (!inf && c == target) {
+        int64_t sfx = 0;
+        for (int d = e.P; d < e.K; ++d) sfx = sfx * e.radix[d] + S(d);
+        atomicMin(&s_first, (unsigned long long)sfx);
+        break;
+      }
+      for (int d = e.K - 1; d >= e.P; --d) {       // odometer step
+        if (o_suffix && d == e.o) continue;
+        if (++S(d) < e.radix[d]) break;
+        S(d) = 0;
+      }
+    }
+  }
+  __syncthreads();
+  if (tid == 0) {
+    const uint64_t sfx = s_first;
+    uint64_t q = sfx;
+    for (int d = e.K - 1; d >= e.P; --d) { S(d) = (uint16_t)(q % e.radix[d]); q /= e.radix[d]; }
+    uint64_t idx = 0;
+    for (int d = 0; d < e.K; ++d) idx = idx * ap.orig_radix[d] + ap.maps[ap.map_off[d] + S(d)];
+    ap.A_out[outi] = (uint64_t)best;
+    ap.I_out[outi] = sfx == ~0ull ? kInf64 : idx;     // ~0: cannot happen (exact arithmetic)
+  }
+}
+
+// --------------------------------------------------------------------------
 // a3 + a4: chain (single CTA).  G_N = terminal; runs processed last to first;
 // a run of L identical square matrices uses powers P_j = M^(2^j) (repeated
 // squaring) and fills its suffix vectors by doubling:
@@ -653,16 +964,25 @@ __global__ void __launch_bounds__(1024) chain_kernel(const ChainParams cp) {
   uint64_t* Pw = SM ? sP : cp.powers;
   const int64_t* goff = SM ? sgoff : cp.goff;
   if constexpr (SM) {
-    for (int m = 0; m < cp.nmat; ++m) {
-      const ChainInst mi = cp.mats[m];
-      const int64_t n = (int64_t)mi.rows * mi.cols;
-      for (int64_t e = tid; e < n; e += nth) {
-        sA[cp.moff[m] + e] = mi.A[e];
-        if (cp.backtrack) sI[cp.moff[m] + e] = mi.I[e];
+    __shared__ __align__(8) uint64_t cbar;
+    const bool tma = (cp.mat_elems & 1) == 0;          // 16-byte multiples
+    if (tma) {
+      if (tid == 0) {
+        mbar_init(&cbar, 1);
+        const uint32_t bytes = (uint32_t)(cp.mat_elems * 8);
+        mbar_expect_tx(&cbar, bytes * (cp.backtrack ? 2 : 1));
+        tma_bulk_g2s(sA, cp.baseA, bytes, &cbar);
+        if (cp.backtrack) tma_bulk_g2s(sI, cp.baseI, bytes, &cbar);
+      }
+    } else {
+      for (int64_t e = tid; e < cp.mat_elems; e += nth) {
+        sA[e] = cp.baseA[e];
+        if (cp.backtrack) sI[e] = cp.baseI[e];
       }
     }
     for (int i = tid; i < N + 2; i += nth) sgoff[i] = cp.goff[i];
     for (int i = tid; i < N; i += nth) sinst[i] = make_int4(cp.inst[i].mat, cp.inst[i].rows, cp.inst[i].cols, 0);
+    if (tma) mbar_wait(&cbar, 0);
     __syncthreads();
   }
   mark();
@@ -737,11 +1057,54 @@ __global__ void __launch_bounds__(1024) chain_kernel(const ChainParams cp) {
   if constexpr (SM)
     for (int64_t e2 = tid; e2 < goff[N + 1]; e2 += nth) cp.G[e2] = G[e2];
   if (!cp.backtrack) return;
-  // forward greedy (warp 0): among optimal successors the least index
+  // forward greedy: at each instance the optimal successor with the least
+  // combination index.  SM mode: the successor of every (n, u) is tabulated in
+  // parallel first, then the walk from u_1 = 0 is a chain of shared loads.
   __shared__ int s_status;
   if (tid == 0) s_status = 0;
   __syncthreads();
-  if (tid < 32) {
+  if constexpr (SM) {
+    int16_t* nxt = reinterpret_cast<int16_t*>(sinst + N);   // [goff[N]] successor of (n, u)
+    const int smax = cp.smax;
+    for (int64_t w = tid; w < (int64_t)N * smax; w += nth) {
+      const int n = (int)(w / smax), u = (int)(w - (int64_t)n * smax);   // instance n + 1
+      if (u >= rows_of(n)) continue;
+      const uint64_t* A = matA(n);
+      const uint64_t* I = matI(n);
+      const int cols = cols_of(n);
+      const uint64_t target = G[goff[n] + u];
+      const uint64_t* Gn = G + goff[n + 1];
+      uint64_t bi = kInf64;
+      int bv = -1;
+      if (target != kInf64)
+        for (int v = 0; v < cols; ++v) {
+          const uint64_t a = A[(int64_t)u * cols + v];
+          if (a == kInf64 || Gn[v] == kInf64 || a + Gn[v] != target) continue;
+          const uint64_t ix = I[(int64_t)u * cols + v];
+          if (bv < 0 || ix < bi) { bi = ix; bv = v; }
+        }
+      nxt[goff[n] + u] = (int16_t)bv;
+    }
+    __syncthreads();
+    mark();
+    if (tid == 0) {
+      if (G[0] == kInf64) {
+        s_status = 3;
+        *cp.total = kInf64;
+      } else {
+        *cp.total = G[0];
+        int u = 0;
+        for (int n = 0; n < N; ++n) {
+          const int v = nxt[goff[n] + u];
+          if (v < 0) { s_status = 3; break; }
+          const int cols = cols_of(n);
+          cp.seg_index[n] = matI(n)[(int64_t)u * cols + v];
+          cp.seg_ns[n] = matA(n)[(int64_t)u * cols + v];
+          u = v;
+        }
+      }
+    }
+  } else if (tid < 32) {
     const int lane = tid;
     int u = 0;
     if (G[0] == kInf64) {
@@ -911,21 +1274,15 @@ cudaError_t launch_fill(V* p, int64_t n, V v, cudaStream_t st) {
 template <typename V, int NB>
 cudaError_t launch_enum_nb(const EnumParams& p, int64_t nthreads, size_t smem, cudaStream_t st) {
   (void)nthreads;
-  const int64_t total = p.W * p.VG * (p.Gpad / kBlock) * p.nM;
-  if (total <= 0) return cudaSuccess;
+  const int64_t blocks = p.W * p.VG * (p.Gpad / kBlock);
+  if (blocks <= 0) return cudaSuccess;
+  const size_t sm = std::max(smem, (size_t)p.smem_epi);
   auto launch = [&](auto kern) -> cudaError_t {
-    if (smem > 48 * 1024) {
-      cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (sm > 48 * 1024) {
+      cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
       if (e != cudaSuccess) return e;
     }
-    int dev = 0, sms = 148, occ = 1;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kBlock, smem);
-    if (occ < 1) occ = 1;
-    int64_t grid = (int64_t)sms * occ;
-    if (grid > total) grid = total;
-    kern<<<(unsigned)grid, kBlock, smem, st>>>(p);
+    kern<<<(unsigned)blocks, kBlock, sm, st>>>(p);
     return cudaGetLastError();
   };
   if (p.staged) return launch(enum_kernel<V, NB, true>);
@@ -946,34 +1303,25 @@ cudaError_t launch_enum(const EnumParams& p, int NB, int64_t nthreads, size_t sm
 }
 
 template <typename V>
-cudaError_t launch_fold(const FoldParams& f, cudaStream_t st) {
-  const int DinP = (f.Din + 3) & ~3, DoP = (f.Do + 3) & ~3;
-  const int nblk = (DinP / 4) * (DoP / 4);
-  const int groups = std::max(1, std::min(256 / nblk, 8));
-  const size_t smem = (size_t)f.CH * (DoP + DinP) * sizeof(V) + (size_t)groups * DinP * DoP * sizeof(V) +
-                      (size_t)((f.CH * f.nq + 3) & ~3) * 4 + (size_t)f.qelems * sizeof(V) + 16;
+cudaError_t launch_fold(const FoldMulti& fm, int grid, cudaStream_t st) {
+  const FoldSmem L = fold_layout(fm, (int)sizeof(V));
+  const size_t smem = (size_t)L.total;
   auto k = fold_kernel<V>;
   if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
   }
-  k<<<(unsigned)f.nchunks, 256, smem, st>>>(f);
+  k<<<(unsigned)grid, 256, smem, st>>>(fm);
   CFP_LAUNCH_CHECK();
   return cudaSuccess;
 }
 
 template <typename V>
 cudaError_t launch_argmin(const ArgminParams& ap, V* Aval, const V* vals, cudaStream_t st) {
+  (void)Aval;
   const int pairs = ap.f.Din * ap.f.Do;
-  fold_reduce_kernel<V><<<(pairs * 32 + 255) / 256, 256, 0, st>>>(ap.f, Aval, ap.pstar);
-  CFP_LAUNCH_CHECK();
-  const size_t smem = (size_t)((ap.e.tab_n + 1) & ~1) * sizeof(V) + (size_t)ap.e.K * 256 * 2 + 16;
-  if (smem > 48 * 1024) {
-    cudaError_t e = cudaFuncSetAttribute(suffix_argmin_kernel<V>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)smem);
-    if (e != cudaSuccess) return e;
-  }
-  suffix_argmin_kernel<V><<<pairs, 256, smem, st>>>(ap, Aval, vals);
+  const size_t smem = (size_t)ap.e.K * 128 * 2 + 16;
+  argmin_kernel<V><<<pairs, 128, smem, st>>>(ap, vals);
   CFP_LAUNCH_CHECK();
   return cudaSuccess;
 }
@@ -1024,8 +1372,8 @@ template cudaError_t launch_fill<uint32_t>(uint32_t*, int64_t, uint32_t, cudaStr
 template cudaError_t launch_fill<uint64_t>(uint64_t*, int64_t, uint64_t, cudaStream_t);
 template cudaError_t launch_enum<uint32_t>(const EnumParams&, int, int64_t, size_t, cudaStream_t);
 template cudaError_t launch_enum<uint64_t>(const EnumParams&, int, int64_t, size_t, cudaStream_t);
-template cudaError_t launch_fold<uint32_t>(const FoldParams&, cudaStream_t);
-template cudaError_t launch_fold<uint64_t>(const FoldParams&, cudaStream_t);
+template cudaError_t launch_fold<uint32_t>(const FoldMulti&, int, cudaStream_t);
+template cudaError_t launch_fold<uint64_t>(const FoldMulti&, int, cudaStream_t);
 template cudaError_t launch_argmin<uint32_t>(const ArgminParams&, uint32_t*, const uint32_t*, cudaStream_t);
 template cudaError_t launch_argmin<uint64_t>(const ArgminParams&, uint64_t*, const uint64_t*, cudaStream_t);
 

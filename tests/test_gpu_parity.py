@@ -143,6 +143,28 @@ def test_minplus_product(ctx, oracle_lib, seed):
     assert np.array_equal(C0, C1) and np.array_equal(a0, a1)
 
 
+@pytest.mark.parametrize("shape,maxv", [((130, 257, 129), 1 << 20), ((64, 300, 200), 1 << 40),
+                                         ((1, 500, 3), 1000), ((200, 17, 1), 1 << 29)])
+def test_minplus_product_tiled(ctx, oracle_lib, shape, maxv):
+    """Multi-tile (min,+) products with ragged edges, narrow (< 2^31) and
+    wide (2^40) values, INF entries, least-k argmin."""
+    rng = np.random.default_rng(sum(shape))
+    m, k, n = shape
+    A = rng.integers(0, maxv, (m, k), dtype=np.uint64)
+    B = rng.integers(0, maxv, (k, n), dtype=np.uint64)
+    A[rng.random(A.shape) < 0.1] = np.uint64(INF64)
+    B[rng.random(B.shape) < 0.1] = np.uint64(INF64)
+    B[:, 0] = np.uint64(INF64)                      # an all-INF column
+    C0, a0 = oracle_lib.minplus(A, B)
+    C1, a1 = ctx.minplus_product(A, B)
+    assert np.array_equal(C0, C1) and np.array_equal(a0, a1)
+
+
+def test_minplus_bench_runs(ctx):
+    ms, ops = ctx.minplus_bench(256, wide=False, argk=False, iters=2)
+    assert ms > 0 and ops > 0
+
+
 @pytest.mark.parametrize("seed", range(10))
 def test_minplus_chain_runs(ctx, oracle_lib, seed):
     rng = np.random.default_rng(100 + seed)
@@ -154,6 +176,22 @@ def test_minplus_chain_runs(ctx, oracle_lib, seed):
     term = rng.integers(0, 1000, S).astype(np.uint64)
     opt, Gs = ctx.minplus_chain([M0, M1], [(0, 1), (1, L)], terminal=term)
     want = oracle_lib.chain([M0] + [M1] * L, terminal=term)
+    assert opt == int(want[0][0])
+    for a, b in zip(Gs, want):
+        assert np.array_equal(a, b)
+
+
+@pytest.mark.parametrize("S,L,maxv", [(100, 13, 1 << 20), (200, 9, 1 << 40), (65, 40, 1000)])
+def test_minplus_chain_large_states(ctx, oracle_lib, S, L, maxv):
+    """State spaces too large for the shared-memory chain kernel: squarings by
+    the tiled (min,+) kernel, doubling by batched matrix-vector launches."""
+    rng = np.random.default_rng(S + L)
+    M0 = rng.integers(0, maxv, (3, S), dtype=np.uint64)
+    M1 = rng.integers(0, maxv, (S, S), dtype=np.uint64)
+    M1[rng.random(M1.shape) < 0.3] = np.uint64(INF64)
+    M2 = rng.integers(0, maxv, (S, 7), dtype=np.uint64)
+    opt, Gs = ctx.minplus_chain([M0, M1, M2], [(0, 1), (1, L), (2, 1)])
+    want = oracle_lib.chain([M0] + [M1] * L + [M2])
     assert opt == int(want[0][0])
     for a, b in zip(Gs, want):
         assert np.array_equal(a, b)
