@@ -31,11 +31,13 @@ template <typename V> cudaError_t launch_compact(const CompactJob*, int, const u
 template <typename V> cudaError_t launch_build_tables(const TableSpec*, int, int64_t, const V*, V*, cudaStream_t);
 template <typename V> cudaError_t launch_fill(V*, int64_t, V, cudaStream_t);
 template <typename V> cudaError_t launch_enum(const EnumParams&, int, int64_t, size_t, cudaStream_t);
-template <typename V> cudaError_t launch_argmin(const ArgminParams&, V*, const V*, cudaStream_t);
+template <typename V> cudaError_t launch_argmin(const ArgminParams*, const ArgminEntry*, const int32_t*, int, int, int, cudaStream_t);
 cudaError_t launch_chain(const ChainParams&, cudaStream_t);
-cudaError_t launch_minplus(int, int, int, const uint64_t*, const uint64_t*, uint64_t*, uint64_t*, cudaStream_t);
-cudaError_t launch_matvec(const uint64_t*, int, int, const uint64_t*, uint64_t*, cudaStream_t);
 cudaError_t launch_intpipe(int, int, int, uint32_t*, cudaStream_t);
+template <typename V> cudaError_t launch_amin(const ArgminParams*, const int64_t*, int, int64_t, cudaStream_t);
+cudaError_t launch_all_pairs(const int64_t*, int, int64_t, ArgminEntry*, int32_t*, cudaStream_t);
+cudaError_t argmin_debug_read(uint64_t*);
+cudaError_t launch_edges_to_pairs(const ArgminParams*, ArgminEntry*, const int32_t*, int64_t, cudaStream_t);
 template <typename V> cudaError_t launch_minplus_tiled(int, int, int, const V*, const V*, V*, uint32_t*, cudaStream_t);
 template <typename V> cudaError_t launch_to_path(const uint64_t*, V*, int64_t, cudaStream_t);
 template <typename V> cudaError_t launch_from_path(const V*, const uint32_t*, uint64_t*, uint64_t*, int64_t, cudaStream_t);
@@ -285,7 +287,11 @@ struct cfp_prepared {
   int64_t spec_max32 = 0, spec_max64 = 0;
   std::vector<CompactJob> hjobs32, hjobs64;
   std::vector<EpiTau> epi_host;
-  DevBuf epi;
+  DevBuf epi, aps, pair_off, locAI, edges, reach;
+  int64_t reach_bytes = 0;
+  int64_t ai = 0, npairs = 0;
+  bool has32 = false, has64 = false, use_edges = false;
+  int kmax_arg = 1, tabn_max = 1;
   std::vector<TableSpec> hspecs32, hspecs64;
   ChainParams cp{};
   int nruns = 0;
@@ -655,7 +661,8 @@ static cfp_status setup_chain_staging(ChainParams& cp, const std::vector<ChainIn
   cp.levels_max = levels_max;
   cp.smax = smax;
   const int64_t need = (tot * (cp.backtrack ? 2 : 1) + g_elems + (int64_t)levels_max * smax * smax) * 8 +
-                       (int64_t)(cp.N + 2) * 8 + (int64_t)cp.N * 16 + 128 + g_elems * 2 + 16;
+                       (int64_t)(cp.N + 2) * 8 + (int64_t)mats.size() * 8 + (int64_t)cp.N * 16 + 128 +
+                       g_elems * 2 + 16 + (int64_t)cp.N * 4 + 16 + ((tot + 31) / 32) * 4 + 16;
   cp.smem_bytes = need <= 200 * 1024 ? need : 0;
   return CFP_OK;
 }
@@ -1053,14 +1060,28 @@ static cfp_status prepare_impl(cfp_ctx* ctx, const cfp_problem* p, bool do_chain
     if (t.empty) continue;
     int off = b.put_map(t.keep[t.o]);
     tx.ap.vmap = reinterpret_cast<const int32_t*>((intptr_t)off);   // rebased below
+    std::vector<int> inv(t.radix[t.o], -1);
+    for (size_t c = 0; c < t.keep[t.o].size(); ++c) inv[t.keep[t.o][c]] = (int)c;
+    int ioff = b.put_map(inv);
+    tx.ap.vinv = reinterpret_cast<const int32_t*>((intptr_t)ioff);
   }
   CUDA_TRY(P->maps.alloc(std::max<size_t>(1, b.maps.size()) * 4));
   CUDA_TRY(cudaMemcpyAsync(P->maps.p, b.maps.data(), b.maps.size() * 4, cudaMemcpyHostToDevice, st));
   const int64_t v32 = (b.vals32 + 3) & ~3LL, v64 = (b.vals64 + 3) & ~3LL;
   CUDA_TRY(P->vals32.alloc((size_t)(v32 + b.der32) * 4));
   CUDA_TRY(P->vals64.alloc((size_t)(v64 + b.der64) * 8));
-  for (auto& s : P->hspecs32) { s.out_off += v32; P->spec_max32 = std::max(P->spec_max32, s.rows * s.row); }
-  for (auto& s : P->hspecs64) { s.out_off += v64; P->spec_max64 = std::max(P->spec_max64, s.rows * s.row); }
+  for (auto& s : P->hspecs32) {
+    s.out_off += v32;
+    s.block0 = P->spec_max32;
+    s.nblocks = std::max<int64_t>(1, (s.rows * s.row + 1023) / 1024);
+    P->spec_max32 += s.nblocks;                       // total CTAs of the build launch
+  }
+  for (auto& s : P->hspecs64) {
+    s.out_off += v64;
+    s.block0 = P->spec_max64;
+    s.nblocks = std::max<int64_t>(1, (s.rows * s.row + 1023) / 1024);
+    P->spec_max64 += s.nblocks;
+  }
   // epilogue transition descriptors (chunkmin pointers patched below)
   CUDA_TRY(P->epi.alloc(std::max<size_t>(1, P->epi_host.size()) * sizeof(EpiTau)));
   P->njobs32 = (int)P->hjobs32.size();
@@ -1088,9 +1109,14 @@ static cfp_status prepare_impl(cfp_ctx* ctx, const cfp_problem* p, bool do_chain
   int64_t ai = 0;
   for (TransExec& tx : P->trans) { tx.out_off = ai; ai += (int64_t)tx.Din * tx.Do_orig; }
   CUDA_TRY(P->outAI.alloc((size_t)ai * 16 + 16));
-  P->merge_keys.alloc((size_t)ai * 8 + 16);
+  CUDA_TRY(P->merge_keys.alloc((size_t)ai * 8 + 16));
+  CUDA_TRY(P->locAI.alloc((size_t)ai * 16 + 16));            // rank-local (A, I) before the merge
+  CUDA_TRY(P->edges.alloc((size_t)(ai + 1) * sizeof(ArgminEntry) + (size_t)(ai + 1) * 4 + 16));
+  P->ai = ai;
   uint64_t* outA = P->outAI.as<uint64_t>();
   uint64_t* outI = outA + ai;
+  uint64_t* argA = ctx->world > 1 ? P->locAI.as<uint64_t>() : outA;
+  uint64_t* argI = ctx->world > 1 ? P->locAI.as<uint64_t>() + ai : outI;
   // rebase pointers
   for (TypeExec& te : P->types) {
     if (te.empty) continue;
@@ -1112,14 +1138,41 @@ static cfp_status prepare_impl(cfp_ctx* ctx, const cfp_problem* p, bool do_chain
       tx.ap.f = tx.fp;
       tx.ap.maps = P->maps.as<int32_t>();
       tx.ap.vmap = P->maps.as<int32_t>() + (intptr_t)tx.ap.vmap;
-      tx.ap.A_out = outA + tx.out_off;
-      tx.ap.I_out = outI + tx.out_off;
+      tx.ap.vinv = P->maps.as<int32_t>() + (intptr_t)tx.ap.vinv;
+      tx.ap.A_out = argA + tx.out_off;
+      tx.ap.I_out = argI + tx.out_off;
+      tx.ap.A_glob = outA + tx.out_off;
+      tx.ap.wide = te.wide ? 1 : 0;
+      tx.ap.slot = trans_slot[x];
       tx.ap.pstar = reinterpret_cast<int64_t*>((char*)P->scratch.p + tx.pstar_off);
     }
     for (size_t q = 0; q < te.trans.size(); ++q)
       P->epi_host[te.epi_off + q].chunkmin = P->trans[trans_slot[te.trans[q]]].fp.chunkmin;
     ep.taus = P->epi.as<EpiTau>() + te.epi_off;
     ep.vals = vals;
+  }
+  {
+    // device copies of the per-transition argmin descriptors + bucket offsets
+    std::vector<ArgminParams> aps(P->trans.size());
+    std::vector<int64_t> poff(P->trans.size() + 1, 0);
+    for (size_t q = 0; q < P->trans.size(); ++q) {
+      TransExec& tx = P->trans[q];
+      aps[q] = tx.ap;
+      const TypeExec& te = P->types[type_slot[tx.type]];
+      const bool live = !te.empty && te.nPl > 0;
+      if (!live) aps[q].f.nchunks = 0;
+      poff[q + 1] = poff[q] + (live ? (int64_t)tx.fp.Din * tx.fp.Do : 0);
+      P->has32 |= live && !te.wide;
+      P->has64 |= live && te.wide;
+      P->kmax_arg = std::max(P->kmax_arg, te.K);
+      P->tabn_max = std::max(P->tabn_max, (int)te.es.tab_n);
+    }
+    P->npairs = poff.back();
+    CUDA_TRY(P->aps.alloc(std::max<size_t>(1, aps.size()) * sizeof(ArgminParams)));
+    CUDA_TRY(P->pair_off.alloc(poff.size() * 8));
+    if (!aps.empty())
+      CUDA_TRY(cudaMemcpyAsync(P->aps.p, aps.data(), aps.size() * sizeof(ArgminParams), cudaMemcpyHostToDevice, st));
+    CUDA_TRY(cudaMemcpyAsync(P->pair_off.p, poff.data(), poff.size() * 8, cudaMemcpyHostToDevice, st));
   }
   if (!P->epi_host.empty())
     CUDA_TRY(cudaMemcpyAsync(P->epi.p, P->epi_host.data(), P->epi_host.size() * sizeof(EpiTau),
@@ -1220,6 +1273,14 @@ static cfp_status prepare_impl(cfp_ctx* ctx, const cfp_problem* p, bool do_chain
         if (r.len > 1) lv = std::max(lv, levels);
       }
       TRY(setup_chain_staging(cp, mats, goff[N + 1], lv, smax, P->chain_mats, P->chain_moff, st));
+      // argmin only on optimal edges reachable from the chain start (<= 256 states)
+      P->use_edges = smax <= 256;
+      cp.edge_list = P->edges.as<ArgminEntry>();
+      cp.edge_count = reinterpret_cast<int32_t*>(P->edges.as<char>() + (size_t)(P->ai + 1) * sizeof(ArgminEntry));
+      cp.edge_flag = reinterpret_cast<int32_t*>(P->merge_keys.p);      // ai ints, zeroed per execute
+      CUDA_TRY(P->reach.alloc((size_t)goff[N] + 16));
+      cp.reach = P->reach.as<uint8_t>();
+      P->reach_bytes = goff[N];
     }
   }
   CUDA_TRY(cudaStreamSynchronize(st));
@@ -1236,14 +1297,6 @@ template <typename V>
 static cfp_status run_type_kernels(cfp_prepared* P, TypeExec& te, cudaStream_t st, bool first_of_prec) {
   (void)first_of_prec;
   CUDA_TRY(launch_enum<V>(te.ep, te.NB, te.nthreads, te.smem, st));
-  P->launches += 1;
-  return CFP_OK;
-}
-
-template <typename V>
-static cfp_status run_trans_kernels(cfp_prepared* P, TransExec& tx, cudaStream_t st) {
-  CUDA_TRY(launch_argmin<V>(tx.ap, reinterpret_cast<V*>((char*)P->scratch.p + tx.aval_off),
-                            static_cast<const V*>(tx.fp.vals), st));
   P->launches += 1;
   return CFP_OK;
 }
@@ -1288,24 +1341,54 @@ static cfp_status execute_impl(cfp_ctx* ctx, cfp_prepared* P) {
   }
   if (P->timing) CUDA_TRY(cudaEventRecord(P->ev[2], st));
   uint64_t* outA = P->outAI.as<uint64_t>();
-  int64_t ai = 0;
-  for (TransExec& tx : P->trans) ai += (int64_t)tx.Din * tx.Do_orig;
+  const int64_t ai = P->ai;
   // outputs default to (INF, NOIDX): covers pruned output strategies, empty types
   CUDA_TRY(launch_fill<uint64_t>(outA, ai * 2, kInf64, st));
   P->launches++;
-  for (TransExec& tx : P->trans) {
-    const TypeExec* te = nullptr;
-    for (auto& t : P->types) if (t.id == tx.type) te = &t;
-    if (te->empty || te->nPl == 0) continue;
-    if (te->wide) TRY(run_trans_kernels<uint64_t>(P, tx, st));
-    else TRY(run_trans_kernels<uint32_t>(P, tx, st));
+  if (ctx->world > 1) {
+    CUDA_TRY(launch_fill<uint64_t>(P->locAI.as<uint64_t>(), ai * 2, kInf64, st));
+    P->launches++;
   }
+  const ArgminParams* aps = P->aps.as<ArgminParams>();
+  const int nslot = (int)P->trans.size();
+  // a1: bucket minima A (values)
+  if (P->has32) { CUDA_TRY(launch_amin<uint32_t>(aps, P->pair_off.as<int64_t>(), nslot, P->npairs, st)); P->launches++; }
+  if (P->has64) { CUDA_TRY(launch_amin<uint64_t>(aps, P->pair_off.as<int64_t>(), nslot, P->npairs, st)); P->launches++; }
+  if (ctx->world > 1) {
+    // rank-local minima were written to locA by the argmin descriptors; amin wrote
+    // them there too -- reduce into the global A
+    NCCL_TRY(ncclAllReduce(P->locAI.p, outA, ai, ncclUint64, ncclMin, ctx->comm, st));
+  }
+  ArgminEntry* list = P->edges.as<ArgminEntry>();
+  int32_t* count = reinterpret_cast<int32_t*>(P->edges.as<char>() + (size_t)(ai + 1) * sizeof(ArgminEntry));
+  const bool edges = P->do_chain && P->use_edges;
+  if (edges) {
+    // a3: suffix vectors + the optimal edges reachable from the chain start
+    CUDA_TRY(cudaMemsetAsync(P->status.p, 0, 4, st));
+    CUDA_TRY(cudaMemsetAsync(count, 0, 4, st));
+    CUDA_TRY(cudaMemsetAsync(P->merge_keys.p, 0, (size_t)ai * 4, st));
+    CUDA_TRY(cudaMemsetAsync(P->reach.p, 0, (size_t)P->reach_bytes, st));
+    ChainParams c1 = P->cp;
+    c1.mode = 1;
+    CUDA_TRY(launch_chain(c1, st));
+    CUDA_TRY(launch_edges_to_pairs(aps, list, count, ai, st));
+    P->launches += 2;
+  } else {
+    CUDA_TRY(launch_all_pairs(P->pair_off.as<int64_t>(), nslot, P->npairs, list, count, st));
+    P->launches++;
+  }
+  // a1: least combination index of the listed buckets
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(edges ? 64 : P->npairs, P->npairs));
+  if (P->has32) { CUDA_TRY(launch_argmin<uint32_t>(aps, list, count, grid, P->kmax_arg, P->tabn_max, st)); P->launches++; }
+  if (P->has64) { CUDA_TRY(launch_argmin<uint64_t>(aps, list, count, grid, P->kmax_arg, P->tabn_max, st)); P->launches++; }
   // a2: merge across ranks
   if (ctx->world > 1) TRY(merge_ranks(P, st));
-  // a3 + a4
+  // a4 (+ a3 when the edge list is not used)
   if (P->do_chain) {
-    CUDA_TRY(cudaMemsetAsync(P->status.p, 0, 4, st));
-    CUDA_TRY(launch_chain(P->cp, st));
+    if (!edges) CUDA_TRY(cudaMemsetAsync(P->status.p, 0, 4, st));
+    ChainParams c2 = P->cp;
+    c2.mode = edges ? 2 : 0;
+    CUDA_TRY(launch_chain(c2, st));
     P->launches++;
   }
   if (P->timing) CUDA_TRY(cudaEventRecord(P->ev[3], st));
@@ -1333,39 +1416,20 @@ __global__ void mask_idx_kernel(const uint64_t* A, const uint64_t* Amin, const u
 }
 
 static cfp_status merge_ranks(cfp_prepared* P, cudaStream_t st) {
+  // (cost, index) lexicographic min over ranks of the rank-local argmins:
+  // round 1 min cost (already the global A in outA), round 2 min index among
+  // ranks attaining it.
   cfp_ctx* ctx = P->ctx;
-  int64_t ai = 0;
-  for (TransExec& tx : P->trans) ai += (int64_t)tx.Din * tx.Do_orig;
+  const int64_t ai = P->ai;
   uint64_t* A = P->outAI.as<uint64_t>();
   uint64_t* I = A + ai;
-  uint64_t* keys = P->merge_keys.as<uint64_t>();
-  // bits: index bits from the largest original combination space; cost bits
-  // from the finite bound (values < 2^31 on narrow types, else wide)
-  int idx_bits = 1;
-  double maxspace = 1;
-  bool any_wide = false;
-  for (auto& te : P->types) {
-    double s = 1;
-    for (int d = 0; d < te.K; ++d) s *= te.es.radix[d];
-    maxspace = std::max(maxspace, s * 64.0);   // original radices >= compact; generous
-    any_wide |= te.wide;
-  }
-  while ((double)(1ull << idx_bits) < maxspace && idx_bits < 63) ++idx_bits;
+  const uint64_t* locA = P->locAI.as<uint64_t>();
+  const uint64_t* locI = locA + ai;
   const unsigned nb = (unsigned)((ai + 255) / 256);
-  if (!any_wide && idx_bits + 32 <= 64) {
-    pack_kernel<<<nb, 256, 0, st>>>(A, I, ai, idx_bits, keys);
-    NCCL_TRY(ncclAllReduce(keys, keys, ai, ncclUint64, ncclMin, ctx->comm, st));
-    unpack_kernel<<<nb, 256, 0, st>>>(keys, ai, idx_bits, A, I);
-    P->launches += 2;
-  } else {
-    // round 1: min cost; round 2: min index among ranks attaining it
-    NCCL_TRY(ncclAllReduce(A, keys, ai, ncclUint64, ncclMin, ctx->comm, st));
-    mask_idx_kernel<<<nb, 256, 0, st>>>(A, keys, I, ai, I);
-    NCCL_TRY(ncclAllReduce(I, I, ai, ncclUint64, ncclMin, ctx->comm, st));
-    CUDA_TRY(cudaMemcpyAsync(A, keys, ai * 8, cudaMemcpyDeviceToDevice, st));
-    P->launches += 1;
-  }
+  mask_idx_kernel<<<nb, 256, 0, st>>>(locA, A, locI, ai, I);
   CUDA_TRY(cudaGetLastError());
+  NCCL_TRY(ncclAllReduce(I, I, ai, ncclUint64, ncclMin, ctx->comm, st));
+  P->launches += 1;
   return CFP_OK;
 }
 
@@ -1379,6 +1443,18 @@ static cfp_status fetch_impl(cfp_ctx* ctx, cfp_prepared* P, cfp_plan* out) {
   CUDA_TRY(cudaMemcpyAsync(buf.data(), P->plan.p, buf.size(), cudaMemcpyDeviceToHost, st));
   CUDA_TRY(cudaStreamSynchronize(st));
   if (P->cp.dbg) {
+    uint64_t a[16];
+    CUDA_TRY(argmin_debug_read(a));
+    int32_t cnt = 0;
+    CUDA_TRY(cudaMemcpy(&cnt, P->edges.as<char>() + (size_t)(P->ai + 1) * sizeof(ArgminEntry), 4,
+                        cudaMemcpyDeviceToHost));
+    fprintf(stderr, "argmin slot-1 phases (us): stage %.2f chunks %.2f rows %.2f suffix %.2f; list %d of %lld; per entry:",
+            (a[1] - a[0]) * 1e-3, (a[2] - a[1]) * 1e-3, (a[3] - a[2]) * 1e-3, (a[4] - a[3]) * 1e-3, cnt,
+            (long long)P->npairs);
+    for (int i = 0; i < cnt && i < 8; ++i)
+      fprintf(stderr, " [slot %d pair %d: %.2f us]", (int)((a[8 + i] >> 12) & 0xF), (int)(a[8 + i] & 0xFFF),
+              (a[8 + i] >> 16) * 1e-3);
+    fprintf(stderr, "\n");
     uint64_t t[64];
     CUDA_TRY(cudaMemcpy(t, P->cp.dbg, sizeof(t), cudaMemcpyDeviceToHost));
     fprintf(stderr, "chain phases (us):");

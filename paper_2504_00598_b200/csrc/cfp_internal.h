@@ -54,6 +54,7 @@ struct TableSpec {
   int64_t row_valid;   // product of radices of the row digits
   int64_t row;         // padded row length
   int64_t out_off;     // element offset of T in the derived blob
+  int64_t block0, nblocks;   // this table's CTAs in the build launch (1024 entries each)
 };
 
 // A transition folded in the enumeration epilogue (cross terms into this type).
@@ -116,48 +117,6 @@ struct FoldParams {
   int64_t W, G, h0, nhb;
 };
 
-struct FoldMulti {              // all transitions into one type (share B_p)
-  int32_t ntau;
-  FoldParams f[kMaxFoldTau];
-};
-
-// Shared-memory layout of the fold kernel (host sizes it, device uses it).
-struct FoldSmem {
-  int DoP, CH, Dl, ngrp, DinP[4], nblk[4], blk0[4], nblk_all, groups;
-  int64_t bs, xs[4], red[4], xh[4], qs[4], ql[4], rows, gdig, total;
-};
-
-__host__ __device__ inline FoldSmem fold_layout(const FoldMulti& fm, int vbytes) {
-  FoldSmem L{};
-  const FoldParams& f0 = fm.f[0];
-  L.DoP = (f0.Do + 3) & ~3;
-  L.CH = f0.CH;
-  L.Dl = f0.P > 0 ? f0.pre_radix[f0.P - 1] : 1;   // rows sharing all but the last prefix digit
-  L.ngrp = L.CH / L.Dl + 2;
-  int64_t off = 0;
-  auto take = [&](int64_t bytes) { const int64_t o = off; off += (bytes + 15) & ~15LL; return o; };
-  L.bs = take(2LL * L.CH * L.DoP * vbytes);
-  L.nblk_all = 0;
-  for (int t = 0; t < fm.ntau; ++t) {
-    L.DinP[t] = (fm.f[t].Din + 3) & ~3;
-    L.nblk[t] = (L.DinP[t] / 4) * (L.DoP / 4);
-    L.blk0[t] = L.nblk_all;
-    L.nblk_all += L.nblk[t];
-  }
-  L.groups = L.nblk_all >= 256 ? 1 : (256 / L.nblk_all < 8 ? 256 / L.nblk_all : 8);
-  for (int t = 0; t < fm.ntau; ++t) {
-    L.xs[t] = take((int64_t)L.CH * L.DinP[t] * vbytes);
-    L.red[t] = take((int64_t)L.groups * L.DinP[t] * L.DoP * vbytes);
-    L.xh[t] = take((int64_t)L.ngrp * L.DinP[t] * vbytes);
-    L.qs[t] = take((int64_t)fm.f[t].qelems * vbytes);
-    L.ql[t] = take((int64_t)L.DinP[t] * L.Dl * vbytes);
-  }
-  L.rows = take((int64_t)L.CH * 2 * 4);             // (group, last digit) per chunk row
-  L.gdig = take((int64_t)L.ngrp * kMaxFoldTau * kMaxCross * 4);
-  L.total = off;
-  return L;
-}
-
 // Generic evaluation of all intra terms of a compact combination (argmin
 // recovery) -- terms reference block ids directly.
 struct EvalSpec {
@@ -185,7 +144,13 @@ struct ArgminParams {
   uint64_t* I_out;
   uint64_t* key_out;            // [Din][Do_orig] local (cost, idx) for merge (nullable)
   int64_t* pstar;               // scratch [Din*Do]
+  const int32_t* vinv;          // original v -> compact v (-1 = pruned)
+  const uint64_t* A_glob;       // [Din][Do_orig] merged bucket minima (amin + all-reduce)
+  int32_t wide;                 // value type of this transition's type (0 u32, 1 u64)
+  int32_t slot;                 // transition slot (list entries)
 };
+
+struct ArgminEntry { int32_t slot, pair; };   // pair = u * Do + compact v
 
 struct ChainInst {
   const uint64_t* A;            // [rows][cols]
@@ -237,6 +202,12 @@ struct ChainParams {
   int64_t smem_bytes;           // 0 = global mode
   int32_t levels_max, smax;
   uint64_t* dbg;                // nullable: %globaltimer at phase boundaries
+  int32_t mode;                 // 0 G + backtrack, 1 G + optimal-edge list, 2 backtrack (G given)
+  int32_t* edge_flag;           // mode 1: [sum Din*Do_orig] dedupe flags (zeroed)
+  const int64_t* flag_off;      // mode 1: per distinct matrix offset into edge_flag
+  ArgminEntry* edge_list;       // mode 1: reachable optimal edges (slot, u * Do_orig + v_orig)
+  uint8_t* reach;               // [goff[N]] state u reachable before instance n (set by mode 1)
+  int32_t* edge_count;
   const uint64_t* baseA;        // all distinct A matrices, contiguous (moff offsets)
   const uint64_t* baseI;        // same for I (backtrack)
 };

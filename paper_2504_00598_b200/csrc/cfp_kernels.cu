@@ -18,6 +18,7 @@
 
 #include <algorithm>
 #include <cstdint>
+#include <cstdio>
 
 #include "cfp_internal.h"
 
@@ -99,6 +100,13 @@ __device__ __forceinline__ int prefix_digit(int64_t pg, int pos, int P, const in
   return dig;
 }
 
+__device__ uint64_t g_enum_dbg2[16];
+__device__ __forceinline__ uint64_t gtimer0() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
 // --------------------------------------------------------------------------
 // a0: compaction.  Each job gathers one table of the pruned problem from the
 // raw uint32 inputs: unary w = p + c (INF absorbing), pair / cross
@@ -139,25 +147,45 @@ __global__ void compact_kernel(const CompactJob* __restrict__ jobs, const uint32
 template <typename V>
 __global__ void build_table_kernel(const TableSpec* __restrict__ specs, const V* __restrict__ vals,
                                    V* __restrict__ out) {
-  const TableSpec& s = specs[blockIdx.y];
-  const int64_t total = s.rows * s.row;
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
-       e += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t r = e / s.row, c = e % s.row;
+  int si = 0;
+  while (blockIdx.x >= specs[si].block0 + specs[si].nblocks) ++si;   // block -> table
+  const TableSpec& s = specs[si];
+  const int64_t total = min(s.rows * s.row, (int64_t)(blockIdx.x - s.block0 + 1) * 1024);
+  __shared__ int32_t sdig[kMaxDigits][256];       // per-thread digits (dynamic index)
+  const bool small = total < 0x7FFFFFFF && s.row < 0x7FFFFFFF;
+  for (int64_t e = (blockIdx.x - s.block0) * 1024 + threadIdx.x; e < total; e += blockDim.x) {
+    int64_t r, c;
+    if (small) {
+      r = (uint32_t)e / (uint32_t)s.row;
+      c = (uint32_t)e - (uint32_t)r * (uint32_t)s.row;
+    } else {
+      r = e / s.row;
+      c = e % s.row;
+    }
     V acc = 0;
     if (c >= s.row_valid) {
       acc = VT<V>::CAP;
     } else {
-      int32_t dig[kMaxDigits];
-      int64_t q = r * s.row_valid + c;
-      for (int d = s.ndig - 1; d >= 0; --d) {
-        dig[d] = (int32_t)(q % s.radix[d]);
-        q /= s.radix[d];
+      int32_t* dig = &sdig[0][threadIdx.x];
+      const int64_t q0 = r * s.row_valid + c;
+      if (q0 < 0x7FFFFFFF) {
+        uint32_t q = (uint32_t)q0;
+        for (int d = s.ndig - 1; d >= 0; --d) {
+          const uint32_t rd = (uint32_t)s.radix[d];
+          dig[d * 256] = (int32_t)(q % rd);
+          q /= rd;
+        }
+      } else {
+        int64_t q = q0;
+        for (int d = s.ndig - 1; d >= 0; --d) {
+          dig[d * 256] = (int32_t)(q % s.radix[d]);
+          q /= s.radix[d];
+        }
       }
       for (int t = 0; t < s.nterm; ++t) {
         const Term& tm = s.term[t];
-        const V v = tm.kind == 0 ? vals[tm.off + dig[tm.a]]
-                                 : vals[tm.off + (int64_t)dig[tm.a] * tm.db + dig[tm.b]];
+        const V v = tm.kind == 0 ? vals[tm.off + dig[tm.a * 256]]
+                                 : vals[tm.off + (int64_t)dig[tm.a * 256] * tm.db + dig[tm.b * 256]];
         acc = VT<V>::sat(acc, v);
       }
     }
@@ -214,11 +242,13 @@ __device__ __forceinline__ void atomic_min_v<uint64_t>(uint64_t* p, uint64_t v) 
 //    X^t_p[u] = sum_{cross (j, Q)} Q[u][s_j(p)]          (Eq. 3 r_n)
 // with 4x4 register-blocked fused add+mins over the chunk's rows.
 template <typename V, int NB, bool STAGED>
-__global__ void __launch_bounds__(kBlock) enum_kernel(const EnumParams p) {
+__global__ void __launch_bounds__(kBlock, 4) enum_kernel(const EnumParams p) {
   using T = VT<V>;
   constexpr int VN = Vec4<V>::N;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int tid = threadIdx.x;
+  const bool edbg = blockIdx.x == 0 && tid == 0 && p.ntau == 2;
+  if (edbg) g_enum_dbg2[0] = gtimer0();
   const int64_t nhb = p.Gpad / kBlock;
   const int64_t g = blockIdx.x / nhb;
   const int64_t hb = blockIdx.x - g * nhb;
@@ -275,6 +305,7 @@ __global__ void __launch_bounds__(kBlock) enum_kernel(const EnumParams p) {
     XT = xs; YT = ys; ZT = zs; MT = ms;
     sx = sy = sz = 0;
   }
+  if (edbg) g_enum_dbg2[1] = gtimer0();
   V* Bp = static_cast<V*>(p.Bp) + row * p.Do;
   V acc[NB];
 #pragma unroll
@@ -332,6 +363,8 @@ __global__ void __launch_bounds__(kBlock) enum_kernel(const EnumParams p) {
       Bp[od] = r;
     }
   }
+  if (edbg) g_enum_dbg2[2] = gtimer0();
+  if (blockIdx.x == 0 && p.ntau == 2 && (tid & 31) == 0) g_enum_dbg2[8 + (tid >> 5)] = gtimer0();
   if (p.ntau == 0) return;
   // ---- epilogue: fold the cross-segment terms of every incoming transition
   __syncthreads();                                // staged tables no longer needed
@@ -355,19 +388,51 @@ __global__ void __launch_bounds__(kBlock) enum_kernel(const EnumParams p) {
   for (int t = 0; t < p.ntau; ++t) {
     const EpiTau& et = p.taus[t];
     const int Din = et.Din, DinP = (Din + 3) & ~3;
-    for (int u = 0; u < DinP; ++u) Xs[tid * DinP + u] = T::CAP;
-    if (live) {
-      for (int u = 0; u < Din; ++u) Xs[tid * DinP + u] = 0;
-      for (int i = 0; i < et.nq; ++i) {
-        const Term& q = et.q[i];
-        const int dig = pg < 0x7FFFFFFF
-                            ? (int)(((uint32_t)pg / (uint32_t)p.pre_stride[q.a]) % (uint32_t)p.pre_radix[q.a])
-                            : (int)((pg / p.pre_stride[q.a]) % p.pre_radix[q.a]);
-        const V* Q = vals + q.off + dig;
-        for (int u = 0; u < Din; ++u) Xs[tid * DinP + u] = T::sat(Xs[tid * DinP + u], Q[(int64_t)u * q.db]);
+    {
+      // X^t_p[u] for this thread's prefix, 4 u at a time; up to 4 cross terms
+      // live in registers (all 16 loads of a u-quad are independent), further
+      // terms are accumulated through shared memory.
+      const int nq = et.nq;
+      auto digit_of = [&](int a) -> int {
+        return pg < 0x7FFFFFFF ? (int)(((uint32_t)pg / (uint32_t)p.pre_stride[a]) % (uint32_t)p.pre_radix[a])
+                               : (int)((pg / p.pre_stride[a]) % p.pre_radix[a]);
+      };
+      const V* q0 = nullptr; const V* q1 = nullptr; const V* q2 = nullptr; const V* q3 = nullptr;
+      int d0 = 0, d1 = 0, d2 = 0, d3 = 0;
+      if (nq > 0) { q0 = vals + et.q[0].off + digit_of(et.q[0].a); d0 = et.q[0].db; }
+      if (nq > 1) { q1 = vals + et.q[1].off + digit_of(et.q[1].a); d1 = et.q[1].db; }
+      if (nq > 2) { q2 = vals + et.q[2].off + digit_of(et.q[2].a); d2 = et.q[2].db; }
+      if (nq > 3) { q3 = vals + et.q[3].off + digit_of(et.q[3].a); d3 = et.q[3].db; }
+      for (int u0 = 0; u0 < DinP; u0 += 4) {
+        V x[4];
+#pragma unroll
+        for (int k2 = 0; k2 < 4; ++k2) x[k2] = (live && u0 + k2 < Din) ? (V)0 : T::CAP;
+        if (live) {
+          V y0[4], y1[4], y2[4], y3[4];
+#pragma unroll
+          for (int k2 = 0; k2 < 4; ++k2) {
+            const int u = min(u0 + k2, Din - 1);
+            y0[k2] = nq > 0 ? __ldg(q0 + (int64_t)u * d0) : (V)0;
+            y1[k2] = nq > 1 ? __ldg(q1 + (int64_t)u * d1) : (V)0;
+            y2[k2] = nq > 2 ? __ldg(q2 + (int64_t)u * d2) : (V)0;
+            y3[k2] = nq > 3 ? __ldg(q3 + (int64_t)u * d3) : (V)0;
+          }
+#pragma unroll
+          for (int k2 = 0; k2 < 4; ++k2)
+            x[k2] = T::sat(T::sat(x[k2], y0[k2]), T::sat(T::sat(y1[k2], y2[k2]), y3[k2]));
+        }
+#pragma unroll
+        for (int k2 = 0; k2 < 4; ++k2) Xs[tid * DinP + u0 + k2] = x[k2];
+      }
+      for (int i = 4; i < nq; ++i) {                 // rare: more than four cross terms
+        const V* qi = vals + et.q[i].off + digit_of(et.q[i].a);
+        if (live)
+          for (int u = 0; u < Din; ++u)
+            Xs[tid * DinP + u] = T::sat(Xs[tid * DinP + u], __ldg(qi + (int64_t)u * et.q[i].db));
       }
     }
     __syncthreads();
+    if (edbg) g_enum_dbg2[3 + 3 * t] = gtimer0();
     const int nblk = (DinP / 4) * (VP / 4);
     const int stripes = nblk >= kBlock ? 1 : min(8, kBlock / nblk);
     V res[4][4];
@@ -407,6 +472,7 @@ __global__ void __launch_bounds__(kBlock) enum_kernel(const EnumParams p) {
       if (stripes > 1) break;
     }
     __syncthreads();                                 // Xs free -> stripe partials
+    if (edbg) g_enum_dbg2[4 + 3 * t] = gtimer0();
     if (nblk < kBlock) {
       V* red = stripes * VP <= kBlock ? Xs : Xs + kBlock * dinp_max;   // [stripes][DinP][VP]
       if (active) {
@@ -425,6 +491,7 @@ __global__ void __launch_bounds__(kBlock) enum_kernel(const EnumParams p) {
       }
       __syncthreads();
     }
+    if (edbg) g_enum_dbg2[5 + 3 * t] = gtimer0();
   }
 }
 
@@ -453,331 +520,6 @@ __device__ __forceinline__ void load4(const V* p, V* out) {
   }
 }
 
-// Persistent fold over all transitions into one segment type (they share
-// B_p).  The local prefixes are cut into chunks of CH rows; CTA c owns a
-// contiguous run of chunks.  Per chunk: B_p rows arrive by double-buffered
-// TMA bulk copies; X_p[u] is built from the prefix's digit structure -- rows
-// sharing all but the last prefix digit ("group") share Xhi[u] = the cross
-// terms on the other digits, so X_p[u] = Xhi[u] + sum of the last-digit terms
-// (1-2 shared loads per entry); then each thread folds a 4x4 (u, v) block
-// over a stripe of the rows (two 4-wide shared loads per 16 fused add+mins)
-// and the stripes are reduced into chunkmin_t[(u * Do + v) * nchunks + chunk].
-template <typename V>
-__global__ void __launch_bounds__(256) fold_kernel(const FoldMulti fm) {
-  using T = VT<V>;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  const FoldSmem L = fold_layout(fm, (int)sizeof(V));
-  const FoldParams& f0 = fm.f[0];
-  const int Do = f0.Do, DoP = L.DoP, CH = L.CH, Dl = L.Dl, P = f0.P;
-  V* bs = reinterpret_cast<V*>(smem_raw + L.bs);
-  __shared__ __align__(8) uint64_t mbar[2];
-  const int tid = threadIdx.x;
-  const int64_t nch = f0.nchunks;
-  const int64_t c_lo = blockIdx.x * nch / gridDim.x, c_hi = (blockIdx.x + 1) * nch / gridDim.x;
-  const V* Bp = static_cast<const V*>(f0.Bp);
-  const V* vals = static_cast<const V*>(f0.vals);
-  const bool tma = f0.tma && DoP == Do;
-  for (int t = 0; t < fm.ntau; ++t) {                 // Q tables -> smem
-    const FoldParams& f = fm.f[t];
-    V* qs = reinterpret_cast<V*>(smem_raw + L.qs[t]);
-    int qo = 0;
-    for (int i = 0; i < f.nq; ++i) {
-      const int ne = f.Din * f.q[i].db;
-      for (int e = tid; e < ne; e += 256) qs[qo + e] = vals[f.q[i].off + e];
-      qo += ne;
-    }
-  }
-  if (tma && tid == 0) { mbar_init(&mbar[0], 1); mbar_init(&mbar[1], 1); }
-  __syncthreads();
-  for (int t = 0; t < fm.ntau; ++t) {                 // QL[u][s]: cross terms on the last digit
-    const FoldParams& f = fm.f[t];
-    const V* qs = reinterpret_cast<const V*>(smem_raw + L.qs[t]);
-    V* ql = reinterpret_cast<V*>(smem_raw + L.ql[t]);      // [s][u] (u contiguous)
-    for (int e = tid; e < L.DinP[t] * Dl; e += 256) {
-      const int s = e / L.DinP[t], u = e - s * L.DinP[t];
-      V x = u < f.Din ? (V)0 : T::CAP;
-      if (u < f.Din) {
-        int qo = 0;
-        for (int i = 0; i < f.nq; ++i) {
-          if (f.q[i].a == P - 1) x = T::sat(x, qs[qo + u * f.q[i].db + s]);
-          qo += f.Din * f.q[i].db;
-        }
-      }
-      ql[e] = x;
-    }
-  }
-  int32_t* rg = reinterpret_cast<int32_t*>(smem_raw + L.rows);
-  int32_t* rs = rg + CH;
-  int32_t* gdig = reinterpret_cast<int32_t*>(smem_raw + L.gdig);
-  auto rows_of = [&](int64_t ch) { return (int)min((int64_t)CH, f0.nPl - ch * CH); };
-  auto issue = [&](int64_t ch, int buf) {             // B_p rows of chunk ch -> bs[buf]
-    const int64_t p0 = ch * CH;
-    const int n = rows_of(ch);
-    V* dst = bs + (int64_t)buf * CH * DoP;
-    if (tma) {
-      if (tid == 0) {
-        const uint32_t bytes = (uint32_t)((int64_t)n * Do * sizeof(V));
-        mbar_expect_tx(&mbar[buf], bytes);
-        tma_bulk_g2s(dst, Bp + p0 * Do, bytes, &mbar[buf]);
-      }
-    } else {
-      for (int e = tid; e < n * DoP; e += 256) {
-        const int pi = e / DoP, v = e - pi * DoP;
-        dst[e] = v < Do ? Bp[(p0 + pi) * Do + v] : T::CAP;
-      }
-    }
-  };
-  if (c_lo < c_hi) issue(c_lo, 0);
-  uint32_t phases = 0;                               // bit b = parity of mbar[b]
-  const int gi = tid / L.nblk_all;
-  for (int64_t ch = c_lo; ch < c_hi; ++ch) {
-    const int buf = (int)((ch - c_lo) & 1);
-    const int64_t p0 = ch * CH;
-    const int n = rows_of(ch);
-    if (ch + 1 < c_hi) issue(ch + 1, buf ^ 1);         // buffer freed by the previous chunk's last sync
-    const int64_t pg0 = f0.p_lo + p0;
-    const int64_t grp0 = pg0 / Dl;
-    const int ng = (int)((pg0 + n - 1) / Dl - grp0 + 1);
-    // per row: (group, last digit); per group: the digits the other cross terms read
-    const int s0 = (int)(pg0 - grp0 * Dl);          // last digit of the chunk's first row
-    for (int pi = tid; pi < n; pi += 256) {
-      const int g = (s0 + pi) / Dl;
-      rg[pi] = g;
-      rs[pi] = s0 + pi - g * Dl;
-    }
-    for (int t = 0, col = 0; t < fm.ntau; ++t)
-      for (int i = 0; i < fm.f[t].nq; ++i, ++col) {
-        const int a = fm.f[t].q[i].a;
-        if (a >= P - 1) continue;
-        const int64_t st = f0.pre_stride[a] / Dl;
-        for (int g = tid; g < ng; g += 256) {
-          const int64_t ghi = grp0 + g;             // prefix value without its last digit
-          gdig[g * kMaxFoldTau * kMaxCross + col] =
-              (ghi < 0x7FFFFFFF && st < 0x7FFFFFFF)
-                  ? (int)(((uint32_t)ghi / (uint32_t)st) % (uint32_t)f0.pre_radix[a])
-                  : (int)((ghi / st) % f0.pre_radix[a]);
-        }
-      }
-    __syncthreads();
-    for (int t = 0, col0 = 0; t < fm.ntau; ++t) {     // Xhi[g][u]
-      const FoldParams& f = fm.f[t];
-      V* xh = reinterpret_cast<V*>(smem_raw + L.xh[t]);
-      const V* qs = reinterpret_cast<const V*>(smem_raw + L.qs[t]);
-      for (int g = tid >> 5; g < ng; g += 8)
-        for (int u = tid & 31; u < L.DinP[t]; u += 32) {
-          V x = u < f.Din ? (V)0 : T::CAP;
-          if (u < f.Din) {
-            int qo = 0;
-            for (int i = 0; i < f.nq; ++i) {
-              if (f.q[i].a < P - 1)
-                x = T::sat(x, qs[qo + u * f.q[i].db + gdig[g * kMaxFoldTau * kMaxCross + col0 + i]]);
-              qo += f.Din * f.q[i].db;
-            }
-          }
-          xh[g * L.DinP[t] + u] = x;
-        }
-      col0 += f.nq;
-    }
-    __syncthreads();
-    for (int t = 0; t < fm.ntau; ++t) {                // X_p[u] = Xhi[g][u] + QL[s][u], 4 u at a time
-      V* xs = reinterpret_cast<V*>(smem_raw + L.xs[t]);
-      const V* xh = reinterpret_cast<const V*>(smem_raw + L.xh[t]);
-      const V* ql = reinterpret_cast<const V*>(smem_raw + L.ql[t]);
-      const int DinP = L.DinP[t], nq4 = DinP / 4;
-      for (int e = tid; e < n * nq4; e += 256) {
-        const int pi = e / nq4, u0 = (e - pi * nq4) * 4;
-        V a[4], b[4];
-        load4<V>(xh + rg[pi] * DinP + u0, a);
-        load4<V>(ql + rs[pi] * DinP + u0, b);
-#pragma unroll
-        for (int i = 0; i < 4; ++i) xs[pi * DinP + u0 + i] = T::sat(a[i], b[i]);
-      }
-    }
-    if (tma) { mbar_wait(&mbar[buf], (phases >> buf) & 1u); phases ^= 1u << buf; }
-    __syncthreads();
-    const V* b = bs + (int64_t)buf * CH * DoP;
-    auto fold_block = [&](int gblk, int pstart, int pstep, int grp) {
-      int t = 0;
-      while (t + 1 < fm.ntau && gblk >= L.blk0[t + 1]) ++t;
-      const int blk = gblk - L.blk0[t];
-      const int DinP = L.DinP[t];
-      const V* xs = reinterpret_cast<const V*>(smem_raw + L.xs[t]);
-      V* red = reinterpret_cast<V*>(smem_raw + L.red[t]) + (int64_t)grp * DinP * DoP;
-      const int u0 = (blk / (DoP / 4)) * 4, v0 = (blk % (DoP / 4)) * 4;
-      V acc[4][4];
-#pragma unroll
-      for (int i = 0; i < 4; ++i)
-#pragma unroll
-        for (int j = 0; j < 4; ++j) acc[i][j] = T::CAP;
-      const V* xp = xs + pstart * DinP + u0;
-      const V* bp = b + pstart * DoP + v0;
-      for (int pi = pstart; pi < n; pi += pstep, xp += pstep * DinP, bp += pstep * DoP) {
-        V x[4], y[4];
-        load4<V>(xp, x);
-        load4<V>(bp, y);
-#pragma unroll
-        for (int i = 0; i < 4; ++i)
-#pragma unroll
-          for (int j = 0; j < 4; ++j) acc[i][j] = T::addmin(x[i], y[j], acc[i][j]);
-      }
-#pragma unroll
-      for (int i = 0; i < 4; ++i)
-#pragma unroll
-        for (int j = 0; j < 4; ++j) red[(u0 + i) * DoP + v0 + j] = acc[i][j];
-    };
-    if (L.groups > 1) {
-      if (gi < L.groups) fold_block(tid - gi * L.nblk_all, gi, L.groups, gi);
-    } else {
-      for (int gb = tid; gb < L.nblk_all; gb += 256) fold_block(gb, 0, 1, 0);
-    }
-    __syncthreads();
-    for (int t = 0; t < fm.ntau; ++t) {              // stripes -> this chunk's minima
-      const FoldParams& f = fm.f[t];
-      const V* red = reinterpret_cast<const V*>(smem_raw + L.red[t]);
-      V* out = static_cast<V*>(f.chunkmin);
-      const int DinP = L.DinP[t];
-      for (int u = tid >> 5; u < f.Din; u += 8)
-        for (int v = tid & 31; v < Do; v += 32) {
-          V m = red[u * DoP + v];
-          for (int g2 = 1; g2 < L.groups; ++g2) m = T::mn(m, red[(int64_t)g2 * DinP * DoP + u * DoP + v]);
-          out[(int64_t)(u * Do + v) * nch + ch] = m;
-        }
-    }
-    __syncthreads();
-  }
-}
-
-// --------------------------------------------------------------------------
-// argmin phase 1: per (u, v): A = min over chunks; the first chunk attaining
-// it, then the least local prefix in that chunk with X_p[u] + B_p[v] == A.
-// One warp per (u, v); chunk minima are contiguous per pair.
-// --------------------------------------------------------------------------
-template <typename V>
-__global__ void fold_reduce_kernel(const FoldParams f, V* __restrict__ Aval, int64_t* __restrict__ pstar) {
-  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
-  if (warp >= f.Din * f.Do) return;
-  const int u = warp / f.Do, v = warp % f.Do;
-  const V* cm = static_cast<const V*>(f.chunkmin) + (int64_t)warp * f.nchunks;
-  V best = VT<V>::CAP;
-  int64_t bc = INT64_MAX;
-  for (int64_t c = lane; c < f.nchunks; c += 32) {
-    const V x = cm[c];
-    if (x < best) { best = x; bc = c; }       // c increasing per lane: first wins
-  }
-  for (int o = 16; o > 0; o >>= 1) {
-    const V ob = __shfl_xor_sync(0xffffffffu, best, o);
-    const int64_t oc = __shfl_xor_sync(0xffffffffu, bc, o);
-    if (ob < best || (ob == best && oc < bc)) { best = ob; bc = oc; }
-  }
-  if (best >= VT<V>::CAP) {
-    if (lane == 0) { Aval[warp] = VT<V>::CAP; pstar[warp] = -1; }
-    return;
-  }
-  const V* Bp = static_cast<const V*>(f.Bp);
-  const V* vals = static_cast<const V*>(f.vals);
-  const int64_t p0 = bc * f.CH;
-  const int n = (int)min((int64_t)f.CH, f.nPl - p0);
-  int64_t first = INT64_MAX;
-  for (int pi = lane; pi < n; pi += 32) {
-    const int64_t pl = p0 + pi;
-    const V x = cross_sum<V>(f, vals, f.p_lo + pl, u);
-    if (VT<V>::sat(x, Bp[pl * f.Do + v]) == best) { first = pl; break; }
-  }
-  for (int o = 16; o > 0; o >>= 1) {
-    const int64_t of = __shfl_xor_sync(0xffffffffu, first, o);
-    first = of < first ? of : first;
-  }
-  if (lane == 0) { Aval[warp] = best; pstar[warp] = first; }
-}
-
-// --------------------------------------------------------------------------
-// argmin phase 2: least suffix (in canonical order, restricted to s_o = v when
-// o is a suffix digit) whose intra cost equals B_p*[v]; then the original
-// combination index and the outputs in the caller's (unpruned) layout.
-// --------------------------------------------------------------------------
-template <typename V>
-__global__ void __launch_bounds__(256) suffix_argmin_kernel(const ArgminParams ap,
-                                                            const V* __restrict__ Aval,
-                                                            const V* __restrict__ vals) {
-  const FoldParams& f = ap.f;
-  const EvalSpec& e = ap.e;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  V* tabs = reinterpret_cast<V*>(smem_raw);                                   // W/R tables
-  uint16_t* sd = reinterpret_cast<uint16_t*>(tabs + ((e.tab_n + 1) & ~1));    // [K][blockDim]
-  const int pair = blockIdx.x;
-  const int u = pair / f.Do, v = pair % f.Do;
-  const int vo = ap.vmap[v];
-  const int64_t outi = (int64_t)u * ap.Do_orig + vo;
-  const int64_t pl = ap.pstar[pair];
-  __shared__ unsigned long long s_first;
-  if (pl < 0) {
-    if (threadIdx.x == 0) {
-      ap.A_out[outi] = kInf64;
-      ap.I_out[outi] = kInf64;
-    }
-    return;
-  }
-  for (int i = threadIdx.x; i < e.tab_n; i += blockDim.x) tabs[i] = vals[e.tab_lo + i];
-  const V* Bp = static_cast<const V*>(f.Bp);
-  const uint64_t target = (uint64_t)Bp[pl * f.Do + v];
-  const int64_t pg = f.p_lo + pl;
-  const int tid = threadIdx.x, nth = blockDim.x;
-  auto S = [&](int d) -> uint16_t& { return sd[d * nth + tid]; };
-  {
-    int64_t q = pg;
-    for (int d = e.P - 1; d >= 0; --d) { S(d) = (uint16_t)(q % e.radix[d]); q /= e.radix[d]; }
-  }
-  const bool o_suffix = e.o >= e.P;
-  const int64_t nrest = o_suffix ? e.nsuffix / e.radix[e.o] : e.nsuffix;
-  if (tid == 0) s_first = ~0ull;
-  __syncthreads();
-  const int64_t per = (nrest + nth - 1) / nth;
-  const int64_t lo = (int64_t)tid * per;
-  const int64_t hi = min(nrest, lo + per);
-  if (lo < hi) {
-    // decode lo over the free suffix digits (canonical order, o fixed to v)
-    int64_t q = lo;
-    for (int d = e.K - 1; d >= e.P; --d) {
-      if (o_suffix && d == e.o) { S(d) = (uint16_t)v; continue; }
-      S(d) = (uint16_t)(q % e.radix[d]);
-      q /= e.radix[d];
-    }
-    for (int64_t r = lo; r < hi; ++r) {
-      uint64_t c = 0;
-      bool inf = false;
-      for (int i = 0; i < e.nterm; ++i) {
-        const Term& tm = e.term[i];
-        const int64_t o = tm.off - e.tab_lo;
-        const V x = tm.kind == 0 ? tabs[o + S(tm.a)] : tabs[o + (int)S(tm.a) * tm.db + S(tm.b)];
-        inf |= x >= VT<V>::CAP;
-        c += (uint64_t)x;
-      }
-      if (!inf && c == target) {
-        int64_t sfx = 0;                       // suffix index in canonical order
-        for (int d = e.P; d < e.K; ++d) sfx = sfx * e.radix[d] + S(d);
-        atomicMin(&s_first, (unsigned long long)sfx);
-        break;
-      }
-      for (int d = e.K - 1; d >= e.P; --d) {   // odometer step
-        if (o_suffix && d == e.o) continue;
-        if (++S(d) < e.radix[d]) break;
-        S(d) = 0;
-      }
-    }
-  }
-  __syncthreads();
-  if (tid == 0) {
-    const uint64_t sfx = s_first;
-    uint64_t q = sfx;
-    for (int d = e.K - 1; d >= e.P; --d) { S(d) = (uint16_t)(q % e.radix[d]); q /= e.radix[d]; }
-    uint64_t idx = 0;
-    for (int d = 0; d < e.K; ++d) idx = idx * ap.orig_radix[d] + ap.maps[ap.map_off[d] + S(d)];
-    ap.A_out[outi] = (uint64_t)Aval[pair];
-    ap.I_out[outi] = sfx == ~0ull ? kInf64 : idx;     // ~0: cannot happen (exact arithmetic)
-  }
-}
-
 // --------------------------------------------------------------------------
 // Fused least-index argmin, one CTA (128 threads) per bucket (u, v):
 //  1. A = min over the chunk minima and the first chunk c* attaining it;
@@ -786,128 +528,246 @@ __global__ void __launch_bounds__(256) suffix_argmin_kernel(const ArgminParams a
 //     whose intra cost equals B_p*[v];
 //  4. outputs in the caller's (unpruned) layout: A[u][v_orig], I[u][v_orig].
 // --------------------------------------------------------------------------
+__device__ uint64_t g_argmin_dbg[16];
+__device__ __forceinline__ uint64_t gtimer2() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
 template <typename V>
-__global__ void __launch_bounds__(128) argmin_kernel(const ArgminParams ap, const V* __restrict__ vals) {
-  const FoldParams& f = ap.f;
-  const EvalSpec& e = ap.e;
-  constexpr int NT = 128;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  uint16_t* sd = reinterpret_cast<uint16_t*>(smem_raw);        // [K][NT] digits
-  __shared__ V s_best[4];
-  __shared__ int64_t s_bc[4];
+__device__ void argmin_pair(const ArgminParams& ap, const int pair, unsigned char* smem_raw) {
+  constexpr int NT = 256;
+  const int tid = threadIdx.x;
+  const bool dbg = ap.slot == 1 && tid == 0;
+  if (dbg) g_argmin_dbg[0] = gtimer2();
+  // descriptor pieces used inside loops -> shared memory (one global read each)
+  __shared__ Term s_terms[kMaxTerms];
+  __shared__ Term s_q[kMaxCross];
+  __shared__ int32_t s_rad[kMaxDigits];          // compact radices (prefix and suffix)
+  __shared__ int64_t s_misc[8];
   __shared__ unsigned long long s_first;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int pair = blockIdx.x;
-  const int u = pair / f.Do, v = pair - (pair / f.Do) * f.Do;
-  const int64_t outi = (int64_t)u * ap.Do_orig + ap.vmap[v];
-  // 1. chunk minima of this pair are contiguous
-  const V* cm = static_cast<const V*>(f.chunkmin) + (int64_t)pair * f.nchunks;
-  V best = VT<V>::CAP;
-  int64_t bc = INT64_MAX;
-  for (int64_t c = tid; c < f.nchunks; c += NT) {
-    const V x = cm[c];
-    if (x < best) { best = x; bc = c; }
+  __shared__ int s_cnt;
+  const EvalSpec& e = ap.e;
+  const FoldParams& f = ap.f;
+  for (int i = tid; i < e.nterm; i += NT) s_terms[i] = e.term[i];
+  for (int i = tid; i < f.nq; i += NT) s_q[i] = f.q[i];
+  for (int i = tid; i < e.K; i += NT) s_rad[i] = e.radix[i];
+  if (tid == 0) {
+    s_misc[0] = f.nchunks; s_misc[1] = f.nhb; s_misc[2] = f.G; s_misc[3] = f.W;
+    s_misc[4] = f.p_lo; s_misc[5] = f.Do; s_misc[6] = (int64_t)(uintptr_t)f.chunkmin;
+    s_misc[7] = (int64_t)(uintptr_t)f.Bp;
+    s_first = ~0ull;
+    s_cnt = 0;
   }
-  for (int o = 16; o > 0; o >>= 1) {
-    const V ob = __shfl_xor_sync(0xffffffffu, best, o);
-    const int64_t oc = __shfl_xor_sync(0xffffffffu, bc, o);
-    if (ob < best || (ob == best && oc < bc)) { best = ob; bc = oc; }
-  }
-  if (lane == 0) { s_best[warp] = best; s_bc[warp] = bc; }
-  if (tid == 0) s_first = ~0ull;
   __syncthreads();
-  best = s_best[0];
-  bc = s_bc[0];
-  for (int w = 1; w < NT / 32; ++w)
-    if (s_best[w] < best || (s_best[w] == best && s_bc[w] < bc)) { best = s_best[w]; bc = s_bc[w]; }
-  if (best >= VT<V>::CAP) {
+  const int64_t nchunks = s_misc[0], nhb = s_misc[1], Gh = s_misc[2], W = s_misc[3], p_lo = s_misc[4];
+  const int Do = (int)s_misc[5];
+  const V* cm = reinterpret_cast<const V*>((uintptr_t)s_misc[6]) + (int64_t)pair * nchunks;
+  const V* Bp = reinterpret_cast<const V*>((uintptr_t)s_misc[7]);
+  const V* vals = static_cast<const V*>(f.vals);
+  const int K = e.K, P = e.P, o = e.o, nterm = e.nterm, nq = f.nq;
+  uint16_t* sd = reinterpret_cast<uint16_t*>(smem_raw);        // [K][NT] digits
+  V* tabs = reinterpret_cast<V*>(smem_raw + (((size_t)K * NT * 2 + 15) & ~(size_t)15));   // W/R tables
+  for (int i = tid; i < e.tab_n; i += NT) tabs[i] = vals[e.tab_lo + i];
+  const int u = pair / Do, v = pair - (pair / Do) * Do;
+  const int64_t outi = (int64_t)u * ap.Do_orig + ap.vmap[v];
+  // 1. the bucket minimum is the (merged) A computed by amin_kernel
+  const uint64_t Ag = ap.A_glob[outi];
+  if (Ag == kInf64) {
     if (tid == 0) { ap.A_out[outi] = kInf64; ap.I_out[outi] = kInf64; }
     return;
   }
-  // 2. least canonical prefix over every chunk attaining the minimum
-  //    (chunk c = (l, hb) holds local rows (hb * kBlock + i) * W + l)
-  const V* Bp = static_cast<const V*>(f.Bp);
-  __shared__ int64_t s_list[NT];
-  __shared__ int s_cnt;
-  for (int64_t base = 0; base < f.nchunks; base += NT) {
-    if (tid == 0) s_cnt = 0;
-    __syncthreads();
-    const int64_t c = base + tid;
-    if (c < f.nchunks && cm[c] == best) s_list[atomicAdd(&s_cnt, 1)] = c;
-    __syncthreads();
-    const int cnt = s_cnt;
-    for (int li = 0; li < cnt; ++li) {
-      const int64_t cc = s_list[li];
-      const int64_t l = cc / f.nhb, hb = cc - l * f.nhb;
-      for (int i = tid; i < kBlock; i += NT) {
-        const int64_t hh = hb * kBlock + i;
-        if (hh >= f.G) break;
-        const int64_t plr = hh * f.W + l;
-        const V x = cross_sum<V>(f, vals, f.p_lo + plr, u);
-        if (VT<V>::sat(x, Bp[plr * f.Do + v]) == best) {
-          atomicMin(&s_first, (unsigned long long)plr);   // local order == canonical order
-          break;
-        }
+  const V best = (V)Ag;
+  if (dbg) g_argmin_dbg[1] = gtimer2();
+  // 2. chunks of this rank attaining it (none: this rank holds no candidate)
+  constexpr int LIST = 4 * NT;
+  __shared__ int64_t s_list[LIST];
+  for (int64_t c0 = (int64_t)tid * 4; c0 < nchunks; c0 += NT * 4) {
+    V x[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) x[q] = c0 + q < nchunks ? cm[c0 + q] : VT<V>::CAP;
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      if (x[q] == best) {
+        const int at = atomicAdd(&s_cnt, 1);
+        if (at < LIST) s_list[at] = c0 + q;
       }
-    }
-    __syncthreads();
   }
+  __syncthreads();
+  const int cnt_all = s_cnt;
+  if (cnt_all == 0) {                               // possible only with world > 1
+    if (tid == 0) { ap.A_out[outi] = kInf64; ap.I_out[outi] = kInf64; }
+    return;
+  }
+  // every row of h-block hb precedes every row of a later h-block in canonical
+  // order and every attaining chunk holds an attaining row: p* lies in the
+  // chunks of the least attaining h-block
+  __shared__ long long s_hbmin;
+  if (tid == 0) s_hbmin = 0x7FFFFFFFFFFFFFFFLL;
+  __syncthreads();
+  if (cnt_all <= LIST) {
+    for (int li = tid; li < cnt_all; li += NT) atomicMin(&s_hbmin, (long long)(s_list[li] % nhb));
+  } else {
+    for (int64_t c = tid; c < nchunks; c += NT)
+      if (cm[c] == best) atomicMin(&s_hbmin, (long long)(c % nhb));
+  }
+  __syncthreads();
+  const int64_t hbmin = s_hbmin;
+  if (dbg) g_argmin_dbg[2] = gtimer2();
+  // rows of the chunks (l, hbmin), l < W, attaining the minimum
+  __shared__ int32_t s_ls[NT];
+  __shared__ int s_nl;
+  if (tid == 0) s_nl = 0;
+  __syncthreads();
+  for (int64_t l = tid; l < W; l += NT)
+    if (cm[l * nhb + hbmin] == best) {
+      const int at = atomicAdd(&s_nl, 1);
+      if (at < NT) s_ls[at] = (int32_t)l;
+    }
+  __syncthreads();
+  const int nl = min(s_nl, NT);                       // W > NT with > NT hits: rare, see below
+  const bool all_l = s_nl > NT;
+  for (int64_t w = tid; w < (all_l ? W : (int64_t)nl) * kBlock; w += NT) {
+    const int64_t li = w / kBlock, i = w - li * kBlock;
+    const int64_t l = all_l ? li : s_ls[li];
+    const int64_t hh = hbmin * kBlock + i;
+    if (hh >= Gh) continue;
+    if (all_l && cm[l * nhb + hbmin] != best) continue;
+    const int64_t plr = hh * W + l;
+    const int64_t pg = p_lo + plr;
+    V x = 0;
+    for (int qi = 0; qi < nq; ++qi) {
+      const Term q = s_q[qi];
+      x = VT<V>::sat(x, vals[q.off + (int64_t)u * q.db + prefix_digit(pg, q.a, P, s_rad)]);
+    }
+    if (VT<V>::sat(x, Bp[plr * Do + v]) == best) atomicMin(&s_first, (unsigned long long)plr);
+  }
+  __syncthreads();
   const int64_t pl = (int64_t)s_first;
+  if (dbg) g_argmin_dbg[3] = gtimer2();
   __syncthreads();
   if (tid == 0) s_first = ~0ull;
-  const uint64_t target = (uint64_t)Bp[pl * f.Do + v];
-  const int64_t pg = f.p_lo + pl;
+  const uint64_t target = (uint64_t)Bp[pl * Do + v];
+  const int64_t pg = p_lo + pl;
   auto S = [&](int d) -> uint16_t& { return sd[d * NT + tid]; };
   {
     int64_t q = pg;
-    for (int d = e.P - 1; d >= 0; --d) { S(d) = (uint16_t)(q % e.radix[d]); q /= e.radix[d]; }
+    for (int d = P - 1; d >= 0; --d) { S(d) = (uint16_t)(q % s_rad[d]); q /= s_rad[d]; }
   }
-  const bool o_suffix = e.o >= e.P;
-  const int64_t nrest = o_suffix ? e.nsuffix / e.radix[e.o] : e.nsuffix;
+  const bool o_suffix = o >= P;
+  const int64_t nrest = o_suffix ? e.nsuffix / s_rad[o] : e.nsuffix;
   __syncthreads();
-  // 3. least suffix with intra cost == B_p*[v]
+  // 3. least suffix (canonical order, s_o = v if o is a suffix digit) whose
+  //    intra cost equals B_p*[v]
   const int64_t per = (nrest + NT - 1) / NT;
   const int64_t lo = (int64_t)tid * per;
   const int64_t hi = min(nrest, lo + per);
   if (lo < hi) {
     int64_t q = lo;
-    for (int d = e.K - 1; d >= e.P; --d) {
-      if (o_suffix && d == e.o) { S(d) = (uint16_t)v; continue; }
-      S(d) = (uint16_t)(q % e.radix[d]);
-      q /= e.radix[d];
+    for (int d = K - 1; d >= P; --d) {
+      if (o_suffix && d == o) { S(d) = (uint16_t)v; continue; }
+      S(d) = (uint16_t)(q % s_rad[d]);
+      q /= s_rad[d];
     }
     for (int64_t r = lo; r < hi; ++r) {
       uint64_t c = 0;
       bool inf = false;
-      for (int i = 0; i < e.nterm; ++i) {
-        const Term& tm = e.term[i];
-        const V x = tm.kind == 0 ? vals[tm.off + S(tm.a)] : vals[tm.off + (int)S(tm.a) * tm.db + S(tm.b)];
+      for (int i = 0; i < nterm; ++i) {
+        const Term tm = s_terms[i];
+        const int64_t to = tm.off - e.tab_lo;
+        const V x = tm.kind == 0 ? tabs[to + S(tm.a)] : tabs[to + (int)S(tm.a) * tm.db + S(tm.b)];
         inf |= x >= VT<V>::CAP;
         c += (uint64_t)x;
       }
       if (!inf && c == target) {
         int64_t sfx = 0;
-        for (int d = e.P; d < e.K; ++d) sfx = sfx * e.radix[d] + S(d);
+        for (int d = P; d < K; ++d) sfx = sfx * s_rad[d] + S(d);
         atomicMin(&s_first, (unsigned long long)sfx);
         break;
       }
-      for (int d = e.K - 1; d >= e.P; --d) {       // odometer step
-        if (o_suffix && d == e.o) continue;
-        if (++S(d) < e.radix[d]) break;
+      for (int d = K - 1; d >= P; --d) {       // odometer step
+        if (o_suffix && d == o) continue;
+        if (++S(d) < s_rad[d]) break;
         S(d) = 0;
       }
     }
   }
   __syncthreads();
+  if (dbg) g_argmin_dbg[4] = gtimer2();
   if (tid == 0) {
     const uint64_t sfx = s_first;
     uint64_t q = sfx;
-    for (int d = e.K - 1; d >= e.P; --d) { S(d) = (uint16_t)(q % e.radix[d]); q /= e.radix[d]; }
+    for (int d = K - 1; d >= P; --d) { S(d) = (uint16_t)(q % s_rad[d]); q /= s_rad[d]; }
     uint64_t idx = 0;
-    for (int d = 0; d < e.K; ++d) idx = idx * ap.orig_radix[d] + ap.maps[ap.map_off[d] + S(d)];
-    ap.A_out[outi] = (uint64_t)best;
+    for (int d = 0; d < K; ++d) idx = idx * ap.orig_radix[d] + ap.maps[ap.map_off[d] + S(d)];
+    ap.A_out[outi] = Ag;
     ap.I_out[outi] = sfx == ~0ull ? kInf64 : idx;     // ~0: cannot happen (exact arithmetic)
   }
+}
+
+// Persistent walk over a list of (transition slot, bucket) entries.
+template <typename V>
+__global__ void __launch_bounds__(256) argmin_kernel(const ArgminParams* __restrict__ aps,
+                                                     const ArgminEntry* __restrict__ list,
+                                                     const int32_t* __restrict__ count, int wide) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int n = *count;
+  for (int it = blockIdx.x; it < n; it += gridDim.x) {
+    const ArgminEntry en = list[it];
+    const ArgminParams& ap = aps[en.slot];
+    if (ap.wide != wide) continue;                  // uniform per CTA
+    const uint64_t t0 = gtimer2();
+    argmin_pair<V>(ap, en.pair, smem_raw);
+    __syncthreads();
+    if (threadIdx.x == 0 && it < 8)
+      g_argmin_dbg[8 + it] = ((gtimer2() - t0) << 16) | (uint64_t)(en.slot << 12) | (uint64_t)(en.pair & 0xFFF);
+  }
+}
+
+// A[u][v] = min over the chunk minima (values only), one warp per bucket.
+template <typename V>
+__global__ void amin_kernel(const ArgminParams* __restrict__ aps, const int64_t* __restrict__ pair_off,
+                            int nslot, int wide) {
+  const int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  int s = 0;
+  while (s < nslot && w >= pair_off[s + 1]) ++s;
+  if (s >= nslot) return;
+  const ArgminParams& ap = aps[s];
+  if (ap.wide != wide || ap.f.nchunks == 0) return;
+  const int pair = (int)(w - pair_off[s]);
+  const V* cm = static_cast<const V*>(ap.f.chunkmin) + (int64_t)pair * ap.f.nchunks;
+  V best = VT<V>::CAP;
+  for (int64_t c = lane; c < ap.f.nchunks; c += 32) best = VT<V>::mn(best, cm[c]);
+  for (int o = 16; o > 0; o >>= 1) best = VT<V>::mn(best, (V)__shfl_xor_sync(0xffffffffu, best, o));
+  if (lane == 0) {
+    const int u = pair / ap.f.Do, v = pair - u * ap.f.Do;
+    ap.A_out[(int64_t)u * ap.Do_orig + ap.vmap[v]] = best >= VT<V>::CAP ? kInf64 : (uint64_t)best;
+  }
+}
+
+// all buckets of every slot (cfp_segment_costs / full tables)
+__global__ void all_pairs_kernel(const int64_t* __restrict__ pair_off, int nslot, ArgminEntry* list, int32_t* count) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i == 0) *count = (int32_t)pair_off[nslot];
+  if (i >= pair_off[nslot]) return;
+  int s = 0;
+  while (i >= pair_off[s + 1]) ++s;
+  list[i] = ArgminEntry{s, (int32_t)(i - pair_off[s])};
+}
+
+// chain edge list (slot, u * Do_orig + v_orig) -> compact bucket entries
+__global__ void edges_to_pairs_kernel(const ArgminParams* __restrict__ aps, ArgminEntry* list,
+                                      const int32_t* __restrict__ count) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= *count) return;
+  ArgminEntry en = list[i];
+  const ArgminParams& ap = aps[en.slot];
+  const int u = en.pair / ap.Do_orig, vo = en.pair - u * ap.Do_orig;
+  const int vc = ap.vinv[vo];
+  en.pair = vc < 0 ? 0 : u * ap.f.Do + vc;       // pruned columns are INF: never optimal
+  list[i] = en;
 }
 
 // --------------------------------------------------------------------------
@@ -924,28 +784,42 @@ __device__ __forceinline__ uint64_t sat64(uint64_t a, uint64_t b) {
 
 
 
-__device__ void matvec(const uint64_t* M, int rows, int cols, const uint64_t* g, uint64_t* out,
-                       int tid, int nth) {
-  for (int u = tid; u < rows; u += nth) {
-    uint64_t best = kInf64;
-    for (int v = 0; v < cols; ++v) {
-      const uint64_t c = sat64(M[(int64_t)u * cols + v], g[v]);
-      best = c < best ? c : best;
-    }
-    out[u] = best;
-  }
-}
-
-// Single-CTA chain.  SM = true: every distinct matrix (A and, for the
-// backtrack, I), every suffix vector G_n, the powers of the current run and the
-// instance metadata live in shared memory; G is copied out at the end.
-// SM = false: same algorithm on global memory (large S).
 __device__ __forceinline__ uint64_t gtimer() {
   uint64_t t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
   return t;
 }
 
+// min_v sat64(row[v], g[v]) with four independent partial minima (ILP)
+__device__ __forceinline__ uint64_t minplus_dot(const uint64_t* row, int rstride, const uint64_t* g, int n) {
+  uint64_t b0 = kInf64, b1 = kInf64, b2 = kInf64, b3 = kInf64;
+  int v = 0;
+  for (; v + 4 <= n; v += 4) {
+    const uint64_t x0 = sat64(row[(int64_t)v * rstride], g[v]);
+    const uint64_t x1 = sat64(row[(int64_t)(v + 1) * rstride], g[v + 1]);
+    const uint64_t x2 = sat64(row[(int64_t)(v + 2) * rstride], g[v + 2]);
+    const uint64_t x3 = sat64(row[(int64_t)(v + 3) * rstride], g[v + 3]);
+    b0 = x0 < b0 ? x0 : b0;
+    b1 = x1 < b1 ? x1 : b1;
+    b2 = x2 < b2 ? x2 : b2;
+    b3 = x3 < b3 ? x3 : b3;
+  }
+  for (; v < n; ++v) {
+    const uint64_t x = sat64(row[(int64_t)v * rstride], g[v]);
+    b0 = x < b0 ? x : b0;
+  }
+  b0 = b1 < b0 ? b1 : b0;
+  b2 = b3 < b2 ? b3 : b2;
+  return b2 < b0 ? b2 : b0;
+}
+
+// Single-CTA chain.  SM = true: every distinct matrix (A and, for the
+// backtrack, I), every suffix vector G_n, the powers of the current run and the
+// instance metadata live in shared memory; G is copied out at the end.
+// SM = false: same algorithm on global memory (large S).
+// mode 0: G + backtrack; 1: G + the optimal edges reachable from u_1 = 0
+// (the only buckets whose least index the backtrack needs); 2: backtrack with
+// G already computed.
 template <bool SM>
 __global__ void __launch_bounds__(1024) chain_kernel(const ChainParams cp) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -959,7 +833,11 @@ __global__ void __launch_bounds__(1024) chain_kernel(const ChainParams cp) {
   uint64_t* sG = sI + (cp.backtrack ? cp.mat_elems : 0);
   uint64_t* sP = sG + cp.goff[N + 1];
   int64_t* sgoff = reinterpret_cast<int64_t*>(sP + (int64_t)cp.levels_max * cp.smax * cp.smax);
-  int4* sinst = reinterpret_cast<int4*>((reinterpret_cast<uintptr_t>(sgoff + N + 2) + 15) & ~uintptr_t(15));
+  int64_t* smoff = sgoff + N + 2;
+  int4* sinst = reinterpret_cast<int4*>((reinterpret_cast<uintptr_t>(smoff + cp.nmat) + 15) & ~uintptr_t(15));
+  int16_t* nxt = reinterpret_cast<int16_t*>(sinst + N);        // [goff[N]] successor of (n, u)
+  int32_t* vseq = reinterpret_cast<int32_t*>((reinterpret_cast<uintptr_t>(nxt + cp.goff[N]) + 15) & ~uintptr_t(15));
+  uint32_t* ebits = reinterpret_cast<uint32_t*>(vseq + N);     // mode 1 dedupe bitset
   uint64_t* G = SM ? sG : cp.G;
   uint64_t* Pw = SM ? sP : cp.powers;
   const int64_t* goff = SM ? sgoff : cp.goff;
@@ -981,81 +859,127 @@ __global__ void __launch_bounds__(1024) chain_kernel(const ChainParams cp) {
       }
     }
     for (int i = tid; i < N + 2; i += nth) sgoff[i] = cp.goff[i];
+    for (int i = tid; i < cp.nmat; i += nth) smoff[i] = cp.moff[i];
     for (int i = tid; i < N; i += nth) sinst[i] = make_int4(cp.inst[i].mat, cp.inst[i].rows, cp.inst[i].cols, 0);
+    if (cp.mode == 1)
+      for (int64_t i = tid; i < (cp.mat_elems + 31) / 32; i += nth) ebits[i] = 0;
     if (tma) mbar_wait(&cbar, 0);
     __syncthreads();
   }
   mark();
   auto rows_of = [&](int n) { return SM ? sinst[n].y : cp.inst[n].rows; };
   auto cols_of = [&](int n) { return SM ? sinst[n].z : cp.inst[n].cols; };
-  auto matA = [&](int n) -> const uint64_t* { return SM ? sA + cp.moff[sinst[n].x] : cp.inst[n].A; };
-  auto matI = [&](int n) -> const uint64_t* { return SM ? sI + cp.moff[sinst[n].x] : cp.inst[n].I; };
+  auto mat_of = [&](int n) { return SM ? sinst[n].x : cp.inst[n].mat; };
+  auto matA = [&](int n) -> const uint64_t* { return SM ? sA + smoff[sinst[n].x] : cp.inst[n].A; };
+  auto matI = [&](int n) -> const uint64_t* { return SM ? sI + smoff[sinst[n].x] : cp.inst[n].I; };
   const int lastc = cols_of(N - 1);
-  for (int v = tid; v < lastc; v += nth) G[goff[N] + v] = cp.terminal ? cp.terminal[v] : 0;
-  __syncthreads();
-  for (int r = cp.nruns - 1; r >= 0; --r) {
-    const ChainRun run = cp.runs[r];
-    const uint64_t* M = matA(run.first);
-    const int R = rows_of(run.first), Cc = cols_of(run.first);
-    const int e = run.first + run.len;             // G_e known (1-based instance e)
-    if (run.len == 1) {
-      const uint64_t* g = G + goff[e];
-      for (int u = tid; u < R; u += nth) {
-        uint64_t best = kInf64;
-        for (int v = 0; v < Cc; ++v) {
-          const uint64_t c = sat64(M[(int64_t)u * Cc + v], g[v]);
-          best = c < best ? c : best;
-        }
-        G[goff[e - 1] + u] = best;
+  if (cp.mode == 2) {                               // suffix vectors already computed
+    if constexpr (SM)
+      for (int64_t e2 = tid; e2 < goff[N + 1]; e2 += nth) G[e2] = cp.G[e2];
+    __syncthreads();
+  } else {
+    for (int v = tid; v < lastc; v += nth) G[goff[N] + v] = cp.terminal ? cp.terminal[v] : 0;
+    __syncthreads();
+    for (int r = cp.nruns - 1; r >= 0; --r) {
+      const ChainRun run = cp.runs[r];
+      const uint64_t* M = matA(run.first);
+      const int R = rows_of(run.first), Cc = cols_of(run.first);
+      const int e = run.first + run.len;             // G_e known (1-based instance e)
+      if (run.len == 1) {
+        const uint64_t* g = G + goff[e];
+        for (int u = tid; u < R; u += nth) G[goff[e - 1] + u] = minplus_dot(M + (int64_t)u * Cc, 1, g, Cc);
+        __syncthreads();
+        mark();
+        continue;
       }
-      __syncthreads();
-      mark();
-      continue;
-    }
-    const int S = R;                                // square
-    int levels = 0;
-    while ((1 << (levels + 1)) <= run.len) ++levels;   // P_0 .. P_levels
-    if (!SM && (int64_t)S * S * levels > cp.powers_cap) {
-      if (tid == 0) *cp.status = 4;
-      return;
-    }
-    // repeated squaring: P_j = P_{j-1} (x) P_{j-1}
-    for (int j = 1; j <= levels; ++j) {
-      const uint64_t* Pa = j == 1 ? M : Pw + (int64_t)(j - 2) * S * S;
-      uint64_t* Pc = Pw + (int64_t)(j - 1) * S * S;
-      for (int64_t c = tid; c < (int64_t)S * S; c += nth) {
-        const int i = (int)(c / S), k2 = (int)(c % S);
-        uint64_t best = kInf64;
-        for (int k = 0; k < S; ++k) {
-          const uint64_t x = sat64(Pa[(int64_t)i * S + k], Pa[(int64_t)k * S + k2]);
-          best = x < best ? x : best;
-        }
-        Pc[c] = best;
+      const int S = R;                                // square
+      int levels = 0;
+      while ((1 << (levels + 1)) <= run.len) ++levels;   // P_0 .. P_levels
+      if (!SM && (int64_t)S * S * levels > cp.powers_cap) {
+        if (tid == 0) *cp.status = 4;
+        return;
       }
-      __syncthreads();
-      mark();
-    }
-    // doubling: G_{e-k} = P_j (x) G_{e-k+2^j}, k in [2^j, 2^(j+1))
-    for (int j = 0; j <= levels; ++j) {
-      const uint64_t* Pj = j == 0 ? M : Pw + (int64_t)(j - 1) * S * S;
-      const int k_lo = 1 << j, k_hi = min(1 << (j + 1), run.len + 1);
-      const int64_t work = (int64_t)(k_hi - k_lo) * S;
-      for (int64_t w = tid; w < work; w += nth) {
-        const int k = k_lo + (int)(w / S), u = (int)(w % S);
-        const uint64_t* g = G + goff[e - k + (1 << j)];
-        uint64_t best = kInf64;
-        for (int v = 0; v < S; ++v) {
-          const uint64_t x = sat64(Pj[(int64_t)u * S + v], g[v]);
-          best = x < best ? x : best;
+      // repeated squaring: P_j = P_{j-1} (x) P_{j-1}
+      for (int j = 1; j <= levels; ++j) {
+        const uint64_t* Pa = j == 1 ? M : Pw + (int64_t)(j - 2) * S * S;
+        uint64_t* Pc = Pw + (int64_t)(j - 1) * S * S;
+        for (int64_t c = tid; c < (int64_t)S * S; c += nth) {
+          const int i = (int)(c / S), k2 = (int)(c - (int64_t)i * S);
+          Pc[c] = minplus_dot(Pa + k2, S, Pa + (int64_t)i * S, S);      // min_k Pa[i][k] + Pa[k][k2]
         }
-        G[goff[e - k] + u] = best;
+        __syncthreads();
+        mark();
       }
-      __syncthreads();
-      mark();
+      // doubling: G_{e-k} = P_j (x) G_{e-k+2^j}, k in [2^j, 2^(j+1))
+      for (int j = 0; j <= levels; ++j) {
+        const uint64_t* Pj = j == 0 ? M : Pw + (int64_t)(j - 1) * S * S;
+        const int k_lo = 1 << j, k_hi = min(1 << (j + 1), run.len + 1);
+        const int64_t work = (int64_t)(k_hi - k_lo) * S;
+        for (int64_t w = tid; w < work; w += nth) {
+          const int k = k_lo + (int)(w / S), u = (int)(w % S);
+          G[goff[e - k] + u] = minplus_dot(Pj + (int64_t)u * S, 1, G + goff[e - k + (1 << j)], S);
+        }
+        __syncthreads();
+        mark();
+      }
     }
+    if constexpr (SM)
+      for (int64_t e2 = tid; e2 < goff[N + 1]; e2 += nth) cp.G[e2] = G[e2];
   }
-  if constexpr (SM)
-    for (int64_t e2 = tid; e2 < goff[N + 1]; e2 += nth) cp.G[e2] = G[e2];
+  if (cp.mode == 1) {
+    // optimal edges reachable from u_1 = 0 (warp 0, sequential over instances;
+    // reachable states found by ballot, edges deduplicated in a shared bitset)
+    __syncthreads();
+    __shared__ int s_cnt;
+    if (tid == 0) s_cnt = 0;
+    __syncthreads();
+    if (tid < 32) {
+      const int lane = tid;
+      __shared__ uint8_t rc[2][256];
+      for (int s = lane; s < 256; s += 32) { rc[0][s] = 0; rc[1][s] = 0; }
+      __syncwarp();
+      if (lane == 0) rc[0][0] = 1;
+      __syncwarp();
+      int cur = 0;
+      for (int n = 0; n < N; ++n) {
+        const int rows = rows_of(n), cols = cols_of(n);
+        const uint64_t* A = matA(n);
+        const uint64_t* Gp = G + goff[n];
+        const uint64_t* Gn = G + goff[n + 1];
+        const int mat = mat_of(n);
+        const int64_t fo = SM ? smoff[mat] : cp.moff[mat];
+        for (int s = lane; s < 256; s += 32) rc[cur ^ 1][s] = 0;
+        __syncwarp();
+        for (int u0 = 0; u0 < rows && u0 < 256; u0 += 32) {
+          unsigned live = __ballot_sync(0xffffffffu, u0 + lane < rows && u0 + lane < 256 && rc[cur][u0 + lane] &&
+                                                         Gp[min(u0 + lane, rows - 1)] != kInf64);
+          if ((live >> lane) & 1u) cp.reach[goff[n] + u0 + lane] = 1;
+          while (live) {
+            const int u = u0 + __ffs(live) - 1;
+            live &= live - 1;
+            const uint64_t target = Gp[u];
+            for (int v = lane; v < cols; v += 32) {
+              const uint64_t a = A[(int64_t)u * cols + v];
+              if (a == kInf64 || Gn[v] == kInf64 || a + Gn[v] != target) continue;
+              if (v < 256) rc[cur ^ 1][v] = 1;
+              const int64_t bit = fo + (int64_t)u * cols + v;
+              bool fresh;
+              if constexpr (SM) {
+                fresh = !(atomicOr(&ebits[bit >> 5], 1u << (bit & 31)) & (1u << (bit & 31)));
+              } else {
+                fresh = atomicExch(cp.edge_flag + bit, 1) == 0;
+              }
+              if (fresh) cp.edge_list[atomicAdd(&s_cnt, 1)] = ArgminEntry{mat, u * cols + v};
+            }
+          }
+        }
+        __syncwarp();
+        cur ^= 1;
+      }
+      if (lane == 0) *cp.edge_count = s_cnt;
+    }
+    return;
+  }
   if (!cp.backtrack) return;
   // forward greedy: at each instance the optimal successor with the least
   // combination index.  SM mode: the successor of every (n, u) is tabulated in
@@ -1063,47 +987,59 @@ __global__ void __launch_bounds__(1024) chain_kernel(const ChainParams cp) {
   __shared__ int s_status;
   if (tid == 0) s_status = 0;
   __syncthreads();
-  if constexpr (SM) {
-    int16_t* nxt = reinterpret_cast<int16_t*>(sinst + N);   // [goff[N]] successor of (n, u)
-    const int smax = cp.smax;
-    for (int64_t w = tid; w < (int64_t)N * smax; w += nth) {
-      const int n = (int)(w / smax), u = (int)(w - (int64_t)n * smax);   // instance n + 1
-      if (u >= rows_of(n)) continue;
-      const uint64_t* A = matA(n);
-      const uint64_t* I = matI(n);
-      const int cols = cols_of(n);
-      const uint64_t target = G[goff[n] + u];
-      const uint64_t* Gn = G + goff[n + 1];
-      uint64_t bi = kInf64;
-      int bv = -1;
-      if (target != kInf64)
-        for (int v = 0; v < cols; ++v) {
-          const uint64_t a = A[(int64_t)u * cols + v];
-          if (a == kInf64 || Gn[v] == kInf64 || a + Gn[v] != target) continue;
-          const uint64_t ix = I[(int64_t)u * cols + v];
-          if (bv < 0 || ix < bi) { bi = ix; bv = v; }
+  if (SM && cp.mode == 2) {
+    // successor of every reachable (n, u) (recorded by mode 1): one warp per
+    // instance, lanes over v; then the walk from u_1 = 0 is a chain of loads
+    {
+      const int warp = tid >> 5, lane = tid & 31, nw = nth >> 5;
+      for (int n = warp; n < N; n += nw) {
+        const int rows = rows_of(n), cols = cols_of(n);
+        const uint64_t* Gn = G + goff[n + 1];
+        for (int u = 0; u < rows; ++u) {
+          if (!cp.reach[goff[n] + u]) continue;       // warp-uniform
+          const uint64_t* A = matA(n) + (int64_t)u * cols;
+          const uint64_t* I = matI(n) + (int64_t)u * cols;
+          const uint64_t target = G[goff[n] + u];
+          uint64_t bi = kInf64;
+          int bv = -1;
+          for (int v = lane; v < cols; v += 32) {
+            const uint64_t a = A[v], gv = Gn[v];
+            if (a == kInf64 || gv == kInf64 || a + gv != target) continue;
+            const uint64_t ix = I[v];
+            if (ix < bi) { bi = ix; bv = v; }
+          }
+          for (int off = 16; off > 0; off >>= 1) {
+            const uint64_t ob = __shfl_xor_sync(0xffffffffu, bi, off);
+            const int ov = __shfl_xor_sync(0xffffffffu, bv, off);
+            if (ov >= 0 && (bv < 0 || ob < bi || (ob == bi && ov < bv))) { bi = ob; bv = ov; }
+          }
+          if (lane == 0) nxt[goff[n] + u] = (int16_t)bv;
         }
-      nxt[goff[n] + u] = (int16_t)bv;
+      }
     }
     __syncthreads();
-    mark();
     if (tid == 0) {
       if (G[0] == kInf64) {
         s_status = 3;
-        *cp.total = kInf64;
       } else {
-        *cp.total = G[0];
         int u = 0;
         for (int n = 0; n < N; ++n) {
-          const int v = nxt[goff[n] + u];
+          const int v = cp.reach[goff[n] + u] ? nxt[goff[n] + u] : -1;
           if (v < 0) { s_status = 3; break; }
-          const int cols = cols_of(n);
-          cp.seg_index[n] = matI(n)[(int64_t)u * cols + v];
-          cp.seg_ns[n] = matA(n)[(int64_t)u * cols + v];
+          vseq[n] = (u << 16) | v;
           u = v;
         }
       }
     }
+    __syncthreads();
+    mark();
+    if (tid == 0) *cp.total = s_status ? kInf64 : G[0];
+    if (s_status == 0)
+      for (int n = tid; n < N; n += nth) {
+        const int u = vseq[n] >> 16, v = vseq[n] & 0xFFFF, cols = cols_of(n);
+        cp.seg_index[n] = matI(n)[(int64_t)u * cols + v];
+        cp.seg_ns[n] = matA(n)[(int64_t)u * cols + v];
+      }
   } else if (tid < 32) {
     const int lane = tid;
     int u = 0;
@@ -1146,60 +1082,21 @@ __global__ void __launch_bounds__(1024) chain_kernel(const ChainParams cp) {
   mark();
   if (tid == 0) *cp.status = s_status;
   if (s_status != 0) return;
+  __syncthreads();
   for (int64_t w = tid; w < (int64_t)N * cp.kmax; w += nth) {
     const int n = (int)(w / cp.kmax), j = (int)(w % cp.kmax);
     const ChainInst in = cp.inst[n];
     int32_t dval = -1;
     if (j < in.K) {
-      uint64_t q = cp.seg_index[n];
-      for (int d = in.K - 1; d > j; --d) q /= (uint64_t)cp.radix_blob[in.radix_off + d];
-      dval = (int32_t)(q % (uint64_t)cp.radix_blob[in.radix_off + j]);
+      uint64_t stride = 1;
+      for (int d = in.K - 1; d > j; --d) stride *= (uint64_t)cp.radix_blob[in.radix_off + d];
+      dval = (int32_t)((cp.seg_index[n] / stride) % (uint64_t)cp.radix_blob[in.radix_off + j]);
     }
     cp.digits[w] = dval;
   }
   __syncthreads();
   mark();
   if (cp.dbg && tid == 0) cp.dbg[63] = dbg_i;
-}
-
-// --------------------------------------------------------------------------
-// (min,+) product with least-k argmin (cfp_minplus_product; also the large-S
-// chain path).  16x16 output tile per CTA, K staged through shared memory.
-// --------------------------------------------------------------------------
-__global__ void __launch_bounds__(256) minplus_kernel(int m, int k, int n, const uint64_t* __restrict__ A,
-                                                      const uint64_t* __restrict__ B, uint64_t* __restrict__ C,
-                                                      uint64_t* __restrict__ argk) {
-  __shared__ uint64_t As[16][17], Bs[16][17];
-  const int ty = threadIdx.x / 16, tx = threadIdx.x % 16;
-  const int i = blockIdx.y * 16 + ty, j = blockIdx.x * 16 + tx;
-  uint64_t best = kInf64, bk = kInf64;
-  for (int k0 = 0; k0 < k; k0 += 16) {
-    As[ty][tx] = (i < m && k0 + tx < k) ? A[(int64_t)i * k + k0 + tx] : kInf64;
-    Bs[ty][tx] = (k0 + ty < k && j < n) ? B[(int64_t)(k0 + ty) * n + j] : kInf64;
-    __syncthreads();
-#pragma unroll
-    for (int q = 0; q < 16; ++q) {
-      const uint64_t x = sat64(As[ty][q], Bs[q][tx]);
-      if (x < best) { best = x; bk = (uint64_t)(k0 + q); }
-    }
-    __syncthreads();
-  }
-  if (i < m && j < n) {
-    C[(int64_t)i * n + j] = best;
-    if (argk) argk[(int64_t)i * n + j] = best == kInf64 ? kInf64 : bk;
-  }
-}
-
-__global__ void matvec_kernel(const uint64_t* __restrict__ M, int rows, int cols,
-                              const uint64_t* __restrict__ g, uint64_t* __restrict__ out) {
-  const int u = blockIdx.x * blockDim.x + threadIdx.x;
-  if (u >= rows) return;
-  uint64_t best = kInf64;
-  for (int v = 0; v < cols; ++v) {
-    const uint64_t c = sat64(M[(int64_t)u * cols + v], g[v]);
-    best = c < best ? c : best;
-  }
-  out[u] = best;
 }
 
 // --------------------------------------------------------------------------
@@ -1253,10 +1150,8 @@ template <typename V>
 cudaError_t launch_build_tables(const TableSpec* specs, int nspecs, int64_t max_entries, const V* vals,
                                 V* out, cudaStream_t st) {
   if (nspecs == 0) return cudaSuccess;
-  int64_t blocks = (max_entries + 255) / 256;
-  if (blocks > 4096) blocks = 4096;
-  if (blocks < 1) blocks = 1;
-  build_table_kernel<V><<<dim3((unsigned)blocks, nspecs), 256, 0, st>>>(specs, vals, out);
+  // max_entries carries the total CTA count (sum of the tables' nblocks)
+  build_table_kernel<V><<<(unsigned)max_entries, 256, 0, st>>>(specs, vals, out);
   CFP_LAUNCH_CHECK();
   return cudaSuccess;
 }
@@ -1282,6 +1177,9 @@ cudaError_t launch_enum_nb(const EnumParams& p, int64_t nthreads, size_t smem, c
       cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
       if (e != cudaSuccess) return e;
     }
+    // maximum shared-memory carveout: four CTAs of the fold epilogue per SM
+    cudaError_t e2 = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    if (e2 != cudaSuccess) return e2;
     kern<<<(unsigned)blocks, kBlock, sm, st>>>(p);
     return cudaGetLastError();
   };
@@ -1302,26 +1200,53 @@ cudaError_t launch_enum(const EnumParams& p, int NB, int64_t nthreads, size_t sm
   }
 }
 
+
+cudaError_t argmin_debug_read(uint64_t* out16) {
+  cudaError_t e = cudaMemcpyFromSymbol(out16, g_argmin_dbg, 16 * sizeof(uint64_t));
+  if (e != cudaSuccess) return e;
+  uint64_t t[16];
+  e = cudaMemcpyFromSymbol(t, g_enum_dbg2, 16 * sizeof(uint64_t));
+  if (e != cudaSuccess) return e;
+  fprintf(stderr, "enum CTA0 (us): prologue %.2f main %.2f | tau0 X %.2f fold %.2f red %.2f | warp main-loop ends:",
+          (t[1] - t[0]) * 1e-3, (t[2] - t[1]) * 1e-3, (t[3] - t[2]) * 1e-3, (t[4] - t[3]) * 1e-3,
+          (t[5] - t[4]) * 1e-3);
+  for (int w = 0; w < 8; ++w) fprintf(stderr, " %.2f", ((int64_t)t[8 + w] - (int64_t)t[1]) * 1e-3);
+  fprintf(stderr, "\n");
+  return cudaSuccess;
+}
+
 template <typename V>
-cudaError_t launch_fold(const FoldMulti& fm, int grid, cudaStream_t st) {
-  const FoldSmem L = fold_layout(fm, (int)sizeof(V));
-  const size_t smem = (size_t)L.total;
-  auto k = fold_kernel<V>;
+cudaError_t launch_argmin(const ArgminParams* aps, const ArgminEntry* list, const int32_t* count, int grid,
+                          int kmax, int tabn_max, cudaStream_t st) {
+  const size_t smem = (((size_t)kmax * 256 * 2 + 15) & ~(size_t)15) + (size_t)tabn_max * sizeof(V) + 16;
   if (smem > 48 * 1024) {
-    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaError_t e = cudaFuncSetAttribute(argmin_kernel<V>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
   }
-  k<<<(unsigned)grid, 256, smem, st>>>(fm);
+  argmin_kernel<V><<<grid, 256, smem, st>>>(aps, list, count, sizeof(V) == 8 ? 1 : 0);
   CFP_LAUNCH_CHECK();
   return cudaSuccess;
 }
 
 template <typename V>
-cudaError_t launch_argmin(const ArgminParams& ap, V* Aval, const V* vals, cudaStream_t st) {
-  (void)Aval;
-  const int pairs = ap.f.Din * ap.f.Do;
-  const size_t smem = (size_t)ap.e.K * 128 * 2 + 16;
-  argmin_kernel<V><<<pairs, 128, smem, st>>>(ap, vals);
+cudaError_t launch_amin(const ArgminParams* aps, const int64_t* pair_off, int nslot, int64_t total,
+                        cudaStream_t st) {
+  if (total <= 0) return cudaSuccess;
+  amin_kernel<V><<<(unsigned)((total * 32 + 255) / 256), 256, 0, st>>>(aps, pair_off, nslot, sizeof(V) == 8 ? 1 : 0);
+  CFP_LAUNCH_CHECK();
+  return cudaSuccess;
+}
+
+cudaError_t launch_all_pairs(const int64_t* pair_off, int nslot, int64_t total, ArgminEntry* list, int32_t* count,
+                             cudaStream_t st) {
+  all_pairs_kernel<<<(unsigned)((total + 255) / 256 + 1), 256, 0, st>>>(pair_off, nslot, list, count);
+  CFP_LAUNCH_CHECK();
+  return cudaSuccess;
+}
+
+cudaError_t launch_edges_to_pairs(const ArgminParams* aps, ArgminEntry* list, const int32_t* count, int64_t cap,
+                                  cudaStream_t st) {
+  edges_to_pairs_kernel<<<(unsigned)((cap + 255) / 256 + 1), 256, 0, st>>>(aps, list, count);
   CFP_LAUNCH_CHECK();
   return cudaSuccess;
 }
@@ -1341,20 +1266,7 @@ cudaError_t launch_chain(const ChainParams& cp, cudaStream_t st) {
   return cudaSuccess;
 }
 
-cudaError_t launch_minplus(int m, int k, int n, const uint64_t* A, const uint64_t* B, uint64_t* C,
-                           uint64_t* argk, cudaStream_t st) {
-  dim3 grid((n + 15) / 16, (m + 15) / 16);
-  minplus_kernel<<<grid, 256, 0, st>>>(m, k, n, A, B, C, argk);
-  CFP_LAUNCH_CHECK();
-  return cudaSuccess;
-}
 
-cudaError_t launch_matvec(const uint64_t* M, int rows, int cols, const uint64_t* g, uint64_t* out,
-                          cudaStream_t st) {
-  matvec_kernel<<<(rows + 255) / 256, 256, 0, st>>>(M, rows, cols, g, out);
-  CFP_LAUNCH_CHECK();
-  return cudaSuccess;
-}
 
 cudaError_t launch_intpipe(int op, int blocks, int iters, uint32_t* out, cudaStream_t st) {
   if (op == 0) intpipe_kernel<0><<<blocks, 1024, 0, st>>>(out, iters, 7u);
@@ -1372,9 +1284,9 @@ template cudaError_t launch_fill<uint32_t>(uint32_t*, int64_t, uint32_t, cudaStr
 template cudaError_t launch_fill<uint64_t>(uint64_t*, int64_t, uint64_t, cudaStream_t);
 template cudaError_t launch_enum<uint32_t>(const EnumParams&, int, int64_t, size_t, cudaStream_t);
 template cudaError_t launch_enum<uint64_t>(const EnumParams&, int, int64_t, size_t, cudaStream_t);
-template cudaError_t launch_fold<uint32_t>(const FoldMulti&, int, cudaStream_t);
-template cudaError_t launch_fold<uint64_t>(const FoldMulti&, int, cudaStream_t);
-template cudaError_t launch_argmin<uint32_t>(const ArgminParams&, uint32_t*, const uint32_t*, cudaStream_t);
-template cudaError_t launch_argmin<uint64_t>(const ArgminParams&, uint64_t*, const uint64_t*, cudaStream_t);
+template cudaError_t launch_argmin<uint32_t>(const ArgminParams*, const ArgminEntry*, const int32_t*, int, int, int, cudaStream_t);
+template cudaError_t launch_argmin<uint64_t>(const ArgminParams*, const ArgminEntry*, const int32_t*, int, int, int, cudaStream_t);
+template cudaError_t launch_amin<uint32_t>(const ArgminParams*, const int64_t*, int, int64_t, cudaStream_t);
+template cudaError_t launch_amin<uint64_t>(const ArgminParams*, const int64_t*, int, int64_t, cudaStream_t);
 
 }  // namespace cfp
