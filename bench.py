@@ -268,6 +268,22 @@ def run_cfp(args, prob, rank, world, local_rank):
     enum_avg_ms = enum_tot / args.steps
     achieved_gops = info.combos_local / (enum_avg_ms * 1e-3) / 1e9
     peak = alu_peak_gops(1965.0)
+    # N5 microbenchmark (measured ALU lane-op rate of VIADDMNMX.U32 on this GPU)
+    ip_ops, ip_ms = ctx.intpipe_bench(0, 4000)
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "r01_ncu_enum.json")) as fh:
+            traffic = json.load(fh)["traffic_bytes_per_launch"]["enum_kernel"]
+    except Exception:
+        pass
+    minplus = None
+    if args.minplus and rank == 0:
+        minplus = []
+        for S in (256, 1024, 4096, 8192):
+            for wide in (False, True):
+                ms, ops = ctx.minplus_bench(S, wide=wide, iters=3 if S < 8192 else 1)
+                minplus.append({"S": S, "dtype": "u64" if wide else "u32", "ms": ms,
+                                "addmin_per_s": ops, "frac_of_alu_peak": ops / (peak * 1e9)})
     out = None
     if rank == 0:
         out = {
@@ -289,14 +305,21 @@ def run_cfp(args, prob, rank, world, local_rank):
                     "plan_search_ms": e2e_med},
             "gpu_launches": info.kernel_launches,
             "roofline": {"bound": "alu", "achieved": achieved_gops, "peak": peak, "unit": "Gop/s",
-                         "frac": achieved_gops / peak, "traffic": None,
+                         "frac": achieved_gops / peak, "traffic": traffic,
                          "note": "op = one VIADDMNMX.U32 lane-op (fused add+min) per strategy combination; "
                                  "peak = 64 lane-ops/clk/SM x 148 SMs x 1965 MHz (derived, DESIGN.md); "
-                                 "achieved over the enumeration phase of each step"},
+                                 "achieved = combos / device time of the enumeration phase (all enum "
+                                 "launches incl. the cross-term fold epilogue); traffic = DRAM bytes per "
+                                 "enum launch from ncu (profiles/r01_ncu_enum.json), algorithmic bytes ~0"},
+            "intpipe_measured": {"op": "VIADDMNMX.U32", "lane_ops_per_s": ip_ops,
+                                 "lane_ops_per_clk_per_sm": ip_ops / (SMS * 1e6 * (clocks["sm_mhz"] or 1965.0)),
+                                 "frac_of_derived_peak": ip_ops / (peak * 1e9)},
             "clocks": clocks,
             "schedule": info.schedule,
             "plan_total_ns": plan.total_ns,
         }
+        if minplus is not None:
+            out["minplus_microbench"] = minplus
     prep.close()
     ctx.close()
     return out
@@ -312,6 +335,7 @@ def main():
     ap.add_argument("--dist", default="shaped")
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--minplus", action="store_true", help="also run the (min,+) product microbenchmark")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))

@@ -364,7 +364,8 @@ double schedule_cost(const HostType& t, int P, const std::vector<int>& role, int
   int64_t Hh = nP / W;
   int64_t Gpad = (Hh + kBlock - 1) / kBlock * kBlock;
   double threads = (double)Gpad * W * VG;
-  double per_thread = (double)nM * ((double)NB * na_pad + NB + 10.0) + 40.0;
+  double per_thread = (double)nM * ((double)NB * na + NB + 10.0) + 40.0;
+  (void)na_pad;
   int regs = NB <= 8 ? 40 : NB <= 16 ? 56 : NB <= 24 ? 72 : 96;
   int ctas_per_sm = std::max(1, std::min(8, 65536 / (regs * kBlock)));
   double slots = (double)sms * ctas_per_sm * kBlock;
@@ -416,9 +417,10 @@ Schedule plan_schedule(const HostType& t, const std::vector<int>& fold_digits, i
       }
       if (na > 4096 || nb > 32) continue;
       const bool b_is_o = nb_d == 1 && role[t.o] == 3;
-      for (int NB : {4, 8, 12, 16, 24, 32}) {
+      for (int NB : {4, 8, 12, 16, 23, 24, 32}) {
         int VG = (int)((nb + NB - 1) / NB);
         if (VG > 1 && !b_is_o) continue;
+        if (NB % 4 != 0 && VG > 1) continue;             // register groups start on 16-byte rows
         if (NB > 4 && NB >= 2 * nb && NB != 4) continue;
         double cost = schedule_cost(t, P, role, NB, VG, ntrans_in, sms, din_max);
         if (cost < best.cost * 0.999) {
@@ -851,7 +853,7 @@ static cfp_status prepare_impl(cfp_ctx* ctx, const cfp_problem* p, bool do_chain
     }
     const int VG = sc.VG, NB = sc.NB;
     const int na_pad = round_up(na, 4);
-    const int nb_pad = VG * NB;
+    const int nb_pad = round_up((int64_t)VG * NB, 4);
     TableSpec sx = make_spec(dx, r, nA, na_pad);
     TableSpec sy = make_spec(dy, r, nBd, nb_pad);
     TableSpec sz = make_spec(dz, r, 0, 1);
@@ -1018,7 +1020,7 @@ static cfp_status prepare_impl(cfp_ctx* ctx, const cfp_problem* p, bool do_chain
     // cross-term fold in the enumeration epilogue: one chunk = one CTA
     {
       const bool simple = ep.o_mode == 0 && ep.o_bstride == 1 && ep.o_bradix == ep.nb;
-      const int64_t VP = simple ? te.NB : ((ep.Do + 3) & ~3);
+      const int64_t VP = simple ? ((te.NB + 3) & ~3) : ((ep.Do + 3) & ~3);   // = the kernel's VP bound
       int64_t dinp_max = 4;
       for (int x : te.trans) dinp_max = std::max<int64_t>(dinp_max, (P->trans[trans_slot[x]].Din + 3) & ~3);
       int64_t epi = kBlock * VP + kBlock * dinp_max;

@@ -24,7 +24,6 @@ namespace cfp {
 constexpr int kMaxDigits = 32;
 constexpr int kMaxTerms = 96;
 constexpr int kMaxCross = 16;    // cross edges per transition
-constexpr int kMaxFoldTau = 4;   // transitions folded by one launch
 constexpr int kBlock = 256;          // threads per CTA of the enumeration kernel
 constexpr uint32_t kCap32 = 0x7FFFFFFFu;            // narrow "infinity" (>= CAP => INF)
 constexpr uint64_t kCap64 = 0x7FFFFFFFFFFFFFFFull;  // wide "infinity"

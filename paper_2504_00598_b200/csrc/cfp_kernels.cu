@@ -1,15 +1,18 @@
 // cfp_kernels.cu -- sm_100a kernels of the CFP plan-search hot path.
 //
 // Hot path and where each step lives:
-//   a0 stage:       compact_kernel (prune + p+c), build_table_kernel (X/Y/Z/K0)
-//   a1 enumerate:   enum_kernel  -- one VIADDMNMX per strategy combination
-//   a1 fold:        fold_kernel  -- cross-segment terms Q_j[u][s_j] folded per
-//                                   prefix: A[u][v] = min_p X_p[u] + B_p[v]
-//   a1 argmin:      fold_reduce_kernel + suffix_argmin_kernel -- least index
-//   a2 merge:       NCCL min-allreduce on packed keys (host side, world > 1)
-//   a3 chain:       chain_kernel -- (min,+) powers by repeated squaring,
-//                                   suffix vectors by doubling
-//   a4 backtrack:   chain_kernel (forward greedy) + plan decode
+//   a0 stage:      compact_kernel (prune + p+c), build_table_kernel (X/Y/Z/K0)
+//   a1 enumerate:  enum_kernel -- one VIADDMNMX per strategy combination; its
+//                  epilogue folds the cross-segment terms of every incoming
+//                  transition into per-CTA chunk minima
+//   a1 reduce:     amin_kernel -- A[u][v] = min over chunk minima
+//   a3 chain:      chain_kernel mode 1 -- (min,+) powers by repeated squaring,
+//                  suffix vectors by doubling, optimal edges reachable from
+//                  the chain start
+//   a1 argmin:     argmin_kernel -- least combination index of those buckets
+//                  (every bucket for cfp_segment_costs)
+//   a2 merge:      NCCL min-allreduce (host side, world > 1)
+//   a4 backtrack:  chain_kernel mode 2 -- forward greedy + plan decode
 // Everything is exact integer arithmetic; the narrow path keeps values in
 // [0, CAP32] with CAP32 = 2^31-1 meaning "infeasible" (any sum >= CAP is
 // infeasible, guaranteed by the host's bound check), so the fused
@@ -224,6 +227,16 @@ __device__ __forceinline__ void load_vec<uint64_t>(const uint64_t* p, uint64_t* 
   const ulonglong2 v = *reinterpret_cast<const ulonglong2*>(p);
   out[0] = v.x; out[1] = v.y;
 }
+template <typename V>
+__device__ __forceinline__ void store_vec(V* p, const V* in);
+template <>
+__device__ __forceinline__ void store_vec<uint32_t>(uint32_t* p, const uint32_t* in) {
+  *reinterpret_cast<uint4*>(p) = make_uint4(in[0], in[1], in[2], in[3]);
+}
+template <>
+__device__ __forceinline__ void store_vec<uint64_t>(uint64_t* p, const uint64_t* in) {
+  *reinterpret_cast<ulonglong2*>(p) = make_ulonglong2(in[0], in[1]);
+}
 
 template <typename V>
 __device__ __forceinline__ void atomic_min_v(V* p, V v);
@@ -319,20 +332,27 @@ __global__ void __launch_bounds__(kBlock, 4) enum_kernel(const EnumParams p) {
       const int4 mt = MT[m];
       const V km = T::sat(k0, ZT[sz + mt.z]);
       const V* yr = YT + sy + mt.y + ybase;
-      V y[NB];
+      constexpr int NBV = (NB + VN - 1) / VN * VN;   // Y rows are padded to whole vectors
+      V y[NBV];
 #pragma unroll
-      for (int j = 0; j < NB; j += VN) load_vec<V>(yr + j, y + j);
+      for (int j = 0; j < NBV; j += VN) load_vec<V>(yr + j, y + j);
 #pragma unroll
       for (int j = 0; j < NB; ++j) y[j] = T::sat(y[j], km);
       const V* xr = XT + sx + mt.x;
+      const int na_v = p.na & ~(VN - 1);
 #pragma unroll 2
-      for (int a = 0; a < p.na_pad; a += VN) {
+      for (int a = 0; a < na_v; a += VN) {
         V x[VN];
         load_vec<V>(xr + a, x);
 #pragma unroll
         for (int q = 0; q < VN; ++q)
 #pragma unroll
           for (int j = 0; j < NB; ++j) acc[j] = T::addmin(x[q], y[j], acc[j]);
+      }
+      for (int a = na_v; a < p.na; ++a) {           // ragged A tail (no padded evaluations)
+        const V x = xr[a];
+#pragma unroll
+        for (int j = 0; j < NB; ++j) acc[j] = T::addmin(x, y[j], acc[j]);
       }
       if (p.o_mode == 1) {                        // bucket digit in M: flush per m
         V r = acc[0];
@@ -364,7 +384,6 @@ __global__ void __launch_bounds__(kBlock, 4) enum_kernel(const EnumParams p) {
     }
   }
   if (edbg) g_enum_dbg2[2] = gtimer0();
-  if (blockIdx.x == 0 && p.ntau == 2 && (tid & 31) == 0) g_enum_dbg2[8 + (tid >> 5)] = gtimer0();
   if (p.ntau == 0) return;
   // ---- epilogue: fold the cross-segment terms of every incoming transition
   __syncthreads();                                // staged tables no longer needed
@@ -374,7 +393,15 @@ __global__ void __launch_bounds__(kBlock, 4) enum_kernel(const EnumParams p) {
   const int VP = (v_cnt + 3) & ~3;
   V* Bs = reinterpret_cast<V*>(smem_raw);                     // [kBlock][VP]
   V* Xs = Bs + kBlock * VP;                                   // [kBlock][DinP] (red afterwards)
-  if (simple) {
+  if (simple && VP == NB) {                       // 16-byte stores (conflict-light rows)
+#pragma unroll
+    for (int j = 0; j < NB; j += VN) {
+      V w[VN];
+#pragma unroll
+      for (int q = 0; q < VN; ++q) w[q] = (live && j + q < v_cnt) ? acc[j + q] : T::CAP;
+      store_vec<V>(Bs + tid * VP + j, w);
+    }
+  } else if (simple) {
 #pragma unroll
     for (int j = 0; j < NB; ++j)
       if (j < VP) Bs[tid * VP + j] = (live && j < v_cnt) ? acc[j] : T::CAP;
@@ -421,8 +448,8 @@ __global__ void __launch_bounds__(kBlock, 4) enum_kernel(const EnumParams p) {
           for (int k2 = 0; k2 < 4; ++k2)
             x[k2] = T::sat(T::sat(x[k2], y0[k2]), T::sat(T::sat(y1[k2], y2[k2]), y3[k2]));
         }
-#pragma unroll
-        for (int k2 = 0; k2 < 4; ++k2) Xs[tid * DinP + u0 + k2] = x[k2];
+        store_vec<V>(Xs + tid * DinP + u0, x);
+        if (VN == 2) store_vec<V>(Xs + tid * DinP + u0 + 2, x + 2);
       }
       for (int i = 4; i < nq; ++i) {                 // rare: more than four cross terms
         const V* qi = vals + et.q[i].off + digit_of(et.q[i].a);
@@ -1194,6 +1221,7 @@ cudaError_t launch_enum(const EnumParams& p, int NB, int64_t nthreads, size_t sm
     case 8: return launch_enum_nb<V, 8>(p, nthreads, smem, st);
     case 12: return launch_enum_nb<V, 12>(p, nthreads, smem, st);
     case 16: return launch_enum_nb<V, 16>(p, nthreads, smem, st);
+    case 23: return launch_enum_nb<V, 23>(p, nthreads, smem, st);
     case 24: return launch_enum_nb<V, 24>(p, nthreads, smem, st);
     case 32: return launch_enum_nb<V, 32>(p, nthreads, smem, st);
     default: return cudaErrorInvalidValue;
@@ -1207,11 +1235,9 @@ cudaError_t argmin_debug_read(uint64_t* out16) {
   uint64_t t[16];
   e = cudaMemcpyFromSymbol(t, g_enum_dbg2, 16 * sizeof(uint64_t));
   if (e != cudaSuccess) return e;
-  fprintf(stderr, "enum CTA0 (us): prologue %.2f main %.2f | tau0 X %.2f fold %.2f red %.2f | warp main-loop ends:",
+  fprintf(stderr, "enum CTA0 (us): prologue %.2f main %.2f | tau0 X %.2f fold %.2f red %.2f\n",
           (t[1] - t[0]) * 1e-3, (t[2] - t[1]) * 1e-3, (t[3] - t[2]) * 1e-3, (t[4] - t[3]) * 1e-3,
           (t[5] - t[4]) * 1e-3);
-  for (int w = 0; w < 8; ++w) fprintf(stderr, " %.2f", ((int64_t)t[8 + w] - (int64_t)t[1]) * 1e-3);
-  fprintf(stderr, "\n");
   return cudaSuccess;
 }
 
