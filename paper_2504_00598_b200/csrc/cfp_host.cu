@@ -958,6 +958,11 @@ static cfp_status prepare_impl(cfp_ctx* ctx, const cfp_problem* p, bool do_chain
     const size_t vbytes = te.wide ? 8 : 4;
     size_t smem = (size_t)(ep.xspan + ep.yspan + ((ep.zspan + 3) & ~3LL)) * vbytes + (size_t)nM * 16;
     ep.staged = smem <= 160 * 1024;
+    {
+      const size_t ymb = (size_t)nM * ep.nb_pad * vbytes;   // merged Y'[m][j] rows
+      ep.ymerge = ep.staged && ymb <= 64 * 1024 && smem + ymb <= 160 * 1024;
+      if (ep.ymerge) smem += ymb;
+    }
     ep.init_row = ep.o_mode != 0 || !(ep.o_bstride == 1 && ep.o_bradix == ep.nb);
     te.smem = ep.staged ? smem : 0;
     te.nthreads = ep.Gpad * ep.W * ep.VG;

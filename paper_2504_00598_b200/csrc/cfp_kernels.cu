@@ -254,8 +254,14 @@ __device__ __forceinline__ void atomic_min_v<uint64_t>(uint64_t* p, uint64_t v) 
 //    chunkmin_t[u][v][chunk] = min_{p in chunk} X^t_p[u] + B_p[v],
 //    X^t_p[u] = sum_{cross (j, Q)} Q[u][s_j(p)]          (Eq. 3 r_n)
 // with 4x4 register-blocked fused add+mins over the chunk's rows.
-template <typename V, int NB, bool STAGED>
+// ST = 0: tables read from global/L2; 1: CTA slices staged in shared memory;
+// 2: staged, and the Z term folded into per-m copies of the Y rows
+// (Y'[m][j] = Y[m][j] + Z[m]) with K0[p] added once after the enumeration --
+// no per-m saturating add in the loop (exact: min(K0 + t) = K0 + min t).
+template <typename V, int NB, int ST>
 __global__ void __launch_bounds__(kBlock, 4) enum_kernel(const EnumParams p) {
+  constexpr bool STAGED = ST > 0;
+  constexpr bool MERGED = ST == 2;
   using T = VT<V>;
   constexpr int VN = Vec4<V>::N;
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -317,6 +323,17 @@ __global__ void __launch_bounds__(kBlock, 4) enum_kernel(const EnumParams p) {
     __syncthreads();
     XT = xs; YT = ys; ZT = zs; MT = ms;
     sx = sy = sz = 0;
+    if constexpr (MERGED) {
+      V* ym = reinterpret_cast<V*>(ms + p.nM);
+      const int64_t n = p.nM * p.nb_pad;
+      for (int64_t e = tid; e < n; e += kBlock) {
+        const int64_t m = e / p.nb_pad;
+        const int4 mt = ms[m];
+        ym[e] = T::sat(ys[mt.y + (e - m * p.nb_pad)], zs[mt.z]);
+      }
+      __syncthreads();
+      YT = ym;
+    }
   }
   if (edbg) g_enum_dbg2[1] = gtimer0();
   V* Bp = static_cast<V*>(p.Bp) + row * p.Do;
@@ -330,14 +347,20 @@ __global__ void __launch_bounds__(kBlock, 4) enum_kernel(const EnumParams p) {
     const V k0 = static_cast<const V*>(p.K0)[pg];
     for (int64_t m = 0; m < p.nM; ++m) {
       const int4 mt = MT[m];
-      const V km = T::sat(k0, ZT[sz + mt.z]);
-      const V* yr = YT + sy + mt.y + ybase;
       constexpr int NBV = (NB + VN - 1) / VN * VN;   // Y rows are padded to whole vectors
       V y[NBV];
+      if constexpr (MERGED) {
+        const V* yr = YT + m * p.nb_pad + ybase;
 #pragma unroll
-      for (int j = 0; j < NBV; j += VN) load_vec<V>(yr + j, y + j);
+        for (int j = 0; j < NBV; j += VN) load_vec<V>(yr + j, y + j);
+      } else {
+        const V km = T::sat(k0, ZT[sz + mt.z]);
+        const V* yr = YT + sy + mt.y + ybase;
 #pragma unroll
-      for (int j = 0; j < NB; ++j) y[j] = T::sat(y[j], km);
+        for (int j = 0; j < NBV; j += VN) load_vec<V>(yr + j, y + j);
+#pragma unroll
+        for (int j = 0; j < NB; ++j) y[j] = T::sat(y[j], km);
+      }
       const V* xr = XT + sx + mt.x;
       const int na_v = p.na & ~(VN - 1);
 #pragma unroll 2
@@ -358,9 +381,16 @@ __global__ void __launch_bounds__(kBlock, 4) enum_kernel(const EnumParams p) {
         V r = acc[0];
 #pragma unroll
         for (int j = 1; j < NB; ++j) r = T::mn(r, acc[j]);
+        if constexpr (MERGED) r = T::sat(r, k0);
         Bp[mt.w] = T::mn(Bp[mt.w], r);
 #pragma unroll
         for (int j = 0; j < NB; ++j) acc[j] = T::CAP;
+      }
+    }
+    if constexpr (MERGED) {
+      if (p.o_mode != 1) {
+#pragma unroll
+        for (int j = 0; j < NB; ++j) acc[j] = T::sat(acc[j], k0);
       }
     }
     if (p.o_mode == 0) {
@@ -1210,8 +1240,9 @@ cudaError_t launch_enum_nb(const EnumParams& p, int64_t nthreads, size_t smem, c
     kern<<<(unsigned)blocks, kBlock, sm, st>>>(p);
     return cudaGetLastError();
   };
-  if (p.staged) return launch(enum_kernel<V, NB, true>);
-  return launch(enum_kernel<V, NB, false>);
+  if (p.staged && p.ymerge) return launch(enum_kernel<V, NB, 2>);
+  if (p.staged) return launch(enum_kernel<V, NB, 1>);
+  return launch(enum_kernel<V, NB, 0>);
 }
 
 template <typename V>
