@@ -323,3 +323,225 @@ int orc_minplus(int32_t m, int32_t k, int32_t n, const uint64_t* A, const uint64
     }
   return ORC_OK;
 }
+
+/* ---------------------------------------------------------------------------
+ * Memory-constrained search (NEXT-1).  Same plain style: every combination's
+ * cost and quantised memory recomputed from the definition.
+ * ------------------------------------------------------------------------- */
+static uint64_t ceil_div(uint64_t a, uint64_t b) { return a / b + (a % b != 0); }
+
+static uint64_t block_q(const orc_type* t, int32_t j, int32_t s, uint64_t quantum) {
+  if (!t->mem) return 0;
+  int64_t off = 0;
+  for (int32_t q = 0; q < j; ++q) off += t->radix[q];
+  return ceil_div((uint64_t)t->mem[off + s], quantum);   /* R-M1: per-block ceiling */
+}
+
+uint64_t orc_mem_q(const orc_type* t, const int32_t* s, uint64_t quantum) {
+  uint64_t q = 0;                                         /* Eq. 4 within a segment */
+  for (int32_t j = 0; j < t->K; ++j) q += block_q(t, j, s[j], quantum);
+  return q;
+}
+
+int orc_mem_range(const orc_type* t, uint64_t quantum, int64_t* qlo, int64_t* qhi) {
+  if (quantum == 0) return ORC_EINVAL;
+  int64_t lo = 0, hi = 0;
+  for (int32_t j = 0; j < t->K; ++j) {
+    uint64_t mn = ORC_INF64, mx = 0;
+    for (int32_t s = 0; s < t->radix[j]; ++s) {
+      uint64_t q = block_q(t, j, s, quantum);
+      if (q < mn) mn = q;
+      if (q > mx) mx = q;
+    }
+    lo += (int64_t)mn;
+    hi += (int64_t)mx;
+  }
+  *qlo = lo;
+  *qhi = hi;
+  return ORC_OK;
+}
+
+int orc_segment_table_mem(const orc_problem* p, int32_t tr, uint64_t quantum,
+                          uint64_t* Am, uint64_t* Im, int nthreads) {
+  if (tr < 0 || tr >= p->ntrans || quantum == 0) return ORC_EINVAL;
+  const orc_type* t = &p->types[p->trans[tr].type];
+  if (t->K > 64) return ORC_ETOOBIG;
+  int64_t qlo, qhi;
+  orc_mem_range(t, quantum, &qlo, &qhi);
+  const int64_t nq = qhi - qlo + 1;
+  const int32_t din = d_in_of(p, tr);
+  const int32_t dout = t->radix[t->out_block];
+  const uint64_t S = space_size(t);
+  const int nt = nthreads_or_default(nthreads);
+  const size_t cells = (size_t)din * dout * nq;
+  uint64_t* LA = (uint64_t*)malloc(sizeof(uint64_t) * cells * nt);
+  uint64_t* LI = (uint64_t*)malloc(sizeof(uint64_t) * cells * nt);
+  if (!LA || !LI) { free(LA); free(LI); return ORC_ENOMEM; }
+  for (size_t c = 0; c < cells * nt; ++c) { LA[c] = ORC_INF64; LI[c] = ORC_NOIDX; }
+#pragma omp parallel for schedule(static, 1) num_threads(nt)
+  for (int ch = 0; ch < nt; ++ch) {
+    uint64_t lo = S * (uint64_t)ch / nt, hi = S * (uint64_t)(ch + 1) / nt;
+    uint64_t* a = LA + cells * ch;
+    uint64_t* ix = LI + cells * ch;
+    int32_t s[64];
+    for (int32_t u = 0; u < din; ++u) {
+      for (uint64_t idx = lo; idx < hi; ++idx) {
+        orc_decode(t->K, t->radix, idx, s);
+        uint64_t c = orc_cost(p, tr, u, s);
+        int64_t q = (int64_t)orc_mem_q(t, s, quantum);
+        size_t cell = ((size_t)u * dout + s[t->out_block]) * nq + (size_t)(q - qlo);
+        if (c < a[cell]) { a[cell] = c; ix[cell] = idx; }
+      }
+    }
+  }
+  for (size_t c = 0; c < cells; ++c) { Am[c] = ORC_INF64; Im[c] = ORC_NOIDX; }
+  for (int ch = 0; ch < nt; ++ch)            /* chunk order == index order */
+    for (size_t c = 0; c < cells; ++c)
+      if (LA[cells * ch + c] < Am[c]) { Am[c] = LA[cells * ch + c]; Im[c] = LI[cells * ch + c]; }
+  free(LA); free(LI);
+  return ORC_OK;
+}
+
+static int64_t* mem_offsets(int32_t N, const int32_t* rows, const int32_t* cols, int64_t Qmax) {
+  int64_t* off = (int64_t*)malloc(sizeof(int64_t) * (N + 2));
+  if (!off) return NULL;
+  off[0] = 0;
+  off[1] = (int64_t)rows[0] * (Qmax + 1);
+  for (int32_t n = 1; n <= N; ++n) off[n + 1] = off[n] + (int64_t)cols[n - 1] * (Qmax + 1);
+  return off;
+}
+
+int orc_chain_mem(int32_t N, const int32_t* rows, const int32_t* cols, const int32_t* nq,
+                  const int64_t* qlo, const uint64_t* const* Am, int64_t Qmax, uint64_t* G) {
+  if (N < 1 || Qmax < 0) return ORC_EINVAL;
+  for (int32_t n = 1; n < N; ++n) if (rows[n] != cols[n - 1]) return ORC_EINVAL;
+  int64_t* off = mem_offsets(N, rows, cols, Qmax);
+  if (!off) return ORC_ENOMEM;
+  const int64_t C = Qmax + 1;
+  uint64_t* GN = G + off[N];
+  for (int64_t i = 0; i < (int64_t)cols[N - 1] * C; ++i) GN[i] = 0;   /* free final layout */
+  for (int32_t n = N; n >= 1; --n) {
+    /* G_{n-1}(u, c) = min_{v, q : c + q <= Qmax} Am_n[u][v][q] + G_n(v, c + q) */
+    const uint64_t* M = Am[n - 1];
+    const uint64_t* Gn = G + off[n];
+    uint64_t* Gp = G + off[n - 1];
+    const int32_t D = cols[n - 1], Q = nq[n - 1];
+    for (int32_t u = 0; u < rows[n - 1]; ++u)
+      for (int64_t c = 0; c < C; ++c) {
+        uint64_t best = ORC_INF64;
+        for (int32_t v = 0; v < D; ++v)
+          for (int32_t k = 0; k < Q; ++k) {
+            const int64_t q = qlo[n - 1] + k;
+            if (c + q > Qmax) continue;
+            uint64_t x = add_inf(M[((int64_t)u * D + v) * Q + k], Gn[(int64_t)v * C + c + q]);
+            if (x < best) best = x;
+          }
+        Gp[(int64_t)u * C + c] = best;
+      }
+  }
+  free(off);
+  return ORC_OK;
+}
+
+int orc_reconstruct_mem(int32_t N, const int32_t* rows, const int32_t* cols, const int32_t* nq,
+                        const int64_t* qlo, const uint64_t* const* Am, const uint64_t* const* Im,
+                        int64_t Qmax, const uint64_t* G, int32_t* v_out, int64_t* q_out,
+                        uint64_t* idx_out, uint64_t* cost_out) {
+  int64_t* off = mem_offsets(N, rows, cols, Qmax);
+  if (!off) return ORC_ENOMEM;
+  const int64_t C = Qmax + 1;
+  if (G[0] == ORC_INF64) { free(off); return ORC_EINFEASIBLE; }
+  int32_t u = 0;                               /* (u_1, c) = (0, 0) */
+  int64_t c = 0;
+  for (int32_t n = 1; n <= N; ++n) {
+    const uint64_t* M = Am[n - 1];
+    const uint64_t* Ix = Im[n - 1];
+    const int32_t D = cols[n - 1], Q = nq[n - 1];
+    const uint64_t target = G[off[n - 1] + (int64_t)u * C + c];
+    const uint64_t* Gn = G + off[n];
+    int64_t best = -1;
+    for (int32_t v = 0; v < D; ++v)
+      for (int32_t k = 0; k < Q; ++k) {
+        const int64_t q = qlo[n - 1] + k;
+        if (c + q > Qmax) continue;
+        const int64_t cell = ((int64_t)u * D + v) * Q + k;
+        uint64_t a = M[cell], g = Gn[(int64_t)v * C + c + q];
+        if (a == ORC_INF64 || g == ORC_INF64 || a + g != target) continue;
+        if (best < 0 || Ix[cell] < Ix[best]) best = cell;
+      }
+    if (best < 0) { free(off); return ORC_EINFEASIBLE; }
+    const int32_t v = (int32_t)((best / Q) % D);
+    const int64_t q = qlo[n - 1] + best % Q;
+    v_out[n - 1] = v;
+    q_out[n - 1] = q;
+    idx_out[n - 1] = Ix[best];
+    cost_out[n - 1] = M[best];
+    u = v;
+    c += q;
+  }
+  free(off);
+  return ORC_OK;
+}
+
+int orc_search_plan_mem(const orc_problem* p, uint64_t quantum, uint64_t mem_limit, int nthreads,
+                        uint64_t* total, uint64_t* seg_index, int32_t* digits, int32_t kmax,
+                        uint64_t* seg_ns, int64_t* seg_q, int64_t* total_q) {
+  const int32_t N = p->N;
+  if (N < 1 || quantum == 0) return ORC_EINVAL;
+  const int64_t Qmax = (int64_t)(mem_limit / quantum);
+  if (Qmax > (1 << 22)) return ORC_ETOOBIG;
+  uint64_t** At = (uint64_t**)calloc(p->ntrans, sizeof(uint64_t*));
+  uint64_t** It = (uint64_t**)calloc(p->ntrans, sizeof(uint64_t*));
+  const uint64_t** An = (const uint64_t**)malloc(sizeof(uint64_t*) * N);
+  const uint64_t** In = (const uint64_t**)malloc(sizeof(uint64_t*) * N);
+  int32_t* rows = (int32_t*)malloc(sizeof(int32_t) * N);
+  int32_t* cols = (int32_t*)malloc(sizeof(int32_t) * N);
+  int32_t* nq = (int32_t*)malloc(sizeof(int32_t) * N);
+  int64_t* qlo = (int64_t*)malloc(sizeof(int64_t) * N);
+  int32_t* vsel = (int32_t*)malloc(sizeof(int32_t) * N);
+  int rc = ORC_OK;
+  uint64_t* G = NULL;
+  if (!At || !It || !An || !In || !rows || !cols || !nq || !qlo || !vsel) { rc = ORC_ENOMEM; goto done; }
+  int64_t gsz = 0;
+  for (int32_t n = 0; n < N; ++n) {
+    int32_t tr = p->inst[n];
+    if (tr < 0 || tr >= p->ntrans) { rc = ORC_EINVAL; goto done; }
+    const orc_type* t = &p->types[p->trans[tr].type];
+    int64_t lo, hi;
+    orc_mem_range(t, quantum, &lo, &hi);
+    rows[n] = d_in_of(p, tr);
+    cols[n] = t->radix[t->out_block];
+    nq[n] = (int32_t)(hi - lo + 1);
+    qlo[n] = lo;
+    gsz += cols[n];
+    if (!At[tr]) {
+      size_t cells = (size_t)rows[n] * cols[n] * nq[n];
+      At[tr] = (uint64_t*)malloc(sizeof(uint64_t) * cells);
+      It[tr] = (uint64_t*)malloc(sizeof(uint64_t) * cells);
+      if (!At[tr] || !It[tr]) { rc = ORC_ENOMEM; goto done; }
+      rc = orc_segment_table_mem(p, tr, quantum, At[tr], It[tr], nthreads);
+      if (rc) goto done;
+    }
+    An[n] = At[tr];
+    In[n] = It[tr];
+  }
+  G = (uint64_t*)malloc(sizeof(uint64_t) * (gsz + rows[0]) * (Qmax + 1));
+  if (!G) { rc = ORC_ENOMEM; goto done; }
+  rc = orc_chain_mem(N, rows, cols, nq, qlo, An, Qmax, G);
+  if (rc) goto done;
+  *total = G[0];
+  rc = orc_reconstruct_mem(N, rows, cols, nq, qlo, An, In, Qmax, G, vsel, seg_q, seg_index, seg_ns);
+  if (rc) goto done;
+  *total_q = 0;
+  for (int32_t n = 0; n < N; ++n) {
+    const orc_type* t = &p->types[p->trans[p->inst[n]].type];
+    for (int32_t j = 0; j < kmax; ++j) digits[(int64_t)n * kmax + j] = -1;
+    orc_decode(t->K, t->radix, seg_index[n], digits + (int64_t)n * kmax);
+    *total_q += seg_q[n];
+  }
+done:
+  if (At) for (int32_t q = 0; q < p->ntrans; ++q) free(At[q]);
+  if (It) for (int32_t q = 0; q < p->ntrans; ++q) free(It[q]);
+  free(At); free(It); free(An); free(In); free(rows); free(cols); free(nq); free(qlo); free(vsel); free(G);
+  return rc;
+}

@@ -23,6 +23,21 @@
  *      G_N = terminal (0); G_{n-1}(u) = min_v A_n[u][v] + G_n(v); OPT = G_0(0).
  *  - reconstruction: forward greedy choosing, among optimal successors, the
  *    least combination index (lexicographically smallest plan tuple).
+ *
+ * Memory-constrained search (Eq. 4):
+ *  - per-block peak memory m_j[s], quantised per block with a
+ *    ceiling: q_j[s] = ceil(m_j[s] / quantum)  (reading R-M1 in DESIGN.md:
+ *    the factored model's profile unit is the ParallelBlock; the
+ *    ceiling over-approximates, so a plan is never falsely feasible);
+ *    segment memory q(s) = sum_j q_j[s_j]  (Eq. 4 restricted to a segment);
+ *  - Am[u][v][q - qlo] = min_{s: s_o = v, q(s) = q} C(u,s), Im = least index;
+ *    qlo/qhi = sum_j min/max_s q_j[s] over all strategies;
+ *  - chain state (u, c), c = quantised memory used so far:
+ *      G_N(v, c) = 0 for c <= Qmax = floor(mem_limit / quantum);
+ *      G_{n-1}(u, c) = min_{v, q: c + q <= Qmax} Am_n[u][v][q] + G_n(v, c + q);
+ *      OPT = G_0(0, 0);
+ *  - reconstruction: forward greedy from (u, c) = (0, 0) choosing, among the
+ *    optimal successors (v, q), the least combination index.
  */
 #ifndef CFP_ORACLE_H
 #define CFP_ORACLE_H
@@ -47,6 +62,7 @@ typedef struct {
   const int32_t* edst;      /* [E] */
   const uint32_t* etab;     /* concat row-major [D_src][D_dst] */
   int32_t out_block;
+  const uint32_t* mem;      /* [sum D] m_j[s] (NEXT-1), nullable = 0 */
 } orc_type;
 
 typedef struct {
@@ -96,6 +112,30 @@ int orc_search_plan(const orc_problem* p, int nthreads, uint64_t* total,
 /* (A (x) B)[i][j] = min_k A[i][k] + B[k][j]; argk = least k (NOIDX if INF). */
 int orc_minplus(int32_t m, int32_t k, int32_t n, const uint64_t* A, const uint64_t* B,
                 uint64_t* C, uint64_t* argk);
+/* ---- memory-constrained search (NEXT-1) ---- */
+/* qlo/qhi of a type: sum_j min/max_s ceil(m_j[s] / quantum). */
+int orc_mem_range(const orc_type* t, uint64_t quantum, int64_t* qlo, int64_t* qhi);
+/* q(s) = sum_j ceil(m_j[s_j] / quantum). */
+uint64_t orc_mem_q(const orc_type* t, const int32_t* s, uint64_t quantum);
+/* Am, Im: [D_in][D_o][qhi - qlo + 1]. */
+int orc_segment_table_mem(const orc_problem* p, int32_t tr, uint64_t quantum,
+                          uint64_t* Am, uint64_t* Im, int nthreads);
+/* Backward DP over (u, c).  Instance n has matrix Am[n] of shape
+ * rows[n] x cols[n] x nq[n] with memory offset qlo[n].  G receives N+1 blocks
+ * [S][Qmax + 1]: G_0 (rows[0]) then G_n (cols[n-1]). */
+int orc_chain_mem(int32_t N, const int32_t* rows, const int32_t* cols, const int32_t* nq,
+                  const int64_t* qlo, const uint64_t* const* Am, int64_t Qmax, uint64_t* G);
+/* Forward greedy from (0, 0): per instance the chosen v, q (absolute), index
+ * and cost.  EINFEASIBLE if G_0(0, 0) is INF. */
+int orc_reconstruct_mem(int32_t N, const int32_t* rows, const int32_t* cols, const int32_t* nq,
+                        const int64_t* qlo, const uint64_t* const* Am, const uint64_t* const* Im,
+                        int64_t Qmax, const uint64_t* G, int32_t* v_out, int64_t* q_out,
+                        uint64_t* idx_out, uint64_t* cost_out);
+/* Full memory-constrained search; seg_q[n] = q of segment n, total_q = sum. */
+int orc_search_plan_mem(const orc_problem* p, uint64_t quantum, uint64_t mem_limit, int nthreads,
+                        uint64_t* total, uint64_t* seg_index, int32_t* digits, int32_t kmax,
+                        uint64_t* seg_ns, int64_t* seg_q, int64_t* total_q);
+
 /* Big-endian mixed-radix decode. */
 void orc_decode(int32_t K, const int32_t* radix, uint64_t idx, int32_t* digits);
 

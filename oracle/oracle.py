@@ -39,7 +39,7 @@ class _Type(C.Structure):
                 ("comp", C.POINTER(C.c_uint32)), ("comm", C.POINTER(C.c_uint32)),
                 ("E", C.c_int32), ("esrc", C.POINTER(C.c_int32)),
                 ("edst", C.POINTER(C.c_int32)), ("etab", C.POINTER(C.c_uint32)),
-                ("out_block", C.c_int32)]
+                ("out_block", C.c_int32), ("mem", C.POINTER(C.c_uint32))]
 
 
 class _Trans(C.Structure):
@@ -78,6 +78,18 @@ def lib():
                                       P(C.c_int32), C.c_int32, P(C.c_uint64)]
         L.orc_minplus.argtypes = [C.c_int32, C.c_int32, C.c_int32, P(C.c_uint64), P(C.c_uint64),
                                   P(C.c_uint64), P(C.c_uint64)]
+        L.orc_mem_range.argtypes = [P(_Type), C.c_uint64, P(C.c_int64), P(C.c_int64)]
+        L.orc_segment_table_mem.argtypes = [P(_Problem), C.c_int32, C.c_uint64, P(C.c_uint64),
+                                            P(C.c_uint64), C.c_int]
+        L.orc_chain_mem.argtypes = [C.c_int32, P(C.c_int32), P(C.c_int32), P(C.c_int32),
+                                    P(C.c_int64), P(P(C.c_uint64)), C.c_int64, P(C.c_uint64)]
+        L.orc_reconstruct_mem.argtypes = [C.c_int32, P(C.c_int32), P(C.c_int32), P(C.c_int32),
+                                          P(C.c_int64), P(P(C.c_uint64)), P(P(C.c_uint64)),
+                                          C.c_int64, P(C.c_uint64), P(C.c_int32), P(C.c_int64),
+                                          P(C.c_uint64), P(C.c_uint64)]
+        L.orc_search_plan_mem.argtypes = [P(_Problem), C.c_uint64, C.c_uint64, C.c_int,
+                                          P(C.c_uint64), P(C.c_uint64), P(C.c_int32), C.c_int32,
+                                          P(C.c_uint64), P(C.c_int64), P(C.c_int64)]
         _lib = L
     return _lib
 
@@ -102,10 +114,12 @@ class Marshalled:
             etab = self._k(np.concatenate([np.ascontiguousarray(e.table, dtype=np.uint32).ravel()
                                            for e in ty.edges]) if ty.edges
                            else np.zeros(1, np.uint32))
+            mem = None if ty.mem is None else self._k(np.ascontiguousarray(ty.mem, dtype=np.uint32))
             types[i] = _Type(ty.K, _ptr(radix, C.c_int32), _ptr(comp, C.c_uint32),
                              _ptr(comm, C.c_uint32) if comm is not None else None,
                              len(ty.edges), _ptr(esrc, C.c_int32), _ptr(edst, C.c_int32),
-                             _ptr(etab, C.c_uint32), ty.out_block)
+                             _ptr(etab, C.c_uint32), ty.out_block,
+                             _ptr(mem, C.c_uint32) if mem is not None else None)
         trans = (_Trans * len(prob.transitions))()
         for i, tr in enumerate(prob.transitions):
             xdst = self._k(np.array([x.dst for x in tr.in_edges] or [0], dtype=np.int32))
@@ -336,3 +350,165 @@ def brute_force_table(prob: Problem, tr: int) -> Tuple[np.ndarray, np.ndarray]:
                 A[u, v] = c
                 I[u, v] = idx
     return A, I
+
+
+# ---------------------------------------------------------------------------
+# memory-constrained search (Eq. 4)
+# ---------------------------------------------------------------------------
+def mem_range(prob: Problem, type_id: int, quantum: int, m: Optional[Marshalled] = None) -> Tuple[int, int]:
+    """(qlo, qhi) = sum_j min/max_s ceil(m_j[s] / quantum)."""
+    m = m or Marshalled(prob)
+    lo, hi = C.c_int64(), C.c_int64()
+    _check(lib().orc_mem_range(C.byref(m.types[type_id]), quantum, C.byref(lo), C.byref(hi)),
+           "mem_range")
+    return int(lo.value), int(hi.value)
+
+
+def segment_table_mem(prob: Problem, tr: int, quantum: int, nthreads: int = 0,
+                      m: Optional[Marshalled] = None) -> Tuple[np.ndarray, np.ndarray, int]:
+    """Am, Im [D_in][D_o][nq] and qlo (Am[u][v][q - qlo])."""
+    m = m or Marshalled(prob)
+    ty = prob.transitions[tr].type
+    qlo, qhi = mem_range(prob, ty, quantum, m)
+    din, dout = prob.d_in(tr), prob.d_out(tr)
+    A = np.empty((din, dout, qhi - qlo + 1), dtype=np.uint64)
+    I = np.empty_like(A)
+    _check(lib().orc_segment_table_mem(m.ref, tr, quantum, _ptr(A, C.c_uint64), _ptr(I, C.c_uint64),
+                                       nthreads), "segment_table_mem")
+    return A, I, qlo
+
+
+def chain_mem(mats: Sequence[np.ndarray], qlos: Sequence[int], Qmax: int) -> List[np.ndarray]:
+    """Backward DP over (u, c); returns [G_0, ..., G_N], G_n of shape [S][Qmax+1]."""
+    mats = [np.ascontiguousarray(M, dtype=np.uint64) for M in mats]
+    N = len(mats)
+    rows = np.array([M.shape[0] for M in mats], dtype=np.int32)
+    cols = np.array([M.shape[1] for M in mats], dtype=np.int32)
+    nq = np.array([M.shape[2] for M in mats], dtype=np.int32)
+    qlo = np.ascontiguousarray(qlos, dtype=np.int64)
+    G = np.empty(int(rows[0] + cols.sum()) * (Qmax + 1), dtype=np.uint64)
+    _check(lib().orc_chain_mem(N, _ptr(rows, C.c_int32), _ptr(cols, C.c_int32), _ptr(nq, C.c_int32),
+                               _ptr(qlo, C.c_int64), _mat_ptrs(mats), Qmax, _ptr(G, C.c_uint64)),
+           "chain_mem")
+    out, off = [G[:rows[0] * (Qmax + 1)].reshape(rows[0], Qmax + 1)], int(rows[0]) * (Qmax + 1)
+    for c in cols:
+        out.append(G[off:off + int(c) * (Qmax + 1)].reshape(int(c), Qmax + 1))
+        off += int(c) * (Qmax + 1)
+    return out
+
+
+def reconstruct_mem(mats, idxs, qlos, Qmax: int, G: List[np.ndarray]):
+    mats = [np.ascontiguousarray(M, dtype=np.uint64) for M in mats]
+    idxs = [np.ascontiguousarray(M, dtype=np.uint64) for M in idxs]
+    N = len(mats)
+    rows = np.array([M.shape[0] for M in mats], dtype=np.int32)
+    cols = np.array([M.shape[1] for M in mats], dtype=np.int32)
+    nq = np.array([M.shape[2] for M in mats], dtype=np.int32)
+    qlo = np.ascontiguousarray(qlos, dtype=np.int64)
+    Gf = np.ascontiguousarray(np.concatenate([g.ravel() for g in G]), dtype=np.uint64)
+    v = np.empty(N, np.int32)
+    q = np.empty(N, np.int64)
+    ix = np.empty(N, np.uint64)
+    cost = np.empty(N, np.uint64)
+    _check(lib().orc_reconstruct_mem(N, _ptr(rows, C.c_int32), _ptr(cols, C.c_int32),
+                                     _ptr(nq, C.c_int32), _ptr(qlo, C.c_int64), _mat_ptrs(mats),
+                                     _mat_ptrs(idxs), Qmax, _ptr(Gf, C.c_uint64), _ptr(v, C.c_int32),
+                                     _ptr(q, C.c_int64), _ptr(ix, C.c_uint64), _ptr(cost, C.c_uint64)),
+           "reconstruct_mem")
+    return v, q, ix, cost
+
+
+def search_plan_mem(prob: Problem, quantum: int, mem_limit: int, nthreads: int = 0) -> Dict:
+    m = Marshalled(prob)
+    N = len(prob.instances)
+    kmax = prob.k_max()
+    total, total_q = C.c_uint64(), C.c_int64()
+    idx = np.empty(N, np.uint64)
+    dig = np.empty(N * kmax, np.int32)
+    seg = np.empty(N, np.uint64)
+    segq = np.empty(N, np.int64)
+    _check(lib().orc_search_plan_mem(m.ref, quantum, mem_limit, nthreads, C.byref(total),
+                                     _ptr(idx, C.c_uint64), _ptr(dig, C.c_int32), kmax,
+                                     _ptr(seg, C.c_uint64), _ptr(segq, C.c_int64), C.byref(total_q)),
+           "search_plan_mem")
+    return dict(total=int(total.value), seg_index=idx, digits=dig.reshape(N, kmax), seg_ns=seg,
+                seg_q=segq, total_q=int(total_q.value))
+
+
+def py_mem_q(ty, s: Sequence[int], quantum: int) -> int:
+    """q(s) = sum_j ceil(m_j[s_j] / quantum) (pure Python, independent of the C code)."""
+    return sum(-(-int(ty.mem_of(j)[s[j]]) // quantum) for j in range(ty.K))
+
+
+def py_mem_exact(ty, s: Sequence[int]) -> int:
+    return sum(int(ty.mem_of(j)[s[j]]) for j in range(ty.K))
+
+
+def brute_force_mem(prob: Problem, quantum: int, mem_limit: int, limit: int = 10 ** 6) -> Dict:
+    """All global plans in lexicographic order; feasible iff
+    sum_n q_n <= floor(mem_limit / quantum) (Eq. 4 with per-block ceilings);
+    minimal Eq. 3 total, lexicographically smallest tuple."""
+    Qmax = mem_limit // quantum
+    spaces = []
+    for t in prob.instances:
+        ty = prob.types[prob.transitions[int(t)].type]
+        spaces.append(range(int(np.prod([int(d) for d in ty.radix]))))
+    n_plans = 1
+    for sp in spaces:
+        n_plans *= len(sp)
+    if n_plans > limit:
+        raise ValueError(f"brute force guard: {n_plans} plans > {limit}")
+    best = None
+    for plan in product(*spaces):
+        u, total, mq, mex = 0, 0, 0, 0
+        segs, qs = [], []
+        ok = True
+        for n, idx in enumerate(plan):
+            tr = int(prob.instances[n])
+            ty = prob.types[prob.transitions[tr].type]
+            s = _digits(ty.radix, idx)
+            c = py_cost(prob, tr, u, s)
+            if c is None:
+                ok = False
+                break
+            q = py_mem_q(ty, s, quantum)
+            segs.append(c)
+            qs.append(q)
+            total += c
+            mq += q
+            mex += py_mem_exact(ty, s)
+            u = s[ty.out_block]
+        if not ok or mq > Qmax:
+            continue
+        if best is None or total < best[0]:
+            best = (total, plan, segs, qs, mq, mex)
+    if best is None:
+        return dict(total=None)
+    total, plan, segs, qs, mq, mex = best
+    return dict(total=total, seg_index=np.array(plan, dtype=np.uint64),
+                seg_ns=np.array(segs, dtype=np.uint64), seg_q=np.array(qs, dtype=np.int64),
+                total_q=mq, mem_exact=mex)
+
+
+def brute_force_table_mem(prob: Problem, tr: int, quantum: int):
+    """Am/Im of one transition by direct enumeration in Python (tiny only)."""
+    ty = prob.types[prob.transitions[tr].type]
+    qs = [[-(-int(x) // quantum) for x in ty.mem_of(j)] for j in range(ty.K)]
+    qlo = sum(min(q) for q in qs)
+    qhi = sum(max(q) for q in qs)
+    din, dout = prob.d_in(tr), prob.d_out(tr)
+    A = np.full((din, dout, qhi - qlo + 1), INF64, dtype=np.uint64)
+    I = np.full_like(A, NOIDX)
+    S = int(np.prod([int(d) for d in ty.radix]))
+    for u in range(din):
+        for idx in range(S):
+            s = _digits(ty.radix, idx)
+            c = py_cost(prob, tr, u, s)
+            if c is None:
+                continue
+            k = py_mem_q(ty, s, quantum) - qlo
+            v = s[ty.out_block]
+            if c < int(A[u, v, k]):
+                A[u, v, k] = c
+                I[u, v, k] = idx
+    return A, I, qlo

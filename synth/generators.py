@@ -134,6 +134,20 @@ def unary_costs(shape: BlockShape, strategy, mesh, jitter: float) -> Tuple[int, 
     return min(int(p), CAP_UNARY), min(int(math.ceil(c)), CAP_UNARY)
 
 
+def block_memory_kib(shape: BlockShape, strategy, mesh) -> int:
+    """Peak memory of one block strategy in KiB (NEXT-1 memory model, App. C
+    style): bf16 weight + fp32 master copy + Adam moments = 16 B per parameter,
+    sharded by the strategy's N and K splits, plus the bf16 output activation
+    kept for backward, sharded by its M and N splits."""
+    pm = _split(strategy, mesh, ("B", "S", "M"))
+    pn = _split(strategy, mesh, ("N",))
+    pk = _split(strategy, mesh, ("K",))
+    M = shape.B * shape.S
+    wstate = 16.0 * shape.K * shape.N / (pn * pk)
+    act = 2.0 * M * shape.N / (pm * pn)
+    return int(math.ceil((wstate + act) / 1024.0))
+
+
 def _out_layout(d):
     return {"B": "B", "S": "S", "M": "M", "N": "H", "K": "P", None: "R"}[d]
 
@@ -265,9 +279,10 @@ def _block_strats(cfg_mesh, spec):
 
 def _segment_type(tables: _Tables, spec, shapes, edges, out_block, name) -> SegmentType:
     mesh, strats = _block_strats(spec["mesh"], spec)
-    comp, comm = [], []
+    comp, comm, mem = [], [], []
     feas = []
     for shape in shapes:
+        mem.append(np.array([block_memory_kib(shape, s, mesh) for s in strats], dtype=np.uint32))
         jit = tables.jitter(len(strats))
         f = np.array([feasible(shape, s, mesh) for s in strats])
         pc = [unary_costs(shape, s, mesh, jit[i]) for i, s in enumerate(strats)]
@@ -285,7 +300,8 @@ def _segment_type(tables: _Tables, spec, shapes, edges, out_block, name) -> Segm
         E.append(Edge(a, b, tables.redraw(R, inf)))
     return SegmentType(radix=np.full(len(shapes), len(strats), dtype=np.int32),
                        comp_ns=np.concatenate(comp), comm_ns=np.concatenate(comm),
-                       edges=E, out_block=out_block, name=name), feas
+                       edges=E, out_block=out_block, name=name,
+                       mem=np.concatenate(mem)), feas
 
 
 def _cross(tables: _Tables, spec, pred_feas, pred_out, dst_feas, j_in) -> List[CrossEdge]:
@@ -389,7 +405,13 @@ def tiny_random(seed: int, mode: Optional[str] = None, max_n: int = 4, max_k: in
                     tab[int(rng.integers(0, radix[a]))] = INF32
                 edges.append(Edge(int(a), int(b), tab))
         o = int(rng.integers(0, K))
-        types.append(SegmentType(radix, comp, comm, edges, o, f"T{t}"))
+        # memory tables from a separate stream (keeps the cost streams of
+        # earlier corpus versions unchanged): small integers so quantum = 1
+        # brute force stays meaningful; None (all 0) w.p. 0.15
+        mrng = np.random.default_rng([seed, 7, t])
+        mem = (None if mrng.random() < 0.15 else
+               mrng.integers(0, 6, size=sD).astype(np.uint32))
+        types.append(SegmentType(radix, comp, comm, edges, o, f"T{t}", mem=mem))
     # chain of types with runs
     seq = []
     N_target = int(rng.integers(1, max_n + 1))

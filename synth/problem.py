@@ -46,6 +46,16 @@ class SegmentType:
     edges: List[Edge]
     out_block: int
     name: str = ""
+    # per-strategy peak memory m_j[s] of each ParallelBlock ("peak memory
+    # consumption", P:608 m_n; NEXT-1), uint32 in caller-chosen units (the
+    # generators use KiB); None -> 0.  Eq. 4 sums it over the plan.
+    mem: Optional[np.ndarray] = None
+
+    def mem_of(self, j: int) -> np.ndarray:
+        o = self.offsets()
+        if self.mem is None:
+            return np.zeros(int(self.radix[j]), dtype=np.uint32)
+        return self.mem[o[j]:o[j + 1]]
 
     @property
     def K(self) -> int:

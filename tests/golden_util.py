@@ -22,7 +22,8 @@ def problem_from(d) -> Problem:
             comp_ns=np.array(t["comp"], np.uint32),
             comm_ns=None if t["comm"] is None else np.array(t["comm"], np.uint32),
             edges=[Edge(a, b, np.array(tab, np.uint32)) for a, b, tab in t["edges"]],
-            out_block=t["out_block"]))
+            out_block=t["out_block"],
+            mem=None if t.get("mem") is None else np.array(t["mem"], np.uint32)))
     trs = [Transition(x["pred"], x["type"], [CrossEdge(j, np.array(tab, np.uint32))
                                              for j, tab in x["in"]]) for x in d["transitions"]]
     return Problem((1,), types, trs, np.array(d["instances"], np.int32), "golden")
