@@ -82,6 +82,12 @@ struct cfp_ctx {
   int world = 1, rank = 0;
   ncclComm_t comm = nullptr;
   int sms = 148;
+  // side streams for concurrent per-type enumerations (fork/join by events):
+  // the types are independent until the bucket reduction, and running them
+  // side by side packs their CTAs into the same waves (no per-launch tail)
+  static constexpr int kLanes = 3;
+  cudaStream_t lane[kLanes] = {};
+  cudaEvent_t fork = nullptr, join[kLanes] = {};
 };
 
 extern "C" cfp_status cfp_nccl_unique_id(void* out128) {
@@ -122,6 +128,11 @@ extern "C" cfp_status cfp_ctx_create(cfp_ctx** out, const cfp_ctx_opts* opts) {
     CUDA_TRY(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
     c->own_stream = true;
   }
+  for (int i = 0; i < cfp_ctx::kLanes; ++i) {
+    CUDA_TRY(cudaStreamCreateWithFlags(&c->lane[i], cudaStreamNonBlocking));
+    CUDA_TRY(cudaEventCreateWithFlags(&c->join[i], cudaEventDisableTiming));
+  }
+  CUDA_TRY(cudaEventCreateWithFlags(&c->fork, cudaEventDisableTiming));
   {
     cudaMemPool_t pool;
     CUDA_TRY(cudaDeviceGetDefaultMemPool(&pool, c->device));
@@ -142,6 +153,11 @@ extern "C" void cfp_ctx_destroy(cfp_ctx* c) {
   if (!c) return;
   cudaSetDevice(c->device);
   if (c->comm) ncclCommDestroy(c->comm);
+  for (int i = 0; i < cfp_ctx::kLanes; ++i) {
+    if (c->lane[i]) cudaStreamDestroy(c->lane[i]);
+    if (c->join[i]) cudaEventDestroy(c->join[i]);
+  }
+  if (c->fork) cudaEventDestroy(c->fork);
   if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
   delete c;
 }
@@ -266,6 +282,7 @@ struct TypeExec {
 struct TransExec {
   int id = 0, type = 0, Din = 1, Do = 1, Do_orig = 1;
   std::vector<int64_t> q_off;               // value blob offsets of compact Q tables
+  std::vector<int64_t> qt_off;              // ... and of their transposed copies
   FoldParams fp{};
   ArgminParams ap{};
   int64_t chunk_off = 0, aval_off = 0, pstar_off = 0;  // scratch offsets (bytes)
@@ -383,6 +400,7 @@ Schedule plan_schedule(const HostType& t, const std::vector<int>& fold_digits, i
   int Pmin = 0;
   for (int d : fold_digits) Pmin = std::max(Pmin, d + 1);
   Schedule best;
+  static const int force_nb = getenv("CFP_ENUM_NB") ? atoi(getenv("CFP_ENUM_NB")) : 0;
   int64_t nP = prod(r, 0, Pmin);
   for (int P = Pmin; P <= t.K; ++P) {
     if (P > Pmin) nP *= r[P - 1];
@@ -418,6 +436,7 @@ Schedule plan_schedule(const HostType& t, const std::vector<int>& fold_digits, i
       if (na > 4096 || nb > 32) continue;
       const bool b_is_o = nb_d == 1 && role[t.o] == 3;
       for (int NB : {4, 8, 12, 16, 23, 24, 32}) {
+        if (force_nb > 0 && NB != force_nb && nb >= force_nb) continue;   // tuning override
         int VG = (int)((nb + NB - 1) / NB);
         if (VG > 1 && !b_is_o) continue;
         if (NB % 4 != 0 && VG > 1) continue;             // register groups start on 16-byte rows
@@ -664,7 +683,8 @@ static cfp_status setup_chain_staging(ChainParams& cp, const std::vector<ChainIn
   cp.smax = smax;
   const int64_t need = (tot * (cp.backtrack ? 2 : 1) + g_elems + (int64_t)levels_max * smax * smax) * 8 +
                        (int64_t)(cp.N + 2) * 8 + (int64_t)mats.size() * 8 + (int64_t)cp.N * 16 + 128 +
-                       g_elems * 2 + 16 + (int64_t)cp.N * 4 + 16 + ((tot + 31) / 32) * 4 + 16;
+                       g_elems * 2 + 16 + (int64_t)cp.N * 4 + 16 + ((tot + 31) / 32) * 4 + 16 +
+                       g_elems * 4 + (int64_t)cp.N * 4 + 16;        // successor / reach masks
   cp.smem_bytes = need <= 200 * 1024 ? need : 0;
   return CFP_OK;
 }
@@ -776,6 +796,13 @@ static cfp_status prepare_impl(cfp_ctx* ctx, const cfp_problem* p, bool do_chain
         tx.q_off.push_back(vc);
         vc += (int64_t)cj.rows * cj.cols;
         jobs.push_back(cj);
+        // transposed copy for the enumeration epilogue (16-byte aligned rows)
+        vc = (vc + 3) & ~3LL;
+        CompactJob ct = cj;
+        ct.kind = 3; ct.rows_pad = (h.Din + 3) & ~3; ct.out_off = vc;
+        tx.qt_off.push_back(vc);
+        vc += (int64_t)ct.rows_pad * ct.cols;
+        jobs.push_back(ct);
       }
     }
     // map offsets for argmin remap
@@ -1039,7 +1066,10 @@ static cfp_status prepare_impl(cfp_ctx* ctx, const cfp_problem* p, bool do_chain
         EpiTau et{};
         et.Din = tx.Din;
         et.nq = tx.fp.nq;
-        for (int q = 0; q < tx.fp.nq; ++q) et.q[q] = tx.fp.q[q];
+        for (int q = 0; q < tx.fp.nq; ++q) {
+          et.q[q] = tx.fp.q[q];
+          et.qt[q] = tx.qt_off[q];
+        }
         P->epi_host.push_back(et);
         tx.fp.CH = kBlock;
         tx.fp.nchunks = ep.nchunks;
@@ -1341,10 +1371,28 @@ static cfp_status execute_impl(cfp_ctx* ctx, cfp_prepared* P) {
   }
   // a1: enumeration per type (largest first), then fold + argmin per transition
   if (P->timing) CUDA_TRY(cudaEventRecord(P->ev[1], st));
-  for (TypeExec& te : P->types) {
-    if (te.empty || te.nPl == 0) continue;
-    if (te.wide) TRY(run_type_kernels<uint64_t>(P, te, st, false));
-    else TRY(run_type_kernels<uint32_t>(P, te, st, false));
+  {
+    // types (largest first) round-robin over the caller's stream and the side
+    // lanes; they write disjoint scratch (own B_p, own transitions' chunks)
+    int nlive = 0;
+    for (TypeExec& te : P->types) nlive += !(te.empty || te.nPl == 0);
+    const int nl = std::min(nlive, cfp_ctx::kLanes + 1);
+    if (nl > 1) {
+      CUDA_TRY(cudaEventRecord(ctx->fork, st));
+      for (int i = 0; i + 1 < nl; ++i) CUDA_TRY(cudaStreamWaitEvent(ctx->lane[i], ctx->fork, 0));
+    }
+    int k = 0;
+    for (TypeExec& te : P->types) {
+      if (te.empty || te.nPl == 0) continue;
+      cudaStream_t ls = (k % nl) == 0 ? st : ctx->lane[(k % nl) - 1];
+      ++k;
+      if (te.wide) TRY(run_type_kernels<uint64_t>(P, te, ls, false));
+      else TRY(run_type_kernels<uint32_t>(P, te, ls, false));
+    }
+    for (int i = 0; i + 1 < nl; ++i) {
+      CUDA_TRY(cudaEventRecord(ctx->join[i], ctx->lane[i]));
+      CUDA_TRY(cudaStreamWaitEvent(st, ctx->join[i], 0));
+    }
   }
   if (P->timing) CUDA_TRY(cudaEventRecord(P->ev[2], st));
   uint64_t* outA = P->outAI.as<uint64_t>();
@@ -1464,9 +1512,12 @@ static cfp_status fetch_impl(cfp_ctx* ctx, cfp_prepared* P, cfp_plan* out) {
     fprintf(stderr, "\n");
     uint64_t t[64];
     CUDA_TRY(cudaMemcpy(t, P->cp.dbg, sizeof(t), cudaMemcpyDeviceToHost));
-    fprintf(stderr, "chain phases (us):");
-    for (uint64_t i = 1; i < t[63] && i < 63; ++i) fprintf(stderr, " %.2f", (t[i] - t[i - 1]) * 1e-3);
-    fprintf(stderr, "\n");
+    for (int m = 0; m < 2; ++m) {
+      const uint64_t* d = t + 32 * m;
+      fprintf(stderr, "chain mode %d phases (us):", m ? 2 : 1);
+      for (uint64_t i = 1; i < d[31] && i < 31; ++i) fprintf(stderr, " %.2f", (d[i] - d[i - 1]) * 1e-3);
+      fprintf(stderr, "\n");
+    }
   }
   if (status == 4) return fail(CFP_ETOOBIG, "chain scratch too small");
   if (status == 3) {

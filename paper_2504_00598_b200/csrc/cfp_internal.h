@@ -61,6 +61,7 @@ struct EpiTau {
   int32_t Din;
   int32_t nq;
   Term q[kMaxCross];            // kind 2: a = prefix position of the consumer, db, off
+  int64_t qt[kMaxCross];        // transposed copies Q^T[s][DinP] (16-byte aligned rows)
   void* chunkmin;               // [Din * Do][nchunks]
 };
 
@@ -167,8 +168,10 @@ struct ChainRun {
 };
 
 struct CompactJob {
-  int32_t kind;          // 0 unary, 1 pair (rows & cols remapped), 2 cross (cols remapped)
+  int32_t kind;          // 0 unary, 1 pair (rows & cols remapped), 2 cross (cols remapped),
+                         // 3 cross transposed: out[c][rows_pad], rows >= `rows` padded with CAP
   int32_t rows, cols;    // compact shape (unary: rows = 1)
+  int32_t rows_pad;      // kind 3 row length of the transposed table
   int32_t raw_cols;      // raw row length
   int64_t raw_off, raw_off2;   // comp / comm (unary), table (pair/cross); raw_off2 < 0: no comm
   int32_t map_r, map_c;  // offsets into the map blob (-1 = identity)

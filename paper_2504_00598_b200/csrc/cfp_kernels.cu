@@ -121,6 +121,20 @@ template <typename V>
 __global__ void compact_kernel(const CompactJob* __restrict__ jobs, const uint32_t* __restrict__ raw,
                                const int32_t* __restrict__ maps, V* __restrict__ out) {
   const CompactJob j = jobs[blockIdx.x];
+  if (j.kind == 3) {                              // transposed cross table Q^T[s][u]
+    const int64_t n = (int64_t)j.cols * j.rows_pad;
+    for (int64_t e = threadIdx.x; e < n; e += blockDim.x) {
+      const int32_t c = (int32_t)(e / j.rows_pad), r = (int32_t)(e % j.rows_pad);
+      V v = VT<V>::CAP;
+      if (r < j.rows) {
+        const int32_t rc = j.map_c >= 0 ? maps[j.map_c + c] : c;
+        const uint32_t x = raw[j.raw_off + (int64_t)r * j.raw_cols + rc];
+        v = (x == 0xFFFFFFFFu || (uint64_t)x >= (uint64_t)VT<V>::CAP) ? VT<V>::CAP : (V)x;
+      }
+      out[j.out_off + e] = v;
+    }
+    return;
+  }
   const int64_t n = (int64_t)j.rows * j.cols;
   for (int64_t e = threadIdx.x; e < n; e += blockDim.x) {
     const int32_t r = (int32_t)(e / j.cols), c = (int32_t)(e % j.cols);
@@ -268,11 +282,11 @@ __global__ void __launch_bounds__(kBlock, 4) enum_kernel(const EnumParams p) {
   const int tid = threadIdx.x;
   const bool edbg = blockIdx.x == 0 && tid == 0 && p.ntau == 2;
   if (edbg) g_enum_dbg2[0] = gtimer0();
-  const int64_t nhb = p.Gpad / kBlock;
-  const int64_t g = blockIdx.x / nhb;
+  const uint32_t nhb = (uint32_t)(p.Gpad / kBlock);          // 32-bit index math (grid < 2^31)
+  const uint32_t g = blockIdx.x / nhb;
   const int64_t hb = blockIdx.x - g * nhb;
-  const int64_t l = g / p.VG;
-  const int vg = (int)(g - l * p.VG);
+  const int64_t l = g / (uint32_t)p.VG;
+  const int vg = (int)(g - (uint32_t)l * (uint32_t)p.VG);
   const int64_t hh = hb * kBlock + tid;
   const bool live = hh < p.G;
   const int64_t pg = (p.h0 + hh) * p.W + l;       // global canonical prefix
@@ -325,11 +339,12 @@ __global__ void __launch_bounds__(kBlock, 4) enum_kernel(const EnumParams p) {
     sx = sy = sz = 0;
     if constexpr (MERGED) {
       V* ym = reinterpret_cast<V*>(ms + p.nM);
-      const int64_t n = p.nM * p.nb_pad;
-      for (int64_t e = tid; e < n; e += kBlock) {
-        const int64_t m = e / p.nb_pad;
+      const int n = (int)(p.nM * p.nb_pad);           // staged: fits shared memory
+      const uint32_t nbp = (uint32_t)p.nb_pad;
+      for (int e = tid; e < n; e += kBlock) {
+        const int m = (int)((uint32_t)e / nbp);
         const int4 mt = ms[m];
-        ym[e] = T::sat(ys[mt.y + (e - m * p.nb_pad)], zs[mt.z]);
+        ym[e] = T::sat(ys[mt.y + (e - m * (int)nbp)], zs[mt.z]);
       }
       __syncthreads();
       YT = ym;
@@ -446,47 +461,37 @@ __global__ void __launch_bounds__(kBlock, 4) enum_kernel(const EnumParams p) {
     const EpiTau& et = p.taus[t];
     const int Din = et.Din, DinP = (Din + 3) & ~3;
     {
-      // X^t_p[u] for this thread's prefix, 4 u at a time; up to 4 cross terms
-      // live in registers (all 16 loads of a u-quad are independent), further
-      // terms are accumulated through shared memory.
-      const int nq = et.nq;
-      auto digit_of = [&](int a) -> int {
-        return pg < 0x7FFFFFFF ? (int)(((uint32_t)pg / (uint32_t)p.pre_stride[a]) % (uint32_t)p.pre_radix[a])
-                               : (int)((pg / p.pre_stride[a]) % p.pre_radix[a]);
-      };
-      const V* q0 = nullptr; const V* q1 = nullptr; const V* q2 = nullptr; const V* q3 = nullptr;
-      int d0 = 0, d1 = 0, d2 = 0, d3 = 0;
-      if (nq > 0) { q0 = vals + et.q[0].off + digit_of(et.q[0].a); d0 = et.q[0].db; }
-      if (nq > 1) { q1 = vals + et.q[1].off + digit_of(et.q[1].a); d1 = et.q[1].db; }
-      if (nq > 2) { q2 = vals + et.q[2].off + digit_of(et.q[2].a); d2 = et.q[2].db; }
-      if (nq > 3) { q3 = vals + et.q[3].off + digit_of(et.q[3].a); d3 = et.q[3].db; }
-      for (int u0 = 0; u0 < DinP; u0 += 4) {
-        V x[4];
+      // X^t_p[u] = sum_i Q_i[u][s_i(p)] for this thread's prefix: each term is
+      // one contiguous row Q_i^T[s_i(p)][0..DinP) of the transposed copy, read
+      // 16 bytes at a time and accumulated in the thread's Xs row.
+      V* xrow = Xs + tid * DinP;
+      for (int i = 0; i < et.nq; ++i) {
+        const int a = et.q[i].a;
+        const int dig = pg < 0x7FFFFFFF ? (int)(((uint32_t)pg / (uint32_t)p.pre_stride[a]) % (uint32_t)p.pre_radix[a])
+                                        : (int)((pg / p.pre_stride[a]) % p.pre_radix[a]);
+        const V* qr = vals + et.qt[i] + dig * DinP;
+        for (int u0 = 0; u0 < DinP; u0 += VN) {
+          V y[VN], x[VN];
+          if (live) load_vec<V>(qr + u0, y);
+          else {
 #pragma unroll
-        for (int k2 = 0; k2 < 4; ++k2) x[k2] = (live && u0 + k2 < Din) ? (V)0 : T::CAP;
-        if (live) {
-          V y0[4], y1[4], y2[4], y3[4];
-#pragma unroll
-          for (int k2 = 0; k2 < 4; ++k2) {
-            const int u = min(u0 + k2, Din - 1);
-            y0[k2] = nq > 0 ? __ldg(q0 + (int64_t)u * d0) : (V)0;
-            y1[k2] = nq > 1 ? __ldg(q1 + (int64_t)u * d1) : (V)0;
-            y2[k2] = nq > 2 ? __ldg(q2 + (int64_t)u * d2) : (V)0;
-            y3[k2] = nq > 3 ? __ldg(q3 + (int64_t)u * d3) : (V)0;
+            for (int k2 = 0; k2 < VN; ++k2) y[k2] = T::CAP;
           }
+          if (i > 0) {
+            load_vec<V>(xrow + u0, x);
 #pragma unroll
-          for (int k2 = 0; k2 < 4; ++k2)
-            x[k2] = T::sat(T::sat(x[k2], y0[k2]), T::sat(T::sat(y1[k2], y2[k2]), y3[k2]));
+            for (int k2 = 0; k2 < VN; ++k2) y[k2] = T::sat(x[k2], y[k2]);
+          }
+          store_vec<V>(xrow + u0, y);
         }
-        store_vec<V>(Xs + tid * DinP + u0, x);
-        if (VN == 2) store_vec<V>(Xs + tid * DinP + u0 + 2, x + 2);
       }
-      for (int i = 4; i < nq; ++i) {                 // rare: more than four cross terms
-        const V* qi = vals + et.q[i].off + digit_of(et.q[i].a);
-        if (live)
-          for (int u = 0; u < Din; ++u)
-            Xs[tid * DinP + u] = T::sat(Xs[tid * DinP + u], __ldg(qi + (int64_t)u * et.q[i].db));
-      }
+      if (et.nq == 0)
+        for (int u0 = 0; u0 < DinP; u0 += VN) {
+          V y[VN];
+#pragma unroll
+          for (int k2 = 0; k2 < VN; ++k2) y[k2] = live ? (V)0 : T::CAP;
+          store_vec<V>(xrow + u0, y);
+        }
     }
     __syncthreads();
     if (edbg) g_enum_dbg2[3 + 3 * t] = gtimer0();
@@ -870,6 +875,22 @@ __device__ __forceinline__ uint64_t minplus_dot(const uint64_t* row, int rstride
   return b2 < b0 ? b2 : b0;
 }
 
+// Warp-cooperative min_v sat64(row[v], g[v]): lanes over v (contiguous,
+// bank-conflict free), butterfly min; every lane returns the result.
+__device__ __forceinline__ uint64_t warp_row_min(const uint64_t* row, const uint64_t* g, int n, int lane) {
+  uint64_t b = kInf64;
+  for (int v = lane; v < n; v += 32) {
+    const uint64_t x = sat64(row[v], g[v]);
+    b = x < b ? x : b;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const uint64_t y = __shfl_xor_sync(0xffffffffu, b, o);
+    b = y < b ? y : b;
+  }
+  return b;
+}
+
 // Single-CTA chain.  SM = true: every distinct matrix (A and, for the
 // backtrack, I), every suffix vector G_n, the powers of the current run and the
 // instance metadata live in shared memory; G is copied out at the end.
@@ -877,11 +898,15 @@ __device__ __forceinline__ uint64_t minplus_dot(const uint64_t* row, int rstride
 // mode 0: G + backtrack; 1: G + the optimal edges reachable from u_1 = 0
 // (the only buckets whose least index the backtrack needs); 2: backtrack with
 // G already computed.
+// goff[N] (rows of all instances) read from the parameter block's table
+__device__ __forceinline__ int64_t goff_n_of(const ChainParams& cp) { return cp.goff[cp.N]; }
+
 template <bool SM>
 __global__ void __launch_bounds__(1024) chain_kernel(const ChainParams cp) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   int dbg_i = 0;
-  auto mark = [&]() { if (cp.dbg && threadIdx.x == 0 && dbg_i < 64) cp.dbg[dbg_i++] = gtimer(); };
+  uint64_t* dbg = cp.dbg ? cp.dbg + (cp.mode == 1 ? 0 : 32) : nullptr;   // per-mode phase marks
+  auto mark = [&]() { if (dbg && threadIdx.x == 0 && dbg_i < 31) dbg[dbg_i++] = gtimer(); };
   mark();
   const int tid = threadIdx.x, nth = blockDim.x;
   const int N = cp.N;
@@ -895,6 +920,8 @@ __global__ void __launch_bounds__(1024) chain_kernel(const ChainParams cp) {
   int16_t* nxt = reinterpret_cast<int16_t*>(sinst + N);        // [goff[N]] successor of (n, u)
   int32_t* vseq = reinterpret_cast<int32_t*>((reinterpret_cast<uintptr_t>(nxt + cp.goff[N]) + 15) & ~uintptr_t(15));
   uint32_t* ebits = reinterpret_cast<uint32_t*>(vseq + N);     // mode 1 dedupe bitset
+  uint32_t* om = ebits + (cp.mat_elems + 31) / 32;               // mode 1: optimal-successor masks [goff[N]]
+  uint32_t* rmask = om + goff_n_of(cp);                           // mode 1: reachable-state masks [N]
   uint64_t* G = SM ? sG : cp.G;
   uint64_t* Pw = SM ? sP : cp.powers;
   const int64_t* goff = SM ? sgoff : cp.goff;
@@ -944,7 +971,11 @@ __global__ void __launch_bounds__(1024) chain_kernel(const ChainParams cp) {
       const int e = run.first + run.len;             // G_e known (1-based instance e)
       if (run.len == 1) {
         const uint64_t* g = G + goff[e];
-        for (int u = tid; u < R; u += nth) G[goff[e - 1] + u] = minplus_dot(M + (int64_t)u * Cc, 1, g, Cc);
+        const int warp = tid >> 5, lane = tid & 31;
+        for (int u = warp; u < R; u += nth >> 5) {              // warp per row
+          const uint64_t b = warp_row_min(M + (int64_t)u * Cc, g, Cc, lane);
+          if (lane == 0) G[goff[e - 1] + u] = b;
+        }
         __syncthreads();
         mark();
         continue;
@@ -982,6 +1013,70 @@ __global__ void __launch_bounds__(1024) chain_kernel(const ChainParams cp) {
     }
     if constexpr (SM)
       for (int64_t e2 = tid; e2 < goff[N + 1]; e2 += nth) cp.G[e2] = G[e2];
+  }
+  if (cp.mode == 1 && SM && cp.smax <= 32) {
+    // optimal edges reachable from u_1 = 0, for <= 32 states per instance:
+    // (1) every (n, u) in parallel: om = {v : A_n[u][v] + G_n(v) = G_{n-1}(u)};
+    // (2) one thread walks the instances: reach_{n+1} = OR_{u in reach_n} om(n, u);
+    // (3) every (n, u) in parallel: emit the reachable optimal edges (deduplicated).
+    __syncthreads();
+    mark();
+    __shared__ int s_cnt2;
+    if (tid == 0) s_cnt2 = 0;
+    const int64_t nrow = goff[N];
+    {
+      const int warp = tid >> 5, lane = tid & 31, nw = nth >> 5;
+      for (int n = warp; n < N; n += nw) {             // warp per instance, lanes over v
+        const int rows = rows_of(n), cols = cols_of(n);
+        const uint64_t* Gn = G + goff[n + 1];
+        const uint64_t gv = lane < cols ? Gn[lane] : kInf64;
+        for (int u = 0; u < rows; ++u) {
+          const uint64_t target = G[goff[n] + u];
+          const uint64_t a = lane < cols ? matA(n)[(int64_t)u * cols + lane] : kInf64;
+          const uint32_t m = __ballot_sync(0xffffffffu, target != kInf64 && a != kInf64 && gv != kInf64 &&
+                                                            a + gv == target);
+          if (lane == 0) om[goff[n] + u] = m;
+        }
+      }
+    }
+    for (int64_t w = tid; w < nrow; w += nth) cp.reach[w] = 0;
+    __syncthreads();
+    mark();
+    if (tid == 0) {
+      uint32_t r = G[0] == kInf64 ? 0u : 1u;
+      for (int n = 0; n < N; ++n) {
+        rmask[n] = r;
+        uint32_t nx = 0, rr = r;
+        while (rr) {
+          const int u = __ffs(rr) - 1;
+          rr &= rr - 1;
+          nx |= om[goff[n] + u];
+        }
+        r = nx;
+      }
+    }
+    __syncthreads();
+    mark();
+    for (int64_t w = tid; w < (int64_t)N * 32; w += nth) {   // (instance, lane = u)
+      const int n = (int)(w >> 5), u = (int)(w & 31);
+      if (u >= rows_of(n) || !((rmask[n] >> u) & 1u)) continue;
+      cp.reach[goff[n] + u] = 1;
+      const int cols = cols_of(n), mat = mat_of(n);
+      const int64_t fo = smoff[mat];
+      uint32_t m = om[goff[n] + u];
+      while (m) {
+        const int v = __ffs(m) - 1;
+        m &= m - 1;
+        const int64_t bit = fo + (int64_t)u * cols + v;
+        if (!(atomicOr(&ebits[bit >> 5], 1u << (bit & 31)) & (1u << (bit & 31))))
+          cp.edge_list[atomicAdd(&s_cnt2, 1)] = ArgminEntry{mat, u * cols + v};
+      }
+    }
+    __syncthreads();
+    if (tid == 0) *cp.edge_count = s_cnt2;
+    mark();
+    if (dbg && tid == 0) dbg[31] = dbg_i;
+    return;
   }
   if (cp.mode == 1) {
     // optimal edges reachable from u_1 = 0 (warp 0, sequential over instances;
@@ -1035,6 +1130,8 @@ __global__ void __launch_bounds__(1024) chain_kernel(const ChainParams cp) {
       }
       if (lane == 0) *cp.edge_count = s_cnt;
     }
+    mark();
+    if (dbg && tid == 0) dbg[31] = dbg_i;
     return;
   }
   if (!cp.backtrack) return;
@@ -1047,13 +1144,19 @@ __global__ void __launch_bounds__(1024) chain_kernel(const ChainParams cp) {
   if (SM && cp.mode == 2) {
     // successor of every reachable (n, u) (recorded by mode 1): one warp per
     // instance, lanes over v; then the walk from u_1 = 0 is a chain of loads
+    for (int64_t w = tid; w < goff[N]; w += nth) nxt[w] = -1;   // unreachable / no successor
+    __syncthreads();
     {
       const int warp = tid >> 5, lane = tid & 31, nw = nth >> 5;
       for (int n = warp; n < N; n += nw) {
         const int rows = rows_of(n), cols = cols_of(n);
         const uint64_t* Gn = G + goff[n + 1];
-        for (int u = 0; u < rows; ++u) {
-          if (!cp.reach[goff[n] + u]) continue;       // warp-uniform
+        for (int u0 = 0; u0 < rows; u0 += 32) {
+         // reachable states of this instance, 32 at a time (one coalesced load)
+         unsigned rmask = __ballot_sync(0xffffffffu, u0 + lane < rows && cp.reach[goff[n] + u0 + lane]);
+         while (rmask) {
+          const int u = u0 + __ffs(rmask) - 1;
+          rmask &= rmask - 1;
           const uint64_t* A = matA(n) + (int64_t)u * cols;
           const uint64_t* I = matI(n) + (int64_t)u * cols;
           const uint64_t target = G[goff[n] + u];
@@ -1071,6 +1174,7 @@ __global__ void __launch_bounds__(1024) chain_kernel(const ChainParams cp) {
             if (ov >= 0 && (bv < 0 || ob < bi || (ob == bi && ov < bv))) { bi = ob; bv = ov; }
           }
           if (lane == 0) nxt[goff[n] + u] = (int16_t)bv;
+         }
         }
       }
     }
@@ -1081,7 +1185,7 @@ __global__ void __launch_bounds__(1024) chain_kernel(const ChainParams cp) {
       } else {
         int u = 0;
         for (int n = 0; n < N; ++n) {
-          const int v = cp.reach[goff[n] + u] ? nxt[goff[n] + u] : -1;
+          const int v = nxt[goff[n] + u];           // shared-memory chain only
           if (v < 0) { s_status = 3; break; }
           vseq[n] = (u << 16) | v;
           u = v;
@@ -1153,7 +1257,7 @@ __global__ void __launch_bounds__(1024) chain_kernel(const ChainParams cp) {
   }
   __syncthreads();
   mark();
-  if (cp.dbg && tid == 0) cp.dbg[63] = dbg_i;
+  if (dbg && tid == 0) dbg[31] = dbg_i;
 }
 
 // --------------------------------------------------------------------------
