@@ -192,6 +192,61 @@ cfp_status cfp_prepared_query(const cfp_prepared* prep, cfp_prepared_info* info)
 cfp_status cfp_prepared_time_kernels(cfp_prepared* prep, int32_t on);
 cfp_status cfp_prepared_kernel_ms(cfp_prepared* prep, double* enum_ms, double* total_ms);
 
+/* ---- memory-constrained search ----------------------
+ * The paper's DP carries a memory constraint: Eq. 4 sums the profiled
+ * peak memory of the chosen strategies, and the search keeps plans whose
+ * memory fits the device.  Reading R-M1
+ * (DESIGN.md): memory is profiled per ParallelBlock strategy, m_j[s], and
+ * quantised per block with a ceiling, q_j[s] = ceil(m_j[s] / quantum), so the
+ * quantised sum never under-estimates (never falsely feasible).
+ *   segment table  Am[u][v][q - qlo] = min_{s: s_o = v, sum_j q_j[s_j] = q} C(u,s)
+ *                  Im = least big-endian index attaining it (CFP_NOIDX if none),
+ *                  qlo/qhi = sum_j min/max_s q_j[s] over ALL strategies;
+ *   chain          states (u, c), c = quantised memory used so far,
+ *                  G_N(v, c) = 0 for c <= Qmax = floor(mem_limit / quantum),
+ *                  G_{n-1}(u, c) = min_{v, q: c + q <= Qmax} Am_n[u][v][q] + G_n(v, c + q),
+ *                  OPT = G_0(0, 0);
+ *   plan           forward greedy from (0, 0), least combination index among
+ *                  the optimal successors (v, q) -- the canonical plan.
+ * Same conventions as above (host memory, caller-allocated outputs, status
+ * codes).  Single-GPU: world > 1 gives CFP_EINVAL.  Limits: Qmax < 65536 and
+ * per-block q_j < 2^20 (else CFP_ETOOBIG). */
+typedef struct {
+  uint64_t quantum;                 /* >= 1, unit of m_j (e.g. KiB) */
+  uint64_t mem_limit;               /* per-device limit in the same unit */
+  const uint32_t* const* type_mem;  /* [num_types] -> [sum D_j] m_j[s]; NULL (array or entry) = 0 */
+} cfp_mem_model;
+
+/* Full memory-constrained search.  out as cfp_search_plan (seg_ns = Am of the
+ * chosen bucket); seg_q [N] receives q of each segment, total_q their sum.
+ * CFP_EINFEASIBLE when no plan fits the limit. */
+cfp_status cfp_search_plan_mem(cfp_ctx* ctx, const cfp_problem* p, const cfp_mem_model* mem,
+                               cfp_plan* out, int64_t* seg_q, int64_t* total_q);
+/* Device-resident split of cfp_search_plan_mem (the bench times execute with
+ * the tables already in HBM): prepare validates and stages, execute runs the
+ * whole path on the ctx stream without host synchronisation, fetch copies the
+ * plan out.  cfp_mem_time_kernels(prep, 1) before execute records events;
+ * cfp_mem_kernel_ms then reports the enumeration+fold ms and the total ms of
+ * the last execute, the combinations per execute and the kernel launches. */
+typedef struct cfp_mem_prepared cfp_mem_prepared;
+cfp_status cfp_mem_prepare(cfp_ctx* ctx, const cfp_problem* p, const cfp_mem_model* mem,
+                           cfp_mem_prepared** out);
+cfp_status cfp_mem_execute(cfp_ctx* ctx, cfp_mem_prepared* prep);
+cfp_status cfp_mem_fetch_plan(cfp_ctx* ctx, cfp_mem_prepared* prep, cfp_plan* out, int64_t* seg_q,
+                              int64_t* total_q);
+void       cfp_mem_free(cfp_mem_prepared* prep);
+cfp_status cfp_mem_time_kernels(cfp_mem_prepared* prep, int32_t on);
+cfp_status cfp_mem_kernel_ms(cfp_mem_prepared* prep, double* tables_ms, double* total_ms,
+                             double* combos, int32_t* launches);
+
+/* One transition's memory-bucketed table: cost_out / index_out are
+ * [d_in][D_o][nq] row-major with nq = qhi - qlo + 1.  Pass cost_out =
+ * index_out = NULL to query qlo_out / nq_out only (no device work). */
+cfp_status cfp_segment_costs_mem(cfp_ctx* ctx, const cfp_segment_type* t, const uint32_t* mem,
+                                 uint64_t quantum, const cfp_transition* tr, int32_t d_in,
+                                 int64_t* qlo_out, int32_t* nq_out,
+                                 uint64_t* cost_out, uint64_t* index_out);
+
 /* ---- host-only helpers (no device work; callable without a GPU) ---------- */
 /* Contiguous, balanced share [lo, hi) of `units` items for `rank` of `world`
  * in multiples of `align`. */

@@ -67,6 +67,10 @@ class cfp_plan(C.Structure):
                 ("kmax", C.c_int32), ("seg_ns", P(C.c_uint64))]
 
 
+class cfp_mem_model(C.Structure):
+    _fields_ = [("quantum", C.c_uint64), ("mem_limit", C.c_uint64), ("type_mem", P(P(C.c_uint32)))]
+
+
 class cfp_ctx_opts(C.Structure):
     _fields_ = [("device", C.c_int32), ("cuda_stream", C.c_void_p), ("world", C.c_int32),
                 ("rank", C.c_int32), ("nccl_unique_id", C.c_void_p)]
@@ -84,7 +88,9 @@ EXPORTS = ["cfp_ctx_create", "cfp_ctx_destroy", "cfp_last_error", "cfp_nccl_uniq
            "cfp_prepare", "cfp_execute", "cfp_fetch_plan", "cfp_prepared_free",
            "cfp_prepared_query", "cfp_prepared_time_kernels", "cfp_prepared_kernel_ms",
            "cfp_shard_range", "cfp_pack_keys", "cfp_unpack_keys", "cfp_intpipe_bench",
-           "cfp_minplus_bench"]
+           "cfp_minplus_bench", "cfp_search_plan_mem", "cfp_segment_costs_mem", "cfp_mem_prepare",
+           "cfp_mem_execute", "cfp_mem_fetch_plan", "cfp_mem_free", "cfp_mem_time_kernels",
+           "cfp_mem_kernel_ms"]
 
 _lib = None
 
@@ -126,6 +132,18 @@ def lib() -> C.CDLL:
     L.cfp_intpipe_bench.argtypes = [vp, C.c_int32, C.c_int32, P(C.c_double), P(C.c_double)]
     L.cfp_minplus_bench.argtypes = [vp, C.c_int32, C.c_int32, C.c_int32, C.c_int32, P(C.c_double),
                                     P(C.c_double)]
+    L.cfp_search_plan_mem.argtypes = [vp, P(cfp_problem), P(cfp_mem_model), P(cfp_plan), P(C.c_int64),
+                                      P(C.c_int64)]
+    L.cfp_segment_costs_mem.argtypes = [vp, P(cfp_segment_type), P(C.c_uint32), C.c_uint64,
+                                        P(cfp_transition), C.c_int32, P(C.c_int64), P(C.c_int32),
+                                        P(C.c_uint64), P(C.c_uint64)]
+    L.cfp_mem_prepare.argtypes = [vp, P(cfp_problem), P(cfp_mem_model), P(vp)]
+    L.cfp_mem_execute.argtypes = [vp, vp]
+    L.cfp_mem_fetch_plan.argtypes = [vp, vp, P(cfp_plan), P(C.c_int64), P(C.c_int64)]
+    L.cfp_mem_free.argtypes = [vp]
+    L.cfp_mem_free.restype = None
+    L.cfp_mem_time_kernels.argtypes = [vp, C.c_int32]
+    L.cfp_mem_kernel_ms.argtypes = [vp, P(C.c_double), P(C.c_double), P(C.c_double), P(C.c_int32)]
     _lib = L
     return L
 
@@ -181,6 +199,17 @@ class _Marshal:
                            _p(inst, C.c_int32))
 
 
+def _mem_model(m: "_Marshal", prob, quantum: int, mem_limit: int) -> cfp_mem_model:
+    """Per-type m_j[s] tables (P:573 peak memory per strategy; NEXT-1)."""
+    ptrs = []
+    for t in prob.types:
+        mem = getattr(t, "mem", None)
+        ptrs.append(None if mem is None else _p(m.arr(mem, np.uint32), C.c_uint32))
+    arr = (P(C.c_uint32) * len(ptrs))(*ptrs)
+    m.keep.append(arr)
+    return cfp_mem_model(int(quantum), int(mem_limit), arr)
+
+
 def _e(e):
     return (e.src, e.dst, e.table) if hasattr(e, "src") else e
 
@@ -195,6 +224,16 @@ class Plan:
     seg_index: np.ndarray      # uint64 [N]
     digits: np.ndarray         # int32 [N, kmax]
     seg_ns: np.ndarray         # uint64 [N]
+
+
+@dataclass
+class PlanMem:
+    total_ns: int
+    seg_index: np.ndarray      # uint64 [N]
+    digits: np.ndarray         # int32 [N, kmax]
+    seg_ns: np.ndarray         # uint64 [N]
+    seg_q: np.ndarray          # int64 [N] quantised memory of each segment
+    total_q: int
 
 
 @dataclass
@@ -306,6 +345,44 @@ class Context:
     def prepare(self, prob) -> "Prepared":
         return Prepared(self, prob)
 
+    # -- memory-constrained search (NEXT-1)
+    def search_plan_mem(self, prob, quantum: int, mem_limit: int) -> PlanMem:
+        m = _Marshal()
+        p = m.problem(prob)
+        mm = _mem_model(m, prob, quantum, mem_limit)
+        N = len(prob.instances)
+        kmax = max(int(len(t.radix)) for t in prob.types)
+        idx = np.empty(N, np.uint64)
+        dig = np.empty(N * kmax, np.int32)
+        seg = np.empty(N, np.uint64)
+        sq = np.empty(N, np.int64)
+        tq = C.c_int64()
+        plan = cfp_plan(0, _p(idx, C.c_uint64), _p(dig, C.c_int32), kmax, _p(seg, C.c_uint64))
+        _check(lib().cfp_search_plan_mem(self._h, C.byref(p), C.byref(mm), C.byref(plan),
+                                         _p(sq, C.c_int64), C.byref(tq)))
+        return PlanMem(int(plan.total_ns), idx, dig.reshape(N, kmax), seg, sq, tq.value)
+
+    def segment_costs_mem(self, seg_type, quantum: int, transition=None, d_in: int = 1):
+        """(Am [d_in][D_o][nq], Im, qlo) of one transition (memory-bucketed)."""
+        m = _Marshal()
+        t = m.segment_type(seg_type)
+        tr = m.transition(transition) if transition is not None else None
+        mem = getattr(seg_type, "mem", None)
+        mp = None if mem is None else _p(m.arr(mem, np.uint32), C.c_uint32)
+        qlo, nq = C.c_int64(), C.c_int32()
+        trp = C.byref(tr) if tr is not None else None
+        _check(lib().cfp_segment_costs_mem(self._h, C.byref(t), mp, int(quantum), trp, d_in,
+                                           C.byref(qlo), C.byref(nq), None, None))
+        do = int(np.asarray(seg_type.radix)[int(seg_type.out_block)])
+        A = np.empty((d_in, do, nq.value), np.uint64)
+        I = np.empty((d_in, do, nq.value), np.uint64)
+        _check(lib().cfp_segment_costs_mem(self._h, C.byref(t), mp, int(quantum), trp, d_in,
+                                           C.byref(qlo), C.byref(nq), _p(A, C.c_uint64), _p(I, C.c_uint64)))
+        return A, I, qlo.value
+
+    def prepare_mem(self, prob, quantum: int, mem_limit: int) -> "PreparedMem":
+        return PreparedMem(self, prob, quantum, mem_limit)
+
     def minplus_bench(self, S: int, wide: bool = False, argk: bool = False, iters: int = 5):
         """(ms per launch, add+min ops per second) of an S^3 (min,+) product."""
         ms, ops = C.c_double(), C.c_double()
@@ -359,6 +436,54 @@ class Prepared:
     def close(self):
         if self._h:
             lib().cfp_prepared_free(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class PreparedMem:
+    """Device-resident memory-constrained search: prepare once, execute many times."""
+
+    def __init__(self, ctx: Context, prob, quantum: int, mem_limit: int):
+        self.ctx = ctx
+        self._m = _Marshal()
+        p = self._m.problem(prob)
+        mm = _mem_model(self._m, prob, quantum, mem_limit)
+        self._h = C.c_void_p()
+        _check(lib().cfp_mem_prepare(ctx._h, C.byref(p), C.byref(mm), C.byref(self._h)))
+        self.N = len(prob.instances)
+        self.kmax = max(int(len(t.radix)) for t in prob.types)
+
+    def execute(self):
+        _check(lib().cfp_mem_execute(self.ctx._h, self._h))
+
+    def fetch(self) -> PlanMem:
+        idx = np.empty(self.N, np.uint64)
+        dig = np.empty(self.N * self.kmax, np.int32)
+        seg = np.empty(self.N, np.uint64)
+        sq = np.empty(self.N, np.int64)
+        tq = C.c_int64()
+        plan = cfp_plan(0, _p(idx, C.c_uint64), _p(dig, C.c_int32), self.kmax, _p(seg, C.c_uint64))
+        _check(lib().cfp_mem_fetch_plan(self.ctx._h, self._h, C.byref(plan), _p(sq, C.c_int64),
+                                        C.byref(tq)))
+        return PlanMem(int(plan.total_ns), idx, dig.reshape(self.N, self.kmax), seg, sq, tq.value)
+
+    def time_kernels(self, on: bool = True):
+        _check(lib().cfp_mem_time_kernels(self._h, 1 if on else 0))
+
+    def kernel_ms(self):
+        """(enumeration+fold ms, total ms, combinations per execute, kernel launches)."""
+        a, b, c, n = C.c_double(), C.c_double(), C.c_double(), C.c_int32()
+        _check(lib().cfp_mem_kernel_ms(self._h, C.byref(a), C.byref(b), C.byref(c), C.byref(n)))
+        return a.value, b.value, c.value, n.value
+
+    def close(self):
+        if self._h:
+            lib().cfp_mem_free(self._h)
             self._h = C.c_void_p()
 
     def __del__(self):

@@ -1964,3 +1964,6 @@ extern "C" cfp_status cfp_intpipe_bench(cfp_ctx* ctx, int32_t op, int32_t iters,
   if (ms) *ms = t;
   return CFP_OK;
 }
+
+// memory-constrained search (NEXT-1)
+#include "cfp_mem_host.inc"

@@ -215,4 +215,120 @@ struct ChainParams {
   const uint64_t* baseI;        // same for I (backtrack)
 };
 
+// ---------------------------------------------------------------------------
+// Memory-constrained search (cfp_mem.cu).
+// A type's digits split into a prefix [0, P) (every cross-edge consumer is
+// here) and a suffix [P, K).  ctx = prefix digits sharing an intra edge with a
+// suffix digit.  For ctx value c and suffix combination sigma the host
+// tabulates T[c][sigma] = every Eq. 3 term touching a suffix digit; K0[p] =
+// every term inside the prefix.  Cost of combination (p, sigma) =
+// K0[p] + T[ctx(p)][sigma].  Buckets: output layout v and quantised memory
+// q = qP(p) + qS(sigma); suffix classes cls = vslot * RQs + (qS - qS_lo),
+// vslot = s_o when o is a suffix digit, else 0 (v then comes from the prefix).
+// ---------------------------------------------------------------------------
+constexpr int kMemFoldRows = 32;     // rows staged per fold step
+constexpr int kMemFoldCols = 128;    // columns (classes) per fold CTA
+constexpr int kMemNPF = 4;           // prefixes per enumeration thread
+
+struct MemPrefixMap {
+  int32_t P;
+  int32_t radix[kMaxDigits];
+  int64_t stride[kMaxDigits];        // natural (big-endian) stride of each prefix digit
+  int32_t nctx;                      // ctx digits (canonical order)
+  int32_t ctx_pos[kMaxDigits];
+  int32_t nnon;                      // other prefix digits (canonical order)
+  int32_t non_pos[kMaxDigits];
+};
+
+struct MemEnumParams {
+  MemPrefixMap pm;
+  int64_t nN;                        // non-ctx prefix values
+  int32_t nblkN;                     // CTAs per ctx value
+  int32_t Wc;                        // classes per prefix row
+  int32_t Tlen;                      // padded sorted row length (multiple of 4)
+  const void* Ts;                    // [nC][Tlen] class-sorted, each class padded with CAP
+  const int32_t* cstart;             // [Wc + 1]
+  const void* K0;                    // [nP]
+  void* B;                           // [nP][Wc] out: K0[p] + min over the class
+};
+
+struct MemFoldParams {
+  MemPrefixMap pm;
+  int32_t Din, DinP;
+  int32_t nq;                        // cross terms
+  int32_t q_pos[kMaxCross];          // prefix position of each consumer
+  int64_t q_off[kMaxCross];          // element offset of Q^T[s][DinP] in `vals`
+  const void* vals;
+  int32_t Wc, ncolblk;
+  const int4* tiles;                 // [ntiles] (row_start, rows, rowclass, 0)
+  const int32_t* perm;               // [nP] prefixes sorted by (rowclass, p)
+  const void* B;                     // [nP][Wc]
+  void* chunk;                       // [ntiles][Din][Wc] out
+};
+
+struct MemAminParams {
+  int32_t Din, Do, nq;               // output [Din][Do][nq] (u64)
+  int32_t RQs, nVp;                  // nVp = Do if o is a prefix digit, else 1
+  int32_t o_in_prefix;
+  int32_t ntiles, Wc;
+  const int4* tiles;
+  const void* chunk;
+  uint64_t* Am;
+};
+
+struct MemArgEntry { int32_t slot, u, v, qi; };
+
+struct MemArgSlot {                  // one transition (argmin side)
+  MemPrefixMap pm;
+  int32_t Din, DinP, Do, nq, RQs, nVp, o_in_prefix, Wc, ntiles;
+  int32_t nqx;
+  int32_t q_pos[kMaxCross];
+  int64_t q_off[kMaxCross];
+  const void* vals;
+  const int4* tiles;
+  const int32_t* perm;
+  const void* B;
+  const void* chunk;
+  const void* K0;
+  const void* Tc;                    // [nC][nS] canonical suffix order
+  const int32_t* sinfo;              // [nS] class of each suffix combination
+  int64_t nS;
+  const uint64_t* Am;
+  uint64_t* Im;                      // [Din][Do][nq]
+};
+
+struct MemInst {                     // one chain instance
+  int32_t slot, rows, cols, nq;
+  int32_t qlo;
+  int32_t K;
+  int32_t radix_off;                 // into MemChainParams::radix
+  int32_t pad_;
+  const uint64_t* Am;
+  const uint64_t* Im;
+};
+
+struct MemChainParams {
+  int32_t N;
+  int32_t C;                         // Qmax + 1
+  const MemInst* inst;
+  const int64_t* goff;               // [N + 2] row offsets (times C)
+  uint64_t* G;
+  // BFS / argmin list
+  uint32_t* need;                    // bitsets per slot
+  const int64_t* need_off;           // [nslot + 1] word offsets
+  int32_t nslot;
+  MemArgEntry* list;
+  int32_t* count;
+  int32_t list_cap;
+  // plan outputs (device)
+  const int32_t* radix;
+  int32_t kmax;
+  uint64_t* total;
+  uint64_t* seg_index;
+  uint64_t* seg_ns;
+  int64_t* seg_q;
+  int32_t* digits;
+  int32_t* status;
+};
+
 }  // namespace cfp

@@ -1,0 +1,572 @@
+// cfp_mem.cu -- sm_100a kernels of the memory-constrained search (SURVEY
+// §8(f) NEXT-1: Eq. 4, DP P:625-628).
+//
+// Steps (host side in cfp_mem_host.inc):
+//   mem_enum_kernel   every combination (p, sigma) of a type: cost
+//                     K0[p] + T[ctx(p)][sigma] formed and min-reduced into its
+//                     suffix class (output layout slot, suffix memory) with one
+//                     fused add+min (VIADDMNMX) per combination; the suffix
+//                     combinations of a class are contiguous in the
+//                     class-sorted table staged in shared memory.
+//   mem_fold_kernel   cross terms of one transition folded over the prefixes
+//                     of one prefix-memory class (a tile): a (min,+) product
+//                     chunk[u][cls] = min_p X_p[u] + B_p[cls], 4x4 register
+//                     blocks, rows staged through shared memory.
+//   mem_amin_kernel   Am[u][v][q] = min over tiles (tile memory k + class rs = q).
+//   mem_chain_kernel  one backward step of the (layout, memory) DP.
+//   mem_bfs_kernel    optimal edges reachable from (0, 0) -> needed buckets.
+//   mem_argmin_kernel least combination index of every needed bucket: least
+//                     prefix among the attaining tiles' rows, then the least
+//                     suffix combination of that prefix.
+//   mem_greedy_kernel forward greedy walk + digit decode.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "cfp_internal.h"
+
+namespace cfp {
+
+template <typename V> struct MT;
+template <> struct MT<uint32_t> {
+  static constexpr uint32_t CAP = kCap32;
+  __device__ static __forceinline__ uint32_t addmin(uint32_t a, uint32_t b, uint32_t c) {
+    return __viaddmin_u32(a, b, c);                 // min(a + b, c): VIADDMNMX.U32
+  }
+  __device__ static __forceinline__ uint32_t sat(uint32_t a, uint32_t b) { return __viaddmin_u32(a, b, CAP); }
+  __device__ static __forceinline__ void load4(const uint32_t* p, uint32_t* v) {
+    const uint4 q = *reinterpret_cast<const uint4*>(p);
+    v[0] = q.x; v[1] = q.y; v[2] = q.z; v[3] = q.w;
+  }
+};
+template <> struct MT<uint64_t> {
+  static constexpr uint64_t CAP = kCap64;
+  __device__ static __forceinline__ uint64_t addmin(uint64_t a, uint64_t b, uint64_t c) {
+    const uint64_t s = a + b;                       // a, b <= CAP: no wrap
+    return s < c ? s : c;
+  }
+  __device__ static __forceinline__ uint64_t sat(uint64_t a, uint64_t b) { return addmin(a, b, CAP); }
+  __device__ static __forceinline__ void load4(const uint64_t* p, uint64_t* v) {
+    const ulonglong2 a = *reinterpret_cast<const ulonglong2*>(p);
+    const ulonglong2 b = *reinterpret_cast<const ulonglong2*>(p + 2);
+    v[0] = a.x; v[1] = a.y; v[2] = b.x; v[3] = b.y;
+  }
+};
+
+// Natural prefix index from (ctx value, other-digit value).
+__device__ __forceinline__ int64_t mem_prefix(const MemPrefixMap& m, int64_t c, int64_t n) {
+  int64_t p = 0;
+  for (int i = m.nctx - 1; i >= 0; --i) {
+    const int pos = m.ctx_pos[i];
+    const int64_t r = m.radix[pos];
+    p += (c % r) * m.stride[pos];
+    c /= r;
+  }
+  for (int i = m.nnon - 1; i >= 0; --i) {
+    const int pos = m.non_pos[i];
+    const int64_t r = m.radix[pos];
+    p += (n % r) * m.stride[pos];
+    n /= r;
+  }
+  return p;
+}
+__device__ __forceinline__ int mem_digit(const MemPrefixMap& m, int64_t p, int pos) {
+  return (int)((p / m.stride[pos]) % m.radix[pos]);
+}
+__device__ __forceinline__ int64_t mem_ctx(const MemPrefixMap& m, int64_t p) {
+  int64_t c = 0;
+  for (int i = 0; i < m.nctx; ++i) c = c * m.radix[m.ctx_pos[i]] + mem_digit(m, p, m.ctx_pos[i]);
+  return c;
+}
+
+// --------------------------------------------------------------------------
+// Enumeration.  CTA = (ctx value c, block of kMemNPF * 256 other-digit values);
+// thread = kMemNPF prefixes sharing c.  T[c] (class-sorted, padded with CAP)
+// is staged in shared memory; every combination of a class is one
+// VIADDMNMX per prefix: acc_i = min(K0[p_i] + T[c][e], acc_i).
+// --------------------------------------------------------------------------
+template <typename V>
+__global__ void __launch_bounds__(256) mem_enum_kernel(const MemEnumParams p) {
+  using M = MT<V>;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  V* ts = reinterpret_cast<V*>(smem_raw);
+  int32_t* cs = reinterpret_cast<int32_t*>(ts + p.Tlen);
+  const int64_t c = blockIdx.x / p.nblkN;
+  const int64_t nb = blockIdx.x - c * p.nblkN;
+  const V* src = static_cast<const V*>(p.Ts) + c * p.Tlen;
+  for (int e = threadIdx.x * 4; e < p.Tlen; e += 256 * 4) {
+    V t[4];
+    M::load4(src + e, t);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) ts[e + q] = t[q];
+  }
+  for (int e = threadIdx.x; e <= p.Wc; e += 256) cs[e] = p.cstart[e];
+  __syncthreads();
+  int64_t pf[kMemNPF];
+  V k0[kMemNPF];
+  bool live[kMemNPF];
+#pragma unroll
+  for (int i = 0; i < kMemNPF; ++i) {
+    const int64_t n = (nb * kMemNPF + i) * 256 + threadIdx.x;
+    live[i] = n < p.nN;
+    pf[i] = live[i] ? mem_prefix(p.pm, c, n) : 0;
+    k0[i] = live[i] ? static_cast<const V*>(p.K0)[pf[i]] : M::CAP;
+  }
+  V* B = static_cast<V*>(p.B);
+  const int64_t ld = (p.Wc + 3) & ~3;
+  for (int cls = 0; cls < p.Wc; ++cls) {
+    const int s0 = cs[cls], s1 = cs[cls + 1];
+    V acc[kMemNPF];
+#pragma unroll
+    for (int i = 0; i < kMemNPF; ++i) acc[i] = M::CAP;
+#pragma unroll 2
+    for (int e = s0; e < s1; e += 4) {
+      V t[4];
+      M::load4(ts + e, t);
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+#pragma unroll
+        for (int i = 0; i < kMemNPF; ++i) acc[i] = M::addmin(k0[i], t[q], acc[i]);
+    }
+#pragma unroll
+    for (int i = 0; i < kMemNPF; ++i)
+      if (live[i]) B[pf[i] * ld + cls] = acc[i];
+  }
+}
+
+// --------------------------------------------------------------------------
+// Fold of one transition.  CTA = (tile of <= 256 prefixes of one prefix-memory
+// class, block of 128 classes).  Thread = 4 input states x 4 classes.
+// --------------------------------------------------------------------------
+template <typename V>
+__global__ void __launch_bounds__(256) mem_fold_kernel(const MemFoldParams p) {
+  using M = MT<V>;
+  constexpr int R = kMemFoldRows, FC = kMemFoldCols;
+  __shared__ __align__(16) V Xs[R][32];
+  __shared__ __align__(16) V Bs[R][FC];
+  __shared__ int64_t rowp[R];
+  const int4 tile = p.tiles[blockIdx.x];
+  const int col0 = blockIdx.y * FC;
+  const int ncols = min(FC, p.Wc - col0);
+  const int64_t ld = (p.Wc + 3) & ~3;
+  const int tid = threadIdx.x;
+  const int tu = tid >> 5, tc = tid & 31;          // u quad (8), class quad (32)
+  const V* vals = static_cast<const V*>(p.vals);
+  const V* B = static_cast<const V*>(p.B);
+  V* out = static_cast<V*>(p.chunk) + (int64_t)blockIdx.x * p.Din * p.Wc;
+  for (int ub = 0; ub < p.Din; ub += 32) {          // input states in blocks of 32
+    const int ucnt = min(32, p.DinP - ub);
+    V res[4][4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) res[i][j] = M::CAP;
+    for (int r0 = 0; r0 < tile.y; r0 += R) {
+      const int nr = min(R, tile.y - r0);
+      if (tid < R) rowp[tid] = tid < nr ? (int64_t)p.perm[tile.x + r0 + tid] : -1;
+      __syncthreads();
+      {   // X_p[u] for the staged rows: thread = (row, u quad)
+        const int r = tid >> 3, uq = tid & 7;
+        if (uq * 4 < ucnt) {
+          V x[4];
+          const int64_t pr = rowp[r];
+          if (pr < 0) {
+#pragma unroll
+            for (int k = 0; k < 4; ++k) x[k] = M::CAP;
+          } else {
+#pragma unroll
+            for (int k = 0; k < 4; ++k) x[k] = 0;
+            for (int i = 0; i < p.nq; ++i) {
+              const int dig = mem_digit(p.pm, pr, p.q_pos[i]);
+              V y[4];
+              M::load4(vals + p.q_off[i] + (int64_t)dig * p.DinP + ub + uq * 4, y);
+#pragma unroll
+              for (int k = 0; k < 4; ++k) x[k] = M::sat(x[k], y[k]);
+            }
+          }
+#pragma unroll
+          for (int k = 0; k < 4; ++k) Xs[r][uq * 4 + k] = x[k];
+        }
+      }
+      for (int e = tid; e < R * (FC / 4); e += 256) {   // B rows of this class block
+        const int r = e / (FC / 4), cq = e % (FC / 4);
+        V y[4];
+        if (rowp[r] >= 0 && cq * 4 < ncols) {
+          M::load4(B + rowp[r] * ld + col0 + cq * 4, y);
+        } else {
+#pragma unroll
+          for (int k = 0; k < 4; ++k) y[k] = M::CAP;
+        }
+#pragma unroll
+        for (int k = 0; k < 4; ++k) Bs[r][cq * 4 + k] = y[k];
+      }
+      __syncthreads();
+      if (tu * 4 < ucnt && tc * 4 < ncols) {
+#pragma unroll 4
+        for (int r = 0; r < nr; ++r) {
+          V x[4], y[4];
+          M::load4(&Xs[r][tu * 4], x);
+          M::load4(&Bs[r][tc * 4], y);
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int j = 0; j < 4; ++j) res[i][j] = M::addmin(x[i], y[j], res[i][j]);
+        }
+      }
+      __syncthreads();
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int u = ub + tu * 4 + i, cl = col0 + tc * 4 + j;
+        if (u < p.Din && cl < p.Wc && tu * 4 + i < ucnt) out[(int64_t)u * p.Wc + cl] = res[i][j];
+      }
+  }
+}
+
+// --------------------------------------------------------------------------
+// Am[u][v][qi] = min over tiles of the tile's chunk at class (vslot, qi - k).
+// One warp per output entry.
+// --------------------------------------------------------------------------
+template <typename V>
+__global__ void mem_amin_kernel(const MemAminParams p) {
+  const int64_t e = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  const int64_t total = (int64_t)p.Din * p.Do * p.nq;
+  if (e >= total) return;
+  const int qi = (int)(e % p.nq);
+  const int v = (int)((e / p.nq) % p.Do);
+  const int u = (int)(e / ((int64_t)p.nq * p.Do));
+  const V* ch = static_cast<const V*>(p.chunk);
+  V best = MT<V>::CAP;
+  for (int t = lane; t < p.ntiles; t += 32) {
+    const int rc = p.tiles[t].z;
+    const int k = rc / p.nVp, vp = rc % p.nVp;
+    int vslot = v;
+    if (p.o_in_prefix) {
+      if (vp != v) continue;
+      vslot = 0;
+    }
+    const int rs = qi - k;
+    if (rs < 0 || rs >= p.RQs) continue;
+    const V x = ch[((int64_t)t * p.Din + u) * p.Wc + vslot * p.RQs + rs];
+    best = x < best ? x : best;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const V y = __shfl_xor_sync(0xffffffffu, best, o);
+    best = y < best ? y : best;
+  }
+  if (lane == 0) p.Am[e] = best >= MT<V>::CAP ? kInf64 : (uint64_t)best;
+}
+
+// --------------------------------------------------------------------------
+// One backward DP step (P:625-628 with the memory state of S:466-474):
+// G_n(u, c) = min_{v, q: c + q <= Qmax} Am[u][v][q - qlo] + G_{n+1}(v, c + q).
+// CTA = (u, block of 256 memory states); Am row u staged in shared memory.
+// --------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) mem_chain_kernel(const MemChainParams cp, int n) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  uint64_t* arow = reinterpret_cast<uint64_t*>(smem_raw);
+  const MemInst in = cp.inst[n];
+  const int u = blockIdx.x;
+  const int C = cp.C;
+  const int rowlen = in.cols * in.nq;
+  for (int e = threadIdx.x; e < rowlen; e += blockDim.x) arow[e] = in.Am[(int64_t)u * rowlen + e];
+  __syncthreads();
+  const int c = blockIdx.y * blockDim.x + threadIdx.x;
+  if (c >= C) return;
+  const uint64_t* Gn = cp.G + cp.goff[n + 1] * C;
+  uint64_t best = kInf64;
+  for (int v = 0; v < in.cols; ++v) {
+    const uint64_t* gv = Gn + (int64_t)v * C;
+    const uint64_t* av = arow + v * in.nq;
+    const int qmax = min(in.nq, C - c - in.qlo);    // c + qlo + qi <= Qmax = C - 1
+    for (int qi = 0; qi < qmax; ++qi) {
+      const uint64_t a = av[qi], g = gv[c + in.qlo + qi];
+      if (a == kInf64 || g == kInf64) continue;
+      const uint64_t s = a + g;
+      best = s < best ? s : best;
+    }
+  }
+  cp.G[(cp.goff[n] + u) * C + c] = best;
+}
+
+// --------------------------------------------------------------------------
+// Optimal edges reachable from (u, c) = (0, 0): single CTA, instance by
+// instance; marks the needed buckets, then lists them.
+// reach: two bitsets of max_rows * C bits (global, zeroed by the host).
+// --------------------------------------------------------------------------
+__global__ void __launch_bounds__(1024) mem_bfs_kernel(const MemChainParams cp, uint32_t* reach0,
+                                                       uint32_t* reach1, int64_t words) {
+  const int C = cp.C;
+  const int tid = threadIdx.x, nth = blockDim.x;
+  if (tid == 0 && cp.G[0] != kInf64) reach0[0] = 1u;
+  __syncthreads();
+  uint32_t* cur = reach0;
+  uint32_t* nxt = reach1;
+  for (int n = 0; n < cp.N; ++n) {
+    const MemInst in = cp.inst[n];
+    for (int64_t w = tid; w < words; w += nth) nxt[w] = 0;
+    __syncthreads();
+    const uint64_t* Gp = cp.G + cp.goff[n] * C;
+    const uint64_t* Gn = cp.G + cp.goff[n + 1] * C;
+    uint32_t* need = cp.need + cp.need_off[in.slot];
+    const int64_t nstates = (int64_t)in.rows * C;
+    for (int64_t s = tid; s < nstates; s += nth) {
+      if (!((cur[s >> 5] >> (s & 31)) & 1u)) continue;
+      const int u = (int)(s / C), c = (int)(s % C);
+      const uint64_t target = Gp[s];
+      for (int v = 0; v < in.cols; ++v)
+        for (int qi = 0; qi < in.nq; ++qi) {
+          const int cc = c + in.qlo + qi;
+          if (cc >= C) break;
+          const int64_t cell = ((int64_t)u * in.cols + v) * in.nq + qi;
+          const uint64_t a = in.Am[cell], g = Gn[(int64_t)v * C + cc];
+          if (a == kInf64 || g == kInf64 || a + g != target) continue;
+          const int64_t t = (int64_t)v * C + cc;
+          atomicOr(&nxt[t >> 5], 1u << (t & 31));
+          atomicOr(&need[cell >> 5], 1u << (cell & 31));
+        }
+    }
+    __syncthreads();
+    uint32_t* tmp = cur;
+    cur = nxt;
+    nxt = tmp;
+  }
+  // list the needed buckets
+  for (int sl = 0; sl < cp.nslot; ++sl) {
+    const int64_t w0 = cp.need_off[sl], w1 = cp.need_off[sl + 1];
+    for (int64_t w = w0 + tid; w < w1; w += nth) {
+      uint32_t m = cp.need[w];
+      while (m) {
+        const int b = __ffs(m) - 1;
+        m &= m - 1;
+        const int64_t cell = (w - w0) * 32 + b;
+        const int k = atomicAdd(cp.count, 1);
+        if (k < cp.list_cap) cp.list[k] = MemArgEntry{sl, (int32_t)cell, 0, 0};   // decoded by the argmin
+      }
+    }
+  }
+}
+
+// --------------------------------------------------------------------------
+// Least combination index of listed buckets.  One CTA per entry (grid-stride).
+// --------------------------------------------------------------------------
+template <typename V>
+__global__ void __launch_bounds__(256) mem_argmin_kernel(const MemArgSlot* __restrict__ slots,
+                                                         const MemArgEntry* __restrict__ list,
+                                                         const int32_t* __restrict__ count, int cell_mode) {
+  using M = MT<V>;
+  __shared__ int32_t s_tiles[1024];
+  __shared__ int s_nt, s_over;
+  __shared__ unsigned long long s_best, s_sig;
+  const int tid = threadIdx.x;
+  const int total = *count;
+  for (int e = blockIdx.x; e < total; e += gridDim.x) {
+    const MemArgEntry ent = list[e];
+    const MemArgSlot& S = slots[ent.slot];
+    int u, v, qi;
+    int64_t cell;
+    if (cell_mode) {                                 // entry = (slot, cell)
+      cell = ent.u;
+      qi = (int)(cell % S.nq);
+      v = (int)((cell / S.nq) % S.Do);
+      u = (int)(cell / ((int64_t)S.nq * S.Do));
+    } else {
+      u = ent.u; v = ent.v; qi = ent.qi;
+      cell = ((int64_t)u * S.Do + v) * S.nq + qi;
+    }
+    const uint64_t A = S.Am[cell];
+    if (A == kInf64) {
+      if (tid == 0) S.Im[cell] = kInf64;
+      continue;
+    }
+    const V target = (V)A;
+    const int vslot = S.o_in_prefix ? 0 : v;
+    if (tid == 0) { s_nt = 0; s_over = 0; s_best = ~0ull; s_sig = ~0ull; }
+    __syncthreads();
+    const V* ch = static_cast<const V*>(S.chunk);
+    for (int t = tid; t < S.ntiles; t += 256) {
+      const int rc = S.tiles[t].z;
+      const int k = rc / S.nVp, vp = rc % S.nVp;
+      if (S.o_in_prefix && vp != v) continue;
+      const int rs = qi - k;
+      if (rs < 0 || rs >= S.RQs) continue;
+      if (ch[((int64_t)t * S.Din + u) * S.Wc + vslot * S.RQs + rs] == target) {
+        const int k2 = atomicAdd(&s_nt, 1);
+        if (k2 < 1024) s_tiles[k2] = t;
+        else s_over = 1;
+      }
+    }
+    __syncthreads();
+    const int nt = s_over ? S.ntiles : s_nt;
+    const V* vals = static_cast<const V*>(S.vals);
+    const V* B = static_cast<const V*>(S.B);
+    const int64_t ld = (S.Wc + 3) & ~3;
+    for (int i = 0; i < nt; ++i) {
+      const int t = s_over ? i : s_tiles[i];
+      const int4 tl = S.tiles[t];
+      const int k = tl.z / S.nVp, vp = tl.z % S.nVp;
+      if (S.o_in_prefix && vp != v) continue;
+      const int rs = qi - k;
+      if (rs < 0 || rs >= S.RQs) continue;
+      for (int r = tid; r < tl.y; r += 256) {
+        const int64_t pr = S.perm[tl.x + r];
+        V x = 0;
+        for (int j = 0; j < S.nqx; ++j)
+          x = M::sat(x, vals[S.q_off[j] + (int64_t)mem_digit(S.pm, pr, S.q_pos[j]) * S.DinP + u]);
+        const uint64_t b = (uint64_t)B[pr * ld + vslot * S.RQs + rs];
+        if ((uint64_t)x + b == (uint64_t)target)
+          atomicMin(&s_best, (unsigned long long)((pr << 16) | (uint64_t)tl.z));
+      }
+    }
+    __syncthreads();
+    if (s_best == ~0ull) {                           // cannot happen for a finite A
+      if (tid == 0) S.Im[cell] = kInf64;
+      __syncthreads();
+      continue;
+    }
+    const int64_t pstar = (int64_t)(s_best >> 16);
+    const int rc = (int)(s_best & 0xFFFF);
+    const int rs = qi - rc / S.nVp;
+    const int cls = vslot * S.RQs + rs;
+    const int64_t c = mem_ctx(S.pm, pstar);
+    V xs = 0;                                        // X_{p*}[u]
+    for (int j = 0; j < S.nqx; ++j)
+      xs = M::sat(xs, vals[S.q_off[j] + (int64_t)mem_digit(S.pm, pstar, S.q_pos[j]) * S.DinP + u]);
+    // the least suffix of p* whose cost K0[p*] + T[c][s] = A - X_{p*}[u]
+    const V rel = target - xs - static_cast<const V*>(S.K0)[pstar];
+    const V* T = static_cast<const V*>(S.Tc) + c * S.nS;
+    for (int64_t s = tid; s < S.nS; s += 256)
+      if (S.sinfo[s] == cls && T[s] == rel) atomicMin(&s_sig, (unsigned long long)s);
+    __syncthreads();
+    if (tid == 0) S.Im[cell] = s_sig == ~0ull ? kInf64 : (uint64_t)pstar * (uint64_t)S.nS + s_sig;
+    __syncthreads();
+  }
+}
+
+// --------------------------------------------------------------------------
+// Forward greedy from (0, 0): among the optimal successors (v, q) the least
+// combination index (canonical plan); then digits (big-endian decode).
+// --------------------------------------------------------------------------
+__global__ void mem_greedy_kernel(const MemChainParams cp) {
+  const int lane = threadIdx.x;
+  const int C = cp.C;
+  int status = 0;
+  if (cp.G[0] == kInf64) status = 3;
+  int u = 0, c = 0;
+  for (int n = 0; n < cp.N && status == 0; ++n) {
+    const MemInst in = cp.inst[n];
+    const uint64_t target = cp.G[(cp.goff[n] + u) * C + c];
+    const uint64_t* Gn = cp.G + cp.goff[n + 1] * C;
+    uint64_t bi = kInf64;
+    int bp = -1;
+    for (int pr = lane; pr < in.cols * in.nq; pr += 32) {
+      const int v = pr / in.nq, qi = pr % in.nq;
+      const int cc = c + in.qlo + qi;
+      if (cc >= C) continue;
+      const int64_t cell = ((int64_t)u * in.cols + v) * in.nq + qi;
+      const uint64_t a = in.Am[cell], g = Gn[(int64_t)v * C + cc];
+      if (a == kInf64 || g == kInf64 || a + g != target) continue;
+      const uint64_t ix = in.Im[cell];
+      if (ix < bi) { bi = ix; bp = pr; }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const uint64_t ob = __shfl_xor_sync(0xffffffffu, bi, o);
+      const int op = __shfl_xor_sync(0xffffffffu, bp, o);
+      if (op >= 0 && (bp < 0 || ob < bi || (ob == bi && op < bp))) { bi = ob; bp = op; }
+    }
+    if (bp < 0) { status = 3; break; }
+    const int v = bp / in.nq, qi = bp % in.nq;
+    if (lane == 0) {
+      cp.seg_index[n] = bi;
+      cp.seg_ns[n] = in.Am[((int64_t)u * in.cols + v) * in.nq + qi];
+      cp.seg_q[n] = in.qlo + qi;
+    }
+    u = v;
+    c += in.qlo + qi;
+  }
+  __syncwarp();
+  if (lane == 0) {
+    *cp.status = status;
+    *cp.total = status ? kInf64 : cp.G[0];
+  }
+  if (status) return;
+  for (int64_t w = lane; w < (int64_t)cp.N * cp.kmax; w += 32) {
+    const int n = (int)(w / cp.kmax), j = (int)(w % cp.kmax);
+    const MemInst in = cp.inst[n];
+    int32_t d = -1;
+    if (j < in.K) {
+      uint64_t st = 1;
+      for (int k = in.K - 1; k > j; --k) st *= (uint64_t)cp.radix[in.radix_off + k];
+      d = (int32_t)((cp.seg_index[n] / st) % (uint64_t)cp.radix[in.radix_off + j]);
+    }
+    cp.digits[w] = d;
+  }
+}
+
+// ---------------------------------------------------------------- launchers
+template <typename V>
+cudaError_t launch_mem_enum(const MemEnumParams& p, int64_t nC, cudaStream_t st) {
+  const size_t smem = (size_t)p.Tlen * sizeof(V) + (size_t)(p.Wc + 1) * 4 + 16;
+  if (smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(mem_enum_kernel<V>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+  }
+  const int64_t grid = nC * p.nblkN;
+  if (grid <= 0) return cudaSuccess;
+  mem_enum_kernel<V><<<(unsigned)grid, 256, smem, st>>>(p);
+  return cudaGetLastError();
+}
+template <typename V>
+cudaError_t launch_mem_fold(const MemFoldParams& p, int64_t ntiles, cudaStream_t st) {
+  if (ntiles <= 0) return cudaSuccess;
+  mem_fold_kernel<V><<<dim3((unsigned)ntiles, (unsigned)p.ncolblk), 256, 0, st>>>(p);
+  return cudaGetLastError();
+}
+template <typename V>
+cudaError_t launch_mem_amin(const MemAminParams& p, cudaStream_t st) {
+  const int64_t total = (int64_t)p.Din * p.Do * p.nq;
+  if (total <= 0) return cudaSuccess;
+  mem_amin_kernel<V><<<(unsigned)((total * 32 + 255) / 256), 256, 0, st>>>(p);
+  return cudaGetLastError();
+}
+cudaError_t launch_mem_chain_step(const MemChainParams& cp, int n, int rows, int rowlen, cudaStream_t st) {
+  const size_t smem = (size_t)rowlen * 8 + 16;
+  if (smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(mem_chain_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+  }
+  mem_chain_kernel<<<dim3((unsigned)rows, (unsigned)((cp.C + 255) / 256)), 256, smem, st>>>(cp, n);
+  return cudaGetLastError();
+}
+cudaError_t launch_mem_bfs(const MemChainParams& cp, uint32_t* r0, uint32_t* r1, int64_t words, cudaStream_t st) {
+  mem_bfs_kernel<<<1, 1024, 0, st>>>(cp, r0, r1, words);
+  return cudaGetLastError();
+}
+template <typename V>
+cudaError_t launch_mem_argmin(const MemArgSlot* slots, const MemArgEntry* list, const int32_t* count, int grid,
+                              int cell_mode, cudaStream_t st) {
+  mem_argmin_kernel<V><<<grid, 256, 0, st>>>(slots, list, count, cell_mode);
+  return cudaGetLastError();
+}
+cudaError_t launch_mem_greedy(const MemChainParams& cp, cudaStream_t st) {
+  mem_greedy_kernel<<<1, 32, 0, st>>>(cp);
+  return cudaGetLastError();
+}
+
+template cudaError_t launch_mem_enum<uint32_t>(const MemEnumParams&, int64_t, cudaStream_t);
+template cudaError_t launch_mem_enum<uint64_t>(const MemEnumParams&, int64_t, cudaStream_t);
+template cudaError_t launch_mem_fold<uint32_t>(const MemFoldParams&, int64_t, cudaStream_t);
+template cudaError_t launch_mem_fold<uint64_t>(const MemFoldParams&, int64_t, cudaStream_t);
+template cudaError_t launch_mem_amin<uint32_t>(const MemAminParams&, cudaStream_t);
+template cudaError_t launch_mem_amin<uint64_t>(const MemAminParams&, cudaStream_t);
+template cudaError_t launch_mem_argmin<uint32_t>(const MemArgSlot*, const MemArgEntry*, const int32_t*, int, int,
+                                                 cudaStream_t);
+template cudaError_t launch_mem_argmin<uint64_t>(const MemArgSlot*, const MemArgEntry*, const int32_t*, int, int,
+                                                 cudaStream_t);
+
+}  // namespace cfp
