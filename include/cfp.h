@@ -226,8 +226,9 @@ cfp_status cfp_search_plan_mem(cfp_ctx* ctx, const cfp_problem* p, const cfp_mem
  * the tables already in HBM): prepare validates and stages, execute runs the
  * whole path on the ctx stream without host synchronisation, fetch copies the
  * plan out.  cfp_mem_time_kernels(prep, 1) before execute records events;
- * cfp_mem_kernel_ms then reports the enumeration+fold ms and the total ms of
- * the last execute, the combinations per execute and the kernel launches. */
+ * cfp_mem_kernel_ms then reports, for the last execute, the ms of the
+ * enumeration kernels, of enumeration + folds + bucket minima, and of the
+ * whole path, plus the combinations per execute and the kernel launches. */
 typedef struct cfp_mem_prepared cfp_mem_prepared;
 cfp_status cfp_mem_prepare(cfp_ctx* ctx, const cfp_problem* p, const cfp_mem_model* mem,
                            cfp_mem_prepared** out);
@@ -236,8 +237,11 @@ cfp_status cfp_mem_fetch_plan(cfp_ctx* ctx, cfp_mem_prepared* prep, cfp_plan* ou
                               int64_t* total_q);
 void       cfp_mem_free(cfp_mem_prepared* prep);
 cfp_status cfp_mem_time_kernels(cfp_mem_prepared* prep, int32_t on);
-cfp_status cfp_mem_kernel_ms(cfp_mem_prepared* prep, double* tables_ms, double* total_ms,
-                             double* combos, int32_t* launches);
+cfp_status cfp_mem_kernel_ms(cfp_mem_prepared* prep, double* enum_ms, double* tables_ms,
+                             double* total_ms, double* combos, int32_t* launches);
+/* Algorithmic (min,+) work of the cross-term folds of one execute: one fused
+ * add+min per (prefix, input state, suffix class) per transition. */
+cfp_status cfp_mem_fold_ops(const cfp_mem_prepared* prep, double* fold_addmins);
 
 /* One transition's memory-bucketed table: cost_out / index_out are
  * [d_in][D_o][nq] row-major with nq = qhi - qlo + 1.  Pass cost_out =

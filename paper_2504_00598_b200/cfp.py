@@ -90,7 +90,7 @@ EXPORTS = ["cfp_ctx_create", "cfp_ctx_destroy", "cfp_last_error", "cfp_nccl_uniq
            "cfp_shard_range", "cfp_pack_keys", "cfp_unpack_keys", "cfp_intpipe_bench",
            "cfp_minplus_bench", "cfp_search_plan_mem", "cfp_segment_costs_mem", "cfp_mem_prepare",
            "cfp_mem_execute", "cfp_mem_fetch_plan", "cfp_mem_free", "cfp_mem_time_kernels",
-           "cfp_mem_kernel_ms"]
+           "cfp_mem_kernel_ms", "cfp_mem_fold_ops"]
 
 _lib = None
 
@@ -143,7 +143,9 @@ def lib() -> C.CDLL:
     L.cfp_mem_free.argtypes = [vp]
     L.cfp_mem_free.restype = None
     L.cfp_mem_time_kernels.argtypes = [vp, C.c_int32]
-    L.cfp_mem_kernel_ms.argtypes = [vp, P(C.c_double), P(C.c_double), P(C.c_double), P(C.c_int32)]
+    L.cfp_mem_kernel_ms.argtypes = [vp, P(C.c_double), P(C.c_double), P(C.c_double), P(C.c_double),
+                                    P(C.c_int32)]
+    L.cfp_mem_fold_ops.argtypes = [vp, P(C.c_double)]
     _lib = L
     return L
 
@@ -476,10 +478,16 @@ class PreparedMem:
         _check(lib().cfp_mem_time_kernels(self._h, 1 if on else 0))
 
     def kernel_ms(self):
-        """(enumeration+fold ms, total ms, combinations per execute, kernel launches)."""
-        a, b, c, n = C.c_double(), C.c_double(), C.c_double(), C.c_int32()
-        _check(lib().cfp_mem_kernel_ms(self._h, C.byref(a), C.byref(b), C.byref(c), C.byref(n)))
-        return a.value, b.value, c.value, n.value
+        """(enumeration ms, enumeration+fold+minima ms, total ms, combinations per
+        execute, kernel launches) of the last execute."""
+        e, a, b, c, n = C.c_double(), C.c_double(), C.c_double(), C.c_double(), C.c_int32()
+        _check(lib().cfp_mem_kernel_ms(self._h, C.byref(e), C.byref(a), C.byref(b), C.byref(c), C.byref(n)))
+        return e.value, a.value, b.value, c.value, n.value
+
+    def fold_ops(self) -> float:
+        f = C.c_double()
+        _check(lib().cfp_mem_fold_ops(self._h, C.byref(f)))
+        return f.value
 
     def close(self):
         if self._h:

@@ -240,16 +240,23 @@ struct MemPrefixMap {
   int32_t non_pos[kMaxDigits];
 };
 
+// Prefix rows are ordered by position pos: prefixes sorted by (ctx value,
+// prefix-memory class, p) -- perm[pos] = p.  Enumeration tiles (<= 1024
+// positions) and fold tiles (<= kMemFoldTile positions) never straddle a ctx
+// value resp. a (ctx, class) group.  B is class-quad-major: B[cls/4][pos][cls%4]
+// (coalesced enumeration stores, 16-byte fold loads).
+constexpr int kMemFoldTile = 1024;
+
 struct MemEnumParams {
-  MemPrefixMap pm;
-  int64_t nN;                        // non-ctx prefix values
-  int32_t nblkN;                     // CTAs per ctx value
   int32_t Wc;                        // classes per prefix row
   int32_t Tlen;                      // padded sorted row length (multiple of 4)
+  int64_t nP;
   const void* Ts;                    // [nC][Tlen] class-sorted, each class padded with CAP
   const int32_t* cstart;             // [Wc + 1]
-  const void* K0;                    // [nP]
-  void* B;                           // [nP][Wc] out: K0[p] + min over the class
+  const int4* etiles;                // (pos_start, count, ctx, 0)
+  const int32_t* perm;
+  const void* K0;                    // [nP] natural prefix order
+  void* B;                           // [Wc/4][nP][4] out: K0[p] + min over the class
 };
 
 struct MemFoldParams {
@@ -260,9 +267,10 @@ struct MemFoldParams {
   int64_t q_off[kMaxCross];          // element offset of Q^T[s][DinP] in `vals`
   const void* vals;
   int32_t Wc, ncolblk;
-  const int4* tiles;                 // [ntiles] (row_start, rows, rowclass, 0)
-  const int32_t* perm;               // [nP] prefixes sorted by (rowclass, p)
-  const void* B;                     // [nP][Wc]
+  int64_t nP;
+  const int4* tiles;                 // [ntiles] (pos_start, rows, rowclass, 0)
+  const int32_t* perm;               // [nP] position -> prefix
+  const void* B;                     // [Wc/4][nP][4]
   void* chunk;                       // [ntiles][Din][Wc] out
 };
 
@@ -282,6 +290,7 @@ struct MemArgSlot {                  // one transition (argmin side)
   MemPrefixMap pm;
   int32_t Din, DinP, Do, nq, RQs, nVp, o_in_prefix, Wc, ntiles;
   int32_t nqx;
+  int64_t nP;
   int32_t q_pos[kMaxCross];
   int64_t q_off[kMaxCross];
   const void* vals;

@@ -21,6 +21,7 @@
 //   mem_greedy_kernel forward greedy walk + digit decode.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdint>
 
 #include "cfp_internal.h"
@@ -73,6 +74,9 @@ __device__ __forceinline__ int64_t mem_prefix(const MemPrefixMap& m, int64_t c, 
 __device__ __forceinline__ int mem_digit(const MemPrefixMap& m, int64_t p, int pos) {
   return (int)((p / m.stride[pos]) % m.radix[pos]);
 }
+__device__ __forceinline__ int mem_digit32(const MemPrefixMap& m, uint32_t p, int pos) {
+  return (int)((p / (uint32_t)m.stride[pos]) % (uint32_t)m.radix[pos]);   // prefix space < 2^31
+}
 __device__ __forceinline__ int64_t mem_ctx(const MemPrefixMap& m, int64_t p) {
   int64_t c = 0;
   for (int i = 0; i < m.nctx; ++i) c = c * m.radix[m.ctx_pos[i]] + mem_digit(m, p, m.ctx_pos[i]);
@@ -80,10 +84,11 @@ __device__ __forceinline__ int64_t mem_ctx(const MemPrefixMap& m, int64_t p) {
 }
 
 // --------------------------------------------------------------------------
-// Enumeration.  CTA = (ctx value c, block of kMemNPF * 256 other-digit values);
-// thread = kMemNPF prefixes sharing c.  T[c] (class-sorted, padded with CAP)
-// is staged in shared memory; every combination of a class is one
-// VIADDMNMX per prefix: acc_i = min(K0[p_i] + T[c][e], acc_i).
+// Enumeration.  CTA = one enumeration tile (<= kMemNPF * 256 positions of one
+// ctx value c); thread = kMemNPF positions.  T[c] (class-sorted, padded with
+// CAP) is staged in shared memory; every combination of a class is one
+// VIADDMNMX per prefix: acc_i = min(K0[p_i] + T[c][e], acc_i).  B[cls][pos]
+// stores are coalesced (consecutive lanes, consecutive positions).
 // --------------------------------------------------------------------------
 template <typename V>
 __global__ void __launch_bounds__(256) mem_enum_kernel(const MemEnumParams p) {
@@ -91,9 +96,8 @@ __global__ void __launch_bounds__(256) mem_enum_kernel(const MemEnumParams p) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   V* ts = reinterpret_cast<V*>(smem_raw);
   int32_t* cs = reinterpret_cast<int32_t*>(ts + p.Tlen);
-  const int64_t c = blockIdx.x / p.nblkN;
-  const int64_t nb = blockIdx.x - c * p.nblkN;
-  const V* src = static_cast<const V*>(p.Ts) + c * p.Tlen;
+  const int4 et = p.etiles[blockIdx.x];
+  const V* src = static_cast<const V*>(p.Ts) + (int64_t)et.z * p.Tlen;
   for (int e = threadIdx.x * 4; e < p.Tlen; e += 256 * 4) {
     V t[4];
     M::load4(src + e, t);
@@ -102,18 +106,17 @@ __global__ void __launch_bounds__(256) mem_enum_kernel(const MemEnumParams p) {
   }
   for (int e = threadIdx.x; e <= p.Wc; e += 256) cs[e] = p.cstart[e];
   __syncthreads();
-  int64_t pf[kMemNPF];
+  int64_t pos[kMemNPF];
   V k0[kMemNPF];
   bool live[kMemNPF];
 #pragma unroll
   for (int i = 0; i < kMemNPF; ++i) {
-    const int64_t n = (nb * kMemNPF + i) * 256 + threadIdx.x;
-    live[i] = n < p.nN;
-    pf[i] = live[i] ? mem_prefix(p.pm, c, n) : 0;
-    k0[i] = live[i] ? static_cast<const V*>(p.K0)[pf[i]] : M::CAP;
+    const int r = i * 256 + threadIdx.x;
+    live[i] = r < et.y;
+    pos[i] = (int64_t)et.x + r;
+    k0[i] = live[i] ? static_cast<const V*>(p.K0)[p.perm[pos[i]]] : M::CAP;
   }
   V* B = static_cast<V*>(p.B);
-  const int64_t ld = (p.Wc + 3) & ~3;
   for (int cls = 0; cls < p.Wc; ++cls) {
     const int s0 = cs[cls], s1 = cs[cls + 1];
     V acc[kMemNPF];
@@ -128,9 +131,10 @@ __global__ void __launch_bounds__(256) mem_enum_kernel(const MemEnumParams p) {
 #pragma unroll
         for (int i = 0; i < kMemNPF; ++i) acc[i] = M::addmin(k0[i], t[q], acc[i]);
     }
+    V* row = B + (int64_t)(cls >> 2) * p.nP * 4 + (cls & 3);     // B[cls/4][pos][cls%4]
 #pragma unroll
     for (int i = 0; i < kMemNPF; ++i)
-      if (live[i]) B[pf[i] * ld + cls] = acc[i];
+      if (live[i]) row[pos[i] * 4] = acc[i];
   }
 }
 
@@ -143,12 +147,11 @@ __global__ void __launch_bounds__(256) mem_fold_kernel(const MemFoldParams p) {
   using M = MT<V>;
   constexpr int R = kMemFoldRows, FC = kMemFoldCols;
   __shared__ __align__(16) V Xs[R][32];
-  __shared__ __align__(16) V Bs[R][FC];
+  __shared__ __align__(16) V Bs[R][FC + 4];         // +4: conflict-free 16-byte row stores
   __shared__ int64_t rowp[R];
   const int4 tile = p.tiles[blockIdx.x];
   const int col0 = blockIdx.y * FC;
   const int ncols = min(FC, p.Wc - col0);
-  const int64_t ld = (p.Wc + 3) & ~3;
   const int tid = threadIdx.x;
   const int tu = tid >> 5, tc = tid & 31;          // u quad (8), class quad (32)
   const V* vals = static_cast<const V*>(p.vals);
@@ -164,6 +167,7 @@ __global__ void __launch_bounds__(256) mem_fold_kernel(const MemFoldParams p) {
     for (int r0 = 0; r0 < tile.y; r0 += R) {
       const int nr = min(R, tile.y - r0);
       if (tid < R) rowp[tid] = tid < nr ? (int64_t)p.perm[tile.x + r0 + tid] : -1;
+      const int64_t pos0 = (int64_t)tile.x + r0;
       __syncthreads();
       {   // X_p[u] for the staged rows: thread = (row, u quad)
         const int r = tid >> 3, uq = tid & 7;
@@ -177,7 +181,7 @@ __global__ void __launch_bounds__(256) mem_fold_kernel(const MemFoldParams p) {
 #pragma unroll
             for (int k = 0; k < 4; ++k) x[k] = 0;
             for (int i = 0; i < p.nq; ++i) {
-              const int dig = mem_digit(p.pm, pr, p.q_pos[i]);
+              const int dig = mem_digit32(p.pm, (uint32_t)pr, p.q_pos[i]);
               V y[4];
               M::load4(vals + p.q_off[i] + (int64_t)dig * p.DinP + ub + uq * 4, y);
 #pragma unroll
@@ -188,11 +192,11 @@ __global__ void __launch_bounds__(256) mem_fold_kernel(const MemFoldParams p) {
           for (int k = 0; k < 4; ++k) Xs[r][uq * 4 + k] = x[k];
         }
       }
-      for (int e = tid; e < R * (FC / 4); e += 256) {   // B rows of this class block
-        const int r = e / (FC / 4), cq = e % (FC / 4);
+      for (int e = tid; e < R * (FC / 4); e += 256) { // B[cls/4][pos][4]: lanes over positions (coalesced)
+        const int r = e % R, cq = e / R;
         V y[4];
-        if (rowp[r] >= 0 && cq * 4 < ncols) {
-          M::load4(B + rowp[r] * ld + col0 + cq * 4, y);
+        if (r < nr && cq * 4 < ncols) {
+          M::load4(B + ((int64_t)(col0 / 4 + cq) * p.nP + pos0 + r) * 4, y);
         } else {
 #pragma unroll
           for (int k = 0; k < 4; ++k) y[k] = M::CAP;
@@ -264,10 +268,12 @@ __global__ void mem_amin_kernel(const MemAminParams p) {
 // --------------------------------------------------------------------------
 // One backward DP step (P:625-628 with the memory state of S:466-474):
 // G_n(u, c) = min_{v, q: c + q <= Qmax} Am[u][v][q - qlo] + G_{n+1}(v, c + q).
-// CTA = (u, block of 256 memory states); Am row u staged in shared memory.
+// CTA = (u, 64 memory states); thread = (state, v group of 4); Am row u in
+// shared memory; the four v-group partial minima are reduced in shared memory.
 // --------------------------------------------------------------------------
 __global__ void __launch_bounds__(256) mem_chain_kernel(const MemChainParams cp, int n) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
+  __shared__ uint64_t part[4][64];
   uint64_t* arow = reinterpret_cast<uint64_t*>(smem_raw);
   const MemInst in = cp.inst[n];
   const int u = blockIdx.x;
@@ -275,65 +281,88 @@ __global__ void __launch_bounds__(256) mem_chain_kernel(const MemChainParams cp,
   const int rowlen = in.cols * in.nq;
   for (int e = threadIdx.x; e < rowlen; e += blockDim.x) arow[e] = in.Am[(int64_t)u * rowlen + e];
   __syncthreads();
-  const int c = blockIdx.y * blockDim.x + threadIdx.x;
-  if (c >= C) return;
+  const int cl = threadIdx.x & 63, vg = threadIdx.x >> 6;
+  const int c = blockIdx.y * 64 + cl;
   const uint64_t* Gn = cp.G + cp.goff[n + 1] * C;
   uint64_t best = kInf64;
-  for (int v = 0; v < in.cols; ++v) {
-    const uint64_t* gv = Gn + (int64_t)v * C;
-    const uint64_t* av = arow + v * in.nq;
+  if (c < C) {
     const int qmax = min(in.nq, C - c - in.qlo);    // c + qlo + qi <= Qmax = C - 1
-    for (int qi = 0; qi < qmax; ++qi) {
-      const uint64_t a = av[qi], g = gv[c + in.qlo + qi];
-      if (a == kInf64 || g == kInf64) continue;
-      const uint64_t s = a + g;
-      best = s < best ? s : best;
+    for (int v = vg; v < in.cols; v += 4) {
+      const uint64_t* gv = Gn + (int64_t)v * C + c + in.qlo;
+      const uint64_t* av = arow + v * in.nq;
+      for (int qi = 0; qi < qmax; ++qi) {
+        const uint64_t a = av[qi], g = gv[qi];
+        if (a == kInf64 || g == kInf64) continue;
+        const uint64_t s = a + g;
+        best = s < best ? s : best;
+      }
     }
   }
-  cp.G[(cp.goff[n] + u) * C + c] = best;
+  part[vg][cl] = best;
+  __syncthreads();
+  if (vg == 0 && c < C) {
+    uint64_t b = part[0][cl];
+#pragma unroll
+    for (int k = 1; k < 4; ++k) b = part[k][cl] < b ? part[k][cl] : b;
+    cp.G[(cp.goff[n] + u) * C + c] = b;
+  }
 }
 
 // --------------------------------------------------------------------------
 // Optimal edges reachable from (u, c) = (0, 0): single CTA, instance by
-// instance; marks the needed buckets, then lists them.
-// reach: two bitsets of max_rows * C bits (global, zeroed by the host).
+// instance.  The reachable states of level n are listed (ballot compaction),
+// then every (state, v, q) candidate is checked in parallel; optimal ones set
+// the next level's reach bit and their bucket's `need` bit.  All levels'
+// reach bitsets are kept (reach + goff[n] * C bits) for the successor table.
 // --------------------------------------------------------------------------
-__global__ void __launch_bounds__(1024) mem_bfs_kernel(const MemChainParams cp, uint32_t* reach0,
-                                                       uint32_t* reach1, int64_t words) {
+__global__ void __launch_bounds__(1024) mem_bfs_kernel(const MemChainParams cp, uint32_t* reach,
+                                                       int32_t* slist, int64_t slist_cap) {
+  __shared__ int s_n;
   const int C = cp.C;
   const int tid = threadIdx.x, nth = blockDim.x;
-  if (tid == 0 && cp.G[0] != kInf64) reach0[0] = 1u;
+  if (tid == 0 && cp.G[0] != kInf64) reach[0] = 1u;   // (u, c) = (0, 0) at level 0
   __syncthreads();
-  uint32_t* cur = reach0;
-  uint32_t* nxt = reach1;
   for (int n = 0; n < cp.N; ++n) {
     const MemInst in = cp.inst[n];
-    for (int64_t w = tid; w < words; w += nth) nxt[w] = 0;
-    __syncthreads();
-    const uint64_t* Gp = cp.G + cp.goff[n] * C;
-    const uint64_t* Gn = cp.G + cp.goff[n + 1] * C;
-    uint32_t* need = cp.need + cp.need_off[in.slot];
+    const int64_t base = cp.goff[n] * C, nbase = cp.goff[n + 1] * C;
     const int64_t nstates = (int64_t)in.rows * C;
-    for (int64_t s = tid; s < nstates; s += nth) {
-      if (!((cur[s >> 5] >> (s & 31)) & 1u)) continue;
-      const int u = (int)(s / C), c = (int)(s % C);
-      const uint64_t target = Gp[s];
-      for (int v = 0; v < in.cols; ++v)
-        for (int qi = 0; qi < in.nq; ++qi) {
-          const int cc = c + in.qlo + qi;
-          if (cc >= C) break;
-          const int64_t cell = ((int64_t)u * in.cols + v) * in.nq + qi;
-          const uint64_t a = in.Am[cell], g = Gn[(int64_t)v * C + cc];
-          if (a == kInf64 || g == kInf64 || a + g != target) continue;
-          const int64_t t = (int64_t)v * C + cc;
-          atomicOr(&nxt[t >> 5], 1u << (t & 31));
-          atomicOr(&need[cell >> 5], 1u << (cell & 31));
-        }
+    if (tid == 0) s_n = 0;
+    __syncthreads();
+    for (int64_t s0 = 0; s0 < nstates; s0 += nth) {  // list the reachable states
+      const int64_t s = s0 + tid;
+      const int64_t b = base + s;
+      const bool on = s < nstates && ((reach[b >> 5] >> (b & 31)) & 1u);
+      const unsigned m = __ballot_sync(0xffffffffu, on);
+      int wb = 0;
+      if ((tid & 31) == 0 && m) wb = atomicAdd(&s_n, __popc(m));
+      wb = __shfl_sync(0xffffffffu, wb, 0);
+      if (on) {
+        const int k = wb + __popc(m & ((1u << (tid & 31)) - 1u));
+        if (k < slist_cap) slist[k] = (int32_t)s;
+      }
     }
     __syncthreads();
-    uint32_t* tmp = cur;
-    cur = nxt;
-    nxt = tmp;
+    const int ns = (int)min((int64_t)s_n, slist_cap);
+    const uint64_t* Gp = cp.G + base;
+    const uint64_t* Gn = cp.G + nbase;
+    uint32_t* need = cp.need + cp.need_off[in.slot];
+    const int per = in.cols * in.nq;
+    const int64_t work = (int64_t)ns * per;
+    for (int64_t w = tid; w < work; w += nth) {
+      const int si = (int)(w / per), r = (int)(w - (int64_t)si * per);
+      const int v = r / in.nq, qi = r - v * in.nq;
+      const int s = slist[si];
+      const int u = s / C, c = s - u * C;
+      const int cc = c + in.qlo + qi;
+      if (cc >= C) continue;
+      const int64_t cell = ((int64_t)u * in.cols + v) * in.nq + qi;
+      const uint64_t a = in.Am[cell], g = Gn[(int64_t)v * C + cc];
+      if (a == kInf64 || g == kInf64 || a + g != Gp[s]) continue;
+      const int64_t t = nbase + (int64_t)v * C + cc;
+      atomicOr(&reach[t >> 5], 1u << (t & 31));
+      atomicOr(&need[cell >> 5], 1u << (cell & 31));
+    }
+    __syncthreads();
   }
   // list the needed buckets
   for (int sl = 0; sl < cp.nslot; ++sl) {
@@ -348,6 +377,49 @@ __global__ void __launch_bounds__(1024) mem_bfs_kernel(const MemChainParams cp, 
         if (k < cp.list_cap) cp.list[k] = MemArgEntry{sl, (int32_t)cell, 0, 0};   // decoded by the argmin
       }
     }
+  }
+}
+
+// --------------------------------------------------------------------------
+// Successor of every reachable state (all levels in parallel, one warp per
+// state): among the optimal (v, q) the least combination index.
+// succ[(goff[n] + u) * C + c] = v * nq + qi, -1 = none.
+// --------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) mem_succ_kernel(const MemChainParams cp, const uint32_t* reach,
+                                                       int32_t* succ) {
+  const int C = cp.C;
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int64_t total = cp.goff[cp.N] * C;        // states of levels 0..N-1
+  for (int64_t b = warp; b < total; b += nwarps) {
+    if (!((reach[b >> 5] >> (b & 31)) & 1u)) continue;            // warp-uniform
+    int n = 0;
+    while (cp.goff[n + 1] * C <= b) ++n;
+    const MemInst in = cp.inst[n];
+    const int64_t s = b - cp.goff[n] * C;
+    const int u = (int)(s / C), c = (int)(s % C);
+    const uint64_t target = cp.G[b];
+    const uint64_t* Gn = cp.G + cp.goff[n + 1] * C;
+    uint64_t bi = kInf64;
+    int bp = -1;
+    for (int pr = lane; pr < in.cols * in.nq; pr += 32) {
+      const int v = pr / in.nq, qi = pr % in.nq;
+      const int cc = c + in.qlo + qi;
+      if (cc >= C) continue;
+      const int64_t cell = ((int64_t)u * in.cols + v) * in.nq + qi;
+      const uint64_t a = in.Am[cell], g = Gn[(int64_t)v * C + cc];
+      if (a == kInf64 || g == kInf64 || a + g != target) continue;
+      const uint64_t ix = in.Im[cell];
+      if (ix < bi) { bi = ix; bp = pr; }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const uint64_t ob = __shfl_xor_sync(0xffffffffu, bi, o);
+      const int op = __shfl_xor_sync(0xffffffffu, bp, o);
+      if (op >= 0 && (bp < 0 || ob < bi || (ob == bi && op < bp))) { bi = ob; bp = op; }
+    }
+    if (lane == 0) succ[b] = bp;
   }
 }
 
@@ -404,7 +476,6 @@ __global__ void __launch_bounds__(256) mem_argmin_kernel(const MemArgSlot* __res
     const int nt = s_over ? S.ntiles : s_nt;
     const V* vals = static_cast<const V*>(S.vals);
     const V* B = static_cast<const V*>(S.B);
-    const int64_t ld = (S.Wc + 3) & ~3;
     for (int i = 0; i < nt; ++i) {
       const int t = s_over ? i : s_tiles[i];
       const int4 tl = S.tiles[t];
@@ -417,9 +488,10 @@ __global__ void __launch_bounds__(256) mem_argmin_kernel(const MemArgSlot* __res
         V x = 0;
         for (int j = 0; j < S.nqx; ++j)
           x = M::sat(x, vals[S.q_off[j] + (int64_t)mem_digit(S.pm, pr, S.q_pos[j]) * S.DinP + u]);
-        const uint64_t b = (uint64_t)B[pr * ld + vslot * S.RQs + rs];
+        const int cl = vslot * S.RQs + rs;
+        const uint64_t b = (uint64_t)B[((int64_t)(cl >> 2) * S.nP + tl.x + r) * 4 + (cl & 3)];
         if ((uint64_t)x + b == (uint64_t)target)
-          atomicMin(&s_best, (unsigned long long)((pr << 16) | (uint64_t)tl.z));
+          atomicMin(&s_best, (unsigned long long)(((uint64_t)pr << 32) | (uint64_t)t));
       }
     }
     __syncthreads();
@@ -428,8 +500,8 @@ __global__ void __launch_bounds__(256) mem_argmin_kernel(const MemArgSlot* __res
       __syncthreads();
       continue;
     }
-    const int64_t pstar = (int64_t)(s_best >> 16);
-    const int rc = (int)(s_best & 0xFFFF);
+    const int64_t pstar = (int64_t)(s_best >> 32);
+    const int rc = S.tiles[(int)(s_best & 0xFFFFFFFFu)].z;
     const int rs = qi - rc / S.nVp;
     const int cls = vslot * S.RQs + rs;
     const int64_t c = mem_ctx(S.pm, pstar);
@@ -448,53 +520,33 @@ __global__ void __launch_bounds__(256) mem_argmin_kernel(const MemArgSlot* __res
 }
 
 // --------------------------------------------------------------------------
-// Forward greedy from (0, 0): among the optimal successors (v, q) the least
-// combination index (canonical plan); then digits (big-endian decode).
+// Forward greedy from (0, 0) through the successor table (the least
+// combination index among the optimal successors = canonical plan), then the
+// digits (big-endian decode), one warp.
 // --------------------------------------------------------------------------
-__global__ void mem_greedy_kernel(const MemChainParams cp) {
+__global__ void mem_greedy_kernel(const MemChainParams cp, const int32_t* succ) {
   const int lane = threadIdx.x;
   const int C = cp.C;
-  int status = 0;
-  if (cp.G[0] == kInf64) status = 3;
-  int u = 0, c = 0;
-  for (int n = 0; n < cp.N && status == 0; ++n) {
-    const MemInst in = cp.inst[n];
-    const uint64_t target = cp.G[(cp.goff[n] + u) * C + c];
-    const uint64_t* Gn = cp.G + cp.goff[n + 1] * C;
-    uint64_t bi = kInf64;
-    int bp = -1;
-    for (int pr = lane; pr < in.cols * in.nq; pr += 32) {
-      const int v = pr / in.nq, qi = pr % in.nq;
-      const int cc = c + in.qlo + qi;
-      if (cc >= C) continue;
-      const int64_t cell = ((int64_t)u * in.cols + v) * in.nq + qi;
-      const uint64_t a = in.Am[cell], g = Gn[(int64_t)v * C + cc];
-      if (a == kInf64 || g == kInf64 || a + g != target) continue;
-      const uint64_t ix = in.Im[cell];
-      if (ix < bi) { bi = ix; bp = pr; }
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      const uint64_t ob = __shfl_xor_sync(0xffffffffu, bi, o);
-      const int op = __shfl_xor_sync(0xffffffffu, bp, o);
-      if (op >= 0 && (bp < 0 || ob < bi || (ob == bi && op < bp))) { bi = ob; bp = op; }
-    }
-    if (bp < 0) { status = 3; break; }
-    const int v = bp / in.nq, qi = bp % in.nq;
-    if (lane == 0) {
-      cp.seg_index[n] = bi;
-      cp.seg_ns[n] = in.Am[((int64_t)u * in.cols + v) * in.nq + qi];
-      cp.seg_q[n] = in.qlo + qi;
-    }
-    u = v;
-    c += in.qlo + qi;
-  }
-  __syncwarp();
   if (lane == 0) {
+    int status = cp.G[0] == kInf64 ? 3 : 0;
+    int u = 0, c = 0;
+    for (int n = 0; n < cp.N && status == 0; ++n) {
+      const MemInst in = cp.inst[n];
+      const int bp = succ[(cp.goff[n] + u) * C + c];
+      if (bp < 0) { status = 3; break; }
+      const int v = bp / in.nq, qi = bp % in.nq;
+      const int64_t cell = ((int64_t)u * in.cols + v) * in.nq + qi;
+      cp.seg_index[n] = in.Im[cell];
+      cp.seg_ns[n] = in.Am[cell];
+      cp.seg_q[n] = in.qlo + qi;
+      u = v;
+      c += in.qlo + qi;
+    }
     *cp.status = status;
     *cp.total = status ? kInf64 : cp.G[0];
   }
-  if (status) return;
+  __syncwarp();
+  if (*cp.status) return;
   for (int64_t w = lane; w < (int64_t)cp.N * cp.kmax; w += 32) {
     const int n = (int)(w / cp.kmax), j = (int)(w % cp.kmax);
     const MemInst in = cp.inst[n];
@@ -516,7 +568,7 @@ cudaError_t launch_mem_enum(const MemEnumParams& p, int64_t nC, cudaStream_t st)
     cudaError_t e = cudaFuncSetAttribute(mem_enum_kernel<V>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
   }
-  const int64_t grid = nC * p.nblkN;
+  const int64_t grid = nC;                           // number of enumeration tiles
   if (grid <= 0) return cudaSuccess;
   mem_enum_kernel<V><<<(unsigned)grid, 256, smem, st>>>(p);
   return cudaGetLastError();
@@ -540,11 +592,18 @@ cudaError_t launch_mem_chain_step(const MemChainParams& cp, int n, int rows, int
     cudaError_t e = cudaFuncSetAttribute(mem_chain_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
   }
-  mem_chain_kernel<<<dim3((unsigned)rows, (unsigned)((cp.C + 255) / 256)), 256, smem, st>>>(cp, n);
+  mem_chain_kernel<<<dim3((unsigned)rows, (unsigned)((cp.C + 63) / 64)), 256, smem, st>>>(cp, n);
   return cudaGetLastError();
 }
-cudaError_t launch_mem_bfs(const MemChainParams& cp, uint32_t* r0, uint32_t* r1, int64_t words, cudaStream_t st) {
-  mem_bfs_kernel<<<1, 1024, 0, st>>>(cp, r0, r1, words);
+cudaError_t launch_mem_bfs(const MemChainParams& cp, uint32_t* reach, int32_t* slist, int64_t slist_cap,
+                           cudaStream_t st) {
+  mem_bfs_kernel<<<1, 1024, 0, st>>>(cp, reach, slist, slist_cap);
+  return cudaGetLastError();
+}
+cudaError_t launch_mem_succ(const MemChainParams& cp, const uint32_t* reach, int32_t* succ, int64_t states,
+                            cudaStream_t st) {
+  const int64_t blocks = std::min<int64_t>(4096, (states * 32 + 255) / 256 + 1);
+  mem_succ_kernel<<<(unsigned)blocks, 256, 0, st>>>(cp, reach, succ);
   return cudaGetLastError();
 }
 template <typename V>
@@ -553,8 +612,8 @@ cudaError_t launch_mem_argmin(const MemArgSlot* slots, const MemArgEntry* list, 
   mem_argmin_kernel<V><<<grid, 256, 0, st>>>(slots, list, count, cell_mode);
   return cudaGetLastError();
 }
-cudaError_t launch_mem_greedy(const MemChainParams& cp, cudaStream_t st) {
-  mem_greedy_kernel<<<1, 32, 0, st>>>(cp);
+cudaError_t launch_mem_greedy(const MemChainParams& cp, const int32_t* succ, cudaStream_t st) {
+  mem_greedy_kernel<<<1, 32, 0, st>>>(cp, succ);
   return cudaGetLastError();
 }
 

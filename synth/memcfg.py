@@ -11,8 +11,14 @@ import math
 from .generators import make_config
 
 
-def mem_workload(cfg: str = "C3", seed: int = 0, dist: str = "shaped", levels: int = 256,
+# quanta per limit: enough that the per-block ceilings of a deep chain still
+# leave room between the smallest and largest quantised plan memory
+LEVELS = {"C1": 64, "C2": 256, "C3": 256, "C4": 512, "C5": 1024}
+
+
+def mem_workload(cfg: str = "C3", seed: int = 0, dist: str = "shaped", levels: int = 0,
                  frac: float = 0.35):
+    levels = levels or LEVELS.get(cfg, 256)
     p = make_config(cfg, seed, dist)
     lo = hi = 0
     for t in p.instances:
