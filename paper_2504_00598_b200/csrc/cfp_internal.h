@@ -226,7 +226,7 @@ struct ChainParams {
 // q = qP(p) + qS(sigma); suffix classes cls = vslot * RQs + (qS - qS_lo),
 // vslot = s_o when o is a suffix digit, else 0 (v then comes from the prefix).
 // ---------------------------------------------------------------------------
-constexpr int kMemFoldRows = 32;     // rows staged per fold step
+constexpr int kMemFoldRows = 64;     // rows staged per fold step
 constexpr int kMemFoldCols = 128;    // columns (classes) per fold CTA
 constexpr int kMemNPF = 4;           // prefixes per enumeration thread
 
@@ -266,7 +266,7 @@ struct MemFoldParams {
   int32_t q_pos[kMaxCross];          // prefix position of each consumer
   int64_t q_off[kMaxCross];          // element offset of Q^T[s][DinP] in `vals`
   const void* vals;
-  int32_t Wc, ncolblk;
+  int32_t Wc, ncolblk, fc;           // fc: columns per block (balanced, multiple of 4)
   int64_t nP;
   const int4* tiles;                 // [ntiles] (pos_start, rows, rowclass, 0)
   const int32_t* perm;               // [nP] position -> prefix

@@ -90,7 +90,7 @@ __device__ __forceinline__ int64_t mem_ctx(const MemPrefixMap& m, int64_t p) {
 // VIADDMNMX per prefix: acc_i = min(K0[p_i] + T[c][e], acc_i).  B[cls][pos]
 // stores are coalesced (consecutive lanes, consecutive positions).
 // --------------------------------------------------------------------------
-template <typename V>
+template <typename V, int NPF>
 __global__ void __launch_bounds__(256) mem_enum_kernel(const MemEnumParams p) {
   using M = MT<V>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -106,11 +106,11 @@ __global__ void __launch_bounds__(256) mem_enum_kernel(const MemEnumParams p) {
   }
   for (int e = threadIdx.x; e <= p.Wc; e += 256) cs[e] = p.cstart[e];
   __syncthreads();
-  int64_t pos[kMemNPF];
-  V k0[kMemNPF];
-  bool live[kMemNPF];
+  int64_t pos[NPF];
+  V k0[NPF];
+  bool live[NPF];
 #pragma unroll
-  for (int i = 0; i < kMemNPF; ++i) {
+  for (int i = 0; i < NPF; ++i) {
     const int r = i * 256 + threadIdx.x;
     live[i] = r < et.y;
     pos[i] = (int64_t)et.x + r;
@@ -119,9 +119,9 @@ __global__ void __launch_bounds__(256) mem_enum_kernel(const MemEnumParams p) {
   V* B = static_cast<V*>(p.B);
   for (int cls = 0; cls < p.Wc; ++cls) {
     const int s0 = cs[cls], s1 = cs[cls + 1];
-    V acc[kMemNPF];
+    V acc[NPF];
 #pragma unroll
-    for (int i = 0; i < kMemNPF; ++i) acc[i] = M::CAP;
+    for (int i = 0; i < NPF; ++i) acc[i] = M::CAP;
 #pragma unroll 2
     for (int e = s0; e < s1; e += 4) {
       V t[4];
@@ -129,11 +129,11 @@ __global__ void __launch_bounds__(256) mem_enum_kernel(const MemEnumParams p) {
 #pragma unroll
       for (int q = 0; q < 4; ++q)
 #pragma unroll
-        for (int i = 0; i < kMemNPF; ++i) acc[i] = M::addmin(k0[i], t[q], acc[i]);
+        for (int i = 0; i < NPF; ++i) acc[i] = M::addmin(k0[i], t[q], acc[i]);
     }
     V* row = B + (int64_t)(cls >> 2) * p.nP * 4 + (cls & 3);     // B[cls/4][pos][cls%4]
 #pragma unroll
-    for (int i = 0; i < kMemNPF; ++i)
+    for (int i = 0; i < NPF; ++i)
       if (live[i]) row[pos[i] * 4] = acc[i];
   }
 }
@@ -145,15 +145,18 @@ __global__ void __launch_bounds__(256) mem_enum_kernel(const MemEnumParams p) {
 template <typename V>
 __global__ void __launch_bounds__(256) mem_fold_kernel(const MemFoldParams p) {
   using M = MT<V>;
-  constexpr int R = kMemFoldRows, FC = kMemFoldCols;
+  constexpr int R = sizeof(V) == 4 ? kMemFoldRows : kMemFoldRows / 2;   // static smem < 48 KB
+  constexpr int FC = kMemFoldCols;
+  const int fc = p.fc;                              // balanced block width (<= FC, multiple of 4)
   __shared__ __align__(16) V Xs[R][32];
   __shared__ __align__(16) V Bs[R][FC + 4];         // +4: conflict-free 16-byte row stores
   __shared__ int64_t rowp[R];
   const int4 tile = p.tiles[blockIdx.x];
-  const int col0 = blockIdx.y * FC;
-  const int ncols = min(FC, p.Wc - col0);
+  const int col0 = blockIdx.y * fc;
+  const int ncols = min(fc, p.Wc - col0);
   const int tid = threadIdx.x;
-  const int tu = tid >> 5, tc = tid & 31;          // u quad (8), class quad (32)
+  const int ncq = (ncols + 3) >> 2;                 // class quads of this block
+  const int tu = tid / ncq, tc = tid - tu * ncq;    // thread = (u quad, class quad)
   const V* vals = static_cast<const V*>(p.vals);
   const V* B = static_cast<const V*>(p.B);
   V* out = static_cast<V*>(p.chunk) + (int64_t)blockIdx.x * p.Din * p.Wc;
@@ -166,11 +169,11 @@ __global__ void __launch_bounds__(256) mem_fold_kernel(const MemFoldParams p) {
       for (int j = 0; j < 4; ++j) res[i][j] = M::CAP;
     for (int r0 = 0; r0 < tile.y; r0 += R) {
       const int nr = min(R, tile.y - r0);
-      if (tid < R) rowp[tid] = tid < nr ? (int64_t)p.perm[tile.x + r0 + tid] : -1;
+      for (int e = tid; e < R; e += 256) rowp[e] = e < nr ? (int64_t)p.perm[tile.x + r0 + e] : -1;
       const int64_t pos0 = (int64_t)tile.x + r0;
       __syncthreads();
-      {   // X_p[u] for the staged rows: thread = (row, u quad)
-        const int r = tid >> 3, uq = tid & 7;
+      for (int e = tid; e < R * 8; e += 256) {   // X_p[u] for the staged rows: (row, u quad)
+        const int r = e >> 3, uq = e & 7;
         if (uq * 4 < ucnt) {
           V x[4];
           const int64_t pr = rowp[r];
@@ -192,7 +195,7 @@ __global__ void __launch_bounds__(256) mem_fold_kernel(const MemFoldParams p) {
           for (int k = 0; k < 4; ++k) Xs[r][uq * 4 + k] = x[k];
         }
       }
-      for (int e = tid; e < R * (FC / 4); e += 256) { // B[cls/4][pos][4]: lanes over positions (coalesced)
+      for (int e = tid; e < R * ncq; e += 256) {     // B[cls/4][pos][4]: lanes over positions (coalesced)
         const int r = e % R, cq = e / R;
         V y[4];
         if (r < nr && cq * 4 < ncols) {
@@ -205,7 +208,7 @@ __global__ void __launch_bounds__(256) mem_fold_kernel(const MemFoldParams p) {
         for (int k = 0; k < 4; ++k) Bs[r][cq * 4 + k] = y[k];
       }
       __syncthreads();
-      if (tu * 4 < ucnt && tc * 4 < ncols) {
+      if (tu < 8 && tu * 4 < ucnt) {
 #pragma unroll 4
         for (int r = 0; r < nr; ++r) {
           V x[4], y[4];
@@ -224,7 +227,7 @@ __global__ void __launch_bounds__(256) mem_fold_kernel(const MemFoldParams p) {
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
         const int u = ub + tu * 4 + i, cl = col0 + tc * 4 + j;
-        if (u < p.Din && cl < p.Wc && tu * 4 + i < ucnt) out[(int64_t)u * p.Wc + cl] = res[i][j];
+        if (tu < 8 && u < p.Din && cl < col0 + ncols && tu * 4 + i < ucnt) out[(int64_t)u * p.Wc + cl] = res[i][j];
       }
   }
 }
@@ -271,7 +274,7 @@ __global__ void mem_amin_kernel(const MemAminParams p) {
 // CTA = (u, 64 memory states); thread = (state, v group of 4); Am row u in
 // shared memory; the four v-group partial minima are reduced in shared memory.
 // --------------------------------------------------------------------------
-__global__ void __launch_bounds__(256) mem_chain_kernel(const MemChainParams cp, int n) {
+__global__ void __launch_bounds__(256) mem_chain_kernel(const MemChainParams cp, int n, int win) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ uint64_t part[4][64];
   uint64_t* arow = reinterpret_cast<uint64_t*>(smem_raw);
@@ -279,16 +282,25 @@ __global__ void __launch_bounds__(256) mem_chain_kernel(const MemChainParams cp,
   const int u = blockIdx.x;
   const int C = cp.C;
   const int rowlen = in.cols * in.nq;
+  const int c0 = blockIdx.y * 64;
+  const uint64_t* Gn = cp.G + cp.goff[n + 1] * C;
   for (int e = threadIdx.x; e < rowlen; e += blockDim.x) arow[e] = in.Am[(int64_t)u * rowlen + e];
+  // window of G_{n+1}: columns [c0 + qlo, c0 + qlo + win) of every row v
+  uint64_t* gw = arow + ((rowlen + 1) & ~1);
+  if (win > 0)
+    for (int e = threadIdx.x; e < in.cols * win; e += blockDim.x) {
+      const int v = e / win, k = e - v * win;
+      const int cc = c0 + in.qlo + k;
+      gw[e] = cc < C ? Gn[(int64_t)v * C + cc] : kInf64;
+    }
   __syncthreads();
   const int cl = threadIdx.x & 63, vg = threadIdx.x >> 6;
-  const int c = blockIdx.y * 64 + cl;
-  const uint64_t* Gn = cp.G + cp.goff[n + 1] * C;
+  const int c = c0 + cl;
   uint64_t best = kInf64;
   if (c < C) {
     const int qmax = min(in.nq, C - c - in.qlo);    // c + qlo + qi <= Qmax = C - 1
     for (int v = vg; v < in.cols; v += 4) {
-      const uint64_t* gv = Gn + (int64_t)v * C + c + in.qlo;
+      const uint64_t* gv = win > 0 ? gw + v * win + cl : Gn + (int64_t)v * C + c + in.qlo;
       const uint64_t* av = arow + v * in.nq;
       for (int qi = 0; qi < qmax; ++qi) {
         const uint64_t a = av[qi], g = gv[qi];
@@ -562,16 +574,20 @@ __global__ void mem_greedy_kernel(const MemChainParams cp, const int32_t* succ) 
 
 // ---------------------------------------------------------------- launchers
 template <typename V>
-cudaError_t launch_mem_enum(const MemEnumParams& p, int64_t nC, cudaStream_t st) {
+cudaError_t launch_mem_enum(const MemEnumParams& p, int64_t ntiles, int npf, cudaStream_t st) {
   const size_t smem = (size_t)p.Tlen * sizeof(V) + (size_t)(p.Wc + 1) * 4 + 16;
-  if (smem > 48 * 1024) {
-    cudaError_t e = cudaFuncSetAttribute(mem_enum_kernel<V>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-  }
-  const int64_t grid = nC;                           // number of enumeration tiles
-  if (grid <= 0) return cudaSuccess;
-  mem_enum_kernel<V><<<(unsigned)grid, 256, smem, st>>>(p);
-  return cudaGetLastError();
+  if (ntiles <= 0) return cudaSuccess;
+  auto go = [&](auto kern) -> cudaError_t {
+    if (smem > 48 * 1024) {
+      cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (e != cudaSuccess) return e;
+    }
+    kern<<<(unsigned)ntiles, 256, smem, st>>>(p);
+    return cudaGetLastError();
+  };
+  if (npf == 4) return go(mem_enum_kernel<V, 4>);
+  if (npf == 2) return go(mem_enum_kernel<V, 2>);
+  return go(mem_enum_kernel<V, 1>);
 }
 template <typename V>
 cudaError_t launch_mem_fold(const MemFoldParams& p, int64_t ntiles, cudaStream_t st) {
@@ -586,13 +602,19 @@ cudaError_t launch_mem_amin(const MemAminParams& p, cudaStream_t st) {
   mem_amin_kernel<V><<<(unsigned)((total * 32 + 255) / 256), 256, 0, st>>>(p);
   return cudaGetLastError();
 }
-cudaError_t launch_mem_chain_step(const MemChainParams& cp, int n, int rows, int rowlen, cudaStream_t st) {
-  const size_t smem = (size_t)rowlen * 8 + 16;
+cudaError_t launch_mem_chain_step(const MemChainParams& cp, int n, int rows, int cols, int nq, cudaStream_t st) {
+  const int rowlen = cols * nq;
+  int win = 64 + nq - 1;                            // G_{n+1} window per CTA in shared memory
+  size_t smem = (size_t)((rowlen + 1) & ~1) * 8 + (size_t)cols * win * 8 + 16;
+  if (smem > 160 * 1024) {                          // too wide: read G_{n+1} from L2
+    win = 0;
+    smem = (size_t)((rowlen + 1) & ~1) * 8 + 16;
+  }
   if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(mem_chain_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
   }
-  mem_chain_kernel<<<dim3((unsigned)rows, (unsigned)((cp.C + 63) / 64)), 256, smem, st>>>(cp, n);
+  mem_chain_kernel<<<dim3((unsigned)rows, (unsigned)((cp.C + 63) / 64)), 256, smem, st>>>(cp, n, win);
   return cudaGetLastError();
 }
 cudaError_t launch_mem_bfs(const MemChainParams& cp, uint32_t* reach, int32_t* slist, int64_t slist_cap,
@@ -617,8 +639,8 @@ cudaError_t launch_mem_greedy(const MemChainParams& cp, const int32_t* succ, cud
   return cudaGetLastError();
 }
 
-template cudaError_t launch_mem_enum<uint32_t>(const MemEnumParams&, int64_t, cudaStream_t);
-template cudaError_t launch_mem_enum<uint64_t>(const MemEnumParams&, int64_t, cudaStream_t);
+template cudaError_t launch_mem_enum<uint32_t>(const MemEnumParams&, int64_t, int, cudaStream_t);
+template cudaError_t launch_mem_enum<uint64_t>(const MemEnumParams&, int64_t, int, cudaStream_t);
 template cudaError_t launch_mem_fold<uint32_t>(const MemFoldParams&, int64_t, cudaStream_t);
 template cudaError_t launch_mem_fold<uint64_t>(const MemFoldParams&, int64_t, cudaStream_t);
 template cudaError_t launch_mem_amin<uint32_t>(const MemAminParams&, cudaStream_t);
