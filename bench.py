@@ -159,6 +159,37 @@ def cpu_baseline(prob, budget_s: float = 12.0):
                       f"states), {dt:.2f} s; value = combos/step x fraction / time"}
 
 
+def cpu_baseline_mem(prob, quantum, budget_s: float = 12.0):
+    """The memory-constrained oracle (as it stands) on a bounded sample: the
+    first fraction of every used transition's combination space (all input
+    states, memory-bucketed tables), scaled to combos/s."""
+    from oracle import oracle as O
+    O.build()
+    cores = len(os.sched_getaffinity(0))
+    m = O.Marshalled(prob)
+    used = sorted(set(int(x) for x in prob.instances))
+
+    def sample(frac):
+        t0 = time.perf_counter()
+        for tr in used:
+            S = prob.num_combinations(prob.transitions[tr].type)
+            O.segment_table_mem_range(prob, tr, quantum, 0, max(1, min(S, int(round(S * frac)))),
+                                      nthreads=cores, m=m)
+        return time.perf_counter() - t0
+
+    frac = 1e-7
+    while True:
+        dt = sample(frac)
+        if dt > budget_s / 8 or frac >= 1.0:
+            break
+        frac = min(1.0, frac * max(2.0, (budget_s / 8) / max(dt, 1e-4)))
+    frac = min(1.0, frac * budget_s / 2 / max(dt, 1e-4))
+    dt = sample(frac)
+    return {"value": combos_of(prob) * frac / dt, "unit": UNIT, "cores": cores, "kind": "oracle",
+            "sample": f"memory-bucketed tables over the first {frac:.3g} of every used transition's "
+                      f"combination space (all input states), {dt:.2f} s; value = combos/step x fraction / time"}
+
+
 def flush_l2(torch, buf):
     buf.zero_()
 
@@ -402,6 +433,8 @@ def run_cfp_mem(args, rank, world, local_rank):
                           "addmins_per_step": fold_ops},
         "clocks": clocks, "plan_total_ns": plan.total_ns, "plan_total_q": plan.total_q,
     }
+    if not args.no_cpu_baseline:
+        out["cpu_baseline"] = cpu_baseline_mem(prob, quantum)
     prep.close()
     ctx.close()
     return out

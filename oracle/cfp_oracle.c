@@ -363,6 +363,15 @@ int orc_mem_range(const orc_type* t, uint64_t quantum, int64_t* qlo, int64_t* qh
 
 int orc_segment_table_mem(const orc_problem* p, int32_t tr, uint64_t quantum,
                           uint64_t* Am, uint64_t* Im, int nthreads) {
+  if (tr < 0 || tr >= p->ntrans) return ORC_EINVAL;
+  return orc_segment_table_mem_range(p, tr, quantum, 0, space_size(&p->types[p->trans[tr].type]),
+                                     Am, Im, nthreads);
+}
+
+/* The same over the combination-index range [lo_idx, hi_idx) only (the
+ * bench's bounded cpu_baseline sample); arithmetic identical. */
+int orc_segment_table_mem_range(const orc_problem* p, int32_t tr, uint64_t quantum, uint64_t lo_idx,
+                                uint64_t hi_idx, uint64_t* Am, uint64_t* Im, int nthreads) {
   if (tr < 0 || tr >= p->ntrans || quantum == 0) return ORC_EINVAL;
   const orc_type* t = &p->types[p->trans[tr].type];
   if (t->K > 64) return ORC_ETOOBIG;
@@ -371,7 +380,10 @@ int orc_segment_table_mem(const orc_problem* p, int32_t tr, uint64_t quantum,
   const int64_t nq = qhi - qlo + 1;
   const int32_t din = d_in_of(p, tr);
   const int32_t dout = t->radix[t->out_block];
-  const uint64_t S = space_size(t);
+  const uint64_t S0 = space_size(t);
+  if (hi_idx > S0) hi_idx = S0;
+  if (lo_idx > hi_idx) lo_idx = hi_idx;
+  const uint64_t S = hi_idx - lo_idx;
   const int nt = nthreads_or_default(nthreads);
   const size_t cells = (size_t)din * dout * nq;
   uint64_t* LA = (uint64_t*)malloc(sizeof(uint64_t) * cells * nt);
@@ -380,7 +392,7 @@ int orc_segment_table_mem(const orc_problem* p, int32_t tr, uint64_t quantum,
   for (size_t c = 0; c < cells * nt; ++c) { LA[c] = ORC_INF64; LI[c] = ORC_NOIDX; }
 #pragma omp parallel for schedule(static, 1) num_threads(nt)
   for (int ch = 0; ch < nt; ++ch) {
-    uint64_t lo = S * (uint64_t)ch / nt, hi = S * (uint64_t)(ch + 1) / nt;
+    uint64_t lo = lo_idx + S * (uint64_t)ch / nt, hi = lo_idx + S * (uint64_t)(ch + 1) / nt;
     uint64_t* a = LA + cells * ch;
     uint64_t* ix = LI + cells * ch;
     int32_t s[64];

@@ -120,6 +120,8 @@ uint64_t orc_mem_q(const orc_type* t, const int32_t* s, uint64_t quantum);
 /* Am, Im: [D_in][D_o][qhi - qlo + 1]. */
 int orc_segment_table_mem(const orc_problem* p, int32_t tr, uint64_t quantum,
                           uint64_t* Am, uint64_t* Im, int nthreads);
+int orc_segment_table_mem_range(const orc_problem* p, int32_t tr, uint64_t quantum, uint64_t lo_idx,
+                                uint64_t hi_idx, uint64_t* Am, uint64_t* Im, int nthreads);
 /* Backward DP over (u, c).  Instance n has matrix Am[n] of shape
  * rows[n] x cols[n] x nq[n] with memory offset qlo[n].  G receives N+1 blocks
  * [S][Qmax + 1]: G_0 (rows[0]) then G_n (cols[n-1]). */

@@ -76,6 +76,8 @@ def lib():
                                       P(C.c_uint64), P(C.c_uint64)]
         L.orc_search_plan.argtypes = [P(_Problem), C.c_int, P(C.c_uint64), P(C.c_uint64),
                                       P(C.c_int32), C.c_int32, P(C.c_uint64)]
+        L.orc_segment_table_mem_range.argtypes = [P(_Problem), C.c_int32, C.c_uint64, C.c_uint64, C.c_uint64,
+                                                  P(C.c_uint64), P(C.c_uint64), C.c_int]
         L.orc_minplus.argtypes = [C.c_int32, C.c_int32, C.c_int32, P(C.c_uint64), P(C.c_uint64),
                                   P(C.c_uint64), P(C.c_uint64)]
         L.orc_mem_range.argtypes = [P(_Type), C.c_uint64, P(C.c_int64), P(C.c_int64)]
@@ -375,6 +377,20 @@ def segment_table_mem(prob: Problem, tr: int, quantum: int, nthreads: int = 0,
     I = np.empty_like(A)
     _check(lib().orc_segment_table_mem(m.ref, tr, quantum, _ptr(A, C.c_uint64), _ptr(I, C.c_uint64),
                                        nthreads), "segment_table_mem")
+    return A, I, qlo
+
+
+def segment_table_mem_range(prob: Problem, tr: int, quantum: int, lo: int, hi: int, nthreads: int = 0,
+                            m: Optional[Marshalled] = None):
+    """segment_table_mem over the combination-index range [lo, hi) only."""
+    m = m or Marshalled(prob)
+    ty = prob.transitions[tr].type
+    qlo, qhi = mem_range(prob, ty, quantum, m)
+    din, dout = prob.d_in(tr), prob.d_out(tr)
+    A = np.empty((din, dout, qhi - qlo + 1), dtype=np.uint64)
+    I = np.empty_like(A)
+    _check(lib().orc_segment_table_mem_range(m.ref, tr, quantum, lo, hi, _ptr(A, C.c_uint64),
+                                             _ptr(I, C.c_uint64), nthreads), "segment_table_mem_range")
     return A, I, qlo
 
 

@@ -188,3 +188,19 @@ def test_chain_mem_zero_memory_is_plain_chain(oracle_lib):
     Gm = O.chain_mem([M[..., None] for M in mats], [0] * 5, 3)
     for a, b in zip(Gp, Gm):
         assert np.array_equal(np.repeat(a[:, None], 4, axis=1), b)
+
+
+@pytest.mark.parametrize("seed", range(10))
+def test_table_mem_range_pieces(oracle_lib, seed):
+    """Ranges [0, k) and [k, S) merged by (cost, index) give the full table."""
+    p = G.tiny_random(3300 + seed, max_d=4)
+    m = O.Marshalled(p)
+    for tr in sorted({int(t) for t in p.instances}):
+        S = p.num_combinations(p.transitions[tr].type)
+        A, I, qlo = O.segment_table_mem(p, tr, 1, m=m)
+        k = S // 3
+        A1, I1, _ = O.segment_table_mem_range(p, tr, 1, 0, k, m=m)
+        A2, I2, _ = O.segment_table_mem_range(p, tr, 1, k, S, m=m)
+        take2 = A2 < A1
+        assert np.array_equal(np.where(take2, A2, A1), A)
+        assert np.array_equal(np.where(take2, I2, I1), I)
