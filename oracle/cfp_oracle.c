@@ -557,3 +557,116 @@ done:
   free(At); free(It); free(An); free(In); free(rows); free(cols); free(nq); free(qlo); free(vsel); free(G);
   return rc;
 }
+
+/* ---------------------------------------------------------------------------
+ * Dense per-plan tables.  The
+ * paper profiles whole-segment plans: W_t[idx] is the profiled time of plan
+ * idx of segment type t (its p_n(i_n) + c_n(i_n), intra-segment resharding
+ * included), INF = 0xFFFFFFFF.  The cross-segment term stays Q2's:
+ *   C(u, s) = W_t[idx(s)] + sum_{cross (j, Q)} Q_j[u][s_j]
+ * everything else (buckets, least index, chain, plan) as the factored model.
+ * ------------------------------------------------------------------------- */
+static uint64_t dense_cost(const orc_problem* p, int32_t tr, const uint32_t* W, int32_t u, uint64_t idx,
+                           const int32_t* s) {
+  const orc_trans* T = &p->trans[tr];
+  const orc_type* t = &p->types[T->type];
+  if (W[idx] == ORC_INF32) return ORC_INF64;
+  uint64_t total = W[idx];
+  for (int32_t x = 0; x < T->X; ++x) {
+    const uint32_t* Q = cross_table(p, tr, x);
+    int32_t j = T->xdst[x];
+    uint32_t r = Q[(int64_t)u * t->radix[j] + s[j]];
+    if (r == ORC_INF32) return ORC_INF64;
+    total += r;
+  }
+  return total;
+}
+
+int orc_dense_segment_table(const orc_problem* p, int32_t tr, const uint32_t* W, uint64_t* A, uint64_t* I,
+                            int nthreads) {
+  if (tr < 0 || tr >= p->ntrans || !W) return ORC_EINVAL;
+  const orc_type* t = &p->types[p->trans[tr].type];
+  if (t->K > 64) return ORC_ETOOBIG;
+  const int32_t din = d_in_of(p, tr);
+  const int32_t dout = t->radix[t->out_block];
+  const uint64_t S = space_size(t);
+  const int nt = nthreads_or_default(nthreads);
+  const size_t cells = (size_t)din * dout;
+  uint64_t* LA = (uint64_t*)malloc(sizeof(uint64_t) * cells * nt);
+  uint64_t* LI = (uint64_t*)malloc(sizeof(uint64_t) * cells * nt);
+  if (!LA || !LI) { free(LA); free(LI); return ORC_ENOMEM; }
+  for (size_t c = 0; c < cells * nt; ++c) { LA[c] = ORC_INF64; LI[c] = ORC_NOIDX; }
+#pragma omp parallel for schedule(static, 1) num_threads(nt)
+  for (int ch = 0; ch < nt; ++ch) {
+    uint64_t lo = S * (uint64_t)ch / nt, hi = S * (uint64_t)(ch + 1) / nt;
+    uint64_t* a = LA + cells * ch;
+    uint64_t* ix = LI + cells * ch;
+    int32_t s[64];
+    for (int32_t u = 0; u < din; ++u)
+      for (uint64_t idx = lo; idx < hi; ++idx) {
+        orc_decode(t->K, t->radix, idx, s);
+        uint64_t c = dense_cost(p, tr, W, u, idx, s);
+        size_t cell = (size_t)u * dout + s[t->out_block];
+        if (c < a[cell]) { a[cell] = c; ix[cell] = idx; }
+      }
+  }
+  for (size_t c = 0; c < cells; ++c) { A[c] = ORC_INF64; I[c] = ORC_NOIDX; }
+  for (int ch = 0; ch < nt; ++ch)            /* chunk order == index order */
+    for (size_t c = 0; c < cells; ++c)
+      if (LA[cells * ch + c] < A[c]) { A[c] = LA[cells * ch + c]; I[c] = LI[cells * ch + c]; }
+  free(LA); free(LI);
+  return ORC_OK;
+}
+
+int orc_dense_search_plan(const orc_problem* p, const uint32_t* const* W, int nthreads, uint64_t* total,
+                          uint64_t* seg_index, int32_t* digits, int32_t kmax, uint64_t* seg_ns) {
+  const int32_t N = p->N;
+  if (N < 1 || !W) return ORC_EINVAL;
+  uint64_t** At = (uint64_t**)calloc(p->ntrans, sizeof(uint64_t*));
+  uint64_t** It = (uint64_t**)calloc(p->ntrans, sizeof(uint64_t*));
+  const uint64_t** An = (const uint64_t**)malloc(sizeof(uint64_t*) * N);
+  const uint64_t** In = (const uint64_t**)malloc(sizeof(uint64_t*) * N);
+  int32_t* rows = (int32_t*)malloc(sizeof(int32_t) * N);
+  int32_t* cols = (int32_t*)malloc(sizeof(int32_t) * N);
+  int32_t* vsel = (int32_t*)malloc(sizeof(int32_t) * N);
+  int rc = ORC_OK;
+  uint64_t* G = NULL;
+  if (!At || !It || !An || !In || !rows || !cols || !vsel) { rc = ORC_ENOMEM; goto done; }
+  int64_t gsz = 0;
+  for (int32_t n = 0; n < N; ++n) {
+    int32_t tr = p->inst[n];
+    if (tr < 0 || tr >= p->ntrans) { rc = ORC_EINVAL; goto done; }
+    const orc_type* t = &p->types[p->trans[tr].type];
+    rows[n] = d_in_of(p, tr);
+    cols[n] = t->radix[t->out_block];
+    gsz += cols[n];
+    if (!At[tr]) {
+      size_t cells = (size_t)rows[n] * cols[n];
+      At[tr] = (uint64_t*)malloc(sizeof(uint64_t) * cells);
+      It[tr] = (uint64_t*)malloc(sizeof(uint64_t) * cells);
+      if (!At[tr] || !It[tr]) { rc = ORC_ENOMEM; goto done; }
+      rc = orc_dense_segment_table(p, tr, W[p->trans[tr].type], At[tr], It[tr], nthreads);
+      if (rc) goto done;
+    }
+    An[n] = At[tr];
+    In[n] = It[tr];
+  }
+  G = (uint64_t*)malloc(sizeof(uint64_t) * (gsz + rows[0]));
+  if (!G) { rc = ORC_ENOMEM; goto done; }
+  rc = orc_chain(N, rows, cols, An, NULL, G);
+  if (rc) goto done;
+  *total = G[0];
+  rc = orc_reconstruct(N, rows, cols, An, In, G, vsel, seg_index, seg_ns);
+  if (rc) goto done;
+  for (int32_t n = 0; n < N; ++n) {
+    const orc_type* t = &p->types[p->trans[p->inst[n]].type];
+    for (int32_t j = 0; j < kmax; ++j) digits[(int64_t)n * kmax + j] = -1;
+    orc_decode(t->K, t->radix, seg_index[n], digits + (int64_t)n * kmax);
+  }
+done:
+  if (At) for (int32_t q = 0; q < p->ntrans; ++q) free(At[q]);
+  if (It) for (int32_t q = 0; q < p->ntrans; ++q) free(It[q]);
+  free(At); free(It); free(An); free(In); free(rows); free(cols); free(vsel); free(G);
+  return rc;
+}
+

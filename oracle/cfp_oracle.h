@@ -138,6 +138,15 @@ int orc_search_plan_mem(const orc_problem* p, uint64_t quantum, uint64_t mem_lim
                         uint64_t* total, uint64_t* seg_index, int32_t* digits, int32_t kmax,
                         uint64_t* seg_ns, int64_t* seg_q, int64_t* total_q);
 
+/* ---- dense per-plan tables (NEXT-2) ----
+ * W: [prod D] profiled time of every whole-segment plan (INF = 0xFFFFFFFF);
+ * C(u, s) = W[idx(s)] + sum_cross Q_j[u][s_j]; tables/chain/plan as above. */
+int orc_dense_segment_table(const orc_problem* p, int32_t tr, const uint32_t* W, uint64_t* A, uint64_t* I,
+                            int nthreads);
+/* W[t] = dense table of type t (NULL for unused types). */
+int orc_dense_search_plan(const orc_problem* p, const uint32_t* const* W, int nthreads, uint64_t* total,
+                          uint64_t* seg_index, int32_t* digits, int32_t kmax, uint64_t* seg_ns);
+
 /* Big-endian mixed-radix decode. */
 void orc_decode(int32_t K, const int32_t* radix, uint64_t idx, int32_t* digits);
 

@@ -78,6 +78,10 @@ def lib():
                                       P(C.c_int32), C.c_int32, P(C.c_uint64)]
         L.orc_segment_table_mem_range.argtypes = [P(_Problem), C.c_int32, C.c_uint64, C.c_uint64, C.c_uint64,
                                                   P(C.c_uint64), P(C.c_uint64), C.c_int]
+        L.orc_dense_segment_table.argtypes = [P(_Problem), C.c_int32, P(C.c_uint32), P(C.c_uint64),
+                                              P(C.c_uint64), C.c_int]
+        L.orc_dense_search_plan.argtypes = [P(_Problem), P(P(C.c_uint32)), C.c_int, P(C.c_uint64),
+                                            P(C.c_uint64), P(C.c_int32), C.c_int32, P(C.c_uint64)]
         L.orc_minplus.argtypes = [C.c_int32, C.c_int32, C.c_int32, P(C.c_uint64), P(C.c_uint64),
                                   P(C.c_uint64), P(C.c_uint64)]
         L.orc_mem_range.argtypes = [P(_Type), C.c_uint64, P(C.c_int64), P(C.c_int64)]
@@ -528,3 +532,73 @@ def brute_force_table_mem(prob: Problem, tr: int, quantum: int):
                 A[u, v, k] = c
                 I[u, v, k] = idx
     return A, I, qlo
+
+
+# ---------------------------------------------------------------- dense per-plan tables (NEXT-2)
+def dense_segment_table(prob: Problem, tr: int, W: np.ndarray, nthreads: int = 0,
+                        m: Optional[Marshalled] = None) -> Tuple[np.ndarray, np.ndarray]:
+    """A, I [D_in][D_o] with C(u, s) = W[idx(s)] + cross terms."""
+    m = m or Marshalled(prob)
+    W = np.ascontiguousarray(W, dtype=np.uint32)
+    din, dout = prob.d_in(tr), prob.d_out(tr)
+    A = np.empty((din, dout), dtype=np.uint64)
+    I = np.empty_like(A)
+    _check(lib().orc_dense_segment_table(m.ref, tr, _ptr(W, C.c_uint32), _ptr(A, C.c_uint64),
+                                         _ptr(I, C.c_uint64), nthreads), "dense_segment_table")
+    return A, I
+
+
+def dense_search_plan(prob: Problem, Ws: Sequence[Optional[np.ndarray]], nthreads: int = 0) -> Dict:
+    m = Marshalled(prob)
+    N = len(prob.instances)
+    kmax = prob.k_max()
+    Ws = [None if w is None else np.ascontiguousarray(w, dtype=np.uint32) for w in Ws]
+    ptrs = (C.POINTER(C.c_uint32) * len(Ws))(*[None if w is None else _ptr(w, C.c_uint32) for w in Ws])
+    total = C.c_uint64()
+    idx = np.empty(N, np.uint64)
+    dig = np.empty(N * kmax, np.int32)
+    seg = np.empty(N, np.uint64)
+    _check(lib().orc_dense_search_plan(m.ref, ptrs, nthreads, C.byref(total), _ptr(idx, C.c_uint64),
+                                       _ptr(dig, C.c_int32), kmax, _ptr(seg, C.c_uint64)), "dense_search_plan")
+    return dict(total=int(total.value), seg_index=idx, digits=dig.reshape(N, kmax), seg_ns=seg)
+
+
+def brute_force_dense(prob: Problem, Ws, limit: int = 10 ** 6) -> Dict:
+    """All global plans in lexicographic order, T = sum_n W[idx_n] + cross terms."""
+    spaces = []
+    for t in prob.instances:
+        ty = prob.types[prob.transitions[int(t)].type]
+        spaces.append(range(int(np.prod([int(d) for d in ty.radix]))))
+    n_plans = 1
+    for sp in spaces:
+        n_plans *= len(sp)
+    if n_plans > limit:
+        raise ValueError(f"brute force guard: {n_plans} plans > {limit}")
+    best = None
+    for plan in product(*spaces):
+        u, total, ok = 0, 0, True
+        for n, idx in enumerate(plan):
+            tr = int(prob.instances[n])
+            T = prob.transitions[tr]
+            ty = prob.types[T.type]
+            w = int(Ws[T.type][idx])
+            if w == int(INF32):
+                ok = False
+                break
+            s = _digits(ty.radix, idx)
+            total += w
+            for x in T.in_edges:
+                r = int(x.table[u, s[x.dst]])
+                if r == int(INF32):
+                    ok = False
+                    break
+                total += r
+            if not ok:
+                break
+            u = s[ty.out_block]
+        if ok and (best is None or total < best[0]):
+            best = (total, plan)
+    if best is None:
+        return dict(total=None)
+    return dict(total=best[0], seg_index=np.array(best[1], dtype=np.uint64))
+

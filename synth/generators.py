@@ -457,3 +457,27 @@ def global_plan_count(p: Problem) -> int:
     for t in p.instances:
         n *= p.num_combinations(p.transitions[int(t)].type)
     return n
+
+
+# --------------------------------------------------------------------------
+# dense per-plan tables: one profiled time per
+# whole-segment plan.  W[idx] from the counter-based hash of
+# (seed, DENSE_TABLE_ID + type, idx): 24-bit ns, INF when the low 12 bits are 0
+# (about one plan in 4096 infeasible).  The library's device generator
+# (cfp_dense_fill) implements the same splitmix64 stream from dense_base().
+# --------------------------------------------------------------------------
+DENSE_TABLE_ID = 1 << 32
+
+
+def dense_base(seed: int, type_id: int) -> int:
+    return _splitmix64_int(_splitmix64_int(seed & MASK64) ^ ((DENSE_TABLE_ID + type_id) & MASK64))
+
+
+def dense_table(seed: int, type_id: int, n: int, lo: int = 0) -> np.ndarray:
+    """W[lo .. lo + n) of type `type_id` as uint32."""
+    e = np.arange(lo, lo + n, dtype=U64)
+    h = _splitmix64_arr(e ^ U64(dense_base(seed, type_id)))
+    w = (h >> U64(40)).astype(np.uint32)
+    w[(h & U64(0xFFF)) == U64(0)] = np.uint32(INF32)
+    return w
+
