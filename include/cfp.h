@@ -251,6 +251,41 @@ cfp_status cfp_segment_costs_mem(cfp_ctx* ctx, const cfp_segment_type* t, const 
                                  int64_t* qlo_out, int32_t* nq_out,
                                  uint64_t* cost_out, uint64_t* index_out);
 
+/* ---- dense per-plan tables ---------------------------
+ * The paper profiles whole-segment plans: p_n(i_n) and c_n(i_n) are measured
+ * per plan i_n of a segment, so the cost of a type is a
+ * dense table W_t[idx] over every combination index (uint32 ns, CFP_INF32 =
+ * infeasible; intra-segment resharding included).  The cross-segment term
+ * stays Q2's factored r_n:  C(u, s) = W_t[idx(s)] + sum_cross Q_j[u][s_j].
+ * Buckets, least index, chain and canonical plan are those of (1)-(3).
+ * Nothing factorises, so every entry is read once: an HBM stream of 4 bytes
+ * per combination (C3: 2 x 18.3 GB).
+ * W arguments are DEVICE pointers (the tables are tens of GB; the caller
+ * allocates them on ctx's device and keeps them resident), 16-byte aligned
+ * for the vector path; the types' comp/comm/edge tables are ignored (comp_ns
+ * must still be non-NULL for validation).  Single GPU (world > 1: EINVAL);
+ * output block with <= 64 strategies (else ETOOBIG). */
+/* Synthetic tables: W[e] = splitmix64 stream of (e ^ base), 24-bit ns,
+ * CFP_INF32 when the low 12 bits are zero (synth.generators.dense_table). */
+cfp_status cfp_dense_fill(cfp_ctx* ctx, uint32_t* W_dev, uint64_t n, uint64_t base);
+cfp_status cfp_search_plan_dense(cfp_ctx* ctx, const cfp_problem* p, const uint32_t* const* W_dev,
+                                 cfp_plan* out);
+/* One transition: cost_out/index_out [d_in][D_o] (host). */
+cfp_status cfp_segment_costs_dense(cfp_ctx* ctx, const cfp_segment_type* t, const uint32_t* W_dev,
+                                   const cfp_transition* tr, int32_t d_in, uint64_t* cost_out,
+                                   uint64_t* index_out);
+typedef struct cfp_dense_prepared cfp_dense_prepared;
+cfp_status cfp_dense_prepare(cfp_ctx* ctx, const cfp_problem* p, const uint32_t* const* W_dev,
+                             cfp_dense_prepared** out);
+cfp_status cfp_dense_execute(cfp_ctx* ctx, cfp_dense_prepared* prep);
+cfp_status cfp_dense_fetch_plan(cfp_ctx* ctx, cfp_dense_prepared* prep, cfp_plan* out);
+void       cfp_dense_free(cfp_dense_prepared* prep);
+cfp_status cfp_dense_time_kernels(cfp_dense_prepared* prep, int32_t on);
+/* ms of the table stream (row minima) and of the whole path of the last
+ * execute; combinations and table bytes per execute; kernel launches. */
+cfp_status cfp_dense_kernel_ms(cfp_dense_prepared* prep, double* stream_ms, double* total_ms,
+                               double* combos, double* bytes, int32_t* launches);
+
 /* ---- host-only helpers (no device work; callable without a GPU) ---------- */
 /* Contiguous, balanced share [lo, hi) of `units` items for `rank` of `world`
  * in multiples of `align`. */

@@ -90,7 +90,9 @@ EXPORTS = ["cfp_ctx_create", "cfp_ctx_destroy", "cfp_last_error", "cfp_nccl_uniq
            "cfp_shard_range", "cfp_pack_keys", "cfp_unpack_keys", "cfp_intpipe_bench",
            "cfp_minplus_bench", "cfp_search_plan_mem", "cfp_segment_costs_mem", "cfp_mem_prepare",
            "cfp_mem_execute", "cfp_mem_fetch_plan", "cfp_mem_free", "cfp_mem_time_kernels",
-           "cfp_mem_kernel_ms", "cfp_mem_fold_ops"]
+           "cfp_mem_kernel_ms", "cfp_mem_fold_ops", "cfp_dense_fill", "cfp_search_plan_dense",
+           "cfp_segment_costs_dense", "cfp_dense_prepare", "cfp_dense_execute", "cfp_dense_fetch_plan",
+           "cfp_dense_free", "cfp_dense_time_kernels", "cfp_dense_kernel_ms"]
 
 _lib = None
 
@@ -146,6 +148,18 @@ def lib() -> C.CDLL:
     L.cfp_mem_kernel_ms.argtypes = [vp, P(C.c_double), P(C.c_double), P(C.c_double), P(C.c_double),
                                     P(C.c_int32)]
     L.cfp_mem_fold_ops.argtypes = [vp, P(C.c_double)]
+    L.cfp_dense_fill.argtypes = [vp, vp, C.c_uint64, C.c_uint64]
+    L.cfp_search_plan_dense.argtypes = [vp, P(cfp_problem), P(vp), P(cfp_plan)]
+    L.cfp_segment_costs_dense.argtypes = [vp, P(cfp_segment_type), vp, P(cfp_transition), C.c_int32,
+                                          P(C.c_uint64), P(C.c_uint64)]
+    L.cfp_dense_prepare.argtypes = [vp, P(cfp_problem), P(vp), P(vp)]
+    L.cfp_dense_execute.argtypes = [vp, vp]
+    L.cfp_dense_fetch_plan.argtypes = [vp, vp, P(cfp_plan)]
+    L.cfp_dense_free.argtypes = [vp]
+    L.cfp_dense_free.restype = None
+    L.cfp_dense_time_kernels.argtypes = [vp, C.c_int32]
+    L.cfp_dense_kernel_ms.argtypes = [vp, P(C.c_double), P(C.c_double), P(C.c_double), P(C.c_double),
+                                      P(C.c_int32)]
     _lib = L
     return L
 
@@ -385,6 +399,38 @@ class Context:
     def prepare_mem(self, prob, quantum: int, mem_limit: int) -> "PreparedMem":
         return PreparedMem(self, prob, quantum, mem_limit)
 
+    # -- dense per-plan tables (NEXT-2); W arguments are device pointers (int)
+    def dense_fill(self, w_ptr: int, n: int, base: int):
+        _check(lib().cfp_dense_fill(self._h, C.c_void_p(w_ptr), n, base))
+
+    def search_plan_dense(self, prob, w_ptrs: Sequence[Optional[int]]) -> Plan:
+        m = _Marshal()
+        p = m.problem(prob)
+        arr = (C.c_void_p * len(w_ptrs))(*[C.c_void_p(x) if x else None for x in w_ptrs])
+        N = len(prob.instances)
+        kmax = max(int(len(t.radix)) for t in prob.types)
+        idx = np.empty(N, np.uint64)
+        dig = np.empty(N * kmax, np.int32)
+        seg = np.empty(N, np.uint64)
+        plan = cfp_plan(0, _p(idx, C.c_uint64), _p(dig, C.c_int32), kmax, _p(seg, C.c_uint64))
+        _check(lib().cfp_search_plan_dense(self._h, C.byref(p), C.cast(arr, P(C.c_void_p)), C.byref(plan)))
+        return Plan(int(plan.total_ns), idx, dig.reshape(N, kmax), seg)
+
+    def segment_costs_dense(self, seg_type, w_ptr: int, transition=None, d_in: int = 1):
+        m = _Marshal()
+        t = m.segment_type(seg_type)
+        tr = m.transition(transition) if transition is not None else None
+        do = int(np.asarray(seg_type.radix)[int(seg_type.out_block)])
+        A = np.empty((d_in, do), np.uint64)
+        I = np.empty((d_in, do), np.uint64)
+        _check(lib().cfp_segment_costs_dense(self._h, C.byref(t), C.c_void_p(w_ptr),
+                                             C.byref(tr) if tr is not None else None, d_in,
+                                             _p(A, C.c_uint64), _p(I, C.c_uint64)))
+        return A, I
+
+    def prepare_dense(self, prob, w_ptrs) -> "PreparedDense":
+        return PreparedDense(self, prob, w_ptrs)
+
     def minplus_bench(self, S: int, wide: bool = False, argk: bool = False, iters: int = 5):
         """(ms per launch, add+min ops per second) of an S^3 (min,+) product."""
         ms, ops = C.c_double(), C.c_double()
@@ -492,6 +538,51 @@ class PreparedMem:
     def close(self):
         if self._h:
             lib().cfp_mem_free(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class PreparedDense:
+    """Device-resident dense-table search (tables stay where the caller put them)."""
+
+    def __init__(self, ctx: Context, prob, w_ptrs):
+        self.ctx = ctx
+        self._m = _Marshal()
+        p = self._m.problem(prob)
+        self._arr = (C.c_void_p * len(w_ptrs))(*[C.c_void_p(x) if x else None for x in w_ptrs])
+        self._h = C.c_void_p()
+        _check(lib().cfp_dense_prepare(ctx._h, C.byref(p), C.cast(self._arr, P(C.c_void_p)), C.byref(self._h)))
+        self.N = len(prob.instances)
+        self.kmax = max(int(len(t.radix)) for t in prob.types)
+
+    def execute(self):
+        _check(lib().cfp_dense_execute(self.ctx._h, self._h))
+
+    def fetch(self) -> Plan:
+        idx = np.empty(self.N, np.uint64)
+        dig = np.empty(self.N * self.kmax, np.int32)
+        seg = np.empty(self.N, np.uint64)
+        plan = cfp_plan(0, _p(idx, C.c_uint64), _p(dig, C.c_int32), self.kmax, _p(seg, C.c_uint64))
+        _check(lib().cfp_dense_fetch_plan(self.ctx._h, self._h, C.byref(plan)))
+        return Plan(int(plan.total_ns), idx, dig.reshape(self.N, self.kmax), seg)
+
+    def time_kernels(self, on: bool = True):
+        _check(lib().cfp_dense_time_kernels(self._h, 1 if on else 0))
+
+    def kernel_ms(self):
+        """(table-stream ms, total ms, combinations, table bytes, kernel launches)."""
+        a, b, c, d, n = C.c_double(), C.c_double(), C.c_double(), C.c_double(), C.c_int32()
+        _check(lib().cfp_dense_kernel_ms(self._h, C.byref(a), C.byref(b), C.byref(c), C.byref(d), C.byref(n)))
+        return a.value, b.value, c.value, d.value, n.value
+
+    def close(self):
+        if self._h:
+            lib().cfp_dense_free(self._h)
             self._h = C.c_void_p()
 
     def __del__(self):

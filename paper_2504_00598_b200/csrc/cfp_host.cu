@@ -208,6 +208,12 @@ struct DevBuf {
   void* p = nullptr;
   size_t n = 0;
   cudaStream_t st = nullptr;
+  DevBuf() = default;
+  DevBuf(const DevBuf& o) : n(0), st(nullptr) {    // copies never share ownership:
+    (void)o;                                        // a copy of an allocated buffer is empty
+    if (o.p) std::abort();                          // (copying a live buffer is a bug)
+  }
+  DevBuf& operator=(const DevBuf&) = delete;
   ~DevBuf() { release(); }
   void release() {
     if (p) cudaFreeAsync(p, st);
@@ -1967,3 +1973,6 @@ extern "C" cfp_status cfp_intpipe_bench(cfp_ctx* ctx, int32_t op, int32_t iters,
 
 // memory-constrained search (NEXT-1)
 #include "cfp_mem_host.inc"
+
+// dense per-plan tables (NEXT-2)
+#include "cfp_dense_host.inc"

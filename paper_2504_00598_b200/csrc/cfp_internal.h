@@ -340,4 +340,55 @@ struct MemChainParams {
   int32_t* status;
 };
 
+// ---------------------------------------------------------------------------
+// Dense per-plan tables (cfp_dense.cu).  W_t[idx] is the
+// profiled time of whole-segment plan idx (uint32, 0xFFFFFFFF = infeasible).
+// Rows: prefix p = the cross-edge consumer digits (and the output digit when
+// it is not the last one); row p = the prod(suffix) consecutive entries.
+// ---------------------------------------------------------------------------
+struct DenseRowParams {
+  const uint32_t* W;
+  int64_t nP, nS;
+  int32_t nVs;                       // Do (output digit last) or 1 (output digit in the prefix)
+  int32_t T;                         // threads per CTA used (4T or T a multiple of Do)
+  int32_t vec;                       // 16-byte loads
+  uint32_t* B;                       // [nP][nVs]
+};
+
+struct DenseSlotParams {             // one transition
+  const uint32_t* W;
+  int64_t nP, nS;
+  int32_t Din, Do, nVs;
+  int64_t o_stride;                  // output digit's stride in the prefix index (nVs == 1)
+  int32_t nq;
+  int64_t q_off[kMaxCross];          // offset of Q_i [Din][radix_i] in Q
+  int64_t q_stride[kMaxCross];       // consumer digit's stride in the prefix index
+  int32_t q_radix[kMaxCross];
+  const uint32_t* Q;
+  const uint32_t* B;
+  int64_t nchunks;                   // ceil(nP / 256)
+  uint64_t* chunk;                   // [nchunks][Din][Do]
+  uint64_t* A;                       // [Din][Do]
+  uint64_t* I;
+};
+
+struct DenseInst {
+  int32_t rows, cols, K, radix_off;
+  const uint64_t* A;
+  const uint64_t* I;
+};
+
+struct DenseChainParams {
+  int32_t N, kmax;
+  const DenseInst* inst;
+  const int64_t* goff;               // [N + 2]
+  uint64_t* G;
+  const int32_t* radix;
+  uint64_t* total;
+  int32_t* status;
+  uint64_t* seg_index;
+  uint64_t* seg_ns;
+  int32_t* digits;
+};
+
 }  // namespace cfp
