@@ -26,6 +26,7 @@ import subprocess
 import sys
 import threading
 import time
+from typing import Tuple
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
@@ -440,6 +441,92 @@ def run_cfp_mem(args, rank, world, local_rank):
     return out
 
 
+def hbm_peak_gbs() -> Tuple[float, str]:
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            return float(json.load(fh)["hbm_gbs"]), "MEASURED_PEAKS.json hbm_gbs (copy, read+write)"
+    except Exception:
+        return 7700.0, "fallback: B200_PROFILING.md nominal 7.7 TB/s"
+
+
+def run_cfp_dense(args, rank, world, local_rank):
+    """Dense per-plan tables: the config's
+    graph with one profiled time per whole-segment plan, generated on the
+    device (synth.generators.dense_table stream); the tables (C3: 2 x 18.3 GB)
+    are streamed once per search.  Roofline: HBM bytes of the table stream."""
+    import numpy as np
+    import torch
+
+    from paper_2504_00598_b200 import build as B
+    B.build()
+    from paper_2504_00598_b200 import cfp
+    from synth import generators as G
+    if world > 1:
+        raise SystemExit("--dense runs on one GPU")
+    torch.cuda.set_device(local_rank)
+    prob = G.make_config(args.config, args.seed, args.dist)
+    ctx = cfp.Context(device=local_rank)
+    used = sorted({prob.transitions[int(t)].type for t in prob.instances})
+    bufs = {}
+    for t in used:
+        n = prob.num_combinations(t)
+        bufs[t] = torch.empty(n, dtype=torch.int32, device="cuda")
+        ctx.dense_fill(bufs[t].data_ptr(), n, G.dense_base(args.seed, t))
+    ptrs = [bufs[t].data_ptr() if t in bufs else 0 for t in range(len(prob.types))]
+    prep = ctx.prepare_dense(prob, ptrs)
+    prep.time_kernels(True)
+    for _ in range(args.warmup):
+        prep.execute()
+        prep.kernel_ms()
+    plan0 = prep.fetch()
+    s_ms, t_ms = [], []
+    with ClockSampler(local_rank) as clk:
+        for _ in range(args.steps):
+            torch.cuda.synchronize()          # tables >> L2 (126 MB): no flush needed
+            prep.execute()
+            a, t, combos, nbytes, launches = prep.kernel_ms()
+            s_ms.append(a)
+            t_ms.append(t)
+        torch.cuda.synchronize()
+    plan = prep.fetch()
+    assert plan.total_ns == plan0.total_ns and np.array_equal(plan.seg_index, plan0.seg_index)
+    clocks = clk.summary()
+    e2e = []
+    for i in range(args.warmup + max(3, min(args.steps, 10))):
+        t0 = time.perf_counter()
+        p2 = ctx.search_plan_dense(prob, ptrs)
+        dt = (time.perf_counter() - t0) * 1e3
+        if i >= args.warmup:
+            e2e.append(dt)
+    assert p2.total_ns == plan0.total_ns
+    ms = statistics.median(t_ms)
+    sm = statistics.median(s_ms)
+    peak, peak_src = hbm_peak_gbs()
+    achieved = nbytes / (sm * 1e-3) / 1e9
+    out = {
+        "metric": METRIC, "value": combos / (ms * 1e-3), "unit": UNIT, "n_gpus": 1, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "u32", "data": "synthetic",
+        "config": {"workload": f"{args.config} with dense per-plan tables (NEXT-2, P:572-574): one hashed "
+                               f"24-bit time per whole-segment plan (seed {args.seed}), {nbytes / 1e9:.1f} GB "
+                               f"of tables resident in HBM",
+                   "combos_per_step": combos, "l2": "tables >> L2: every step streams them from HBM"},
+        "plan_search_ms": {"device_median": ms, "table_stream_ms": sm, "e2e_median": statistics.median(e2e)},
+        "e2e": {"value": combos / (statistics.median(e2e) * 1e-3), "unit": UNIT,
+                "h2d_bytes_per_step": problem_bytes(prob), "d2h_bytes_per_step": plan_bytes(prob),
+                "note": "tables are device-resident inputs (tens of GB); e2e covers the search call"},
+        "gpu_launches": launches,
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": None,
+                     "note": f"dense_rows_kernel: 4 B read per combination (algorithmic) / stream time; "
+                             f"peak: {peak_src}"},
+        "clocks": clocks, "plan_total_ns": plan.total_ns,
+    }
+    prep.close()
+    ctx.close()
+    return out
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -452,6 +539,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--minplus", action="store_true", help="also run the (min,+) product microbenchmark")
     ap.add_argument("--mem", action="store_true", help="memory-constrained search (NEXT-1) instead")
+    ap.add_argument("--dense", action="store_true", help="dense per-plan tables (NEXT-2) instead")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -467,6 +555,9 @@ def main():
         return
     if args.mem:
         print(json.dumps(run_cfp_mem(args, rank, world, local_rank)), flush=True)
+        return
+    if args.dense:
+        print(json.dumps(run_cfp_dense(args, rank, world, local_rank)), flush=True)
         return
     if world > 1:
         import torch

@@ -281,8 +281,10 @@ cfp_status cfp_dense_execute(cfp_ctx* ctx, cfp_dense_prepared* prep);
 cfp_status cfp_dense_fetch_plan(cfp_ctx* ctx, cfp_dense_prepared* prep, cfp_plan* out);
 void       cfp_dense_free(cfp_dense_prepared* prep);
 cfp_status cfp_dense_time_kernels(cfp_dense_prepared* prep, int32_t on);
-/* ms of the table stream (row minima) and of the whole path of the last
- * execute; combinations and table bytes per execute; kernel launches. */
+/* ms of the table stream (row minima; window from the first type's stream
+ * start to the last one's end -- the types stream concurrently) and of the
+ * whole path of the last execute; combinations and table bytes per execute;
+ * kernel launches. */
 cfp_status cfp_dense_kernel_ms(cfp_dense_prepared* prep, double* stream_ms, double* total_ms,
                                double* combos, double* bytes, int32_t* launches);
 

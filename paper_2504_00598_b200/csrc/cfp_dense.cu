@@ -123,15 +123,16 @@ __device__ __forceinline__ int dense_vp(const DenseSlotParams& s, int64_t p) {
 }
 
 // --------------------------------------------------------------------------
-// Fold: chunk c = prefixes [c * 256, ...).  Thread = (u, v) pairs.
+// Fold: chunk c = prefixes [c * kDenseChunk, ...).  Thread = (u, v) pairs.
 // --------------------------------------------------------------------------
 __global__ void __launch_bounds__(256) dense_fold_kernel(const DenseSlotParams s) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  uint64_t (*Xs)[32] = reinterpret_cast<uint64_t (*)[32]>(smem_raw);           // [256][32]
-  uint32_t* Bs = reinterpret_cast<uint32_t*>(smem_raw + 256 * 32 * 8);          // [256][nVs]
-  int32_t* vps = reinterpret_cast<int32_t*>(Bs + 256 * s.nVs);                  // [256]
-  const int64_t p0 = (int64_t)blockIdx.x * 256;
-  const int rows = s.nP - p0 < 256 ? (int)(s.nP - p0) : 256;
+  constexpr int R = kDenseChunk;
+  uint64_t (*Xs)[32] = reinterpret_cast<uint64_t (*)[32]>(smem_raw);           // [R][32]
+  uint32_t* Bs = reinterpret_cast<uint32_t*>(smem_raw + R * 32 * 8);            // [R][nVs]
+  int32_t* vps = reinterpret_cast<int32_t*>(Bs + R * s.nVs);                    // [R]
+  const int64_t p0 = (int64_t)blockIdx.x * R;
+  const int rows = s.nP - p0 < R ? (int)(s.nP - p0) : R;
   const int tid = threadIdx.x;
   for (int ub = 0; ub < s.Din; ub += 32) {
     const int uc = min(32, s.Din - ub);
@@ -217,8 +218,8 @@ __global__ void __launch_bounds__(256) dense_argmin_kernel(const DenseSlotParams
     for (int64_t c = tid; c < s.nchunks; c += 256)
       if (s.chunk[(c * s.Din + u) * s.Do + v] == A) atomicMin(&s_c, (unsigned long long)c);
     __syncthreads();
-    const int64_t p0 = (int64_t)s_c * 256;
-    const int rows = s.nP - p0 < 256 ? (int)(s.nP - p0) : 256;
+    const int64_t p0 = (int64_t)s_c * kDenseChunk;
+    const int rows = s.nP - p0 < kDenseChunk ? (int)(s.nP - p0) : kDenseChunk;
     for (int r = tid; r < rows; r += 256) {
       const int64_t p = p0 + r;
       if (s.nVs == 1 && dense_vp(s, p) != v) continue;
@@ -325,7 +326,7 @@ cudaError_t launch_dense_rows(const DenseRowParams& p, int sms, cudaStream_t st)
   return cudaGetLastError();
 }
 cudaError_t launch_dense_fold(const DenseSlotParams& s, cudaStream_t st) {
-  const size_t smem = 256 * 32 * 8 + (size_t)256 * s.nVs * 4 + 256 * 4;
+  const size_t smem = kDenseChunk * 32 * 8 + (size_t)kDenseChunk * s.nVs * 4 + kDenseChunk * 4;
   if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(dense_fold_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;

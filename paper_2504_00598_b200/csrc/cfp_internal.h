@@ -346,6 +346,8 @@ struct MemChainParams {
 // Rows: prefix p = the cross-edge consumer digits (and the output digit when
 // it is not the last one); row p = the prod(suffix) consecutive entries.
 // ---------------------------------------------------------------------------
+constexpr int kDenseChunk = 128;     // prefixes per fold chunk
+
 struct DenseRowParams {
   const uint32_t* W;
   int64_t nP, nS;
@@ -366,7 +368,7 @@ struct DenseSlotParams {             // one transition
   int32_t q_radix[kMaxCross];
   const uint32_t* Q;
   const uint32_t* B;
-  int64_t nchunks;                   // ceil(nP / 256)
+  int64_t nchunks;                   // ceil(nP / kDenseChunk)
   uint64_t* chunk;                   // [nchunks][Din][Do]
   uint64_t* A;                       // [Din][Do]
   uint64_t* I;
