@@ -44,22 +44,24 @@ class cfp_mesh(C.Structure):
     _fields_ = [("ndim", C.c_int32), ("axes", P(C.c_int32))]
 
 
+# pointer members are declared c_void_p (same ABI as the typed pointers of
+# cfp.h) so that marshalling assigns raw addresses without ctypes casts
 class cfp_segment_type(C.Structure):
-    _fields_ = [("num_blocks", C.c_int32), ("radix", P(C.c_int32)), ("comp_ns", P(C.c_uint32)),
-                ("comm_ns", P(C.c_uint32)), ("num_edges", C.c_int32), ("edge_src", P(C.c_int32)),
-                ("edge_dst", P(C.c_int32)), ("edge_ns", P(C.c_uint32)), ("out_block", C.c_int32)]
+    _fields_ = [("num_blocks", C.c_int32), ("radix", C.c_void_p), ("comp_ns", C.c_void_p),
+                ("comm_ns", C.c_void_p), ("num_edges", C.c_int32), ("edge_src", C.c_void_p),
+                ("edge_dst", C.c_void_p), ("edge_ns", C.c_void_p), ("out_block", C.c_int32)]
 
 
 class cfp_transition(C.Structure):
     _fields_ = [("pred_type", C.c_int32), ("type", C.c_int32), ("num_in_edges", C.c_int32),
-                ("in_dst", P(C.c_int32)), ("in_ns", P(C.c_uint32))]
+                ("in_dst", C.c_void_p), ("in_ns", C.c_void_p)]
 
 
 class cfp_problem(C.Structure):
     _fields_ = [("abi_version", C.c_int32), ("mesh", cfp_mesh), ("num_types", C.c_int32),
                 ("types", P(cfp_segment_type)), ("num_transitions", C.c_int32),
                 ("transitions", P(cfp_transition)), ("num_instances", C.c_int32),
-                ("inst_transition", P(C.c_int32))]
+                ("inst_transition", C.c_void_p)]
 
 
 class cfp_plan(C.Structure):
@@ -173,13 +175,19 @@ def _p(a: Optional[np.ndarray], ct):
     return None if a is None else a.ctypes.data_as(P(ct))
 
 
+def _a(a: Optional[np.ndarray]) -> Optional[int]:
+    """Raw address of a contiguous array (for c_void_p members)."""
+    return None if a is None else a.__array_interface__["data"][0]
+
+
 # ---------------------------------------------------------------- marshalling
 class _Marshal:
     def __init__(self):
         self.keep = []
 
     def arr(self, a, dtype):
-        a = np.ascontiguousarray(a, dtype=dtype)
+        if not (isinstance(a, np.ndarray) and a.dtype == dtype and a.flags.c_contiguous):
+            a = np.ascontiguousarray(a, dtype=dtype)
         self.keep.append(a)
         return a
 
@@ -192,17 +200,15 @@ class _Marshal:
         dst = self.arr([_e(e)[1] for e in edges] or [0], np.int32)
         tab = self.arr(np.concatenate([np.asarray(_e(e)[2], np.uint32).ravel() for e in edges])
                        if edges else np.zeros(1, np.uint32), np.uint32)
-        return cfp_segment_type(len(radix), _p(radix, C.c_int32), _p(comp, C.c_uint32),
-                                _p(comm, C.c_uint32), len(edges), _p(src, C.c_int32),
-                                _p(dst, C.c_int32), _p(tab, C.c_uint32), int(ty.out_block))
+        return cfp_segment_type(len(radix), _a(radix), _a(comp), _a(comm), len(edges), _a(src),
+                                _a(dst), _a(tab), int(ty.out_block))
 
     def transition(self, tr) -> cfp_transition:
         xs = list(tr.in_edges)
         dst = self.arr([_x(x)[0] for x in xs] or [0], np.int32)
         tab = self.arr(np.concatenate([np.asarray(_x(x)[1], np.uint32).ravel() for x in xs])
                        if xs else np.zeros(1, np.uint32), np.uint32)
-        return cfp_transition(int(tr.pred_type), int(tr.type), len(xs), _p(dst, C.c_int32),
-                              _p(tab, C.c_uint32))
+        return cfp_transition(int(tr.pred_type), int(tr.type), len(xs), _a(dst), _a(tab))
 
     def problem(self, prob) -> cfp_problem:
         types = (cfp_segment_type * len(prob.types))(*[self.segment_type(t) for t in prob.types])
@@ -211,8 +217,7 @@ class _Marshal:
         mesh = self.arr(list(prob.mesh) or [1], np.int32)
         inst = self.arr(prob.instances, np.int32)
         return cfp_problem(CFP_ABI_VERSION, cfp_mesh(len(prob.mesh), _p(mesh, C.c_int32)),
-                           len(prob.types), types, len(prob.transitions), trans, len(inst),
-                           _p(inst, C.c_int32))
+                           len(prob.types), types, len(prob.transitions), trans, len(inst), _a(inst))
 
 
 def _mem_model(m: "_Marshal", prob, quantum: int, mem_limit: int) -> cfp_mem_model:

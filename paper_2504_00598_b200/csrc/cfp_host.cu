@@ -18,6 +18,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <ctime>
 #include <map>
 #include <memory>
 #include <string>
@@ -695,14 +696,36 @@ static cfp_status setup_chain_staging(ChainParams& cp, const std::vector<ChainIn
   return CFP_OK;
 }
 
+// CFP_DEBUG_PREP=1: host-side phase times of prepare (stderr)
+struct PrepTimer {
+  bool on = getenv("CFP_DEBUG_PREP") != nullptr;
+  std::vector<std::pair<const char*, double>> marks;
+  double t0 = now();
+  static double now() {
+    timespec ts;
+    clock_gettime(CLOCK_MONOTONIC, &ts);
+    return ts.tv_sec * 1e6 + ts.tv_nsec * 1e-3;
+  }
+  void mark(const char* what) { if (on) marks.emplace_back(what, now()); }
+  ~PrepTimer() {
+    if (!on) return;
+    double prev = t0;
+    fprintf(stderr, "prepare (us):");
+    for (auto& m : marks) { fprintf(stderr, " %s %.1f", m.first, m.second - prev); prev = m.second; }
+    fprintf(stderr, "\n");
+  }
+};
+
 static cfp_status prepare_impl(cfp_ctx* ctx, const cfp_problem* p, bool do_chain,
                                cfp_prepared** out) {
+  PrepTimer tm;
   *out = nullptr;
   g_alloc_stream = ctx->stream;
   std::vector<HostType> T;
   std::vector<HostTrans> X;
   Builder b;
   TRY(validate_and_model(p, T, X, b, do_chain));
+  tm.mark("validate");
   std::unique_ptr<cfp_prepared> P(new cfp_prepared());
   P->ctx = ctx;
   P->do_chain = do_chain;
@@ -821,6 +844,7 @@ static cfp_status prepare_impl(cfp_ctx* ctx, const cfp_problem* p, bool do_chain
     }
   }
 
+  tm.mark("types");
   // ---- schedules + derived tables
   std::vector<int4> mtab_all;
   int64_t bp_bytes = 0, scratch_bytes = 0;
@@ -1092,6 +1116,7 @@ static cfp_status prepare_impl(cfp_ctx* ctx, const cfp_problem* p, bool do_chain
       }
     }
   }
+  tm.mark("schedules");
   // ---- device allocation + H2D
   CUDA_TRY(cudaSetDevice(ctx->device));
   cudaStream_t st = ctx->stream;
@@ -1229,6 +1254,7 @@ static cfp_status prepare_impl(cfp_ctx* ctx, const cfp_problem* p, bool do_chain
     P->combos += te.combos;
     P->combos_local += te.combos_local;
   }
+  tm.mark("alloc+h2d");
   // ---- chain setup
   if (do_chain) {
     const int N = P->N;
@@ -1326,7 +1352,9 @@ static cfp_status prepare_impl(cfp_ctx* ctx, const cfp_problem* p, bool do_chain
       P->reach_bytes = goff[N];
     }
   }
+  tm.mark("chain");
   CUDA_TRY(cudaStreamSynchronize(st));
+  tm.mark("sync");
   *out = P.release();
   return CFP_OK;
 }
