@@ -271,6 +271,7 @@ struct MemFoldParams {
   const int4* tiles;                 // [ntiles] (pos_start, rows, rowclass, 0)
   const int32_t* perm;               // [nP] position -> prefix
   const void* B;                     // [Wc/4][nP][4]
+  void* X;                           // [nP][DinP] cross terms per position (mem_xrows_kernel)
   void* chunk;                       // [ntiles][Din][Wc] out
 };
 

@@ -139,88 +139,114 @@ __global__ void __launch_bounds__(256) mem_enum_kernel(const MemEnumParams p) {
 }
 
 // --------------------------------------------------------------------------
-// Fold of one transition.  CTA = (tile of <= 256 prefixes of one prefix-memory
-// class, block of 128 classes).  Thread = 4 input states x 4 classes.
+// Cross terms of every prefix position: X[pos][u] = sum_i Q_i[u][s_i(perm[pos])]
+// (Eq. 3 r_n), saturated; one thread per (position, u quad).
+// --------------------------------------------------------------------------
+template <typename V>
+__global__ void mem_xrows_kernel(const MemFoldParams p) {
+  using M = MT<V>;
+  const int nuq = p.DinP >> 2;
+  const int64_t total = p.nP * nuq;
+  const V* vals = static_cast<const V*>(p.vals);
+  V* X = static_cast<V*>(p.X);
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t pos = e / nuq;
+    const int uq = (int)(e - pos * nuq);
+    const uint32_t pr = (uint32_t)p.perm[pos];
+    V x[4] = {0, 0, 0, 0};
+    for (int i = 0; i < p.nq; ++i) {
+      V y[4];
+      M::load4(vals + p.q_off[i] + (int64_t)mem_digit32(p.pm, pr, p.q_pos[i]) * p.DinP + uq * 4, y);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) x[k] = M::sat(x[k], y[k]);
+    }
+    V* o = X + pos * p.DinP + uq * 4;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) o[k] = x[k];
+  }
+}
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  const uint32_t s = (uint32_t)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+// --------------------------------------------------------------------------
+// Fold of one transition.  CTA = (tile of <= kMemFoldTile positions of one
+// (ctx, prefix-memory class) group, balanced block of classes).  Thread = 4
+// input states x 4 classes, 16 fused add+mins per row.  X rows and B rows are
+// staged by cp.async into a two-stage shared-memory ring: the copies of
+// chunk c+1 overlap the (min,+) work on chunk c.
 // --------------------------------------------------------------------------
 template <typename V>
 __global__ void __launch_bounds__(256) mem_fold_kernel(const MemFoldParams p) {
   using M = MT<V>;
-  constexpr int R = sizeof(V) == 4 ? kMemFoldRows : kMemFoldRows / 2;   // static smem < 48 KB
+  constexpr int R = sizeof(V) == 4 ? 32 : 16;       // rows per stage (static smem < 48 KB)
   constexpr int FC = kMemFoldCols;
-  const int fc = p.fc;                              // balanced block width (<= FC, multiple of 4)
-  __shared__ __align__(16) V Xs[R][32];
-  __shared__ __align__(16) V Bs[R][FC + 4];         // +4: conflict-free 16-byte row stores
-  __shared__ int64_t rowp[R];
+  constexpr int VPU = 16 / sizeof(V);               // elements per 16-byte copy
+  __shared__ __align__(16) V Xs[2][R][32];
+  __shared__ __align__(16) V Bs[2][R][FC + 4];      // +4: conflict-free row stores
+  const int fc = p.fc;
   const int4 tile = p.tiles[blockIdx.x];
   const int col0 = blockIdx.y * fc;
   const int ncols = min(fc, p.Wc - col0);
   const int tid = threadIdx.x;
   const int ncq = (ncols + 3) >> 2;                 // class quads of this block
   const int tu = tid / ncq, tc = tid - tu * ncq;    // thread = (u quad, class quad)
-  const V* vals = static_cast<const V*>(p.vals);
   const V* B = static_cast<const V*>(p.B);
+  const V* X = static_cast<const V*>(p.X);
   V* out = static_cast<V*>(p.chunk) + (int64_t)blockIdx.x * p.Din * p.Wc;
+  const int nchunk = (tile.y + R - 1) / R;
   for (int ub = 0; ub < p.Din; ub += 32) {          // input states in blocks of 32
     const int ucnt = min(32, p.DinP - ub);
+    const int xu = ucnt / VPU;                      // 16-byte units per X row
+    auto issue = [&](int st, int c) {
+      const int64_t pos0 = (int64_t)tile.x + (int64_t)c * R;
+      const int nr = min(R, tile.y - c * R);
+      for (int e = tid; e < nr * xu; e += 256) {
+        const int r = e / xu, k = e - r * xu;
+        cp_async16(&Xs[st][r][k * VPU], X + (pos0 + r) * p.DinP + ub + k * VPU);
+      }
+      for (int e = tid; e < nr * ncq * (4 / VPU); e += 256) {   // lanes over positions (coalesced)
+        const int r = e % nr, q = e / nr;
+        const int cq = q / (4 / VPU), h = q - cq * (4 / VPU);
+        cp_async16(&Bs[st][r][cq * 4 + h * VPU], B + ((int64_t)(col0 / 4 + cq) * p.nP + pos0 + r) * 4 + h * VPU);
+      }
+      cp_async_commit();
+    };
     V res[4][4];
 #pragma unroll
     for (int i = 0; i < 4; ++i)
 #pragma unroll
       for (int j = 0; j < 4; ++j) res[i][j] = M::CAP;
-    for (int r0 = 0; r0 < tile.y; r0 += R) {
-      const int nr = min(R, tile.y - r0);
-      for (int e = tid; e < R; e += 256) rowp[e] = e < nr ? (int64_t)p.perm[tile.x + r0 + e] : -1;
-      const int64_t pos0 = (int64_t)tile.x + r0;
-      __syncthreads();
-      for (int e = tid; e < R * 8; e += 256) {   // X_p[u] for the staged rows: (row, u quad)
-        const int r = e >> 3, uq = e & 7;
-        if (uq * 4 < ucnt) {
-          V x[4];
-          const int64_t pr = rowp[r];
-          if (pr < 0) {
-#pragma unroll
-            for (int k = 0; k < 4; ++k) x[k] = M::CAP;
-          } else {
-#pragma unroll
-            for (int k = 0; k < 4; ++k) x[k] = 0;
-            for (int i = 0; i < p.nq; ++i) {
-              const int dig = mem_digit32(p.pm, (uint32_t)pr, p.q_pos[i]);
-              V y[4];
-              M::load4(vals + p.q_off[i] + (int64_t)dig * p.DinP + ub + uq * 4, y);
-#pragma unroll
-              for (int k = 0; k < 4; ++k) x[k] = M::sat(x[k], y[k]);
-            }
-          }
-#pragma unroll
-          for (int k = 0; k < 4; ++k) Xs[r][uq * 4 + k] = x[k];
-        }
-      }
-      for (int e = tid; e < R * ncq; e += 256) {     // B[cls/4][pos][4]: lanes over positions (coalesced)
-        const int r = e % R, cq = e / R;
-        V y[4];
-        if (r < nr && cq * 4 < ncols) {
-          M::load4(B + ((int64_t)(col0 / 4 + cq) * p.nP + pos0 + r) * 4, y);
-        } else {
-#pragma unroll
-          for (int k = 0; k < 4; ++k) y[k] = M::CAP;
-        }
-#pragma unroll
-        for (int k = 0; k < 4; ++k) Bs[r][cq * 4 + k] = y[k];
+    issue(0, 0);
+    for (int c = 0; c < nchunk; ++c) {
+      if (c + 1 < nchunk) {
+        issue((c + 1) & 1, c + 1);
+        cp_async_wait<1>();
+      } else {
+        cp_async_wait<0>();
       }
       __syncthreads();
+      const int st = c & 1;
+      const int nr = min(R, tile.y - c * R);
       if (tu < 8 && tu * 4 < ucnt) {
 #pragma unroll 4
         for (int r = 0; r < nr; ++r) {
           V x[4], y[4];
-          M::load4(&Xs[r][tu * 4], x);
-          M::load4(&Bs[r][tc * 4], y);
+          M::load4(&Xs[st][r][tu * 4], x);
+          M::load4(&Bs[st][r][tc * 4], y);
 #pragma unroll
           for (int i = 0; i < 4; ++i)
 #pragma unroll
             for (int j = 0; j < 4; ++j) res[i][j] = M::addmin(x[i], y[j], res[i][j]);
         }
       }
-      __syncthreads();
+      __syncthreads();                               // stage st is refilled by the next issue
     }
 #pragma unroll
     for (int i = 0; i < 4; ++i)
@@ -592,6 +618,10 @@ cudaError_t launch_mem_enum(const MemEnumParams& p, int64_t ntiles, int npf, cud
 template <typename V>
 cudaError_t launch_mem_fold(const MemFoldParams& p, int64_t ntiles, cudaStream_t st) {
   if (ntiles <= 0) return cudaSuccess;
+  const int64_t xthreads = p.nP * (p.DinP / 4);
+  mem_xrows_kernel<V><<<(unsigned)std::min<int64_t>(148 * 16, (xthreads + 255) / 256), 256, 0, st>>>(p);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
   mem_fold_kernel<V><<<dim3((unsigned)ntiles, (unsigned)p.ncolblk), 256, 0, st>>>(p);
   return cudaGetLastError();
 }
