@@ -116,7 +116,12 @@ typedef struct {
   int32_t device;              /* CUDA device ordinal */
   void* cuda_stream;           /* cudaStream_t; NULL = a stream owned by the ctx */
   int32_t world, rank;         /* world > 1: enumeration sharded over ranks */
-  const void* nccl_unique_id;  /* world > 1: 128-byte ncclUniqueId (same on all ranks) */
+  const void* nccl_unique_id;  /* world > 1: 128-byte ncclUniqueId (same on all ranks).
+                                * NULL with world > 1 = shard simulation (test hook, one
+                                * process): no collective; cfp_segment_costs returns this
+                                * rank's shard-local (cost, least index) per bucket, whose
+                                * lexicographic min over ranks is the world-1 result;
+                                * cfp_search_plan / cfp_prepare are rejected (EINVAL). */
 } cfp_ctx_opts;
 
 typedef struct cfp_ctx cfp_ctx;

@@ -277,9 +277,9 @@ class Context:
         L = lib()
         self._h = C.c_void_p()
         uid = None
-        if world > 1:
-            if nccl_unique_id is None or len(nccl_unique_id) != 128:
-                raise CfpError(CFP_EINVAL, "world > 1 needs a 128-byte nccl unique id")
+        if world > 1 and nccl_unique_id is not None:     # None: shard simulation (cfp.h)
+            if len(nccl_unique_id) != 128:
+                raise CfpError(CFP_EINVAL, "the nccl unique id has 128 bytes")
             uid = C.create_string_buffer(bytes(nccl_unique_id), 128)
         opts = cfp_ctx_opts(device, stream, world, rank, C.cast(uid, C.c_void_p) if uid else None)
         _check(L.cfp_ctx_create(C.byref(self._h), C.byref(opts)))

@@ -83,6 +83,7 @@ struct cfp_ctx {
   int world = 1, rank = 0;
   ncclComm_t comm = nullptr;
   int sms = 148;
+  bool sim = false;                 // world > 1 without a communicator: shard simulation (test hook)
   // side streams for concurrent per-type enumerations (fork/join by events):
   // the types are independent until the bucket reduction, and running them
   // side by side packs their CTAs into the same waves (no per-launch tail)
@@ -140,8 +141,9 @@ extern "C" cfp_status cfp_ctx_create(cfp_ctx** out, const cfp_ctx_opts* opts) {
     uint64_t thr = ~0ull;
     CUDA_TRY(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
   }
-  if (c->world > 1) {
-    if (!opts->nccl_unique_id) return fail(CFP_EINVAL, "world > 1 needs nccl_unique_id");
+  if (c->world > 1 && !opts->nccl_unique_id) {
+    c->sim = true;                  // single-process shard simulation: no collective
+  } else if (c->world > 1) {
     ncclUniqueId id;
     memcpy(&id, opts->nccl_unique_id, sizeof(id));
     NCCL_TRY(ncclCommInitRank(&c->comm, c->world, id, c->rank));
@@ -1445,8 +1447,9 @@ static cfp_status execute_impl(cfp_ctx* ctx, cfp_prepared* P) {
   if (P->has64) { CUDA_TRY(launch_amin<uint64_t>(aps, P->pair_off.as<int64_t>(), nslot, P->npairs, st)); P->launches++; }
   if (ctx->world > 1) {
     // rank-local minima were written to locA by the argmin descriptors; amin wrote
-    // them there too -- reduce into the global A
-    NCCL_TRY(ncclAllReduce(P->locAI.p, outA, ai, ncclUint64, ncclMin, ctx->comm, st));
+    // them there too -- reduce into the global A (shard simulation: the local A)
+    if (ctx->comm) NCCL_TRY(ncclAllReduce(P->locAI.p, outA, ai, ncclUint64, ncclMin, ctx->comm, st));
+    else CUDA_TRY(cudaMemcpyAsync(outA, P->locAI.p, (size_t)ai * 8, cudaMemcpyDeviceToDevice, st));
   }
   ArgminEntry* list = P->edges.as<ArgminEntry>();
   int32_t* count = reinterpret_cast<int32_t*>(P->edges.as<char>() + (size_t)(ai + 1) * sizeof(ArgminEntry));
@@ -1517,7 +1520,7 @@ static cfp_status merge_ranks(cfp_prepared* P, cudaStream_t st) {
   const unsigned nb = (unsigned)((ai + 255) / 256);
   mask_idx_kernel<<<nb, 256, 0, st>>>(locA, A, locI, ai, I);
   CUDA_TRY(cudaGetLastError());
-  NCCL_TRY(ncclAllReduce(I, I, ai, ncclUint64, ncclMin, ctx->comm, st));
+  if (ctx->comm) NCCL_TRY(ncclAllReduce(I, I, ai, ncclUint64, ncclMin, ctx->comm, st));
   P->launches += 1;
   return CFP_OK;
 }
@@ -1594,6 +1597,7 @@ static cfp_status fetch_impl(cfp_ctx* ctx, cfp_prepared* P, cfp_plan* out) {
 // ---------------------------------------------------------------- public API
 extern "C" cfp_status cfp_prepare(cfp_ctx* ctx, const cfp_problem* p, cfp_prepared** out) {
   if (!ctx || !out) return fail(CFP_EINVAL, "null argument");
+  if (ctx->sim) return fail(CFP_EINVAL, "shard simulation ctx (world > 1 without nccl_unique_id): tables only");
   return prepare_impl(ctx, p, true, out);
 }
 
@@ -1609,6 +1613,7 @@ extern "C" cfp_status cfp_fetch_plan(cfp_ctx* ctx, cfp_prepared* prep, cfp_plan*
 
 extern "C" cfp_status cfp_search_plan(cfp_ctx* ctx, const cfp_problem* p, cfp_plan* out) {
   if (!ctx || !p || !out) return fail(CFP_EINVAL, "null argument");
+  if (ctx->sim) return fail(CFP_EINVAL, "shard simulation ctx (world > 1 without nccl_unique_id): tables only");
   cfp_prepared* prep = nullptr;
   TRY(prepare_impl(ctx, p, true, &prep));
   std::unique_ptr<cfp_prepared> guard(prep);

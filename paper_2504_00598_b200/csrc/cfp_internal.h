@@ -245,7 +245,7 @@ struct MemPrefixMap {
 // positions) and fold tiles (<= kMemFoldTile positions) never straddle a ctx
 // value resp. a (ctx, class) group.  B is class-quad-major: B[cls/4][pos][cls%4]
 // (coalesced enumeration stores, 16-byte fold loads).
-constexpr int kMemFoldTile = 1024;
+constexpr int kMemFoldTile = 512;
 
 struct MemEnumParams {
   int32_t Wc;                        // classes per prefix row

@@ -316,3 +316,49 @@ def test_prepared_execute_matches(ctx, oracle_lib):
     info = prep.info()
     assert info.combos == 3 + 81 + 81 + 3
     prep.close()
+
+
+# ---------------------------------------------------------------- sharded enumeration (one GPU)
+def _merge_shards(parts):
+    """Lexicographic (cost, index) min over the ranks' shard-local tables."""
+    A = parts[0][0].copy()
+    I = parts[0][1].copy()
+    for a, i in parts[1:]:
+        take = (a < A) | ((a == A) & (i < I))
+        A = np.where(take, a, A)
+        I = np.where(take, i, I)
+    return A, I
+
+
+def _shard_tables(cfp, ty, tr, din, world):
+    parts = []
+    for r in range(world):
+        c = cfp.Context(device=0, world=world, rank=r)       # no unique id: shard simulation
+        parts.append(c.segment_costs(ty, tr, din))
+        c.close()
+    return _merge_shards(parts)
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_shard_simulation_random(ctx, oracle_lib, seed):
+    """The world > 1 enumeration path (shard ranges, rank-local fold, minima and
+    least indices) on one GPU: every world size's merged shards == world 1."""
+    cfp = _cfp()
+    p = G.tiny_random(8800 + seed, max_k=6, max_d=6, max_plans=None)
+    for tr in sorted({int(t) for t in p.instances}):
+        ty = p.types[p.transitions[tr].type]
+        A1, I1 = ctx.segment_costs(ty, p.transitions[tr], p.d_in(tr))
+        for world in (2, 3, 8):
+            A, I = _shard_tables(cfp, ty, p.transitions[tr], p.d_in(tr), world)
+            assert np.array_equal(A, A1) and np.array_equal(I, I1), (seed, tr, world)
+
+
+@pytest.mark.parametrize("cfg,world", [("C2", 4), ("C3", 2), ("C3", 8), ("C5", 3)])
+def test_shard_simulation_configs(ctx, cfg, world):
+    cfp = _cfp()
+    p = G.make_config(cfg, 0, "shaped")
+    for tr in sorted({int(t) for t in p.instances}):
+        ty = p.types[p.transitions[tr].type]
+        A1, I1 = ctx.segment_costs(ty, p.transitions[tr], p.d_in(tr))
+        A, I = _shard_tables(cfp, ty, p.transitions[tr], p.d_in(tr), world)
+        assert np.array_equal(A, A1) and np.array_equal(I, I1), (cfg, tr, world)
