@@ -84,6 +84,8 @@ struct cfp_ctx {
   ncclComm_t comm = nullptr;
   int sms = 148;
   bool sim = false;                 // world > 1 without a communicator: shard simulation (test hook)
+  bool no_full_a = false;           // CFP_ENUM_FULL_A=0: runtime-length A loop only (A/B tests)
+  int64_t msplit_min_m = 128;       // M split when nM >= this (CFP_ENUM_MSPLIT_MIN_M; tests force 2)
   // side streams for concurrent per-type enumerations (fork/join by events):
   // the types are independent until the bucket reduction, and running them
   // side by side packs their CTAs into the same waves (no per-launch tail)
@@ -124,6 +126,8 @@ extern "C" cfp_status cfp_ctx_create(cfp_ctx** out, const cfp_ctx_opts* opts) {
     return fail(CFP_ECUDA, "this library is built for sm_100a (B200); found sm_" +
                                std::to_string(prop.major) + std::to_string(prop.minor));
   c->sms = prop.multiProcessorCount;
+  if (const char* fa = getenv("CFP_ENUM_FULL_A")) c->no_full_a = atoi(fa) == 0;
+  if (const char* ms = getenv("CFP_ENUM_MSPLIT_MIN_M")) c->msplit_min_m = std::max(2LL, atoll(ms));
   if (opts && opts->cuda_stream) {
     c->stream = (cudaStream_t)opts->cuda_stream;
   } else {
@@ -910,6 +914,7 @@ static cfp_status prepare_impl(cfp_ctx* ctx, const cfp_problem* p, bool do_chain
       if (B[d]) nb *= r[d];
       if (M[d]) nM *= r[d];
     }
+    if (nM >= INT32_MAX) return fail(CFP_ETOOBIG, "M loop space >= 2^31");
     const int VG = sc.VG, NB = sc.NB;
     const int na_pad = round_up(na, 4);
     const int nb_pad = round_up((int64_t)VG * NB, 4);
@@ -1023,13 +1028,22 @@ static cfp_status prepare_impl(cfp_ctx* ctx, const cfp_problem* p, bool do_chain
       if (ep.ymerge) smem += ymb;
     }
     ep.init_row = ep.o_mode != 0 || !(ep.o_bstride == 1 && ep.o_bradix == ep.nb);
+    // M split (B = {o}): two threads per prefix halve the work unit, so the
+    // CTAs of a launch fill the last wave of 148 x 4 slots twice as finely.
+    // It doubles the CTAs' fixed costs (staging, fold epilogue), so it pays
+    // only for long M loops (measured: C4 nM = 529 10.35 -> 10.21 ms; C3/C5
+    // nM = 24/23 0.69 -> 0.75 ms)
+    ep.MS = (!ep.init_row && ep.o_mode == 0 && nM >= ctx->msplit_min_m && ep.staged && ep.ymerge) ? 2 : 1;
+    ep.CH = kBlock / ep.MS;
+    ep.no_full_a = ctx->no_full_a ? 1 : 0;
+    ep.Gpad = (ep.G + ep.CH - 1) / ep.CH * ep.CH;
     te.smem = ep.staged ? smem : 0;
-    te.nthreads = ep.Gpad * ep.W * ep.VG;
+    te.nthreads = ep.Gpad * ep.W * ep.VG * ep.MS;
     if (te.nthreads / kBlock > 0x7FFFFFFF) return fail(CFP_ETOOBIG, "grid too large");
     te.bp_off = bp_bytes;
     bp_bytes += ((te.nPl * ep.Do * vbytes) + 255) & ~255LL;
     for (int i = 0; i < Pp; ++i) ep.pre_stride[i] = prod(r, i + 1, Pp);
-    ep.nchunks = ep.W * (ep.Gpad / kBlock);
+    ep.nchunks = ep.W * (ep.Gpad / ep.CH);
     // eval spec for argmin recovery
     EvalSpec& es = te.es;
     es.K = K;
@@ -1087,8 +1101,8 @@ static cfp_status prepare_impl(cfp_ctx* ctx, const cfp_problem* p, bool do_chain
       const int64_t VP = simple ? ((te.NB + 3) & ~3) : ((ep.Do + 3) & ~3);   // = the kernel's VP bound
       int64_t dinp_max = 4;
       for (int x : te.trans) dinp_max = std::max<int64_t>(dinp_max, (P->trans[trans_slot[x]].Din + 3) & ~3);
-      int64_t epi = kBlock * VP + kBlock * dinp_max;
-      if (8 * VP > kBlock) epi += 8 * dinp_max * VP;
+      int64_t epi = ep.CH * VP + ep.CH * dinp_max;
+      if (8 * VP > ep.CH) epi += 8 * dinp_max * VP;
       ep.smem_epi = (int32_t)(te.trans.empty() ? 0 : epi * (int64_t)vbytes);
       if (ep.smem_epi > 200 * 1024) return fail(CFP_ETOOBIG, "D_in x D_o too large for the fold epilogue");
       ep.ntau = (int)te.trans.size();
@@ -1103,12 +1117,12 @@ static cfp_status prepare_impl(cfp_ctx* ctx, const cfp_problem* p, bool do_chain
           et.qt[q] = tx.qt_off[q];
         }
         P->epi_host.push_back(et);
-        tx.fp.CH = kBlock;
+        tx.fp.CH = ep.CH;
         tx.fp.nchunks = ep.nchunks;
         tx.fp.W = ep.W;
         tx.fp.G = ep.G;
         tx.fp.h0 = ep.h0;
-        tx.fp.nhb = ep.Gpad / kBlock;
+        tx.fp.nhb = ep.Gpad / ep.CH;
         tx.chunk_off = scratch_bytes;
         scratch_bytes += ((ep.nchunks * tx.fp.Din * tx.fp.Do * vbytes) + 255) & ~255LL;
         tx.aval_off = scratch_bytes;

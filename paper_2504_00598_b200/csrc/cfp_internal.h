@@ -70,8 +70,12 @@ struct EnumParams {
   int32_t P;                    // prefix length
   int32_t pre_radix[kMaxDigits];
   int64_t W;                    // size of the low prefix part (canonical last digits)
-  int64_t G, Gpad, h0;          // high values handled, padded to a multiple of kBlock
+  int64_t G, Gpad, h0;          // high values handled, padded to a multiple of CH
   int32_t VG;                   // register groups per prefix (B split)
+  int32_t MS;                   // M-loop split: 1, or 2 (threads t and t + CH share a prefix
+                                // and take the two halves of the M values; B = {o} only)
+  int32_t CH;                   // prefixes per CTA (= chunk) = kBlock / MS
+  int32_t no_full_a;            // 1: do not take the fully unrolled A loop (A/B tests)
   int64_t pre_sx[kMaxDigits], pre_sy[kMaxDigits], pre_sz[kMaxDigits];  // ctx strides
   int64_t nM;                   // |M space| (mtab rows)
   int32_t na, na_pad;           // |A space| (XT row length), padded
@@ -94,7 +98,7 @@ struct EnumParams {
   int32_t ntau;
   const EpiTau* taus;           // device [ntau]
   const void* vals;             // value blob (compact Q tables)
-  int64_t nchunks;              // W * (Gpad / kBlock)
+  int64_t nchunks;              // W * (Gpad / CH)
   int32_t smem_epi;             // bytes of the epilogue region
 };
 
@@ -114,7 +118,7 @@ struct FoldParams {
   const void* Bp;
   const void* vals;             // value blob (compact Q tables)
   void* chunkmin;               // [Din * Do][nchunks]
-  // chunk -> rows: chunk = l * nhb + hb holds local rows (hb*kBlock + i) * W + l
+  // chunk -> rows: chunk = l * nhb + hb holds local rows (hb*CH + i) * W + l
   int64_t W, G, h0, nhb;
 };
 

@@ -272,7 +272,10 @@ __device__ __forceinline__ void atomic_min_v<uint64_t>(uint64_t* p, uint64_t v) 
 // 2: staged, and the Z term folded into per-m copies of the Y rows
 // (Y'[m][j] = Y[m][j] + Z[m]) with K0[p] added once after the enumeration --
 // no per-m saturating add in the loop (exact: min(K0 + t) = K0 + min t).
-template <typename V, int NB, int ST>
+// NA > 0: the A space has exactly NA values (compile time) -- the A loop is
+// fully unrolled with all NA x values loaded at the top of each M step, so no
+// x load latency sits between consecutive VIADDMNMX groups.
+template <typename V, int NB, int ST, int MSPLIT, int NA = 0>
 __global__ void __launch_bounds__(kBlock, 4) enum_kernel(const EnumParams p) {
   constexpr bool STAGED = ST > 0;
   constexpr bool MERGED = ST == 2;
@@ -282,12 +285,15 @@ __global__ void __launch_bounds__(kBlock, 4) enum_kernel(const EnumParams p) {
   const int tid = threadIdx.x;
   const bool edbg = blockIdx.x == 0 && tid == 0 && p.ntau == 2;
   if (edbg) g_enum_dbg2[0] = gtimer0();
-  const uint32_t nhb = (uint32_t)(p.Gpad / kBlock);          // 32-bit index math (grid < 2^31)
+  constexpr int CH = kBlock / MSPLIT;                       // prefixes per CTA (= p.CH)
+  const int slot = MSPLIT == 2 ? (tid & (CH - 1)) : tid;    // this thread's prefix slot
+  const int half = MSPLIT == 2 ? tid / CH : 0;              // its share of the M values
+  const uint32_t nhb = (uint32_t)(p.Gpad / CH);             // 32-bit index math (grid < 2^31)
   const uint32_t g = blockIdx.x / nhb;
   const int64_t hb = blockIdx.x - g * nhb;
   const int64_t l = g / (uint32_t)p.VG;
   const int vg = (int)(g - (uint32_t)l * (uint32_t)p.VG);
-  const int64_t hh = hb * kBlock + tid;
+  const int64_t hh = hb * CH + slot;
   const bool live = hh < p.G;
   const int64_t pg = (p.h0 + hh) * p.W + l;       // global canonical prefix
   const int64_t row = hh * p.W + l;               // local canonical prefix
@@ -360,7 +366,11 @@ __global__ void __launch_bounds__(kBlock, 4) enum_kernel(const EnumParams p) {
     if (p.init_row)
       for (int v = 0; v < p.Do; ++v) Bp[v] = T::CAP;
     const V k0 = static_cast<const V*>(p.K0)[pg];
-    for (int64_t m = 0; m < p.nM; ++m) {
+    // MS = 2: warps of half 0 take m in [0, mh), warps of half 1 [mh, nM)
+    const int nM = (int)p.nM;                      // host: nM < 2^31 (mtab rows)
+    const int mh = MSPLIT == 2 ? (nM + 1) / 2 : nM;
+    const int m_lo = half ? mh : 0, m_hi = half ? nM : mh;
+    for (int m = m_lo; m < m_hi; ++m) {
       const int4 mt = MT[m];
       constexpr int NBV = (NB + VN - 1) / VN * VN;   // Y rows are padded to whole vectors
       V y[NBV];
@@ -377,7 +387,17 @@ __global__ void __launch_bounds__(kBlock, 4) enum_kernel(const EnumParams p) {
         for (int j = 0; j < NB; ++j) y[j] = T::sat(y[j], km);
       }
       const V* xr = XT + sx + mt.x;
-      const int na_v = p.na & ~(VN - 1);
+      if constexpr (NA > 0) {
+        constexpr int NAV = (NA + VN - 1) / VN * VN;  // X rows are padded to whole vectors
+        V x[NAV];
+#pragma unroll
+        for (int a = 0; a < NAV; a += VN) load_vec<V>(xr + a, x + a);
+#pragma unroll
+        for (int a = 0; a < NA; ++a)
+#pragma unroll
+          for (int j = 0; j < NB; ++j) acc[j] = T::addmin(x[a], y[j], acc[j]);
+      }
+      const int na_v = NA > 0 ? 0 : p.na & ~(VN - 1);
 #pragma unroll 2
       for (int a = 0; a < na_v; a += VN) {
         V x[VN];
@@ -387,7 +407,7 @@ __global__ void __launch_bounds__(kBlock, 4) enum_kernel(const EnumParams p) {
 #pragma unroll
           for (int j = 0; j < NB; ++j) acc[j] = T::addmin(x[q], y[j], acc[j]);
       }
-      for (int a = na_v; a < p.na; ++a) {           // ragged A tail (no padded evaluations)
+      for (int a = na_v; NA == 0 && a < p.na; ++a) {   // ragged A tail (no padded evaluations)
         const V x = xr[a];
 #pragma unroll
         for (int j = 0; j < NB; ++j) acc[j] = T::addmin(x, y[j], acc[j]);
@@ -408,7 +428,9 @@ __global__ void __launch_bounds__(kBlock, 4) enum_kernel(const EnumParams p) {
         for (int j = 0; j < NB; ++j) acc[j] = T::sat(acc[j], k0);
       }
     }
-    if (p.o_mode == 0) {
+    if (MSPLIT == 2) {
+      // written after the two halves are merged (below)
+    } else if (p.o_mode == 0) {
       if (p.o_bstride == 1 && p.o_bradix == p.nb) {       // B = {o}: slot j <-> v
 #pragma unroll
         for (int j = 0; j < NB; ++j)
@@ -429,16 +451,49 @@ __global__ void __launch_bounds__(kBlock, 4) enum_kernel(const EnumParams p) {
     }
   }
   if (edbg) g_enum_dbg2[2] = gtimer0();
-  if (p.ntau == 0) return;
-  // ---- epilogue: fold the cross-segment terms of every incoming transition
-  __syncthreads();                                // staged tables no longer needed
   const bool simple = p.o_mode == 0 && p.o_bstride == 1 && p.o_bradix == p.nb;
   const int v_lo = simple ? ybase : 0;
   const int v_cnt = simple ? min(NB, p.nb - ybase) : p.Do;
   const int VP = (v_cnt + 3) & ~3;
-  V* Bs = reinterpret_cast<V*>(smem_raw);                     // [kBlock][VP]
-  V* Xs = Bs + kBlock * VP;                                   // [kBlock][DinP] (red afterwards)
-  if (simple && VP == NB) {                       // 16-byte stores (conflict-light rows)
+  V* Bs = reinterpret_cast<V*>(smem_raw);                     // [CH][VP]
+  V* Xs = Bs + CH * VP;                                       // [CH][DinP] (red afterwards)
+  if constexpr (MSPLIT == 2) {
+    // merge the two halves' bucket minima of each prefix (B = {o}, simple):
+    // half 1 parks its registers in Bs, half 0 takes the min, writes B_p and
+    // leaves the merged row in Bs for the fold
+    __syncthreads();                              // staged tables no longer needed
+    if (half == 1) {
+#pragma unroll
+      for (int j = 0; j < NB; j += VN) {
+        V w[VN];
+#pragma unroll
+        for (int q = 0; q < VN; ++q) w[q] = j + q < NB ? acc[j + q] : T::CAP;
+        if (j + VN <= VP) store_vec<V>(Bs + slot * VP + j, w);
+        else
+          for (int q = 0; q < VN && j + q < VP; ++q) Bs[slot * VP + j + q] = w[q];
+      }
+    }
+    __syncthreads();
+    if (half == 0) {
+#pragma unroll
+      for (int j = 0; j < NB; ++j)
+        if (j < VP) acc[j] = T::mn(acc[j], Bs[slot * VP + j]);
+      if (live) {
+#pragma unroll
+        for (int j = 0; j < NB; ++j)
+          if (ybase + j < p.nb) Bp[ybase + j] = acc[j];
+      }
+#pragma unroll
+      for (int j = 0; j < NB; ++j)
+        if (j < VP) Bs[slot * VP + j] = (live && j < v_cnt) ? acc[j] : T::CAP;
+    }
+  }
+  if (p.ntau == 0) return;
+  // ---- epilogue: fold the cross-segment terms of every incoming transition
+  __syncthreads();                                // staged tables no longer needed / Bs merged
+  if (MSPLIT == 2) {
+    // Bs already holds the merged rows
+  } else if (simple && VP == NB) {                // 16-byte stores (conflict-light rows)
 #pragma unroll
     for (int j = 0; j < NB; j += VN) {
       V w[VN];
@@ -464,8 +519,8 @@ __global__ void __launch_bounds__(kBlock, 4) enum_kernel(const EnumParams p) {
       // X^t_p[u] = sum_i Q_i[u][s_i(p)] for this thread's prefix: each term is
       // one contiguous row Q_i^T[s_i(p)][0..DinP) of the transposed copy, read
       // 16 bytes at a time and accumulated in the thread's Xs row.
-      V* xrow = Xs + tid * DinP;
-      for (int i = 0; i < et.nq; ++i) {
+      V* xrow = Xs + slot * DinP;
+      for (int i = 0; half == 0 && i < et.nq; ++i) {
         const int a = et.q[i].a;
         const int dig = pg < 0x7FFFFFFF ? (int)(((uint32_t)pg / (uint32_t)p.pre_stride[a]) % (uint32_t)p.pre_radix[a])
                                         : (int)((pg / p.pre_stride[a]) % p.pre_radix[a]);
@@ -485,7 +540,7 @@ __global__ void __launch_bounds__(kBlock, 4) enum_kernel(const EnumParams p) {
           store_vec<V>(xrow + u0, y);
         }
       }
-      if (et.nq == 0)
+      if (et.nq == 0 && half == 0)
         for (int u0 = 0; u0 < DinP; u0 += VN) {
           V y[VN];
 #pragma unroll
@@ -511,7 +566,7 @@ __global__ void __launch_bounds__(kBlock, 4) enum_kernel(const EnumParams p) {
 #pragma unroll
         for (int j = 0; j < 4; ++j) res[i][j] = T::CAP;
       const int rs = stripes > 1 ? gi : 0;
-      for (int r = rs; r < kBlock; r += stripes) {
+      for (int r = rs; r < CH; r += stripes) {
         V x[4], y[4];
         load_vec<V>(Xs + r * DinP + u0, x);
         if (VN == 2) load_vec<V>(Xs + r * DinP + u0 + 2, x + 2);
@@ -536,7 +591,7 @@ __global__ void __launch_bounds__(kBlock, 4) enum_kernel(const EnumParams p) {
     __syncthreads();                                 // Xs free -> stripe partials
     if (edbg) g_enum_dbg2[4 + 3 * t] = gtimer0();
     if (nblk < kBlock) {
-      V* red = stripes * VP <= kBlock ? Xs : Xs + kBlock * dinp_max;   // [stripes][DinP][VP]
+      V* red = stripes * VP <= CH ? Xs : Xs + CH * dinp_max;   // [stripes][DinP][VP]
       if (active) {
 #pragma unroll
         for (int i = 0; i < 4; ++i)
@@ -690,10 +745,11 @@ __device__ void argmin_pair(const ArgminParams& ap, const int pair, unsigned cha
   __syncthreads();
   const int nl = min(s_nl, NT);                       // W > NT with > NT hits: rare, see below
   const bool all_l = s_nl > NT;
-  for (int64_t w = tid; w < (all_l ? W : (int64_t)nl) * kBlock; w += NT) {
-    const int64_t li = w / kBlock, i = w - li * kBlock;
+  const int64_t CH = f.CH;
+  for (int64_t w = tid; w < (all_l ? W : (int64_t)nl) * CH; w += NT) {
+    const int64_t li = w / CH, i = w - li * CH;
     const int64_t l = all_l ? li : s_ls[li];
-    const int64_t hh = hbmin * kBlock + i;
+    const int64_t hh = hbmin * CH + i;
     if (hh >= Gh) continue;
     if (all_l && cm[l * nhb + hbmin] != best) continue;
     const int64_t plr = hh * W + l;
@@ -1330,7 +1386,7 @@ cudaError_t launch_fill(V* p, int64_t n, V v, cudaStream_t st) {
 template <typename V, int NB>
 cudaError_t launch_enum_nb(const EnumParams& p, int64_t nthreads, size_t smem, cudaStream_t st) {
   (void)nthreads;
-  const int64_t blocks = p.W * p.VG * (p.Gpad / kBlock);
+  const int64_t blocks = p.W * p.VG * (p.Gpad / p.CH);
   if (blocks <= 0) return cudaSuccess;
   const size_t sm = std::max(smem, (size_t)p.smem_epi);
   auto launch = [&](auto kern) -> cudaError_t {
@@ -1344,9 +1400,17 @@ cudaError_t launch_enum_nb(const EnumParams& p, int64_t nthreads, size_t smem, c
     kern<<<(unsigned)blocks, kBlock, sm, st>>>(p);
     return cudaGetLastError();
   };
-  if (p.staged && p.ymerge) return launch(enum_kernel<V, NB, 2>);
-  if (p.staged) return launch(enum_kernel<V, NB, 1>);
-  return launch(enum_kernel<V, NB, 0>);
+  if (p.MS == 2) {                                  // host: B = {o}, staged + merged Y
+    if (!(p.staged && p.ymerge)) return cudaErrorInvalidValue;
+    return launch(enum_kernel<V, NB, 2, 2>);
+  }
+  if constexpr (sizeof(V) == 4 && (NB == 23 || NB == 24)) {
+    if (p.staged && p.ymerge && p.na == NB && p.na_pad >= (NB + 3) / 4 * 4 && !p.no_full_a)
+      return launch(enum_kernel<V, NB, 2, 1, NB>);
+  }
+  if (p.staged && p.ymerge) return launch(enum_kernel<V, NB, 2, 1>);
+  if (p.staged) return launch(enum_kernel<V, NB, 1, 1>);
+  return launch(enum_kernel<V, NB, 0, 1>);
 }
 
 template <typename V>

@@ -362,3 +362,72 @@ def test_shard_simulation_configs(ctx, cfg, world):
         A1, I1 = ctx.segment_costs(ty, p.transitions[tr], p.d_in(tr))
         A, I = _shard_tables(cfp, ty, p.transitions[tr], p.d_in(tr), world)
         assert np.array_equal(A, A1) and np.array_equal(I, I1), (cfg, tr, world)
+
+
+# ---------------------------------------------------------------- M split
+# The enumeration's M-split path (two threads per prefix, each taking half of
+# the M loop, merged in shared memory before the fold) runs by default only
+# for long M loops (nM >= 128, C4); a ctx created with
+# CFP_ENUM_MSPLIT_MIN_M=2 takes it for every eligible type.
+
+
+@pytest.fixture(scope="module")
+def ctx_ms():
+    import os
+    from paper_2504_00598_b200 import build as B
+    B.build()
+    from paper_2504_00598_b200 import cfp
+    old = os.environ.get("CFP_ENUM_MSPLIT_MIN_M")
+    os.environ["CFP_ENUM_MSPLIT_MIN_M"] = "2"
+    try:
+        c = cfp.Context(device=0)
+    finally:
+        if old is None:
+            del os.environ["CFP_ENUM_MSPLIT_MIN_M"]
+        else:
+            os.environ["CFP_ENUM_MSPLIT_MIN_M"] = old
+    yield c
+    c.close()
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_msplit_random_segment_tables(ctx_ms, oracle_lib, seed):
+    O = oracle_lib
+    p = G.tiny_random(7000 + seed, mode=("ties", "random")[seed % 2], max_plans=None, max_n=3,
+                      max_k=6, max_d=6, max_edges=6, p_inf=0.03)
+    for tr_id, tr in enumerate(p.transitions):
+        A0, I0 = O.segment_table(p, tr_id)
+        A, I = ctx_ms.segment_costs(p.types[tr.type], tr, p.d_in(tr_id))
+        assert np.array_equal(A, A0), (seed, tr_id)
+        assert np.array_equal(I, I0), (seed, tr_id)
+
+
+@pytest.mark.parametrize("cfg,dist", [("C1", "shaped"), ("C2", "random"), ("C2", "ties")])
+def test_msplit_small_configs(ctx_ms, oracle_lib, cfg, dist):
+    p = G.make_config(cfg, seed=1, dist=dist)
+    _search_or_infeasible(ctx_ms, oracle_lib, p)
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("cfg", ["C3", "C5"])
+def test_msplit_large_config(ctx_ms, oracle_lib, cfg):
+    """Full-size C3/C5 with the split on: sampled buckets against the oracle
+    and the plan's Eq. 3 recomputation."""
+    O = oracle_lib
+    p = G.make_config(cfg, seed=0, dist="shaped")
+    m = O.Marshalled(p)
+    rng = np.random.default_rng(2)
+    tr_id = 3
+    tr = p.transitions[tr_id]
+    A, I = ctx_ms.segment_costs(p.types[tr.type], tr, p.d_in(tr_id))
+    samples = [(int(rng.integers(0, A.shape[0])), int(rng.integers(0, A.shape[1]))) for _ in range(2)]
+    _check_table_properties(O, p, tr_id, A, I, m, samples)
+    got = ctx_ms.search_plan(p)
+    u, tot = 0, 0
+    for n, t in enumerate(p.instances):
+        ty = p.types[p.transitions[int(t)].type]
+        c = O.cost_index(p, int(t), u, int(got.seg_index[n]), m)
+        assert c == int(got.seg_ns[n])
+        tot += c
+        u = O._digits(ty.radix, int(got.seg_index[n]))[ty.out_block]
+    assert tot == got.total_ns
