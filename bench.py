@@ -527,6 +527,95 @@ def run_cfp_dense(args, rank, world, local_rank):
     return out
 
 
+def run_cfp_budget(args, rank, world, local_rank):
+    """Dynamic profiling budget: every whole-segment
+    plan task of the config's used types screened in index order against
+    f x best (f = 2) over the dense per-plan tables of NEXT-2 (device
+    generator), one scan per type.  Roofline: HBM, 4 B read per task."""
+    import torch
+
+    from paper_2504_00598_b200 import build as B
+    B.build()
+    from paper_2504_00598_b200 import cfp
+    from synth import generators as G
+    if world > 1:
+        raise SystemExit("--budget runs on one GPU")
+    torch.cuda.set_device(local_rank)
+    prob = G.make_config(args.config, args.seed, args.dist)
+    ctx = cfp.Context(device=local_rank)
+    used = sorted({prob.transitions[int(t)].type for t in prob.instances})
+    bufs, ns = {}, {}
+    for t in used:
+        ns[t] = prob.num_combinations(t)
+        bufs[t] = torch.empty(ns[t] + 8, dtype=torch.int32, device="cuda")
+        ctx.dense_fill(bufs[t].data_ptr(), ns[t], G.dense_base(args.seed, t))
+    num, den = 2, 1
+    tasks = float(sum(ns.values()))
+
+    def step():
+        res, ms = {}, 0.0
+        for t in used:
+            r, k = ctx.profile_budget(bufs[t].data_ptr(), ns[t], num, den, timed=True)
+            res[t] = r
+            ms += k
+        return res, ms
+
+    for _ in range(args.warmup):
+        ref, _ = step()
+    k_ms, big_ms, e2e = [], [], []
+    big = max(used, key=lambda t: ns[t])
+    with ClockSampler(local_rank) as clk:
+        for _ in range(args.steps):
+            torch.cuda.synchronize()          # tables >> L2: every step streams them from HBM
+            t0 = time.perf_counter()
+            res, ms = step()
+            e2e.append((time.perf_counter() - t0) * 1e3)
+            assert res == ref
+            k_ms.append(ms)
+            _, kb = ctx.profile_budget(bufs[big].data_ptr(), ns[big], num, den, timed=True)
+            big_ms.append(kb)
+        torch.cuda.synchronize()
+    clocks = clk.summary()
+    ms = statistics.median(k_ms)
+    kb = statistics.median(big_ms)
+    peak, peak_src = hbm_peak_gbs()
+    achieved = ns[big] * 4 / (kb * 1e-3) / 1e9
+    pruned = sum(r["pruned"] for r in ref.values())
+    out = {
+        "metric": "budgeted profiling tasks screened/sec (dense per-plan tables, NEXT-3)",
+        "value": tasks / (ms * 1e-3), "unit": "tasks/s", "n_gpus": 1, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "u32", "data": "synthetic",
+        "config": {"workload": f"{args.config} dense per-plan tables (seed {args.seed}), every plan task of "
+                               f"the {len(used)} used types screened against f x best, f = {num}/{den}",
+                   "tasks_per_step": tasks, "l2": "tables >> L2: every step streams them from HBM"},
+        "budget": {"pruned": pruned, "infeasible": sum(r["infeasible"] for r in ref.values()),
+                   "spent_ns": sum(r["spent"] for r in ref.values()),
+                   "full_ns": sum(r["full"] for r in ref.values())},
+        "e2e": {"value": tasks / (statistics.median(e2e) * 1e-3), "unit": "tasks/s",
+                "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 64 * len(used),
+                "note": "tables are device-resident inputs (tens of GB); e2e = host wall time of the calls"},
+        "gpu_launches": len(used),
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": None,
+                     "note": f"budget_kernel on the largest type ({ns[big]} tasks): 4 B read per task "
+                             f"(algorithmic) / device time of the call; peak: {peak_src}"},
+        "clocks": clocks,
+    }
+    if not args.no_cpu_baseline:
+        from oracle import profiling as PR
+        m = 1 << 24
+        W = G.dense_table(args.seed, big, m)
+        t0 = time.perf_counter()
+        PR.budget(W, num, den)
+        dt = time.perf_counter() - t0
+        out["cpu_baseline"] = {"value": m / dt, "unit": "tasks/s", "cores": 1, "kind": "oracle",
+                               "sample": f"first {m} tasks of type {big} (numpy prefix-minimum oracle, "
+                                         f"{dt:.2f} s)"}
+    ctx.close()
+    return out
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -540,6 +629,7 @@ def main():
     ap.add_argument("--minplus", action="store_true", help="also run the (min,+) product microbenchmark")
     ap.add_argument("--mem", action="store_true", help="memory-constrained search (NEXT-1) instead")
     ap.add_argument("--dense", action="store_true", help="dense per-plan tables (NEXT-2) instead")
+    ap.add_argument("--budget", action="store_true", help="dynamic profiling budget (NEXT-3) instead")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -558,6 +648,9 @@ def main():
         return
     if args.dense:
         print(json.dumps(run_cfp_dense(args, rank, world, local_rank)), flush=True)
+        return
+    if args.budget:
+        print(json.dumps(run_cfp_budget(args, rank, world, local_rank)), flush=True)
         return
     if world > 1:
         import torch

@@ -293,6 +293,42 @@ cfp_status cfp_dense_time_kernels(cfp_dense_prepared* prep, int32_t on);
 cfp_status cfp_dense_kernel_ms(cfp_dense_prepared* prep, double* stream_ms, double* total_ms,
                                double* combos, double* bytes, int32_t* launches);
 
+/* ---- profiling space and dynamic profiling budget ----
+ * cfp_profile_space: Eq. 2 term by term, host arithmetic (callable
+ * without a GPU):  type_plans[t] = prod_j D_j of type t (the whole-segment
+ * plans to profile), trans_pairs[x] = sum over the cross edges (o_pred -> k)
+ * of transition x of D_{pred,o} * D_k (the reshard kernel groups; 0 for a
+ * chain start), total = their sum.  type_plans [num_types] and trans_pairs
+ * [num_transitions] are nullable caller-owned host arrays.  EINVAL for bad
+ * ids / radices, ETOOBIG when a count exceeds 2^62.
+ * Pins: 2 x 81 + 2 x 9 = 180 for the GPT layer segments,
+ * prod S_j + S_1 * S_K.
+ *
+ * cfp_profile_budget: the dynamic profiling time budget ("continuously
+ * updated based on the fastest observed parallelism plans, aggressively
+ * trimming the profiling of inefficient or stalled executions") over one
+ * type's dense per-plan table W [n] (DEVICE pointer, 16-byte aligned, uint32
+ * ns, CFP_INF32 = infeasible program), tasks run in canonical index order
+ * (DESIGN R-B1..R-B4): with best_i = min_{j<i} W[j], task i is pruned iff
+ * W[i] and best_i are finite and W[i] * den > best_i * num (f = num/den,
+ * 1 <= den <= num <= 65535, else EINVAL); a pruned task costs
+ * floor(best_i * num / den), a completed one W[i], an infeasible one 0.
+ * One read of W (a single-pass prefix-minimum scan).  n < 2^44 (ETOOBIG);
+ * single GPU.  kernel_ms (nullable): device time of the call's kernels. */
+typedef struct {
+  uint64_t tasks;                     /* n */
+  uint64_t pruned;                    /* tasks trimmed by the budget */
+  uint64_t infeasible;                /* CFP_INF32 entries */
+  uint64_t spent_lo, spent_hi;        /* profiling ns under the budget (128-bit) */
+  uint64_t full_lo, full_hi;          /* profiling ns without it: sum of finite W (128-bit) */
+  uint64_t best;                      /* least finite W, CFP_INF64 if none */
+  uint64_t best_index;                /* least index attaining it, CFP_NOIDX if none */
+} cfp_budget_result;
+cfp_status cfp_profile_space(const cfp_problem* p, int64_t* type_plans, int64_t* trans_pairs,
+                             int64_t* total);
+cfp_status cfp_profile_budget(cfp_ctx* ctx, const uint32_t* W_dev, uint64_t n, uint32_t num,
+                              uint32_t den, cfp_budget_result* out, double* kernel_ms);
+
 /* ---- host-only helpers (no device work; callable without a GPU) ---------- */
 /* Contiguous, balanced share [lo, hi) of `units` items for `rank` of `world`
  * in multiples of `align`. */

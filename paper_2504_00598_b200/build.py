@@ -14,7 +14,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libcfp.so")
-SOURCES = ["cfp_kernels.cu", "cfp_minplus.cu", "cfp_mem.cu", "cfp_dense.cu", "cfp_host.cu"]
+SOURCES = ["cfp_kernels.cu", "cfp_minplus.cu", "cfp_mem.cu", "cfp_dense.cu", "cfp_profile.cu", "cfp_host.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

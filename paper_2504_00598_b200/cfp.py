@@ -73,6 +73,12 @@ class cfp_mem_model(C.Structure):
     _fields_ = [("quantum", C.c_uint64), ("mem_limit", C.c_uint64), ("type_mem", P(P(C.c_uint32)))]
 
 
+class cfp_budget_result(C.Structure):
+    _fields_ = [("tasks", C.c_uint64), ("pruned", C.c_uint64), ("infeasible", C.c_uint64),
+                ("spent_lo", C.c_uint64), ("spent_hi", C.c_uint64), ("full_lo", C.c_uint64),
+                ("full_hi", C.c_uint64), ("best", C.c_uint64), ("best_index", C.c_uint64)]
+
+
 class cfp_ctx_opts(C.Structure):
     _fields_ = [("device", C.c_int32), ("cuda_stream", C.c_void_p), ("world", C.c_int32),
                 ("rank", C.c_int32), ("nccl_unique_id", C.c_void_p)]
@@ -94,7 +100,8 @@ EXPORTS = ["cfp_ctx_create", "cfp_ctx_destroy", "cfp_last_error", "cfp_nccl_uniq
            "cfp_mem_execute", "cfp_mem_fetch_plan", "cfp_mem_free", "cfp_mem_time_kernels",
            "cfp_mem_kernel_ms", "cfp_mem_fold_ops", "cfp_dense_fill", "cfp_search_plan_dense",
            "cfp_segment_costs_dense", "cfp_dense_prepare", "cfp_dense_execute", "cfp_dense_fetch_plan",
-           "cfp_dense_free", "cfp_dense_time_kernels", "cfp_dense_kernel_ms"]
+           "cfp_dense_free", "cfp_dense_time_kernels", "cfp_dense_kernel_ms", "cfp_profile_space",
+           "cfp_profile_budget"]
 
 _lib = None
 
@@ -162,6 +169,9 @@ def lib() -> C.CDLL:
     L.cfp_dense_time_kernels.argtypes = [vp, C.c_int32]
     L.cfp_dense_kernel_ms.argtypes = [vp, P(C.c_double), P(C.c_double), P(C.c_double), P(C.c_double),
                                       P(C.c_int32)]
+    L.cfp_profile_space.argtypes = [P(cfp_problem), P(C.c_int64), P(C.c_int64), P(C.c_int64)]
+    L.cfp_profile_budget.argtypes = [vp, vp, C.c_uint64, C.c_uint32, C.c_uint32, P(cfp_budget_result),
+                                     P(C.c_double)]
     _lib = L
     return L
 
@@ -237,6 +247,18 @@ def _e(e):
 
 def _x(x):
     return (x.dst, x.table) if hasattr(x, "dst") else x
+
+
+def profile_space(prob) -> dict:
+    """Eq. 2 counts through the C-ABI (host arithmetic, no GPU):
+    whole-segment plans per type, reshard pairs per transition, total."""
+    m = _Marshal()
+    p = m.problem(prob)
+    tp = np.zeros(len(prob.types), np.int64)
+    xp = np.zeros(len(prob.transitions), np.int64)
+    tot = C.c_int64(0)
+    _check(lib().cfp_profile_space(C.byref(p), _p(tp, C.c_int64), _p(xp, C.c_int64), C.byref(tot)))
+    return dict(type_plans=[int(x) for x in tp], trans_pairs=[int(x) for x in xp], total=int(tot.value))
 
 
 @dataclass
@@ -435,6 +457,21 @@ class Context:
 
     def prepare_dense(self, prob, w_ptrs) -> "PreparedDense":
         return PreparedDense(self, prob, w_ptrs)
+
+    # -- dynamic profiling budget (NEXT-3); W is a device pointer (int)
+    def profile_budget(self, w_ptr: int, n: int, num: int, den: int, timed: bool = False):
+        """Budgeted profiling of one type's dense table in index order; returns
+        a dict (tasks, pruned, infeasible, spent, full, best, best_index) and,
+        with timed=True, also the device ms of the call's kernels."""
+        r = cfp_budget_result()
+        ms = C.c_double(0.0)
+        _check(lib().cfp_profile_budget(self._h, C.c_void_p(w_ptr) if w_ptr else None, int(n), int(num),
+                                        int(den), C.byref(r), C.byref(ms) if timed else None))
+        out = dict(tasks=int(r.tasks), pruned=int(r.pruned), infeasible=int(r.infeasible),
+                   spent=(int(r.spent_hi) << 64) | int(r.spent_lo),
+                   full=(int(r.full_hi) << 64) | int(r.full_lo),
+                   best=int(r.best), best_index=int(r.best_index))
+        return (out, ms.value) if timed else out
 
     def minplus_bench(self, S: int, wide: bool = False, argk: bool = False, iters: int = 5):
         """(ms per launch, add+min ops per second) of an S^3 (min,+) product."""

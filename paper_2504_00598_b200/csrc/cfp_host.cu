@@ -1383,6 +1383,16 @@ template <> constexpr uint64_t VTcap<uint64_t>() { return kCap64; }
 template <typename V>
 static cfp_status run_type_kernels(cfp_prepared* P, TypeExec& te, cudaStream_t st, bool first_of_prec) {
   (void)first_of_prec;
+  static const bool dbg = getenv("CFP_DEBUG_ENUM") != nullptr;
+  if (dbg) {
+    const EnumParams& e = te.ep;
+    fprintf(stderr, "enum: P=%d W=%lld G=%lld NB=%d VG=%d nM=%lld na=%d nb=%d staged=%d ymerge=%d MS=%d "
+            "CH=%d full_a=%d ntau=%d smem=%zu epi=%d\n", e.P, (long long)e.W, (long long)e.G, te.NB, e.VG,
+            (long long)e.nM, e.na, e.nb, e.staged, e.ymerge, e.MS, e.CH,
+            (int)(sizeof(V) == 4 && e.MS == 1 && e.staged && e.ymerge && e.na == te.NB &&
+                  (te.NB == 23 || te.NB == 24) && !e.no_full_a),
+            e.ntau, te.smem, e.smem_epi);
+  }
   CUDA_TRY(launch_enum<V>(te.ep, te.NB, te.nthreads, te.smem, st));
   P->launches += 1;
   return CFP_OK;
@@ -2023,3 +2033,6 @@ extern "C" cfp_status cfp_intpipe_bench(cfp_ctx* ctx, int32_t op, int32_t iters,
 
 // dense per-plan tables (NEXT-2)
 #include "cfp_dense_host.inc"
+
+// profiling space and dynamic profiling budget (NEXT-3)
+#include "cfp_profile_host.inc"

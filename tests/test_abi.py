@@ -79,3 +79,38 @@ def test_pack_rejects_overflow(cfp):
     with pytest.raises(cfp.CfpError) as ei:
         cfp.pack_keys(np.array([1 << 40], np.uint64), np.array([0], np.uint64), 33)
     assert ei.value.status == cfp.CFP_EOVERFLOW
+
+
+# ---------------------------------------------------------------- NEXT-3 counts
+# cfp_profile_space is host arithmetic behind the C-ABI: checked here (no GPU)
+# against the pinned oracle (tests/test_oracle_profiling.py).
+
+
+@pytest.mark.parametrize("cfg", ["C1", "C2", "C3", "C4", "C5"])
+def test_profile_space_configs(cfp, cfg):
+    from oracle import profiling as PR
+    from synth import make_config
+    p = make_config(cfg, 0, "shaped")
+    assert cfp.profile_space(p) == PR.profile_space(p)
+
+
+@pytest.mark.parametrize("seed", range(25))
+def test_profile_space_random(cfp, seed):
+    from oracle import profiling as PR
+    from synth import generators as G
+    p = G.tiny_random(9300 + seed, max_plans=None, max_n=4, max_k=5)
+    assert cfp.profile_space(p) == PR.profile_space(p)
+
+
+def test_profile_space_errors(cfp):
+    from synth import make_config
+    p = make_config("C2", 0, "shaped")
+    p.transitions[2].in_edges[0].dst = 9          # consumer block out of range
+    with pytest.raises(cfp.CfpError) as ei:
+        cfp.profile_space(p)
+    assert ei.value.status == cfp.CFP_EINVAL
+    p = make_config("C2", 0, "shaped")
+    p.transitions[1].pred_type = 7
+    with pytest.raises(cfp.CfpError) as ei:
+        cfp.profile_space(p)
+    assert ei.value.status == cfp.CFP_EINVAL
