@@ -304,7 +304,7 @@ def run_cfp(args, prob, rank, world, local_rank):
     ip_ops, ip_ms = ctx.intpipe_bench(0, 4000)
     traffic = None
     try:
-        with open(os.path.join(ROOT, "profiles", "r01_ncu_enum.json")) as fh:
+        with open(os.path.join(ROOT, "profiles", "r01_ncu_enum_v7.json")) as fh:
             traffic = json.load(fh)["traffic_bytes_per_launch"]["enum_kernel"]
     except Exception:
         pass
@@ -342,7 +342,7 @@ def run_cfp(args, prob, rank, world, local_rank):
                                  "peak = 64 lane-ops/clk/SM x 148 SMs x 1965 MHz (derived, DESIGN.md); "
                                  "achieved = combos / device time of the enumeration phase (all enum "
                                  "launches incl. the cross-term fold epilogue); traffic = DRAM bytes per "
-                                 "enum launch from ncu (profiles/r01_ncu_enum.json), algorithmic bytes ~0"},
+                                 "enum launch from ncu (profiles/r01_ncu_enum_v7.json), algorithmic bytes ~0"},
             "intpipe_measured": {"op": "VIADDMNMX.U32", "lane_ops_per_s": ip_ops,
                                  "lane_ops_per_clk_per_sm": ip_ops / (SMS * 1e6 * (clocks["sm_mhz"] or 1965.0)),
                                  "frac_of_derived_peak": ip_ops / (peak * 1e9)},
@@ -581,6 +581,12 @@ def run_cfp_budget(args, rank, world, local_rank):
     peak, peak_src = hbm_peak_gbs()
     achieved = ns[big] * 4 / (kb * 1e-3) / 1e9
     pruned = sum(r["pruned"] for r in ref.values())
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "r01_ncu_budget.json")) as fh:
+            traffic = json.load(fh)["traffic_bytes_per_launch"]["budget_kernel"]
+    except Exception:
+        pass
     out = {
         "metric": "budgeted profiling tasks screened/sec (dense per-plan tables, NEXT-3)",
         "value": tasks / (ms * 1e-3), "unit": "tasks/s", "n_gpus": 1, "steps": args.steps,
@@ -597,9 +603,11 @@ def run_cfp_budget(args, rank, world, local_rank):
                 "note": "tables are device-resident inputs (tens of GB); e2e = host wall time of the calls"},
         "gpu_launches": len(used),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": None,
+                     "frac": achieved / peak, "traffic": traffic,
                      "note": f"budget_kernel on the largest type ({ns[big]} tasks): 4 B read per task "
-                             f"(algorithmic) / device time of the call; peak: {peak_src}"},
+                             f"(algorithmic, {ns[big] * 4} B per launch) / device time of the call; "
+                             f"traffic = DRAM bytes of that launch (profiles/r01_ncu_budget.json); "
+                             f"peak: {peak_src}"},
         "clocks": clocks,
     }
     if not args.no_cpu_baseline:

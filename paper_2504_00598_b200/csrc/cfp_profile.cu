@@ -9,13 +9,14 @@
 //    pruned  = W[i] finite, best_i finite, W[i] > thr_i  (== W*den > best*num)
 //    spent  += pruned ? thr_i : (W[i] finite ? W[i] : 0)
 //
-// One pass over HBM (4 bytes per task): a persistent grid takes 4096-element
-// tiles in index order from a ticket counter; each tile scans its minima
-// with warp shuffles and obtains the minimum of every earlier tile by a
-// decoupled look-back over per-tile status words (aggregate published before
-// the look-back, inclusive prefix after it), so no second pass re-reads W.
+// HBM sees each task once: a persistent grid takes 32768-task slices (128 KB)
+// in index order from a ticket counter; pass 1 streams the slice from HBM for
+// its minimum (published at once), a decoupled look-back over the earlier
+// slices' status words (aggregate published before the look-back, inclusive
+// prefix after it) gives the minimum of everything before the slice, and pass
+// 2 re-reads the slice from L2 for the per-task decisions.
 // The exclusive minimum changes only at a strict new best (rare): the
-// division for thr runs there, every other task costs a compare and adds.
+// division for thr runs there, every other task costs a few ops.
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -74,7 +75,9 @@ __device__ __forceinline__ void budget_load(const BudgetParams& p, uint64_t tbas
   }
 }
 
-// A CTA takes a slice of kBudSlice tasks (ticket order) and reads it twice:
+// A CTA takes a slice of kBudSlice tasks (ticket order) and reads it twice
+// (16 loads of 16 bytes in flight per thread in pass 1; pass 2 prefetches
+// the next tile):
 // pass 1 streams it from HBM for its minimum (published at once for the
 // look-back of later slices), pass 2 re-reads it -- still L2-resident: the
 // slices in flight total <= grid x 128 KB -- for the per-task decisions.
@@ -104,12 +107,12 @@ __global__ void __launch_bounds__(kBudThreads, 3) budget_kernel(const BudgetPara
     if (send - sbase == (uint64_t)kBudSlice) {
       const uint4* q = reinterpret_cast<const uint4*>(p.W + sbase);
 #pragma unroll
-      for (int i0 = 0; i0 < kBudSlice / 4 / kBudThreads; i0 += 8) {
-        uint4 x[8];
+      for (int i0 = 0; i0 < kBudSlice / 4 / kBudThreads; i0 += 16) {
+        uint4 x[16];
 #pragma unroll
-        for (int i = 0; i < 8; ++i) x[i] = q[(i0 + i) * kBudThreads + tid];
+        for (int i = 0; i < 16; ++i) x[i] = q[(i0 + i) * kBudThreads + tid];
 #pragma unroll
-        for (int i = 0; i < 8; ++i) m = min(m, min(min(x[i].x, x[i].y), min(x[i].z, x[i].w)));
+        for (int i = 0; i < 16; ++i) m = min(m, min(min(x[i].x, x[i].y), min(x[i].z, x[i].w)));
       }
     } else {
       for (uint64_t i = sbase + tid; i < send; i += kBudThreads) m = min(m, p.W[i]);
@@ -157,9 +160,13 @@ __global__ void __launch_bounds__(kBudThreads, 3) budget_kernel(const BudgetPara
     __syncthreads();
     uint32_t slice_run = s_excl;                       // every task before the current tile
     // ---- pass 2: per-task decisions, tile by tile (L2 re-read)
+    uint32_t vn[16];
+    budget_load(p, sbase, warp, lane, vn);
     for (uint64_t tbase = sbase; tbase < send; tbase += kBudTile) {
       uint32_t v[16];
-      budget_load(p, tbase, warp, lane, v);
+#pragma unroll
+      for (int k = 0; k < 16; ++k) v[k] = vn[k];
+      if (tbase + kBudTile < send) budget_load(p, tbase + kBudTile, warp, lane, vn);   // prefetch
       const uint64_t base = tbase + (uint64_t)warp * 512 + (uint64_t)lane * 16;
       uint32_t lmin = v[0];
 #pragma unroll

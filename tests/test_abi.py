@@ -103,13 +103,15 @@ def test_profile_space_random(cfp, seed):
 
 
 def test_profile_space_errors(cfp):
+    import copy
+
     from synth import make_config
-    p = make_config("C2", 0, "shaped")
+    p = copy.deepcopy(make_config("C2", 0, "shaped"))   # make_config caches: never mutate its result
     p.transitions[2].in_edges[0].dst = 9          # consumer block out of range
     with pytest.raises(cfp.CfpError) as ei:
         cfp.profile_space(p)
     assert ei.value.status == cfp.CFP_EINVAL
-    p = make_config("C2", 0, "shaped")
+    p = copy.deepcopy(make_config("C2", 0, "shaped"))
     p.transitions[1].pred_type = 7
     with pytest.raises(cfp.CfpError) as ei:
         cfp.profile_space(p)
