@@ -121,7 +121,11 @@ typedef struct {
                                 * process): no collective; cfp_segment_costs returns this
                                 * rank's shard-local (cost, least index) per bucket, whose
                                 * lexicographic min over ranks is the world-1 result;
-                                * cfp_search_plan / cfp_prepare are rejected (EINVAL). */
+                                * cfp_search_plan / cfp_prepare are rejected (EINVAL).
+                                * world == 1 with an id: a one-rank communicator; the
+                                * sharded path (rank-local tables, NCCL min-all-reduce
+                                * merge) runs on one GPU with results identical to
+                                * world == 1 without an id. */
 } cfp_ctx_opts;
 
 typedef struct cfp_ctx cfp_ctx;

@@ -299,7 +299,7 @@ class Context:
         L = lib()
         self._h = C.c_void_p()
         uid = None
-        if world > 1 and nccl_unique_id is not None:     # None: shard simulation (cfp.h)
+        if nccl_unique_id is not None:     # world > 1 without one: shard simulation (cfp.h)
             if len(nccl_unique_id) != 128:
                 raise CfpError(CFP_EINVAL, "the nccl unique id has 128 bytes")
             uid = C.create_string_buffer(bytes(nccl_unique_id), 128)

@@ -84,6 +84,7 @@ struct cfp_ctx {
   ncclComm_t comm = nullptr;
   int sms = 148;
   bool sim = false;                 // world > 1 without a communicator: shard simulation (test hook)
+  bool sharded = false;             // rank-local tables + merge path (world > 1, or a 1-rank communicator)
   bool no_full_a = false;           // CFP_ENUM_FULL_A=0: runtime-length A loop only (A/B tests)
   int64_t msplit_min_m = 128;       // M split when nM >= this (CFP_ENUM_MSPLIT_MIN_M; tests force 2)
   // side streams for concurrent per-type enumerations (fork/join by events):
@@ -147,10 +148,14 @@ extern "C" cfp_status cfp_ctx_create(cfp_ctx** out, const cfp_ctx_opts* opts) {
   }
   if (c->world > 1 && !opts->nccl_unique_id) {
     c->sim = true;                  // single-process shard simulation: no collective
-  } else if (c->world > 1) {
+    c->sharded = true;
+  } else if (opts && opts->nccl_unique_id) {
+    // world > 1: one rank per GPU; world == 1 with an id: a one-rank
+    // communicator, so the merge path and its NCCL calls run on one GPU
     ncclUniqueId id;
     memcpy(&id, opts->nccl_unique_id, sizeof(id));
     NCCL_TRY(ncclCommInitRank(&c->comm, c->world, id, c->rank));
+    c->sharded = true;
   }
   *out = c.release();
   return CFP_OK;
@@ -1199,8 +1204,8 @@ static cfp_status prepare_impl(cfp_ctx* ctx, const cfp_problem* p, bool do_chain
   P->ai = ai;
   uint64_t* outA = P->outAI.as<uint64_t>();
   uint64_t* outI = outA + ai;
-  uint64_t* argA = ctx->world > 1 ? P->locAI.as<uint64_t>() : outA;
-  uint64_t* argI = ctx->world > 1 ? P->locAI.as<uint64_t>() + ai : outI;
+  uint64_t* argA = ctx->sharded ? P->locAI.as<uint64_t>() : outA;
+  uint64_t* argI = ctx->sharded ? P->locAI.as<uint64_t>() + ai : outI;
   // rebase pointers
   for (TypeExec& te : P->types) {
     if (te.empty) continue;
@@ -1460,7 +1465,7 @@ static cfp_status execute_impl(cfp_ctx* ctx, cfp_prepared* P) {
   // outputs default to (INF, NOIDX): covers pruned output strategies, empty types
   CUDA_TRY(launch_fill<uint64_t>(outA, ai * 2, kInf64, st));
   P->launches++;
-  if (ctx->world > 1) {
+  if (ctx->sharded) {
     CUDA_TRY(launch_fill<uint64_t>(P->locAI.as<uint64_t>(), ai * 2, kInf64, st));
     P->launches++;
   }
@@ -1469,7 +1474,7 @@ static cfp_status execute_impl(cfp_ctx* ctx, cfp_prepared* P) {
   // a1: bucket minima A (values)
   if (P->has32) { CUDA_TRY(launch_amin<uint32_t>(aps, P->pair_off.as<int64_t>(), nslot, P->npairs, st)); P->launches++; }
   if (P->has64) { CUDA_TRY(launch_amin<uint64_t>(aps, P->pair_off.as<int64_t>(), nslot, P->npairs, st)); P->launches++; }
-  if (ctx->world > 1) {
+  if (ctx->sharded) {
     // rank-local minima were written to locA by the argmin descriptors; amin wrote
     // them there too -- reduce into the global A (shard simulation: the local A)
     if (ctx->comm) NCCL_TRY(ncclAllReduce(P->locAI.p, outA, ai, ncclUint64, ncclMin, ctx->comm, st));
@@ -1498,7 +1503,7 @@ static cfp_status execute_impl(cfp_ctx* ctx, cfp_prepared* P) {
   if (P->has32) { CUDA_TRY(launch_argmin<uint32_t>(aps, list, count, grid, P->kmax_arg, P->tabn_max, st)); P->launches++; }
   if (P->has64) { CUDA_TRY(launch_argmin<uint64_t>(aps, list, count, grid, P->kmax_arg, P->tabn_max, st)); P->launches++; }
   // a2: merge across ranks
-  if (ctx->world > 1) TRY(merge_ranks(P, st));
+  if (ctx->sharded) TRY(merge_ranks(P, st));
   // a4 (+ a3 when the edge list is not used)
   if (P->do_chain) {
     if (!edges) CUDA_TRY(cudaMemsetAsync(P->status.p, 0, 4, st));

@@ -431,3 +431,39 @@ def test_msplit_large_config(ctx_ms, oracle_lib, cfg):
         tot += c
         u = O._digits(ty.radix, int(got.seg_index[n]))[ty.out_block]
     assert tot == got.total_ns
+
+
+# ---------------------------------------------------------------- NCCL merge path
+# A ctx with world = 1 and an ncclUniqueId builds a one-rank communicator and
+# runs the sharded path (rank-local tables, ncclAllReduce(ncclMin) of the
+# bucket minima, masked least indices, second ncclAllReduce) on one GPU.
+
+
+@pytest.fixture(scope="module")
+def ctx_nccl():
+    from paper_2504_00598_b200 import build as B
+    B.build()
+    from paper_2504_00598_b200 import cfp
+    c = cfp.Context(device=0, world=1, rank=0, nccl_unique_id=cfp.nccl_unique_id())
+    yield c
+    c.close()
+
+
+@pytest.mark.parametrize("seed", range(8))
+def test_nccl_one_rank_tables_and_plans(ctx_nccl, oracle_lib, seed):
+    O = oracle_lib
+    p = G.tiny_random(7300 + seed, mode=("ties", "random")[seed % 2], max_plans=None, max_n=3,
+                      max_k=5, max_d=5, max_edges=5, p_inf=0.03)
+    for tr_id, tr in enumerate(p.transitions):
+        A0, I0 = O.segment_table(p, tr_id)
+        A, I = ctx_nccl.segment_costs(p.types[tr.type], tr, p.d_in(tr_id))
+        assert np.array_equal(A, A0) and np.array_equal(I, I0), (seed, tr_id)
+    _search_or_infeasible(ctx_nccl, oracle_lib, p)
+
+
+@pytest.mark.parametrize("cfg", ["C2", "C3", "C5"])
+def test_nccl_one_rank_configs(ctx, ctx_nccl, cfg):
+    p = G.make_config(cfg, seed=0, dist="shaped")
+    a, b = ctx.search_plan(p), ctx_nccl.search_plan(p)
+    assert a.total_ns == b.total_ns
+    assert a.seg_index.tolist() == b.seg_index.tolist() and a.seg_ns.tolist() == b.seg_ns.tolist()
