@@ -86,6 +86,7 @@ struct cfp_ctx {
   int sms = 148;
   bool sim = false;                 // world > 1 without a communicator: shard simulation (test hook)
   bool sharded = false;             // rank-local tables + merge path (world > 1, or a 1-rank communicator)
+  bool dedup = true;                // CFP_DEDUP=0: fold identical transitions separately (A/B tests)
   bool no_full_a = false;           // CFP_ENUM_FULL_A=0: runtime-length A loop only (A/B tests)
   int64_t msplit_min_m = 128;       // M split when nM >= this (CFP_ENUM_MSPLIT_MIN_M; tests force 2)
   // side streams for concurrent per-type enumerations (fork/join by events):
@@ -129,6 +130,7 @@ extern "C" cfp_status cfp_ctx_create(cfp_ctx** out, const cfp_ctx_opts* opts) {
                                std::to_string(prop.major) + std::to_string(prop.minor));
   c->sms = prop.multiProcessorCount;
   if (const char* fa = getenv("CFP_ENUM_FULL_A")) c->no_full_a = atoi(fa) == 0;
+  if (const char* dd = getenv("CFP_DEDUP")) c->dedup = atoi(dd) != 0;
   if (const char* ms = getenv("CFP_ENUM_MSPLIT_MIN_M")) c->msplit_min_m = std::max(2LL, atoll(ms));
   if (opts && opts->cuda_stream) {
     c->stream = (cudaStream_t)opts->cuda_stream;
@@ -744,6 +746,37 @@ static cfp_status prepare_impl(cfp_ctx* ctx, const cfp_problem* p, bool do_chain
   P->N = p->num_instances;
   P->inst.assign(p->inst_transition, p->inst_transition + P->N);
   const int world = ctx->world, rank = ctx->rank;
+  // ---- identical transitions.  Two used transitions into the same type with
+  // the same predecessor output strategies (radix and feasible set), the same
+  // consumer blocks and byte-identical cross tables have identical segment
+  // tables (A, I): instances of the later one use the first, which alone is
+  // folded (C3/C5: L1 -> L and L -> L carry the same reshard profiles).
+  if (ctx->dedup) {
+    auto out_keep = [&](int pred) {
+      return pred < 0 ? std::vector<int>{0} : T[pred].keep[T[pred].o];
+    };
+    std::vector<int> canon(X.size());
+    for (int x = 0; x < (int)X.size(); ++x) {
+      canon[x] = x;
+      if (!X[x].used) continue;
+      for (int y = 0; y < x; ++y) {
+        const HostTrans& a = X[x];
+        const HostTrans& c = X[y];
+        if (!c.used || canon[y] != y || a.type != c.type || a.Din != c.Din || a.X != c.X || a.xdst != c.xdst)
+          continue;
+        if (out_keep(a.pred) != out_keep(c.pred)) continue;
+        bool same = true;
+        for (int q = 0; q < a.X && same; ++q) {
+          const int64_t n = (int64_t)a.Din * T[a.type].radix[a.xdst[q]];
+          same = std::equal(b.raw.begin() + a.x_off[q], b.raw.begin() + a.x_off[q] + n, b.raw.begin() + c.x_off[q]);
+        }
+        if (same) { canon[x] = y; break; }
+      }
+    }
+    for (int& t : P->inst) t = canon[t];
+    for (int x = 0; x < (int)X.size(); ++x)
+      if (canon[x] != x) X[x].used = false;
+  }
 
   // ---- chain overflow guard: sum over instances of the finite bound < 2^63
   {

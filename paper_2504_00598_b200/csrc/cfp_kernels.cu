@@ -520,7 +520,28 @@ __global__ void __launch_bounds__(kBlock, 4) enum_kernel(const EnumParams p) {
       // one contiguous row Q_i^T[s_i(p)][0..DinP) of the transposed copy, read
       // 16 bytes at a time and accumulated in the thread's Xs row.
       V* xrow = Xs + slot * DinP;
-      for (int i = 0; half == 0 && i < et.nq; ++i) {
+      constexpr int DPC = (NB + 3) & ~3;            // compile-time row length (D_in = D_o of a layer chain)
+      const bool fastx = NA > 0 && DinP == DPC && pg < 0x7FFFFFFF;
+      if (fastx && half == 0 && et.nq > 0) {
+        // the whole row in registers: per term its DPC / VN 16-byte loads are
+        // issued together (one L1/L2 round trip per term, not one per vector)
+        V xa[DPC];
+#pragma unroll
+        for (int k2 = 0; k2 < DPC; ++k2) xa[k2] = live ? (V)0 : T::CAP;
+        for (int i = 0; i < et.nq; ++i) {
+          const int a = et.q[i].a;
+          const int dig = (int)(((uint32_t)pg / (uint32_t)p.pre_stride[a]) % (uint32_t)p.pre_radix[a]);
+          const V* qr = vals + et.qt[i] + dig * DPC;
+          V y[DPC];
+#pragma unroll
+          for (int u0 = 0; u0 < DPC; u0 += VN) load_vec<V>(qr + u0, y + u0);
+#pragma unroll
+          for (int k2 = 0; k2 < DPC; ++k2) xa[k2] = T::sat(xa[k2], y[k2]);
+        }
+#pragma unroll
+        for (int u0 = 0; u0 < DPC; u0 += VN) store_vec<V>(xrow + u0, xa + u0);
+      }
+      for (int i = 0; !fastx && half == 0 && i < et.nq; ++i) {
         const int a = et.q[i].a;
         const int dig = pg < 0x7FFFFFFF ? (int)(((uint32_t)pg / (uint32_t)p.pre_stride[a]) % (uint32_t)p.pre_radix[a])
                                         : (int)((pg / p.pre_stride[a]) % p.pre_radix[a]);

@@ -467,3 +467,54 @@ def test_nccl_one_rank_configs(ctx, ctx_nccl, cfg):
     a, b = ctx.search_plan(p), ctx_nccl.search_plan(p)
     assert a.total_ns == b.total_ns
     assert a.seg_index.tolist() == b.seg_index.tolist() and a.seg_ns.tolist() == b.seg_ns.tolist()
+
+
+# ---------------------------------------------------------------- transition dedup
+# Transitions into the same type with identical predecessor output strategies,
+# consumers and cross tables share one fold (C3/C5: L1 -> L and L -> L).
+
+
+@pytest.fixture(scope="module")
+def ctx_nodedup():
+    import os
+    from paper_2504_00598_b200 import build as B
+    B.build()
+    from paper_2504_00598_b200 import cfp
+    old = os.environ.get("CFP_DEDUP")
+    os.environ["CFP_DEDUP"] = "0"
+    try:
+        c = cfp.Context(device=0)
+    finally:
+        if old is None:
+            del os.environ["CFP_DEDUP"]
+        else:
+            os.environ["CFP_DEDUP"] = old
+    yield c
+    c.close()
+
+
+@pytest.mark.parametrize("cfg", ["C2", "C3", "C5"])
+def test_dedup_configs_equal_undeduplicated(ctx, ctx_nodedup, cfg):
+    p = G.make_config(cfg, seed=0, dist="shaped")
+    a, b = ctx.search_plan(p), ctx_nodedup.search_plan(p)
+    assert a.total_ns == b.total_ns
+    assert a.seg_index.tolist() == b.seg_index.tolist() and a.seg_ns.tolist() == b.seg_ns.tolist()
+
+
+@pytest.mark.parametrize("seed", range(10))
+def test_dedup_duplicated_transitions_random(ctx, oracle_lib, seed):
+    """A chain E -> T, T -> T whose T -> T copy is byte-identical to a second
+    transition from a different predecessor type with the same output radix."""
+    import copy
+    rng = np.random.default_rng(seed)
+    p = copy.deepcopy(G.tiny_random(7700 + seed, mode="random", max_plans=None, max_n=2, max_k=4,
+                                    max_d=4, max_edges=4, p_inf=0.0))
+    # make every transition into the same type with the same D_in share its
+    # first sibling's cross edges
+    first = {}
+    for tr_id, tr in enumerate(p.transitions):
+        key = (tr.type, p.d_in(tr_id))
+        if key in first and rng.random() < 0.8:
+            tr.in_edges = copy.deepcopy(p.transitions[first[key]].in_edges)
+        first.setdefault(key, tr_id)
+    _search_or_infeasible(ctx, oracle_lib, p)
