@@ -633,6 +633,40 @@ static cfp_status validate_and_model(const cfp_problem* p, std::vector<HostType>
   return CFP_OK;
 }
 
+// Identical transitions.  Two used transitions into the same type with the
+// same predecessor output strategies (radix and feasible set), the same
+// consumer blocks and byte-identical cross tables have identical segment
+// tables (A, I): instances of the later one are pointed at the first, and the
+// later one is marked unused (not folded).  C3/C5: L1 -> L and L -> L carry
+// the same reshard profiles.
+static void dedup_transitions(const std::vector<HostType>& T, std::vector<HostTrans>& X, const Builder& b,
+                              std::vector<int>& inst) {
+  auto out_keep = [&](int pred) {
+    return pred < 0 ? std::vector<int>{0} : T[pred].keep[T[pred].o];
+  };
+  std::vector<int> canon(X.size());
+  for (int x = 0; x < (int)X.size(); ++x) {
+    canon[x] = x;
+    if (!X[x].used) continue;
+    for (int y = 0; y < x; ++y) {
+      const HostTrans& a = X[x];
+      const HostTrans& c = X[y];
+      if (!c.used || canon[y] != y || a.type != c.type || a.Din != c.Din || a.X != c.X || a.xdst != c.xdst)
+        continue;
+      if (out_keep(a.pred) != out_keep(c.pred)) continue;
+      bool same = true;
+      for (int q = 0; q < a.X && same; ++q) {
+        const int64_t n = (int64_t)a.Din * T[a.type].radix[a.xdst[q]];
+        same = std::equal(b.raw.begin() + a.x_off[q], b.raw.begin() + a.x_off[q] + n, b.raw.begin() + c.x_off[q]);
+      }
+      if (same) { canon[x] = y; break; }
+    }
+  }
+  for (int& t : inst) t = canon[t];
+  for (int x = 0; x < (int)X.size(); ++x)
+    if (canon[x] != x) X[x].used = false;
+}
+
 // Derived-table spec over an ordered digit list.  `row_digits` trailing digits
 // form a row, padded to `row_pad` entries.
 static TableSpec make_spec(const std::vector<int>& digits, const std::vector<int>& radix_c,
@@ -746,37 +780,7 @@ static cfp_status prepare_impl(cfp_ctx* ctx, const cfp_problem* p, bool do_chain
   P->N = p->num_instances;
   P->inst.assign(p->inst_transition, p->inst_transition + P->N);
   const int world = ctx->world, rank = ctx->rank;
-  // ---- identical transitions.  Two used transitions into the same type with
-  // the same predecessor output strategies (radix and feasible set), the same
-  // consumer blocks and byte-identical cross tables have identical segment
-  // tables (A, I): instances of the later one use the first, which alone is
-  // folded (C3/C5: L1 -> L and L -> L carry the same reshard profiles).
-  if (ctx->dedup) {
-    auto out_keep = [&](int pred) {
-      return pred < 0 ? std::vector<int>{0} : T[pred].keep[T[pred].o];
-    };
-    std::vector<int> canon(X.size());
-    for (int x = 0; x < (int)X.size(); ++x) {
-      canon[x] = x;
-      if (!X[x].used) continue;
-      for (int y = 0; y < x; ++y) {
-        const HostTrans& a = X[x];
-        const HostTrans& c = X[y];
-        if (!c.used || canon[y] != y || a.type != c.type || a.Din != c.Din || a.X != c.X || a.xdst != c.xdst)
-          continue;
-        if (out_keep(a.pred) != out_keep(c.pred)) continue;
-        bool same = true;
-        for (int q = 0; q < a.X && same; ++q) {
-          const int64_t n = (int64_t)a.Din * T[a.type].radix[a.xdst[q]];
-          same = std::equal(b.raw.begin() + a.x_off[q], b.raw.begin() + a.x_off[q] + n, b.raw.begin() + c.x_off[q]);
-        }
-        if (same) { canon[x] = y; break; }
-      }
-    }
-    for (int& t : P->inst) t = canon[t];
-    for (int x = 0; x < (int)X.size(); ++x)
-      if (canon[x] != x) X[x].used = false;
-  }
+  if (ctx->dedup) dedup_transitions(T, X, b, P->inst);
 
   // ---- chain overflow guard: sum over instances of the finite bound < 2^63
   {
