@@ -332,14 +332,33 @@ __global__ void __launch_bounds__(kBlock, 4) enum_kernel(const EnumParams p) {
     V* ys = xs + p.xspan;
     V* zs = ys + p.yspan;
     int4* ms = reinterpret_cast<int4*>(zs + ((p.zspan + 3) & ~3LL));
-    for (int64_t e = tid * VN; e < p.xspan; e += kBlock * VN)
-      *reinterpret_cast<typename Vec4<V>::T*>(xs + e) =
-          *reinterpret_cast<const typename Vec4<V>::T*>(XT + sx + e);
-    for (int64_t e = tid * VN; e < p.yspan; e += kBlock * VN)
-      *reinterpret_cast<typename Vec4<V>::T*>(ys + e) =
-          *reinterpret_cast<const typename Vec4<V>::T*>(YT + sy + e);
+    // the CTA's X and Y slices and the M table arrive by TMA bulk copies
+    // (one thread issues, an mbarrier counts the bytes); Z (a few values,
+    // any alignment) by plain loads meanwhile
+    __shared__ __align__(8) uint64_t sbar;
+    const bool tma = p.xspan % VN == 0 && p.yspan % VN == 0 &&
+                     ((reinterpret_cast<uintptr_t>(XT + sx) | reinterpret_cast<uintptr_t>(YT + sy)) & 15) == 0;
+    if (tma) {
+      if (tid == 0) {
+        const uint32_t xb = (uint32_t)(p.xspan * sizeof(V)), yb = (uint32_t)(p.yspan * sizeof(V));
+        const uint32_t mb = (uint32_t)(p.nM * sizeof(int4));
+        mbar_init(&sbar, 1);
+        mbar_expect_tx(&sbar, xb + yb + mb);
+        tma_bulk_g2s(xs, XT + sx, xb, &sbar);
+        tma_bulk_g2s(ys, YT + sy, yb, &sbar);
+        tma_bulk_g2s(ms, MT, mb, &sbar);
+      }
+    } else {
+      for (int64_t e = tid * VN; e < p.xspan; e += kBlock * VN)
+        *reinterpret_cast<typename Vec4<V>::T*>(xs + e) =
+            *reinterpret_cast<const typename Vec4<V>::T*>(XT + sx + e);
+      for (int64_t e = tid * VN; e < p.yspan; e += kBlock * VN)
+        *reinterpret_cast<typename Vec4<V>::T*>(ys + e) =
+            *reinterpret_cast<const typename Vec4<V>::T*>(YT + sy + e);
+      for (int64_t e = tid; e < p.nM; e += kBlock) ms[e] = MT[e];
+    }
     for (int64_t e = tid; e < p.zspan; e += kBlock) zs[e] = ZT[sz + e];
-    for (int64_t e = tid; e < p.nM; e += kBlock) ms[e] = MT[e];
+    if (tma && tid == 0) mbar_wait(&sbar, 0);       // the barrier below releases everyone after it
     __syncthreads();
     XT = xs; YT = ys; ZT = zs; MT = ms;
     sx = sy = sz = 0;
@@ -1411,7 +1430,7 @@ cudaError_t launch_enum_nb(const EnumParams& p, int64_t nthreads, size_t smem, c
   if (blocks <= 0) return cudaSuccess;
   const size_t sm = std::max(smem, (size_t)p.smem_epi);
   auto launch = [&](auto kern) -> cudaError_t {
-    if (sm > 48 * 1024) {
+    if (sm > 40 * 1024) {                          // opt in above the 48 KB default (static smem counts too)
       cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
       if (e != cudaSuccess) return e;
     }
