@@ -1112,41 +1112,36 @@ __global__ void __launch_bounds__(1024) chain_kernel(const ChainParams cp) {
   }
   if (cp.mode == 1 && SM && cp.smax <= 32) {
     // optimal edges reachable from u_1 = 0, for <= 32 states per instance:
-    // (1) every (n, u) in parallel: om = {v : A_n[u][v] + G_n(v) = G_{n-1}(u)};
-    // (2) one thread walks the instances: reach_{n+1} = OR_{u in reach_n} om(n, u);
-    // (3) every (n, u) in parallel: emit the reachable optimal edges (deduplicated).
+    // (1) warp 0 walks the instances; for each reachable state u its optimal
+    //     successors om = {v : A_n[u][v] + G_n(v) = G_{n-1}(u)} by one ballot
+    //     (lanes = v), reach_{n+1} = OR of them -- only reachable rows are
+    //     evaluated (usually one per instance);
+    // (2) every (n, u) in parallel: emit the reachable optimal edges (deduplicated).
     __syncthreads();
     mark();
     __shared__ int s_cnt2;
     if (tid == 0) s_cnt2 = 0;
-    const int64_t nrow = goff[N];
-    {
-      const int warp = tid >> 5, lane = tid & 31, nw = nth >> 5;
-      for (int n = warp; n < N; n += nw) {             // warp per instance, lanes over v
-        const int rows = rows_of(n), cols = cols_of(n);
-        const uint64_t* Gn = G + goff[n + 1];
-        const uint64_t gv = lane < cols ? Gn[lane] : kInf64;
-        for (int u = 0; u < rows; ++u) {
-          const uint64_t target = G[goff[n] + u];
-          const uint64_t a = lane < cols ? matA(n)[(int64_t)u * cols + lane] : kInf64;
-          const uint32_t m = __ballot_sync(0xffffffffu, target != kInf64 && a != kInf64 && gv != kInf64 &&
-                                                            a + gv == target);
-          if (lane == 0) om[goff[n] + u] = m;
-        }
-      }
-    }
-    for (int64_t w = tid; w < nrow; w += nth) cp.reach[w] = 0;
-    __syncthreads();
+    for (int64_t w = tid; w < goff[N]; w += nth) cp.reach[w] = 0;
     mark();
-    if (tid == 0) {
+    if (tid < 32) {
+      const int lane = tid;
       uint32_t r = G[0] == kInf64 ? 0u : 1u;
       for (int n = 0; n < N; ++n) {
-        rmask[n] = r;
+        if (lane == 0) rmask[n] = r;
+        const int cols = cols_of(n);
+        const int64_t g0 = goff[n];
+        const uint64_t gv = lane < cols ? G[goff[n + 1] + lane] : kInf64;
+        const uint64_t* An = matA(n);
         uint32_t nx = 0, rr = r;
         while (rr) {
           const int u = __ffs(rr) - 1;
           rr &= rr - 1;
-          nx |= om[goff[n] + u];
+          const uint64_t target = G[g0 + u];
+          const uint64_t a = lane < cols ? An[(int64_t)u * cols + lane] : kInf64;
+          const uint32_t m = __ballot_sync(0xffffffffu, target != kInf64 && a != kInf64 && gv != kInf64 &&
+                                                          a + gv == target);
+          if (lane == 0) om[g0 + u] = m;
+          nx |= m;
         }
         r = nx;
       }
