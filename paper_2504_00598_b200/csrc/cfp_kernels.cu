@@ -726,7 +726,14 @@ __device__ void argmin_pair(const ArgminParams& ap, const int pair, unsigned cha
   const int K = e.K, P = e.P, o = e.o, nterm = e.nterm, nq = f.nq;
   uint16_t* sd = reinterpret_cast<uint16_t*>(smem_raw);        // [K][NT] digits
   V* tabs = reinterpret_cast<V*>(smem_raw + (((size_t)K * NT * 2 + 15) & ~(size_t)15));   // W/R tables
-  for (int i = tid; i < e.tab_n; i += NT) tabs[i] = vals[e.tab_lo + i];
+  for (int i0 = tid; i0 < e.tab_n; i0 += NT * 8) {   // 8 loads in flight per thread
+    V t8[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) t8[k] = i0 + k * NT < e.tab_n ? vals[e.tab_lo + i0 + k * NT] : (V)0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k)
+      if (i0 + k * NT < e.tab_n) tabs[i0 + k * NT] = t8[k];
+  }
   const int u = pair / Do, v = pair - (pair / Do) * Do;
   const int64_t outi = (int64_t)u * ap.Do_orig + ap.vmap[v];
   // 1. the bucket minimum is the (merged) A computed by amin_kernel
