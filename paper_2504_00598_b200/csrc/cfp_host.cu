@@ -86,6 +86,7 @@ struct cfp_ctx {
   int sms = 148;
   bool sim = false;                 // world > 1 without a communicator: shard simulation (test hook)
   bool sharded = false;             // rank-local tables + merge path (world > 1, or a 1-rank communicator)
+  bool mem_chain_fused = true;      // CFP_MEM_CHAIN_FUSED=0: one launch per DP step (A/B tests)
   bool dedup = true;                // CFP_DEDUP=0: fold identical transitions separately (A/B tests)
   bool no_full_a = false;           // CFP_ENUM_FULL_A=0: runtime-length A loop only (A/B tests)
   int64_t msplit_min_m = 128;       // M split when nM >= this (CFP_ENUM_MSPLIT_MIN_M; tests force 2)
@@ -131,6 +132,7 @@ extern "C" cfp_status cfp_ctx_create(cfp_ctx** out, const cfp_ctx_opts* opts) {
   c->sms = prop.multiProcessorCount;
   if (const char* fa = getenv("CFP_ENUM_FULL_A")) c->no_full_a = atoi(fa) == 0;
   if (const char* dd = getenv("CFP_DEDUP")) c->dedup = atoi(dd) != 0;
+  if (const char* mf = getenv("CFP_MEM_CHAIN_FUSED")) c->mem_chain_fused = atoi(mf) != 0;
   if (const char* ms = getenv("CFP_ENUM_MSPLIT_MIN_M")) c->msplit_min_m = std::max(2LL, atoll(ms));
   if (opts && opts->cuda_stream) {
     c->stream = (cudaStream_t)opts->cuda_stream;

@@ -347,6 +347,100 @@ __global__ void __launch_bounds__(256) mem_chain_kernel(const MemChainParams cp,
 }
 
 // --------------------------------------------------------------------------
+// All N backward DP steps in one persistent launch: the (row u, 64-column
+// block) tiles of instance n are spread over the co-resident CTAs (the same
+// arithmetic as mem_chain_kernel), then a grid barrier, then instance n - 1.
+// One launch instead of N (each step is a few microseconds of work).
+// --------------------------------------------------------------------------
+constexpr uint64_t kBig = (1ull << 63) - 1;   // kBig + kBig < 2^64: no wrap
+__device__ __forceinline__ uint64_t to_big(uint64_t x) { return x == kInf64 ? kBig : x; }
+
+__device__ __forceinline__ void mem_grid_sync(unsigned int* bar, unsigned int nblocks, unsigned int& gen) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    ++gen;
+    __threadfence();
+    const unsigned int arrived = atomicAdd(bar, 1u) + 1u;
+    if (arrived == nblocks * gen) {
+      atomicExch(bar + 1, gen);
+    } else {
+      while (*reinterpret_cast<volatile unsigned int*>(bar + 1) < gen) __nanosleep(64);
+    }
+    __threadfence();
+  } else {
+    ++gen;
+  }
+  __syncthreads();
+}
+
+__global__ void __launch_bounds__(256) mem_chain_all_kernel(const MemChainParams cp, size_t smem_bytes,
+                                                            unsigned int* bar) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  __shared__ uint64_t part[4][64];
+  uint64_t* arow = reinterpret_cast<uint64_t*>(smem_raw);
+  const int C = cp.C;
+  const int nblk = (C + 63) / 64;
+  unsigned int gen = 0;
+  for (int n = cp.N - 1; n >= 0; --n) {
+    const MemInst in = cp.inst[n];
+    const int rowlen = in.cols * in.nq;
+    int win = 64 + in.nq - 1;                       // as launch_mem_chain_step, against this launch's smem
+    if ((size_t)((rowlen + 1) & ~1) * 8 + (size_t)in.cols * win * 8 + 16 > smem_bytes) win = 0;
+    const uint64_t* Gn = cp.G + cp.goff[n + 1] * C;
+    for (int tile = blockIdx.x; tile < in.rows * nblk; tile += gridDim.x) {
+      const int u = tile / nblk;
+      const int c0 = (tile - u * nblk) * 64;
+      // staged with INF -> kBig = 2^63 - 1: finite sums stay below it (the
+      // EOVERFLOW guard bounds every plan total by 9.2e18), a + g never wraps
+      // (2 kBig < 2^64) and a sum >= kBig means INF -- the inner loop is a
+      // plain add and min
+      for (int e = threadIdx.x; e < rowlen; e += blockDim.x) arow[e] = to_big(in.Am[(int64_t)u * rowlen + e]);
+      uint64_t* gw = arow + ((rowlen + 1) & ~1);
+      if (win > 0)
+        for (int e = threadIdx.x; e < in.cols * win; e += blockDim.x) {
+          const int v = e / win, k = e - v * win;
+          const int cc = c0 + in.qlo + k;
+          gw[e] = cc < C ? to_big(Gn[(int64_t)v * C + cc]) : kBig;
+        }
+      __syncthreads();
+      const int cl = threadIdx.x & 63, vg = threadIdx.x >> 6;
+      const int c = c0 + cl;
+      uint64_t best = kBig;
+      if (c < C) {
+        const int qmax = min(in.nq, C - c - in.qlo);
+        for (int v = vg; v < in.cols; v += 4) {
+          const uint64_t* av = arow + v * in.nq;
+          if (win > 0) {
+            const uint64_t* gv = gw + v * win + cl;
+#pragma unroll 4
+            for (int qi = 0; qi < qmax; ++qi) {
+              const uint64_t s2 = av[qi] + gv[qi];
+              best = s2 < best ? s2 : best;
+            }
+          } else {
+            const uint64_t* gv = Gn + (int64_t)v * C + c + in.qlo;
+            for (int qi = 0; qi < qmax; ++qi) {
+              const uint64_t s2 = av[qi] + to_big(gv[qi]);
+              best = s2 < best ? s2 : best;
+            }
+          }
+        }
+      }
+      part[vg][cl] = best;
+      __syncthreads();
+      if (vg == 0 && c < C) {
+        uint64_t b = part[0][cl];
+#pragma unroll
+        for (int k = 1; k < 4; ++k) b = part[k][cl] < b ? part[k][cl] : b;
+        cp.G[(cp.goff[n] + u) * C + c] = b >= kBig ? kInf64 : b;
+      }
+      __syncthreads();                              // arow / gw / part reused by the next tile
+    }
+    if (n > 0) mem_grid_sync(bar, gridDim.x, gen);  // G_n complete before step n - 1 reads it
+  }
+}
+
+// --------------------------------------------------------------------------
 // Optimal edges reachable from (u, c) = (0, 0): single CTA, instance by
 // instance.  The reachable states of level n are listed (ballot compaction),
 // then every (state, v, q) candidate is checked in parallel; optimal ones set
@@ -646,6 +740,25 @@ cudaError_t launch_mem_chain_step(const MemChainParams& cp, int n, int rows, int
   }
   mem_chain_kernel<<<dim3((unsigned)rows, (unsigned)((cp.C + 63) / 64)), 256, smem, st>>>(cp, n, win);
   return cudaGetLastError();
+}
+// every step of the backward DP in one cooperative launch; bar: 2 zeroed words
+cudaError_t launch_mem_chain_all(const MemChainParams& cp, int max_rowlen, int max_cols, int max_nq, int max_rows,
+                                 unsigned int* bar, int sms, cudaStream_t st) {
+  size_t smem = (size_t)((max_rowlen + 1) & ~1) * 8 + (size_t)max_cols * (64 + max_nq - 1) * 8 + 16;
+  if (smem > 160 * 1024) smem = (size_t)((max_rowlen + 1) & ~1) * 8 + 16;   // windows off for the widest
+  cudaError_t e = cudaFuncSetAttribute(mem_chain_all_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  int per_sm = 0;
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, mem_chain_all_kernel, 256, smem);
+  if (e != cudaSuccess) return e;
+  if (per_sm < 1) return cudaErrorInvalidConfiguration;
+  const int tiles = max_rows * ((cp.C + 63) / 64);
+  int grid = std::min(sms * per_sm, tiles);
+  if (grid < 1) grid = 1;
+  e = cudaMemsetAsync(bar, 0, 8, st);
+  if (e != cudaSuccess) return e;
+  void* args[] = {const_cast<MemChainParams*>(&cp), &smem, &bar};
+  return cudaLaunchCooperativeKernel((void*)mem_chain_all_kernel, dim3((unsigned)grid), dim3(256), args, smem, st);
 }
 cudaError_t launch_mem_bfs(const MemChainParams& cp, uint32_t* reach, int32_t* slist, int64_t slist_cap,
                            cudaStream_t st) {
