@@ -448,29 +448,35 @@ __global__ void __launch_bounds__(256) mem_chain_all_kernel(const MemChainParams
 // reach bitsets are kept (reach + goff[n] * C bits) for the successor table.
 // --------------------------------------------------------------------------
 __global__ void __launch_bounds__(1024) mem_bfs_kernel(const MemChainParams cp, uint32_t* reach,
-                                                       int32_t* slist, int64_t slist_cap) {
+                                                       int32_t* slist, int64_t slist_cap, int maxw) {
+  // the current and next levels' reach bits live in shared memory (the
+  // global copy, for mem_succ_kernel, is written alongside)
+  extern __shared__ uint32_t sbits[];
+  uint32_t* cur = sbits;
+  uint32_t* nxt = sbits + maxw;
   __shared__ int s_n;
   const int C = cp.C;
   const int tid = threadIdx.x, nth = blockDim.x;
-  if (tid == 0 && cp.G[0] != kInf64) reach[0] = 1u;   // (u, c) = (0, 0) at level 0
+  for (int w = tid; w < maxw; w += nth) cur[w] = 0;
   __syncthreads();
+  if (tid == 0 && cp.G[0] != kInf64) { reach[0] = 1u; cur[0] = 1u; }   // (u, c) = (0, 0) at level 0
   for (int n = 0; n < cp.N; ++n) {
     const MemInst in = cp.inst[n];
     const int64_t base = cp.goff[n] * C, nbase = cp.goff[n + 1] * C;
-    const int64_t nstates = (int64_t)in.rows * C;
+    const int nw_cur = (int)(((int64_t)in.rows * C + 31) / 32);
+    const int nw_nxt = (int)(((int64_t)in.cols * C + 31) / 32);
+    for (int w = tid; w < nw_nxt; w += nth) nxt[w] = 0;
     if (tid == 0) s_n = 0;
     __syncthreads();
-    for (int64_t s0 = 0; s0 < nstates; s0 += nth) {  // list the reachable states
-      const int64_t s = s0 + tid;
-      const int64_t b = base + s;
-      const bool on = s < nstates && ((reach[b >> 5] >> (b & 31)) & 1u);
-      const unsigned m = __ballot_sync(0xffffffffu, on);
-      int wb = 0;
-      if ((tid & 31) == 0 && m) wb = atomicAdd(&s_n, __popc(m));
-      wb = __shfl_sync(0xffffffffu, wb, 0);
-      if (on) {
-        const int k = wb + __popc(m & ((1u << (tid & 31)) - 1u));
-        if (k < slist_cap) slist[k] = (int32_t)s;
+    for (int w = tid; w < nw_cur; w += nth) {          // list the reachable states, a word at a time
+      uint32_t m = cur[w];
+      if (!m) continue;
+      int k = atomicAdd(&s_n, __popc(m));
+      while (m) {
+        const int b = __ffs(m) - 1;
+        m &= m - 1;
+        if (k < slist_cap) slist[k] = w * 32 + b;
+        ++k;
       }
     }
     __syncthreads();
@@ -490,11 +496,14 @@ __global__ void __launch_bounds__(1024) mem_bfs_kernel(const MemChainParams cp, 
       const int64_t cell = ((int64_t)u * in.cols + v) * in.nq + qi;
       const uint64_t a = in.Am[cell], g = Gn[(int64_t)v * C + cc];
       if (a == kInf64 || g == kInf64 || a + g != Gp[s]) continue;
-      const int64_t t = nbase + (int64_t)v * C + cc;
+      const int tl = v * C + cc;
+      atomicOr(&nxt[tl >> 5], 1u << (tl & 31));
+      const int64_t t = nbase + tl;
       atomicOr(&reach[t >> 5], 1u << (t & 31));
       atomicOr(&need[cell >> 5], 1u << (cell & 31));
     }
     __syncthreads();
+    uint32_t* tmp = cur; cur = nxt; nxt = tmp;
   }
   // list the needed buckets
   for (int sl = 0; sl < cp.nslot; ++sl) {
@@ -761,8 +770,15 @@ cudaError_t launch_mem_chain_all(const MemChainParams& cp, int max_rowlen, int m
   return cudaLaunchCooperativeKernel((void*)mem_chain_all_kernel, dim3((unsigned)grid), dim3(256), args, smem, st);
 }
 cudaError_t launch_mem_bfs(const MemChainParams& cp, uint32_t* reach, int32_t* slist, int64_t slist_cap,
-                           cudaStream_t st) {
-  mem_bfs_kernel<<<1, 1024, 0, st>>>(cp, reach, slist, slist_cap);
+                           int max_dim, cudaStream_t st) {
+  const int maxw = (int)(((int64_t)max_dim * cp.C + 31) / 32);
+  const size_t smem = (size_t)maxw * 2 * 4;
+  if (smem > 200 * 1024) return cudaErrorInvalidValue;
+  if (smem > 40 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(mem_bfs_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+  }
+  mem_bfs_kernel<<<1, 1024, smem, st>>>(cp, reach, slist, slist_cap, maxw);
   return cudaGetLastError();
 }
 cudaError_t launch_mem_succ(const MemChainParams& cp, const uint32_t* reach, int32_t* succ, int64_t states,
