@@ -196,6 +196,14 @@ def flush_l2(torch, buf):
 
 
 # ---------------------------------------------------------------- arms
+def workload_name(args) -> str:
+    """The default arm's workload string (the reference arm reports the same)."""
+    if args.config == "C3":
+        return (f"{args.config}: LLaMA-7B-shaped graph, 2x4 target mesh, 34 segment instances, "
+                f"4 distinct types ({args.dist} tables, seed {args.seed})")
+    return f"{args.config} ({args.dist}, seed {args.seed})"
+
+
 def run_reference(args, prob, rank, world):
     if rank != 0:
         return None
@@ -217,7 +225,7 @@ def run_reference(args, prob, rank, world):
             "warmup": args.warmup, "ms_per_step": tot / args.steps * 1e3, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
             "impl": "reference",
-            "config": {"workload": f"{args.config} ({prob.name}) {args.dist} seed {args.seed}",
+            "config": {"workload": workload_name(args),
                        "combos_per_step": combos, "l2": "n/a (CPU oracle)"},
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle",
                              "sample": sample},
@@ -323,9 +331,7 @@ def run_cfp(args, prob, rank, world, local_rank):
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None,
             "dtype": "u64" if info.wide_types else "u32", "data": "synthetic",
-            "config": {"workload": f"{args.config}: LLaMA-7B-shaped graph, 2x4 target mesh, 34 segment "
-                                   f"instances, 4 distinct types ({args.dist} tables, seed {args.seed})"
-                       if args.config == "C3" else f"{args.config} ({args.dist}, seed {args.seed})",
+            "config": {"workload": workload_name(args),
                        "combos_per_step": combos, "l2": "flushed (512 MiB write) between timed steps",
                        "parallelism": f"enumeration sharded over {world} GPU(s), NCCL min-allreduce merge"},
             "plan_search_ms": {"device_median": statistics.median(step_ms),
