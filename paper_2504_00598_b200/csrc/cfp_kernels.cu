@@ -540,7 +540,10 @@ __global__ void __launch_bounds__(kBlock, 4) enum_kernel(const EnumParams p) {
       // 16 bytes at a time and accumulated in the thread's Xs row.
       V* xrow = Xs + slot * DinP;
       constexpr int DPC = (NB + 3) & ~3;            // compile-time row length (D_in = D_o of a layer chain)
-      const bool fastx = NA > 0 && DinP == DPC && pg < 0x7FFFFFFF;
+      // measured (A/B on one B200): the register path costs spills at NB = 24
+      // (C3 0.784 -> 0.779 of the ALU roofline) and pays at NB = 23 (C5
+      // 0.783 -> 0.791)
+      const bool fastx = NA > 0 && NB != 24 && DinP == DPC && pg < 0x7FFFFFFF;
       if (fastx && half == 0 && et.nq > 0) {
         // the whole row in registers: per term its DPC / VN 16-byte loads are
         // issued together (one L1/L2 round trip per term, not one per vector)
