@@ -312,7 +312,7 @@ def run_cfp(args, prob, rank, world, local_rank):
     ip_ops, ip_ms = ctx.intpipe_bench(0, 4000)
     traffic = None
     try:
-        with open(os.path.join(ROOT, "profiles", "r01_ncu_enum_v8.json")) as fh:
+        with open(os.path.join(ROOT, "profiles", "r01_ncu_enum_v11.json")) as fh:
             traffic = json.load(fh)["traffic_bytes_per_launch"]["enum_kernel"]
     except Exception:
         pass
@@ -348,7 +348,7 @@ def run_cfp(args, prob, rank, world, local_rank):
                                  "peak = 64 lane-ops/clk/SM x 148 SMs x 1965 MHz (derived, DESIGN.md); "
                                  "achieved = combos / device time of the enumeration phase (all enum "
                                  "launches incl. the cross-term fold epilogue); traffic = DRAM bytes per "
-                                 "enum launch from ncu (profiles/r01_ncu_enum_v8.json), algorithmic bytes ~0"},
+                                 "enum launch from ncu (profiles/r01_ncu_enum_v11.json), algorithmic bytes ~0"},
             "intpipe_measured": {"op": "VIADDMNMX.U32", "lane_ops_per_s": ip_ops,
                                  "lane_ops_per_clk_per_sm": ip_ops / (SMS * 1e6 * (clocks["sm_mhz"] or 1965.0)),
                                  "frac_of_derived_peak": ip_ops / (peak * 1e9)},
