@@ -157,6 +157,12 @@ cfp_status cfp_minplus_chain(cfp_ctx* ctx, int32_t num_mats, const int32_t* rows
 
 /* (3) Full search: identical result on every rank. */
 cfp_status cfp_search_plan(cfp_ctx* ctx, const cfp_problem* p, cfp_plan* out);
+/* cfp_search_plan keeps the last call's prepared plan in the ctx (schedule,
+ * device buffers; freed by the next structural miss or cfp_ctx_destroy): a
+ * call whose problem has the same structure -- shapes, feasible strategy
+ * sets, term maxima, deduplicated instances -- uploads only its table values
+ * and re-runs the path.  CFP_PLAN_CACHE=0 in the environment at ctx creation
+ * disables it. */
 
 /* One (min,+) product C = A (x) B with the least k attaining each entry
  * (CFP_NOIDX if the row/column pair is all-infinite).  argk nullable.

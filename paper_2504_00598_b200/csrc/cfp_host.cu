@@ -86,6 +86,9 @@ struct cfp_ctx {
   int sms = 148;
   bool sim = false;                 // world > 1 without a communicator: shard simulation (test hook)
   bool sharded = false;             // rank-local tables + merge path (world > 1, or a 1-rank communicator)
+  bool plan_cache = true;           // CFP_PLAN_CACHE=0: no structure-keyed reuse in cfp_search_plan
+  cfp_prepared* cached = nullptr;   // last cfp_search_plan's prepared plan (device buffers, schedule)
+  std::vector<int64_t> cached_key;  //   and its structural key (plan_key)
   bool mem_chain_fused = true;      // CFP_MEM_CHAIN_FUSED=0: one launch per DP step (A/B tests)
   bool dedup = true;                // CFP_DEDUP=0: fold identical transitions separately (A/B tests)
   bool no_full_a = false;           // CFP_ENUM_FULL_A=0: runtime-length A loop only (A/B tests)
@@ -133,6 +136,7 @@ extern "C" cfp_status cfp_ctx_create(cfp_ctx** out, const cfp_ctx_opts* opts) {
   if (const char* fa = getenv("CFP_ENUM_FULL_A")) c->no_full_a = atoi(fa) == 0;
   if (const char* dd = getenv("CFP_DEDUP")) c->dedup = atoi(dd) != 0;
   if (const char* mf = getenv("CFP_MEM_CHAIN_FUSED")) c->mem_chain_fused = atoi(mf) != 0;
+  if (const char* pc = getenv("CFP_PLAN_CACHE")) c->plan_cache = atoi(pc) != 0;
   if (const char* ms = getenv("CFP_ENUM_MSPLIT_MIN_M")) c->msplit_min_m = std::max(2LL, atoll(ms));
   if (opts && opts->cuda_stream) {
     c->stream = (cudaStream_t)opts->cuda_stream;
@@ -169,6 +173,7 @@ extern "C" cfp_status cfp_ctx_create(cfp_ctx** out, const cfp_ctx_opts* opts) {
 extern "C" void cfp_ctx_destroy(cfp_ctx* c) {
   if (!c) return;
   cudaSetDevice(c->device);
+  if (c->cached) cfp_prepared_free(c->cached);     // frees on c->stream: before the streams go
   if (c->comm) ncclCommDestroy(c->comm);
   for (int i = 0; i < cfp_ctx::kLanes; ++i) {
     if (c->lane[i]) cudaStreamDestroy(c->lane[i]);
@@ -667,6 +672,50 @@ static void dedup_transitions(const std::vector<HostType>& T, std::vector<HostTr
   for (int& t : inst) t = canon[t];
   for (int x = 0; x < (int)X.size(); ++x)
     if (canon[x] != x) X[x].used = false;
+}
+
+// Structural key of a validated problem for cfp_search_plan's plan reuse.
+// Everything prepare derives on the host from the problem -- shapes, the
+// feasible strategy sets (INF pattern), the term maxima (precision and
+// overflow decisions), the deduplicated instance list -- is in the key; the
+// table values themselves reach the device through the raw blob, which is
+// uploaded again on every call.
+static std::vector<int64_t> plan_key(const cfp_problem* p, const std::vector<HostType>& T,
+                                     const std::vector<HostTrans>& X, const std::vector<int>& inst,
+                                     const Builder& b) {
+  std::vector<int64_t> k;
+  k.push_back((int64_t)T.size());
+  k.push_back((int64_t)X.size());
+  k.push_back((int64_t)b.raw.size());
+  k.push_back((int64_t)p->mesh.ndim);
+  for (const HostType& h : T) {
+    k.push_back(h.K);
+    k.push_back(h.o);
+    k.push_back(h.E);
+    k.insert(k.end(), h.radix.begin(), h.radix.end());
+    k.insert(k.end(), h.esrc.begin(), h.esrc.end());
+    k.insert(k.end(), h.edst.begin(), h.edst.end());
+    for (int64_t o : h.comm_off) k.push_back(o < 0 ? -1 : 1);
+    for (const auto& kp : h.keep) {
+      k.push_back((int64_t)kp.size());
+      k.insert(k.end(), kp.begin(), kp.end());
+    }
+    for (uint64_t m : h.wmax) k.push_back((int64_t)m);
+    for (uint64_t m : h.emax) k.push_back((int64_t)m);
+    k.push_back(h.used ? 1 : 0);
+  }
+  for (const HostTrans& x : X) {
+    k.push_back(x.pred);
+    k.push_back(x.type);
+    k.push_back(x.X);
+    k.push_back(x.Din);
+    k.push_back(x.used ? 1 : 0);
+    k.insert(k.end(), x.xdst.begin(), x.xdst.end());
+    for (uint64_t m : x.xmax) k.push_back((int64_t)m);
+  }
+  k.push_back((int64_t)inst.size());
+  k.insert(k.end(), inst.begin(), inst.end());
+  return k;
 }
 
 // Derived-table spec over an ordered digit list.  `row_digits` trailing digits
@@ -1683,11 +1732,37 @@ extern "C" cfp_status cfp_fetch_plan(cfp_ctx* ctx, cfp_prepared* prep, cfp_plan*
 extern "C" cfp_status cfp_search_plan(cfp_ctx* ctx, const cfp_problem* p, cfp_plan* out) {
   if (!ctx || !p || !out) return fail(CFP_EINVAL, "null argument");
   if (ctx->sim) return fail(CFP_EINVAL, "shard simulation ctx (world > 1 without nccl_unique_id): tables only");
+  std::vector<int64_t> key;
+  if (ctx->plan_cache) {
+    // the same structure as the last call: reuse its prepared plan (schedule,
+    // device buffers, chain setup) and upload only this call's values
+    std::vector<HostType> T;
+    std::vector<HostTrans> X;
+    Builder b;
+    TRY(validate_and_model(p, T, X, b, true));
+    std::vector<int> inst(p->inst_transition, p->inst_transition + p->num_instances);
+    if (ctx->dedup) dedup_transitions(T, X, b, inst);
+    key = plan_key(p, T, X, inst, b);
+    if (ctx->cached && key == ctx->cached_key) {
+      CUDA_TRY(cudaSetDevice(ctx->device));
+      g_alloc_stream = ctx->stream;
+      cfp_prepared* P = ctx->cached;
+      CUDA_TRY(cudaMemcpyAsync(P->raw.p, b.raw.data(), b.raw.size() * 4, cudaMemcpyHostToDevice, ctx->stream));
+      TRY(execute_impl(ctx, P));
+      return fetch_impl(ctx, P, out);
+    }
+  }
   cfp_prepared* prep = nullptr;
   TRY(prepare_impl(ctx, p, true, &prep));
   std::unique_ptr<cfp_prepared> guard(prep);
   TRY(execute_impl(ctx, prep));
-  return fetch_impl(ctx, prep, out);
+  TRY(fetch_impl(ctx, prep, out));
+  if (ctx->plan_cache) {
+    if (ctx->cached) cfp_prepared_free(ctx->cached);
+    ctx->cached = guard.release();
+    ctx->cached_key = std::move(key);
+  }
+  return CFP_OK;
 }
 
 extern "C" cfp_status cfp_prepared_query(const cfp_prepared* P, cfp_prepared_info* info) {

@@ -518,3 +518,53 @@ def test_dedup_duplicated_transitions_random(ctx, oracle_lib, seed):
             tr.in_edges = copy.deepcopy(p.transitions[first[key]].in_edges)
         first.setdefault(key, tr_id)
     _search_or_infeasible(ctx, oracle_lib, p)
+
+
+# ---------------------------------------------------------------- plan reuse
+# cfp_search_plan reuses the previous call's prepared plan when the structure
+# (shapes, feasible sets, term maxima, deduplicated instances) is unchanged
+# and uploads only the new values: alternate problems that share a structure
+# but not their values (finite entries permuted within each table, so every
+# maximum is unchanged), and problems that do not.
+
+
+def _permuted(p, seed):
+    import copy
+    q = copy.deepcopy(p)
+    rng = np.random.default_rng(seed)
+    for ty in q.types:
+        comp = np.array(ty.comp_ns, np.uint32)
+        comm = None if ty.comm_ns is None else np.array(ty.comm_ns, np.uint32)
+        off = 0
+        for d in ty.radix:                    # one permutation per block, shared by p and c
+            d = int(d)
+            perm = rng.permutation(d)
+            comp[off:off + d] = comp[off:off + d][perm]
+            if comm is not None:
+                comm[off:off + d] = comm[off:off + d][perm]
+            off += d
+        ty.comp_ns, ty.comm_ns = comp, comm
+        for e in ty.edges:
+            e.table = rng.permutation(e.table.ravel()).reshape(e.table.shape).astype(np.uint32)
+    for tr in q.transitions:
+        for x in tr.in_edges:
+            x.table = rng.permutation(x.table.ravel()).reshape(x.table.shape).astype(np.uint32)
+    return q
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_plan_reuse_same_structure_new_values(ctx, oracle_lib, seed):
+    O = oracle_lib
+    p = G.tiny_random(7900 + seed, mode="random", max_plans=None, max_n=4, max_k=4, max_d=4,
+                      max_edges=4, p_inf=0.0)
+    variants = [p, _permuted(p, seed), _permuted(p, seed + 100), p]
+    for q in variants:
+        _search_or_infeasible(ctx, O, q)
+
+
+def test_plan_reuse_alternating_configs(ctx, oracle_lib):
+    O = oracle_lib
+    probs = [G.make_config("C2", 0, "shaped"), G.make_config("C1", 0, "shaped"),
+             G.make_config("C2", 1, "random"), G.make_config("C2", 0, "shaped")]
+    for q in probs:
+        _search_or_infeasible(ctx, O, q)
