@@ -338,6 +338,10 @@ def run_cfp(args, prob, rank, world, local_rank):
                                "device_p10": sorted(step_ms)[max(0, len(step_ms) // 10)],
                                "device_p90": sorted(step_ms)[min(len(step_ms) - 1, len(step_ms) * 9 // 10)],
                                "e2e_median": e2e_med, "enum_ms_avg": enum_avg_ms},
+            # (combination x input state) costs C(u, s) the search minimises over, per
+            # second; each combination is enumerated once per type and
+            # its D_in input states enter through the per-prefix cross-term fold
+            "evals_per_s": info.evals / (ms_per_step * 1e-3),
             "e2e": {"value": combos / (e2e_med * 1e-3), "unit": UNIT,
                     "h2d_bytes_per_step": problem_bytes(prob), "d2h_bytes_per_step": plan_bytes(prob),
                     "plan_search_ms": e2e_med},

@@ -194,7 +194,7 @@ void       cfp_prepared_free(cfp_prepared* prep);
 typedef struct {
   double combos;               /* sum over distinct used types of prod_j feasible D_j */
   double combos_local;         /* this rank's share */
-  double evals;                /* combos x (#incoming transitions folded) */
+  double evals;                /* sum over used transitions of combos(type) x D_in */
   int32_t num_types, num_transitions, wide_types;  /* wide = 64-bit path */
   int32_t kernel_launches;     /* kernels launched by one cfp_execute */
   int32_t prefix_len[CFP_MAX_BLOCKS];   /* per type: enumeration schedule summary */

@@ -1357,8 +1357,7 @@ static cfp_status prepare_impl(cfp_ctx* ctx, const cfp_problem* p, bool do_chain
                              cudaMemcpyHostToDevice, st));
   for (TransExec& tx : P->trans) {
     const TypeExec& te = P->types[type_slot[tx.type]];
-    P->evals += te.combos;
-    (void)tx;
+    P->evals += te.combos * (double)tx.Din;          // (combination, input state) costs minimised over
   }
   for (TypeExec& te : P->types) {
     P->combos += te.combos;
