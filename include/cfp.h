@@ -136,6 +136,9 @@ void        cfp_ctx_destroy(cfp_ctx* ctx);
 const char* cfp_last_error(void);
 /* Writes a fresh 128-byte ncclUniqueId (call on one rank, broadcast it). */
 cfp_status  cfp_nccl_unique_id(void* out128);
+/* The ctx's communicator: ranks (ncclCommCount) and NCCL version code;
+ * both 0 when the ctx has no communicator.  EINVAL on null arguments. */
+cfp_status  cfp_ctx_nccl_info(cfp_ctx* ctx, int32_t* nranks, int32_t* version);
 
 /* (1) One transition: cost_out/index_out are [d_in][D_o] row-major.
  * tr == NULL: no cross edges and d_in must be 1.  Collective if world > 1. */
@@ -201,11 +204,18 @@ typedef struct {
   int32_t nb[CFP_MAX_BLOCKS], na[CFP_MAX_BLOCKS];
 } cfp_prepared_info;
 cfp_status cfp_prepared_query(const cfp_prepared* prep, cfp_prepared_info* info);
-/* Record CUDA events around the enumeration kernel of the given type's next
- * cfp_execute (ms via cfp_prepared_enum_ms after the stream completes).
- * Used for the bench's per-kernel roofline; 0 = off. */
+/* Record CUDA events on the ctx stream during the next cfp_execute calls
+ * (bench instrumentation).  on = 0: off; 1: events at the start, after a0
+ * staging, after the enumeration (all side lanes joined) and at the end --
+ * cfp_prepared_kernel_ms reports enumeration ms and whole-path ms; 2: also an
+ * event after every later phase -- cfp_prepared_phase_ms reports ms[6] =
+ * {a0 stage, a1 enumerate, a1 bucket minima + a2 all-reduce of A, a3 chain,
+ * a1 argmin + a2 index merge, a4 backtrack} of the last execute (SURVEY §8(d)
+ * per-phase breakdown).  EINVAL: on outside [0, 2], or the level needed for
+ * the query was not enabled.  Both queries synchronise on the end event. */
 cfp_status cfp_prepared_time_kernels(cfp_prepared* prep, int32_t on);
 cfp_status cfp_prepared_kernel_ms(cfp_prepared* prep, double* enum_ms, double* total_ms);
+cfp_status cfp_prepared_phase_ms(cfp_prepared* prep, double* ms /* [6] */);
 
 /* ---- memory-constrained search ----------------------
  * The paper's DP carries a memory constraint: Eq. 4 sums the profiled

@@ -29,8 +29,10 @@ def build(force: bool = False) -> str:
     src = os.path.join(HERE, "cfp_oracle.c")
     if force or not os.path.exists(LIB_PATH) or os.path.getmtime(LIB_PATH) < max(
             os.path.getmtime(src), os.path.getmtime(os.path.join(HERE, "cfp_oracle.h"))):
+        tmp = LIB_PATH + ".tmp"   # rename into place: a running process keeps its mapping
         subprocess.check_call(["gcc", "-O2", "-std=c11", "-fopenmp", "-fPIC", "-shared",
-                               "-o", LIB_PATH, src])
+                               "-o", tmp, src])
+        os.replace(tmp, LIB_PATH)
     return LIB_PATH
 
 

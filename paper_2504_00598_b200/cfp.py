@@ -15,7 +15,7 @@ from __future__ import annotations
 import ctypes as C
 import os
 from dataclasses import dataclass
-from typing import List, Optional, Sequence, Tuple
+from typing import Dict, List, Optional, Sequence, Tuple
 
 import numpy as np
 
@@ -94,7 +94,7 @@ class cfp_prepared_info(C.Structure):
 EXPORTS = ["cfp_ctx_create", "cfp_ctx_destroy", "cfp_last_error", "cfp_nccl_unique_id",
            "cfp_segment_costs", "cfp_minplus_chain", "cfp_search_plan", "cfp_minplus_product",
            "cfp_prepare", "cfp_execute", "cfp_fetch_plan", "cfp_prepared_free",
-           "cfp_prepared_query", "cfp_prepared_time_kernels", "cfp_prepared_kernel_ms",
+           "cfp_ctx_nccl_info", "cfp_prepared_query", "cfp_prepared_time_kernels", "cfp_prepared_kernel_ms", "cfp_prepared_phase_ms",
            "cfp_shard_range", "cfp_pack_keys", "cfp_unpack_keys", "cfp_intpipe_bench",
            "cfp_minplus_bench", "cfp_search_plan_mem", "cfp_segment_costs_mem", "cfp_mem_prepare",
            "cfp_mem_execute", "cfp_mem_fetch_plan", "cfp_mem_free", "cfp_mem_time_kernels",
@@ -137,6 +137,8 @@ def lib() -> C.CDLL:
     L.cfp_prepared_query.argtypes = [vp, P(cfp_prepared_info)]
     L.cfp_prepared_time_kernels.argtypes = [vp, C.c_int32]
     L.cfp_prepared_kernel_ms.argtypes = [vp, P(C.c_double), P(C.c_double)]
+    L.cfp_prepared_phase_ms.argtypes = [vp, P(C.c_double)]
+    L.cfp_ctx_nccl_info.argtypes = [vp, P(C.c_int32), P(C.c_int32)]
     L.cfp_shard_range.argtypes = [C.c_int64, C.c_int64, C.c_int32, C.c_int32, P(C.c_int64), P(C.c_int64)]
     L.cfp_pack_keys.argtypes = [C.c_int64, P(C.c_uint64), P(C.c_uint64), C.c_int32, P(C.c_uint64)]
     L.cfp_unpack_keys.argtypes = [C.c_int64, P(C.c_uint64), C.c_int32, P(C.c_uint64), P(C.c_uint64)]
@@ -306,6 +308,12 @@ class Context:
         opts = cfp_ctx_opts(device, stream, world, rank, C.cast(uid, C.c_void_p) if uid else None)
         _check(L.cfp_ctx_create(C.byref(self._h), C.byref(opts)))
         self.world, self.rank, self.device = world, rank, device
+
+    def nccl_info(self) -> Tuple[int, int]:
+        """(ranks of the ctx's communicator, NCCL version code); (0, 0) without one."""
+        n, v = C.c_int32(), C.c_int32()
+        _check(lib().cfp_ctx_nccl_info(self._h, C.byref(n), C.byref(v)))
+        return n.value, v.value
 
     def close(self):
         if self._h:
@@ -515,8 +523,18 @@ class Prepared:
         return PreparedInfo(i.combos, i.combos_local, i.evals, i.num_types, i.num_transitions,
                             i.wide_types, i.kernel_launches, sched)
 
-    def time_kernels(self, on: bool = True):
-        _check(lib().cfp_prepared_time_kernels(self._h, 1 if on else 0))
+    def time_kernels(self, on=True):
+        """0 off, 1 (True): events around a0 / enumeration / whole path, 2: + every phase."""
+        _check(lib().cfp_prepared_time_kernels(self._h, int(on)))
+
+    PHASES = ("a0_stage", "a1_enumerate", "a1_reduce_a2_allreduce", "a3_chain", "a1_argmin_a2_merge",
+              "a4_backtrack")
+
+    def phase_ms(self) -> Dict[str, float]:
+        """Device ms of each hot-path phase of the last execute (timing level 2)."""
+        ms = (C.c_double * 6)()
+        _check(lib().cfp_prepared_phase_ms(self._h, ms))
+        return {k: float(v) for k, v in zip(self.PHASES, ms)}
 
     def kernel_ms(self) -> Tuple[float, float]:
         a, b = C.c_double(), C.c_double()

@@ -38,7 +38,6 @@ cudaError_t launch_chain(const ChainParams&, cudaStream_t);
 cudaError_t launch_intpipe(int, int, int, uint32_t*, cudaStream_t);
 template <typename V> cudaError_t launch_amin(const ArgminParams*, const int64_t*, int, int64_t, cudaStream_t);
 cudaError_t launch_all_pairs(const int64_t*, int, int64_t, ArgminEntry*, int32_t*, cudaStream_t);
-cudaError_t argmin_debug_read(uint64_t*);
 cudaError_t launch_edges_to_pairs(const ArgminParams*, ArgminEntry*, const int32_t*, int64_t, cudaStream_t);
 template <typename V> cudaError_t launch_minplus_tiled(int, int, int, const V*, const V*, V*, uint32_t*, cudaStream_t);
 template <typename V> cudaError_t launch_to_path(const uint64_t*, V*, int64_t, cudaStream_t);
@@ -167,6 +166,19 @@ extern "C" cfp_status cfp_ctx_create(cfp_ctx** out, const cfp_ctx_opts* opts) {
     c->sharded = true;
   }
   *out = c.release();
+  return CFP_OK;
+}
+
+extern "C" cfp_status cfp_ctx_nccl_info(cfp_ctx* c, int32_t* nranks, int32_t* version) {
+  if (!c || !nranks || !version) return fail(CFP_EINVAL, "null argument");
+  *nranks = 0;
+  *version = 0;
+  if (!c->comm) return CFP_OK;
+  int n = 0, v = 0;
+  NCCL_TRY(ncclCommCount(c->comm, &n));
+  NCCL_TRY(ncclGetVersion(&v));
+  *nranks = n;
+  *version = v;
   return CFP_OK;
 }
 
@@ -345,8 +357,9 @@ struct cfp_prepared {
   // host-side copies for diagnostics
   std::vector<int> inst_rows, inst_cols;
   // timing
-  bool timing = false;
-  cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+  int timing = 0;                 // 1: events around a0 / enumeration / whole; 2: + every phase
+  cudaEvent_t ev[7] = {};         // 0 start, 1 a0 done, 2 enumeration done, 3 end,
+                                  // 4 bucket minima (+ all-reduce), 5 chain, 6 argmin (+ merge)
   ~cfp_prepared() {
     for (auto& e : ev) if (e) cudaEventDestroy(e);
   }
@@ -674,6 +687,40 @@ static void dedup_transitions(const std::vector<HostType>& T, std::vector<HostTr
     if (canon[x] != x) X[x].used = false;
 }
 
+// Precision of a type: narrow (uint32) iff the sum of the finite maxima of
+// every term of one combination (unary, intra, worst incoming cross) < CAP32.
+static bool type_is_wide(const std::vector<HostType>& T, const std::vector<HostTrans>& X, int i) {
+  long double bound = 0;
+  for (auto v : T[i].wmax) bound += v;
+  for (auto v : T[i].emax) bound += v;
+  long double xb = 0;
+  for (const HostTrans& x : X) {
+    if (!x.used || x.type != i) continue;
+    long double s = 0;
+    for (auto v : x.xmax) s += v;
+    xb = std::max(xb, s);
+  }
+  bound += xb;
+  return !(bound < (long double)kCap32);
+}
+
+// Chain overflow guard: the sum over instances of every term's finite maximum < 2^63.
+static cfp_status check_chain_overflow(const std::vector<HostType>& T, const std::vector<HostTrans>& X,
+                                       const std::vector<int>& inst) {
+  long double tot = 0;
+  for (int t : inst) {
+    const HostTrans& h = X[t];
+    const HostType& ty = T[h.type];
+    long double s = 0;
+    for (auto v : ty.wmax) s += v;
+    for (auto v : ty.emax) s += v;
+    for (auto v : h.xmax) s += v;
+    tot += s;
+  }
+  if (tot >= 9.2e18L) return fail(CFP_EOVERFLOW, "a finite plan cost could reach 2^63");
+  return CFP_OK;
+}
+
 // Structural key of a validated problem for cfp_search_plan's plan reuse.
 // Everything prepare derives on the host from the problem -- shapes, the
 // feasible strategy sets (INF pattern), the term maxima (precision and
@@ -700,8 +747,6 @@ static std::vector<int64_t> plan_key(const cfp_problem* p, const std::vector<Hos
       k.push_back((int64_t)kp.size());
       k.insert(k.end(), kp.begin(), kp.end());
     }
-    for (uint64_t m : h.wmax) k.push_back((int64_t)m);
-    for (uint64_t m : h.emax) k.push_back((int64_t)m);
     k.push_back(h.used ? 1 : 0);
   }
   for (const HostTrans& x : X) {
@@ -711,8 +756,9 @@ static std::vector<int64_t> plan_key(const cfp_problem* p, const std::vector<Hos
     k.push_back(x.Din);
     k.push_back(x.used ? 1 : 0);
     k.insert(k.end(), x.xdst.begin(), x.xdst.end());
-    for (uint64_t m : x.xmax) k.push_back((int64_t)m);
   }
+  // the term maxima enter only through the precision of each type
+  for (int i = 0; i < (int)T.size(); ++i) k.push_back(T[i].used ? (int64_t)type_is_wide(T, X, i) : -1);
   k.push_back((int64_t)inst.size());
   k.insert(k.end(), inst.begin(), inst.end());
   return k;
@@ -815,38 +861,44 @@ struct PrepTimer {
   }
 };
 
-static cfp_status prepare_impl(cfp_ctx* ctx, const cfp_problem* p, bool do_chain,
-                               cfp_prepared** out) {
-  PrepTimer tm;
-  *out = nullptr;
-  g_alloc_stream = ctx->stream;
+// The validated host model of a problem (validate_and_model + dedup): built
+// once per cfp_search_plan call and handed to prepare_impl on a cache miss.
+struct HostModel {
   std::vector<HostType> T;
   std::vector<HostTrans> X;
   Builder b;
-  TRY(validate_and_model(p, T, X, b, do_chain));
+  std::vector<int> inst;
+};
+
+static cfp_status build_model(cfp_ctx* ctx, const cfp_problem* p, bool do_chain, HostModel& m) {
+  TRY(validate_and_model(p, m.T, m.X, m.b, do_chain));
+  m.inst.assign(p->inst_transition, p->inst_transition + p->num_instances);
+  if (ctx->dedup) dedup_transitions(m.T, m.X, m.b, m.inst);
+  return CFP_OK;
+}
+
+static cfp_status prepare_impl(cfp_ctx* ctx, const cfp_problem* p, bool do_chain,
+                               cfp_prepared** out, HostModel* pre = nullptr) {
+  PrepTimer tm;
+  *out = nullptr;
+  g_alloc_stream = ctx->stream;
+  HostModel local;
+  if (!pre) {
+    TRY(build_model(ctx, p, do_chain, local));
+    pre = &local;
+  }
+  std::vector<HostType>& T = pre->T;
+  std::vector<HostTrans>& X = pre->X;
+  Builder& b = pre->b;
   tm.mark("validate");
   std::unique_ptr<cfp_prepared> P(new cfp_prepared());
   P->ctx = ctx;
   P->do_chain = do_chain;
   P->N = p->num_instances;
-  P->inst.assign(p->inst_transition, p->inst_transition + P->N);
+  P->inst = pre->inst;
   const int world = ctx->world, rank = ctx->rank;
-  if (ctx->dedup) dedup_transitions(T, X, b, P->inst);
 
-  // ---- chain overflow guard: sum over instances of the finite bound < 2^63
-  {
-    long double tot = 0;
-    for (int n = 0; n < P->N; ++n) {
-      const HostTrans& h = X[P->inst[n]];
-      const HostType& t = T[h.type];
-      long double s = 0;
-      for (auto v : t.wmax) s += v;
-      for (auto v : t.emax) s += v;
-      for (auto v : h.xmax) s += v;
-      tot += s;
-    }
-    if (tot >= 9.2e18L) return fail(CFP_EOVERFLOW, "a finite plan cost could reach 2^63");
-  }
+  TRY(check_chain_overflow(T, X, P->inst));
 
   // ---- per type: precision, schedule, value-blob layout
   std::map<int, int> type_slot, trans_slot;
@@ -859,18 +911,7 @@ static cfp_status prepare_impl(cfp_ctx* ctx, const cfp_problem* p, bool do_chain
     te.empty = T[i].empty;
     for (int x = 0; x < (int)X.size(); ++x)
       if (X[x].used && X[x].type == i) te.trans.push_back(x);
-    // precision: sum of finite maxima of every term of one combination
-    long double bound = 0;
-    for (auto v : T[i].wmax) bound += v;
-    for (auto v : T[i].emax) bound += v;
-    long double xb = 0;
-    for (int x : te.trans) {
-      long double s = 0;
-      for (auto v : X[x].xmax) s += v;
-      xb = std::max(xb, s);
-    }
-    bound += xb;
-    te.wide = !(bound < (long double)kCap32);
+    te.wide = type_is_wide(T, X, i);
     double c = 1;
     for (int d : T[i].radix_c) c *= d;
     te.combos = te.empty ? 0 : c;
@@ -1436,7 +1477,6 @@ static cfp_status prepare_impl(cfp_ctx* ctx, const cfp_problem* p, bool do_chain
     cp.kmax = kmax;
     cp.radix_blob = P->radix_blob.as<int32_t>();
     cp.status = P->status.as<int32_t>();
-    cp.dbg = getenv("CFP_DEBUG_CHAIN") ? reinterpret_cast<uint64_t*>(P->status.as<char>() + 16) : nullptr;
     {
       std::vector<ChainInst> mats(P->trans.size());
       int lv = 0, smax = 1;
@@ -1501,6 +1541,9 @@ static cfp_status execute_impl(cfp_ctx* ctx, cfp_prepared* P) {
     for (auto& e : P->ev) if (!e) CUDA_TRY(cudaEventCreate(&e));
     CUDA_TRY(cudaEventRecord(P->ev[0], st));
   }
+  auto phase = [&](int i) -> cudaError_t {
+    return P->timing >= 2 ? cudaEventRecord(P->ev[i], st) : cudaSuccess;
+  };
   // a0: compaction + derived tables
   if (P->njobs32) {
     CUDA_TRY(launch_compact<uint32_t>(P->jobs32.as<CompactJob>(), P->njobs32, P->raw.as<uint32_t>(),
@@ -1568,6 +1611,7 @@ static cfp_status execute_impl(cfp_ctx* ctx, cfp_prepared* P) {
     if (ctx->comm) NCCL_TRY(ncclAllReduce(P->locAI.p, outA, ai, ncclUint64, ncclMin, ctx->comm, st));
     else CUDA_TRY(cudaMemcpyAsync(outA, P->locAI.p, (size_t)ai * 8, cudaMemcpyDeviceToDevice, st));
   }
+  CUDA_TRY(phase(4));
   ArgminEntry* list = P->edges.as<ArgminEntry>();
   int32_t* count = reinterpret_cast<int32_t*>(P->edges.as<char>() + (size_t)(ai + 1) * sizeof(ArgminEntry));
   const bool edges = P->do_chain && P->use_edges;
@@ -1586,12 +1630,14 @@ static cfp_status execute_impl(cfp_ctx* ctx, cfp_prepared* P) {
     CUDA_TRY(launch_all_pairs(P->pair_off.as<int64_t>(), nslot, P->npairs, list, count, st));
     P->launches++;
   }
+  CUDA_TRY(phase(5));
   // a1: least combination index of the listed buckets
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(edges ? 64 : P->npairs, P->npairs));
   if (P->has32) { CUDA_TRY(launch_argmin<uint32_t>(aps, list, count, grid, P->kmax_arg, P->tabn_max, st)); P->launches++; }
   if (P->has64) { CUDA_TRY(launch_argmin<uint64_t>(aps, list, count, grid, P->kmax_arg, P->tabn_max, st)); P->launches++; }
   // a2: merge across ranks
   if (ctx->sharded) TRY(merge_ranks(P, st));
+  CUDA_TRY(phase(6));
   // a4 (+ a3 when the edge list is not used)
   if (P->do_chain) {
     if (!edges) CUDA_TRY(cudaMemsetAsync(P->status.p, 0, 4, st));
@@ -1651,28 +1697,6 @@ static cfp_status fetch_impl(cfp_ctx* ctx, cfp_prepared* P, cfp_plan* out) {
   std::vector<char> buf(8 + (size_t)N * 16 + (size_t)N * P->kmax * 4);
   CUDA_TRY(cudaMemcpyAsync(buf.data(), P->plan.p, buf.size(), cudaMemcpyDeviceToHost, st));
   CUDA_TRY(cudaStreamSynchronize(st));
-  if (P->cp.dbg) {
-    uint64_t a[16];
-    CUDA_TRY(argmin_debug_read(a));
-    int32_t cnt = 0;
-    CUDA_TRY(cudaMemcpy(&cnt, P->edges.as<char>() + (size_t)(P->ai + 1) * sizeof(ArgminEntry), 4,
-                        cudaMemcpyDeviceToHost));
-    fprintf(stderr, "argmin slot-1 phases (us): stage %.2f chunks %.2f rows %.2f suffix %.2f; list %d of %lld; per entry:",
-            (a[1] - a[0]) * 1e-3, (a[2] - a[1]) * 1e-3, (a[3] - a[2]) * 1e-3, (a[4] - a[3]) * 1e-3, cnt,
-            (long long)P->npairs);
-    for (int i = 0; i < cnt && i < 8; ++i)
-      fprintf(stderr, " [slot %d pair %d: %.2f us]", (int)((a[8 + i] >> 12) & 0xF), (int)(a[8 + i] & 0xFFF),
-              (a[8 + i] >> 16) * 1e-3);
-    fprintf(stderr, "\n");
-    uint64_t t[64];
-    CUDA_TRY(cudaMemcpy(t, P->cp.dbg, sizeof(t), cudaMemcpyDeviceToHost));
-    for (int m = 0; m < 2; ++m) {
-      const uint64_t* d = t + 32 * m;
-      fprintf(stderr, "chain mode %d phases (us):", m ? 2 : 1);
-      for (uint64_t i = 1; i < d[31] && i < 31; ++i) fprintf(stderr, " %.2f", (d[i] - d[i - 1]) * 1e-3);
-      fprintf(stderr, "\n");
-    }
-  }
   if (status == 4) return fail(CFP_ETOOBIG, "chain scratch too small");
   if (status == 3) {
     // diagnostic: forward reachability over finite entries of A_n
@@ -1732,32 +1756,36 @@ extern "C" cfp_status cfp_search_plan(cfp_ctx* ctx, const cfp_problem* p, cfp_pl
   if (!ctx || !p || !out) return fail(CFP_EINVAL, "null argument");
   if (ctx->sim) return fail(CFP_EINVAL, "shard simulation ctx (world > 1 without nccl_unique_id): tables only");
   std::vector<int64_t> key;
+  HostModel model;
+  TRY(build_model(ctx, p, true, model));
   if (ctx->plan_cache) {
     // the same structure as the last call: reuse its prepared plan (schedule,
     // device buffers, chain setup) and upload only this call's values
-    std::vector<HostType> T;
-    std::vector<HostTrans> X;
-    Builder b;
-    TRY(validate_and_model(p, T, X, b, true));
-    std::vector<int> inst(p->inst_transition, p->inst_transition + p->num_instances);
-    if (ctx->dedup) dedup_transitions(T, X, b, inst);
-    key = plan_key(p, T, X, inst, b);
+    key = plan_key(p, model.T, model.X, model.inst, model.b);
     if (ctx->cached && key == ctx->cached_key) {
+      TRY(check_chain_overflow(model.T, model.X, model.inst));
       CUDA_TRY(cudaSetDevice(ctx->device));
       g_alloc_stream = ctx->stream;
       cfp_prepared* P = ctx->cached;
-      CUDA_TRY(cudaMemcpyAsync(P->raw.p, b.raw.data(), b.raw.size() * 4, cudaMemcpyHostToDevice, ctx->stream));
+      CUDA_TRY(cudaMemcpyAsync(P->raw.p, model.b.raw.data(), model.b.raw.size() * 4, cudaMemcpyHostToDevice,
+                               ctx->stream));
       TRY(execute_impl(ctx, P));
       return fetch_impl(ctx, P, out);
     }
   }
+  // structure changed: release the previous plan's device buffers first, so a
+  // search that fits the device alone never needs old + new plan at once
+  if (ctx->cached) {
+    cfp_prepared_free(ctx->cached);
+    ctx->cached = nullptr;
+    ctx->cached_key.clear();
+  }
   cfp_prepared* prep = nullptr;
-  TRY(prepare_impl(ctx, p, true, &prep));
+  TRY(prepare_impl(ctx, p, true, &prep, &model));
   std::unique_ptr<cfp_prepared> guard(prep);
   TRY(execute_impl(ctx, prep));
   TRY(fetch_impl(ctx, prep, out));
   if (ctx->plan_cache) {
-    if (ctx->cached) cfp_prepared_free(ctx->cached);
     ctx->cached = guard.release();
     ctx->cached_key = std::move(key);
   }
@@ -1784,7 +1812,21 @@ extern "C" cfp_status cfp_prepared_query(const cfp_prepared* P, cfp_prepared_inf
 
 extern "C" cfp_status cfp_prepared_time_kernels(cfp_prepared* P, int32_t on) {
   if (!P) return fail(CFP_EINVAL, "null argument");
-  P->timing = on != 0;
+  if (on < 0 || on > 2) return fail(CFP_EINVAL, "timing level must be 0, 1 or 2");
+  P->timing = on;
+  return CFP_OK;
+}
+
+extern "C" cfp_status cfp_prepared_phase_ms(cfp_prepared* P, double* ms) {
+  if (!P || !ms) return fail(CFP_EINVAL, "null argument");
+  if (P->timing < 2 || !P->ev[6]) return fail(CFP_EINVAL, "phase timing (level 2) not enabled");
+  CUDA_TRY(cudaEventSynchronize(P->ev[3]));
+  const int from[6] = {0, 1, 2, 4, 5, 6}, to[6] = {1, 2, 4, 5, 6, 3};
+  for (int i = 0; i < 6; ++i) {
+    float t = 0;
+    CUDA_TRY(cudaEventElapsedTime(&t, P->ev[from[i]], P->ev[to[i]]));
+    ms[i] = t;
+  }
   return CFP_OK;
 }
 

@@ -208,7 +208,6 @@ struct ChainParams {
   int64_t mat_elems;            // sum rows*cols
   int64_t smem_bytes;           // 0 = global mode
   int32_t levels_max, smax;
-  uint64_t* dbg;                // nullable: %globaltimer at phase boundaries
   int32_t mode;                 // 0 G + backtrack, 1 G + optimal-edge list, 2 backtrack (G given)
   int32_t* edge_flag;           // mode 1: [sum Din*Do_orig] dedupe flags (zeroed)
   const int64_t* flag_off;      // mode 1: per distinct matrix offset into edge_flag

@@ -103,13 +103,6 @@ __device__ __forceinline__ int prefix_digit(int64_t pg, int pos, int P, const in
   return dig;
 }
 
-__device__ uint64_t g_enum_dbg2[16];
-__device__ __forceinline__ uint64_t gtimer0() {
-  uint64_t t;
-  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-  return t;
-}
-
 // --------------------------------------------------------------------------
 // a0: compaction.  Each job gathers one table of the pruned problem from the
 // raw uint32 inputs: unary w = p + c (INF absorbing), pair / cross
@@ -283,8 +276,6 @@ __global__ void __launch_bounds__(kBlock, 4) enum_kernel(const EnumParams p) {
   constexpr int VN = Vec4<V>::N;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int tid = threadIdx.x;
-  const bool edbg = blockIdx.x == 0 && tid == 0 && p.ntau == 2;
-  if (edbg) g_enum_dbg2[0] = gtimer0();
   constexpr int CH = kBlock / MSPLIT;                       // prefixes per CTA (= p.CH)
   const int slot = MSPLIT == 2 ? (tid & (CH - 1)) : tid;    // this thread's prefix slot
   const int half = MSPLIT == 2 ? tid / CH : 0;              // its share of the M values
@@ -375,7 +366,6 @@ __global__ void __launch_bounds__(kBlock, 4) enum_kernel(const EnumParams p) {
       YT = ym;
     }
   }
-  if (edbg) g_enum_dbg2[1] = gtimer0();
   V* Bp = static_cast<V*>(p.Bp) + row * p.Do;
   V acc[NB];
 #pragma unroll
@@ -469,7 +459,6 @@ __global__ void __launch_bounds__(kBlock, 4) enum_kernel(const EnumParams p) {
       Bp[od] = r;
     }
   }
-  if (edbg) g_enum_dbg2[2] = gtimer0();
   const bool simple = p.o_mode == 0 && p.o_bstride == 1 && p.o_bradix == p.nb;
   const int v_lo = simple ? ybase : 0;
   const int v_cnt = simple ? min(NB, p.nb - ybase) : p.Do;
@@ -592,7 +581,6 @@ __global__ void __launch_bounds__(kBlock, 4) enum_kernel(const EnumParams p) {
         }
     }
     __syncthreads();
-    if (edbg) g_enum_dbg2[3 + 3 * t] = gtimer0();
     const int nblk = (DinP / 4) * (VP / 4);
     const int stripes = nblk >= kBlock ? 1 : min(8, kBlock / nblk);
     V res[4][4];
@@ -632,7 +620,6 @@ __global__ void __launch_bounds__(kBlock, 4) enum_kernel(const EnumParams p) {
       if (stripes > 1) break;
     }
     __syncthreads();                                 // Xs free -> stripe partials
-    if (edbg) g_enum_dbg2[4 + 3 * t] = gtimer0();
     if (nblk < kBlock) {
       V* red = stripes * VP <= CH ? Xs : Xs + CH * dinp_max;   // [stripes][DinP][VP]
       if (active) {
@@ -651,7 +638,6 @@ __global__ void __launch_bounds__(kBlock, 4) enum_kernel(const EnumParams p) {
       }
       __syncthreads();
     }
-    if (edbg) g_enum_dbg2[5 + 3 * t] = gtimer0();
   }
 }
 
@@ -688,19 +674,10 @@ __device__ __forceinline__ void load4(const V* p, V* out) {
 //     whose intra cost equals B_p*[v];
 //  4. outputs in the caller's (unpruned) layout: A[u][v_orig], I[u][v_orig].
 // --------------------------------------------------------------------------
-__device__ uint64_t g_argmin_dbg[16];
-__device__ __forceinline__ uint64_t gtimer2() {
-  uint64_t t;
-  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-  return t;
-}
-
 template <typename V>
 __device__ void argmin_pair(const ArgminParams& ap, const int pair, unsigned char* smem_raw) {
   constexpr int NT = 256;
   const int tid = threadIdx.x;
-  const bool dbg = ap.slot == 1 && tid == 0;
-  if (dbg) g_argmin_dbg[0] = gtimer2();
   // descriptor pieces used inside loops -> shared memory (one global read each)
   __shared__ Term s_terms[kMaxTerms];
   __shared__ Term s_q[kMaxCross];
@@ -746,7 +723,6 @@ __device__ void argmin_pair(const ArgminParams& ap, const int pair, unsigned cha
     return;
   }
   const V best = (V)Ag;
-  if (dbg) g_argmin_dbg[1] = gtimer2();
   // 2. chunks of this rank attaining it (none: this rank holds no candidate)
   constexpr int LIST = 4 * NT;
   __shared__ int64_t s_list[LIST];
@@ -781,7 +757,6 @@ __device__ void argmin_pair(const ArgminParams& ap, const int pair, unsigned cha
   }
   __syncthreads();
   const int64_t hbmin = s_hbmin;
-  if (dbg) g_argmin_dbg[2] = gtimer2();
   // rows of the chunks (l, hbmin), l < W, attaining the minimum
   __shared__ int32_t s_ls[NT];
   __shared__ int s_nl;
@@ -813,7 +788,6 @@ __device__ void argmin_pair(const ArgminParams& ap, const int pair, unsigned cha
   }
   __syncthreads();
   const int64_t pl = (int64_t)s_first;
-  if (dbg) g_argmin_dbg[3] = gtimer2();
   __syncthreads();
   if (tid == 0) s_first = ~0ull;
   const uint64_t target = (uint64_t)Bp[pl * Do + v];
@@ -862,7 +836,6 @@ __device__ void argmin_pair(const ArgminParams& ap, const int pair, unsigned cha
     }
   }
   __syncthreads();
-  if (dbg) g_argmin_dbg[4] = gtimer2();
   if (tid == 0) {
     const uint64_t sfx = s_first;
     uint64_t q = sfx;
@@ -885,11 +858,8 @@ __global__ void __launch_bounds__(256) argmin_kernel(const ArgminParams* __restr
     const ArgminEntry en = list[it];
     const ArgminParams& ap = aps[en.slot];
     if (ap.wide != wide) continue;                  // uniform per CTA
-    const uint64_t t0 = gtimer2();
     argmin_pair<V>(ap, en.pair, smem_raw);
     __syncthreads();
-    if (threadIdx.x == 0 && it < 8)
-      g_argmin_dbg[8 + it] = ((gtimer2() - t0) << 16) | (uint64_t)(en.slot << 12) | (uint64_t)(en.pair & 0xFFF);
   }
 }
 
@@ -952,11 +922,6 @@ __device__ __forceinline__ uint64_t sat64(uint64_t a, uint64_t b) {
 
 
 
-__device__ __forceinline__ uint64_t gtimer() {
-  uint64_t t;
-  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-  return t;
-}
 
 // min_v sat64(row[v], g[v]) with four independent partial minima (ILP)
 __device__ __forceinline__ uint64_t minplus_dot(const uint64_t* row, int rstride, const uint64_t* g, int n) {
@@ -1010,10 +975,6 @@ __device__ __forceinline__ int64_t goff_n_of(const ChainParams& cp) { return cp.
 template <bool SM>
 __global__ void __launch_bounds__(1024) chain_kernel(const ChainParams cp) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  int dbg_i = 0;
-  uint64_t* dbg = cp.dbg ? cp.dbg + (cp.mode == 1 ? 0 : 32) : nullptr;   // per-mode phase marks
-  auto mark = [&]() { if (dbg && threadIdx.x == 0 && dbg_i < 31) dbg[dbg_i++] = gtimer(); };
-  mark();
   const int tid = threadIdx.x, nth = blockDim.x;
   const int N = cp.N;
   uint64_t* sA = reinterpret_cast<uint64_t*>(smem_raw);
@@ -1056,7 +1017,6 @@ __global__ void __launch_bounds__(1024) chain_kernel(const ChainParams cp) {
     if (tma) mbar_wait(&cbar, 0);
     __syncthreads();
   }
-  mark();
   auto rows_of = [&](int n) { return SM ? sinst[n].y : cp.inst[n].rows; };
   auto cols_of = [&](int n) { return SM ? sinst[n].z : cp.inst[n].cols; };
   auto mat_of = [&](int n) { return SM ? sinst[n].x : cp.inst[n].mat; };
@@ -1083,7 +1043,6 @@ __global__ void __launch_bounds__(1024) chain_kernel(const ChainParams cp) {
           if (lane == 0) G[goff[e - 1] + u] = b;
         }
         __syncthreads();
-        mark();
         continue;
       }
       const int S = R;                                // square
@@ -1102,7 +1061,6 @@ __global__ void __launch_bounds__(1024) chain_kernel(const ChainParams cp) {
           Pc[c] = minplus_dot(Pa + k2, S, Pa + (int64_t)i * S, S);      // min_k Pa[i][k] + Pa[k][k2]
         }
         __syncthreads();
-        mark();
       }
       // doubling: G_{e-k} = P_j (x) G_{e-k+2^j}, k in [2^j, 2^(j+1))
       for (int j = 0; j <= levels; ++j) {
@@ -1114,7 +1072,6 @@ __global__ void __launch_bounds__(1024) chain_kernel(const ChainParams cp) {
           G[goff[e - k] + u] = minplus_dot(Pj + (int64_t)u * S, 1, G + goff[e - k + (1 << j)], S);
         }
         __syncthreads();
-        mark();
       }
     }
     if constexpr (SM)
@@ -1128,11 +1085,9 @@ __global__ void __launch_bounds__(1024) chain_kernel(const ChainParams cp) {
     //     evaluated (usually one per instance);
     // (2) every (n, u) in parallel: emit the reachable optimal edges (deduplicated).
     __syncthreads();
-    mark();
     __shared__ int s_cnt2;
     if (tid == 0) s_cnt2 = 0;
     for (int64_t w = tid; w < goff[N]; w += nth) cp.reach[w] = 0;
-    mark();
     if (tid < 32) {
       const int lane = tid;
       uint32_t r = G[0] == kInf64 ? 0u : 1u;
@@ -1157,7 +1112,6 @@ __global__ void __launch_bounds__(1024) chain_kernel(const ChainParams cp) {
       }
     }
     __syncthreads();
-    mark();
     for (int64_t w = tid; w < (int64_t)N * 32; w += nth) {   // (instance, lane = u)
       const int n = (int)(w >> 5), u = (int)(w & 31);
       if (u >= rows_of(n) || !((rmask[n] >> u) & 1u)) continue;
@@ -1175,8 +1129,6 @@ __global__ void __launch_bounds__(1024) chain_kernel(const ChainParams cp) {
     }
     __syncthreads();
     if (tid == 0) *cp.edge_count = s_cnt2;
-    mark();
-    if (dbg && tid == 0) dbg[31] = dbg_i;
     return;
   }
   if (cp.mode == 1) {
@@ -1231,8 +1183,6 @@ __global__ void __launch_bounds__(1024) chain_kernel(const ChainParams cp) {
       }
       if (lane == 0) *cp.edge_count = s_cnt;
     }
-    mark();
-    if (dbg && tid == 0) dbg[31] = dbg_i;
     return;
   }
   if (!cp.backtrack) return;
@@ -1294,7 +1244,6 @@ __global__ void __launch_bounds__(1024) chain_kernel(const ChainParams cp) {
       }
     }
     __syncthreads();
-    mark();
     if (tid == 0) *cp.total = s_status ? kInf64 : G[0];
     if (s_status == 0)
       for (int n = tid; n < N; n += nth) {
@@ -1341,7 +1290,6 @@ __global__ void __launch_bounds__(1024) chain_kernel(const ChainParams cp) {
     }
   }
   __syncthreads();
-  mark();
   if (tid == 0) *cp.status = s_status;
   if (s_status != 0) return;
   __syncthreads();
@@ -1357,8 +1305,6 @@ __global__ void __launch_bounds__(1024) chain_kernel(const ChainParams cp) {
     cp.digits[w] = dval;
   }
   __syncthreads();
-  mark();
-  if (dbg && tid == 0) dbg[31] = dbg_i;
 }
 
 // --------------------------------------------------------------------------
@@ -1473,17 +1419,6 @@ cudaError_t launch_enum(const EnumParams& p, int NB, int64_t nthreads, size_t sm
 }
 
 
-cudaError_t argmin_debug_read(uint64_t* out16) {
-  cudaError_t e = cudaMemcpyFromSymbol(out16, g_argmin_dbg, 16 * sizeof(uint64_t));
-  if (e != cudaSuccess) return e;
-  uint64_t t[16];
-  e = cudaMemcpyFromSymbol(t, g_enum_dbg2, 16 * sizeof(uint64_t));
-  if (e != cudaSuccess) return e;
-  fprintf(stderr, "enum CTA0 (us): prologue %.2f main %.2f | tau0 X %.2f fold %.2f red %.2f\n",
-          (t[1] - t[0]) * 1e-3, (t[2] - t[1]) * 1e-3, (t[3] - t[2]) * 1e-3, (t[4] - t[3]) * 1e-3,
-          (t[5] - t[4]) * 1e-3);
-  return cudaSuccess;
-}
 
 template <typename V>
 cudaError_t launch_argmin(const ArgminParams* aps, const ArgminEntry* list, const int32_t* count, int grid,
