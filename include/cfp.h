@@ -202,6 +202,9 @@ typedef struct {
   int32_t kernel_launches;     /* kernels launched by one cfp_execute */
   int32_t prefix_len[CFP_MAX_BLOCKS];   /* per type: enumeration schedule summary */
   int32_t nb[CFP_MAX_BLOCKS], na[CFP_MAX_BLOCKS];
+  int32_t fused_tail;          /* 1: bucket minima + chain + argmin + backtrack run as one
+                                  cooperative launch (world 1); 0: separate launches */
+  int32_t tail_grid;           /* CTAs of that launch */
 } cfp_prepared_info;
 cfp_status cfp_prepared_query(const cfp_prepared* prep, cfp_prepared_info* info);
 /* Record CUDA events on the ctx stream during the next cfp_execute calls

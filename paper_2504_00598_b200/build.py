@@ -47,7 +47,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
 
     def compile_one(src_obj):
         src, obj = src_obj
-        cmd = [nvcc, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
+        extra = os.environ.get("CFP_NVCC_DEFINES", "").split()   # development builds only (e.g. -DCFP_TAIL_TRACE)
+        cmd = [nvcc, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", *extra,
                "-Xptxas", "-v" if verbose else "-O3", "-I", inc, "-I", os.path.join(ROOT, "include"),
                "-c", os.path.join(CSRC, src), "-o", obj]
         subprocess.check_call(cmd)

@@ -88,7 +88,8 @@ class cfp_prepared_info(C.Structure):
     _fields_ = [("combos", C.c_double), ("combos_local", C.c_double), ("evals", C.c_double),
                 ("num_types", C.c_int32), ("num_transitions", C.c_int32), ("wide_types", C.c_int32),
                 ("kernel_launches", C.c_int32), ("prefix_len", C.c_int32 * 32),
-                ("nb", C.c_int32 * 32), ("na", C.c_int32 * 32)]
+                ("nb", C.c_int32 * 32), ("na", C.c_int32 * 32), ("fused_tail", C.c_int32),
+                ("tail_grid", C.c_int32)]
 
 
 EXPORTS = ["cfp_ctx_create", "cfp_ctx_destroy", "cfp_last_error", "cfp_nccl_unique_id",
@@ -291,6 +292,8 @@ class PreparedInfo:
     wide_types: int
     kernel_launches: int
     schedule: List[Tuple[int, int, int, int]]   # per type (prefix_len, NB, VG, na)
+    fused_tail: bool = False
+    tail_grid: int = 0
 
 
 class Context:
@@ -521,7 +524,7 @@ class Prepared:
         _check(lib().cfp_prepared_query(self._h, C.byref(i)))
         sched = [(i.prefix_len[t], i.nb[t] // 100, i.nb[t] % 100, i.na[t]) for t in range(i.num_types)]
         return PreparedInfo(i.combos, i.combos_local, i.evals, i.num_types, i.num_transitions,
-                            i.wide_types, i.kernel_launches, sched)
+                            i.wide_types, i.kernel_launches, sched, bool(i.fused_tail), i.tail_grid)
 
     def time_kernels(self, on=True):
         """0 off, 1 (True): events around a0 / enumeration / whole path, 2: + every phase."""

@@ -35,6 +35,8 @@ template <typename V> cudaError_t launch_fill(V*, int64_t, V, cudaStream_t);
 template <typename V> cudaError_t launch_enum(const EnumParams&, int, int64_t, size_t, cudaStream_t);
 template <typename V> cudaError_t launch_argmin(const ArgminParams*, const ArgminEntry*, const int32_t*, int, int, int, cudaStream_t);
 cudaError_t launch_chain(const ChainParams&, cudaStream_t);
+cudaError_t launch_tail(const TailParams&, int, size_t, cudaStream_t);
+cudaError_t tail_max_blocks(size_t, int*);
 cudaError_t launch_intpipe(int, int, int, uint32_t*, cudaStream_t);
 template <typename V> cudaError_t launch_amin(const ArgminParams*, const int64_t*, int, int64_t, cudaStream_t);
 cudaError_t launch_all_pairs(const int64_t*, int, int64_t, ArgminEntry*, int32_t*, cudaStream_t);
@@ -86,6 +88,8 @@ struct cfp_ctx {
   bool sim = false;                 // world > 1 without a communicator: shard simulation (test hook)
   bool sharded = false;             // rank-local tables + merge path (world > 1, or a 1-rank communicator)
   bool plan_cache = true;           // CFP_PLAN_CACHE=0: no structure-keyed reuse in cfp_search_plan
+  bool fused_tail = true;           // CFP_FUSED_TAIL=0: separate launches after the enumeration (A/B, tests)
+  bool tail_squaring = false;       // CFP_TAIL_SQUARING=1: fused chain by repeated squaring (A/B, tests)
   cfp_prepared* cached = nullptr;   // last cfp_search_plan's prepared plan (device buffers, schedule)
   std::vector<int64_t> cached_key;  //   and its structural key (plan_key)
   bool mem_chain_fused = true;      // CFP_MEM_CHAIN_FUSED=0: one launch per DP step (A/B tests)
@@ -136,6 +140,8 @@ extern "C" cfp_status cfp_ctx_create(cfp_ctx** out, const cfp_ctx_opts* opts) {
   if (const char* dd = getenv("CFP_DEDUP")) c->dedup = atoi(dd) != 0;
   if (const char* mf = getenv("CFP_MEM_CHAIN_FUSED")) c->mem_chain_fused = atoi(mf) != 0;
   if (const char* pc = getenv("CFP_PLAN_CACHE")) c->plan_cache = atoi(pc) != 0;
+  if (const char* ft = getenv("CFP_FUSED_TAIL")) c->fused_tail = atoi(ft) != 0;
+  if (const char* sq = getenv("CFP_TAIL_SQUARING")) c->tail_squaring = atoi(sq) != 0;
   if (const char* ms = getenv("CFP_ENUM_MSPLIT_MIN_M")) c->msplit_min_m = std::max(2LL, atoll(ms));
   if (opts && opts->cuda_stream) {
     c->stream = (cudaStream_t)opts->cuda_stream;
@@ -345,6 +351,12 @@ struct cfp_prepared {
   std::vector<CompactJob> hjobs32, hjobs64;
   std::vector<EpiTau> epi_host;
   DevBuf epi, aps, pair_off, locAI, edges, reach;
+  // fused tail (world 1): one cooperative launch after the enumeration
+  bool fused_tail = false;
+  int tail_grid = 0;
+  size_t tail_smem = 0;
+  TailParams tp{};
+  DevBuf orig_off, tail_sync, phase_ts;
   int64_t reach_bytes = 0;
   int64_t ai = 0, npairs = 0;
   bool has32 = false, has64 = false, use_edges = false;
@@ -1292,13 +1304,13 @@ static cfp_status prepare_impl(cfp_ctx* ctx, const cfp_problem* p, bool do_chain
   for (auto& s : P->hspecs32) {
     s.out_off += v32;
     s.block0 = P->spec_max32;
-    s.nblocks = std::max<int64_t>(1, (s.rows * s.row + 1023) / 1024);
+    s.nblocks = std::max<int64_t>(1, (s.rows * s.row + kBuildChunk - 1) / kBuildChunk);
     P->spec_max32 += s.nblocks;                       // total CTAs of the build launch
   }
   for (auto& s : P->hspecs64) {
     s.out_off += v64;
     s.block0 = P->spec_max64;
-    s.nblocks = std::max<int64_t>(1, (s.rows * s.row + 1023) / 1024);
+    s.nblocks = std::max<int64_t>(1, (s.rows * s.row + kBuildChunk - 1) / kBuildChunk);
     P->spec_max64 += s.nblocks;
   }
   // epilogue transition descriptors (chunkmin pointers patched below)
@@ -1369,6 +1381,14 @@ static cfp_status prepare_impl(cfp_ctx* ctx, const cfp_problem* p, bool do_chain
       P->epi_host[te.epi_off + q].chunkmin = P->trans[trans_slot[te.trans[q]]].fp.chunkmin;
     ep.taus = P->epi.as<EpiTau>() + te.epi_off;
     ep.vals = vals;
+  }
+  for (size_t q = 0; q < P->trans.size(); ++q) {   // outputs of every transition, empty types included
+    TransExec& tx = P->trans[q];
+    tx.ap.A_out = argA + tx.out_off;
+    tx.ap.I_out = argI + tx.out_off;
+    tx.ap.A_glob = outA + tx.out_off;
+    tx.ap.slot = (int)q;
+    tx.ap.Do_orig = tx.Do_orig;
   }
   {
     // device copies of the per-transition argmin descriptors + bucket offsets
@@ -1501,6 +1521,81 @@ static cfp_status prepare_impl(cfp_ctx* ctx, const cfp_problem* p, bool do_chain
       P->reach_bytes = goff[N];
     }
   }
+  // ---- fused tail (world 1): bucket minima, chain, argmin, backtrack in one launch
+  int chain_levels = 0, chain_smax = 1;
+  if (do_chain) {
+    for (const TransExec& tx : P->trans) chain_smax = std::max(chain_smax, std::max(tx.Din, tx.Do_orig));
+    for (int n = 0; n < P->N;) {                     // runs as the chain setup forms them
+      int m = n + 1;
+      while (m < P->N && P->inst[m] == P->inst[n] && P->inst_rows[n] == P->inst_cols[n]) ++m;
+      int levels = 0;
+      while ((1 << (levels + 1)) <= m - n) ++levels;
+      if (m - n > 1) chain_levels = std::max(chain_levels, levels);
+      n = m;
+    }
+  }
+  if (ctx->fused_tail && !ctx->sharded && P->trans.size() <= 32 &&
+      (!do_chain || (P->use_edges && chain_smax <= 32))) {
+    // worker CTAs: digit scratch [K][threads] u16, descriptor copies, every slot's W/R tables
+    auto al = [](size_t x) { return (x + 15) & ~(size_t)15; };
+    size_t off = al((size_t)P->kmax_arg * kTailThreads * 2);
+    const size_t desc_off = off;
+    off = al(off + P->trans.size() * sizeof(ArgminParams));
+    std::vector<int64_t> tab_off(P->trans.size(), 0);
+    for (size_t q = 0; q < P->trans.size(); ++q) {
+      const TypeExec& te = P->types[type_slot[P->trans[q].type]];
+      tab_off[q] = (int64_t)off;
+      off = al(off + (size_t)te.es.tab_n * (te.wide ? 8 : 4));
+    }
+    size_t smem = off;
+    if (do_chain) {
+      const FusedChainLayout L(P->cp.mat_elems, P->inst_rows[0] + [&] {
+        int64_t c = 0;
+        for (int n = 0; n < P->N; ++n) c += P->inst_cols[n];
+        return c;
+      }(), [&] {
+        int64_t r = 0;
+        for (int n = 0; n < P->N; ++n) r += P->inst_rows[n];
+        return r;
+      }(), P->N, P->cp.nmat, chain_levels, chain_smax);
+      smem = std::max(smem, (size_t)L.bytes);
+    }
+    int optin = 0, per_sm = 0;
+    CUDA_TRY(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, ctx->device));
+    if (smem + 40 * 1024 <= (size_t)optin) CUDA_TRY(tail_max_blocks(smem, &per_sm));
+    if (per_sm >= 1 && ctx->sms >= 2) {              // co-resident CTAs (cooperative launch)
+      std::vector<int64_t> oo(P->trans.size() + 1, 0);
+      for (size_t q = 0; q < P->trans.size(); ++q)
+        oo[q + 1] = oo[q] + (int64_t)P->trans[q].Din * P->trans[q].Do_orig;
+      CUDA_TRY(P->orig_off.alloc(oo.size() * 8));
+      CUDA_TRY(cudaMemcpyAsync(P->orig_off.p, oo.data(), oo.size() * 8, cudaMemcpyHostToDevice, st));
+      CUDA_TRY(P->tail_sync.alloc(16));
+      CUDA_TRY(cudaMemsetAsync(P->tail_sync.p, 0, 16, st));
+      CUDA_TRY(P->phase_ts.alloc(8 * 8));
+      TailParams& tp = P->tp;
+      tp.aps = P->aps.as<ArgminParams>();
+      tp.pair_off = P->pair_off.as<int64_t>();
+      tp.orig_off = P->orig_off.as<int64_t>();
+      tp.nslot = (int)P->trans.size();
+      tp.chain = do_chain ? 1 : 0;
+      if (do_chain) tp.cp = P->cp;
+      tp.sync = P->tail_sync.as<unsigned int>();
+      tp.phase_ts = nullptr;
+      tp.squaring = ctx->tail_squaring ? 1 : 0;
+      tp.levels = chain_levels;
+      tp.smax = chain_smax;
+      tp.kmax_arg = P->kmax_arg;
+      tp.arg_desc_off = (int64_t)desc_off;
+      for (size_t q = 0; q < P->trans.size(); ++q) tp.arg_tab_off[q] = tab_off[q];
+      const int64_t warps = oo.back();                // phase 1: a warp per bucket
+      const int64_t wpc = kTailThreads / 32;
+      int64_t g = do_chain ? std::max<int64_t>(8, (warps + wpc - 1) / wpc + 1) : std::max<int64_t>(1, P->npairs);
+      g = std::max<int64_t>(2, std::min<int64_t>(g, (int64_t)ctx->sms * per_sm));
+      P->tail_grid = (int)g;
+      P->tail_smem = smem;
+      P->fused_tail = true;
+    }
+  }
   tm.mark("chain");
   CUDA_TRY(cudaStreamSynchronize(st));
   tm.mark("sync");
@@ -1591,6 +1686,17 @@ static cfp_status execute_impl(cfp_ctx* ctx, cfp_prepared* P) {
     }
   }
   if (P->timing) CUDA_TRY(cudaEventRecord(P->ev[2], st));
+  if (P->fused_tail) {
+    TailParams tp = P->tp;
+    tp.phase_ts = P->timing >= 2 ? P->phase_ts.as<uint64_t>() : nullptr;
+    CUDA_TRY(launch_tail(tp, P->tail_grid, P->tail_smem, st));
+    P->launches++;
+    CUDA_TRY(phase(4));
+    CUDA_TRY(phase(5));
+    CUDA_TRY(phase(6));
+    if (P->timing) CUDA_TRY(cudaEventRecord(P->ev[3], st));
+    return CFP_OK;
+  }
   uint64_t* outA = P->outAI.as<uint64_t>();
   const int64_t ai = P->ai;
   // outputs default to (INF, NOIDX): covers pruned output strategies, empty types
@@ -1801,6 +1907,8 @@ extern "C" cfp_status cfp_prepared_query(const cfp_prepared* P, cfp_prepared_inf
   info->num_types = (int)P->types.size();
   info->num_transitions = (int)P->trans.size();
   info->kernel_launches = P->launches;
+  info->fused_tail = P->fused_tail ? 1 : 0;
+  info->tail_grid = P->tail_grid;
   for (size_t i = 0; i < P->types.size() && i < CFP_MAX_BLOCKS; ++i) {
     info->wide_types += P->types[i].wide;
     info->prefix_len[i] = P->types[i].P;
@@ -1826,6 +1934,16 @@ extern "C" cfp_status cfp_prepared_phase_ms(cfp_prepared* P, double* ms) {
     float t = 0;
     CUDA_TRY(cudaEventElapsedTime(&t, P->ev[from[i]], P->ev[to[i]]));
     ms[i] = t;
+  }
+  if (P->fused_tail && P->tp.chain) {
+    // one launch: split its event time by CTA 0's %globaltimer marks (phase
+    // boundaries: start, bucket minima done, chain done, argmins done, end)
+    uint64_t t[5];
+    CUDA_TRY(cudaMemcpy(t, P->phase_ts.p, sizeof(t), cudaMemcpyDeviceToHost));
+    const double tail = ms[2];
+    const double tot = (double)(t[4] - t[0]);
+    const double f[4] = {(double)(t[1] - t[0]), (double)(t[2] - t[1]), (double)(t[3] - t[2]), (double)(t[4] - t[3])};
+    for (int i = 0; i < 4; ++i) ms[2 + i] = tot > 0 ? tail * f[i] / tot : 0.0;
   }
   return CFP_OK;
 }

@@ -25,6 +25,7 @@ constexpr int kMaxDigits = 32;
 constexpr int kMaxTerms = 96;
 constexpr int kMaxCross = 16;    // cross edges per transition
 constexpr int kBlock = 256;          // threads per CTA of the enumeration kernel
+constexpr int kBuildChunk = 1024;    // table entries per CTA of build_table_kernel
 constexpr uint32_t kCap32 = 0x7FFFFFFFu;            // narrow "infinity" (>= CAP => INF)
 constexpr uint64_t kCap64 = 0x7FFFFFFFFFFFFFFFull;  // wide "infinity"
 constexpr uint64_t kInf64 = 0xFFFFFFFFFFFFFFFFull;
@@ -217,6 +218,57 @@ struct ChainParams {
   const uint64_t* baseA;        // all distinct A matrices, contiguous (moff offsets)
   const uint64_t* baseI;        // same for I (backtrack)
 };
+
+#ifndef CFP_TAIL_THREADS
+#define CFP_TAIL_THREADS 512
+#endif
+constexpr int kTailThreads = CFP_TAIL_THREADS;   // threads per CTA of the fused tail kernel
+
+// Shared-memory layout of the fused tail's chain (CTA 0; every state count
+// <= 32).  Host and device compute it from the same numbers.
+struct FusedChainLayout {
+  int64_t sA, sG, sP, sgoff, smoff, sinst, om, rmask, ebits, nxt, vseq, bytes;
+  __host__ __device__ static int64_t al(int64_t x) { return (x + 15) & ~int64_t(15); }
+  __host__ __device__ FusedChainLayout(int64_t mat_elems, int64_t gtot, int64_t goffN, int N, int nmat,
+                                       int levels, int S) {
+    int64_t o = 0;
+    sA = o;    o = al(o + mat_elems * 8);
+    sG = o;    o = al(o + gtot * 8);
+    sP = o;    o = al(o + (int64_t)(levels + 1) * S * S * 8);   // P_0 .. P_levels (big encoding)
+    sgoff = o; o = al(o + (int64_t)(N + 2) * 8);
+    smoff = o; o = al(o + (int64_t)nmat * 8);
+    sinst = o; o = al(o + (int64_t)N * 16);
+    om = o;    o = al(o + goffN * 4);
+    rmask = o; o = al(o + (int64_t)N * 4);
+    ebits = o; o = al(o + ((mat_elems + 31) / 32) * 4);
+    nxt = o;   o = al(o + goffN * 1);
+    vseq = o;  o = al(o + (int64_t)N * 4);
+    bytes = o;
+  }
+};
+
+// Fused tail of one execute (world 1): bucket minima of every transition,
+// then (chain = 1) suffix vectors + reachable optimal edges on CTA 0, the
+// least-index argmin of those buckets on the other CTAs, and the backtrack on
+// CTA 0 -- one cooperative launch with grid barriers between the phases
+// (chain = 0: the argmin of every bucket, cfp_segment_costs).
+struct TailParams {
+  const ArgminParams* aps;      // [nslot]
+  const int64_t* pair_off;      // [nslot + 1] compact buckets (Din * Do) per slot
+  const int64_t* orig_off;      // [nslot + 1] caller-layout buckets (Din * Do_orig) per slot
+  int32_t nslot;
+  int32_t chain;
+  ChainParams cp;               // shared-memory chain (cp.mode set per part by the kernel)
+  unsigned int* sync;           // [4] zero between launches (the kernel leaves them zero)
+  uint64_t* phase_ts;           // nullable: %globaltimer of CTA 0 at each phase boundary [5]
+  int32_t squaring;             // chain: 1 repeated squaring + doubling for runs, 0 sequential recurrence
+  int32_t levels;               // chain: largest squaring level of a run (P_0 .. P_levels)
+  int32_t smax;                 // chain: largest state count (<= 32)
+  int32_t kmax_arg;             // argmin: largest K (digit scratch [K][1024] u16)
+  int64_t arg_tab_off[32];      // argmin: byte offset of slot s's staged W/R tables (16-aligned), nslot <= 32
+  int64_t arg_desc_off;         // argmin: byte offset of the descriptor copies [nslot]
+};
+
 
 // ---------------------------------------------------------------------------
 // Memory-constrained search (cfp_mem.cu).

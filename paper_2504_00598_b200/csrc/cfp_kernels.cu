@@ -27,6 +27,23 @@
 
 namespace cfp {
 
+// Development-only phase trace of the fused tail (build with -DCFP_TAIL_TRACE;
+// compiled out of the library otherwise).
+#ifdef CFP_TAIL_TRACE
+__device__ uint64_t g_trace[64];
+__device__ uint64_t g_trace_cta[256];
+#define TTRACE(cta, i)                                                                      \
+  do {                                                                                     \
+    if (threadIdx.x == 0 && blockIdx.x == (cta)) {                                         \
+      uint64_t t_;                                                                         \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                              \
+      g_trace[(i)] = t_;                                                                   \
+    }                                                                                      \
+  } while (0)
+#else
+#define TTRACE(cta, i) do { } while (0)
+#endif
+
 template <typename V> struct VT;
 template <> struct VT<uint32_t> {
   static constexpr uint32_t CAP = kCap32;
@@ -117,7 +134,7 @@ __global__ void compact_kernel(const CompactJob* __restrict__ jobs, const uint32
   if (j.kind == 3) {                              // transposed cross table Q^T[s][u]
     const int64_t n = (int64_t)j.cols * j.rows_pad;
     for (int64_t e = threadIdx.x; e < n; e += blockDim.x) {
-      const int32_t c = (int32_t)(e / j.rows_pad), r = (int32_t)(e % j.rows_pad);
+      const int32_t c = (int32_t)((uint32_t)e / (uint32_t)j.rows_pad), r = (int32_t)((uint32_t)e % (uint32_t)j.rows_pad);
       V v = VT<V>::CAP;
       if (r < j.rows) {
         const int32_t rc = j.map_c >= 0 ? maps[j.map_c + c] : c;
@@ -128,9 +145,9 @@ __global__ void compact_kernel(const CompactJob* __restrict__ jobs, const uint32
     }
     return;
   }
-  const int64_t n = (int64_t)j.rows * j.cols;
+  const int64_t n = (int64_t)j.rows * j.cols;       // tables are small: 32-bit index math
   for (int64_t e = threadIdx.x; e < n; e += blockDim.x) {
-    const int32_t r = (int32_t)(e / j.cols), c = (int32_t)(e % j.cols);
+    const int32_t r = (int32_t)((uint32_t)e / (uint32_t)j.cols), c = (int32_t)((uint32_t)e % (uint32_t)j.cols);
     const int32_t rc = j.map_c >= 0 ? maps[j.map_c + c] : c;
     V v;
     if (j.kind == 0) {
@@ -155,15 +172,38 @@ __global__ void compact_kernel(const CompactJob* __restrict__ jobs, const uint32
 // host assigned to each table, over the table's mixed-radix index space.
 // --------------------------------------------------------------------------
 template <typename V>
-__global__ void build_table_kernel(const TableSpec* __restrict__ specs, const V* __restrict__ vals,
+__global__ void build_table_kernel(const TableSpec* __restrict__ specs, int nspecs, const V* __restrict__ vals,
                                    V* __restrict__ out) {
-  int si = 0;
-  while (blockIdx.x >= specs[si].block0 + specs[si].nblocks) ++si;   // block -> table
-  const TableSpec& s = specs[si];
-  const int64_t total = min(s.rows * s.row, (int64_t)(blockIdx.x - s.block0 + 1) * 1024);
+  // block -> table: the specs' block ranges tested in parallel (one round trip)
+  __shared__ int s_si;
+  if (threadIdx.x < 32) {
+    int found = -1;
+    for (int base = 0; found < 0 && base < nspecs; base += 32) {
+      const int i = base + (int)threadIdx.x;
+      const bool in = i < nspecs && (int64_t)blockIdx.x >= specs[i].block0 &&
+                      (int64_t)blockIdx.x < specs[i].block0 + specs[i].nblocks;
+      const unsigned m = __ballot_sync(0xffffffffu, in);
+      if (m) found = base + __ffs(m) - 1;
+    }
+    if (threadIdx.x == 0) s_si = found;
+  }
+  __syncthreads();
+  const int si = s_si;
+  // the spec (radices, term list) in shared memory: the per-entry loop reads
+  // it for every term, and a global read per field made that a chain of
+  // dependent L1/L2 round trips
+  __shared__ __align__(16) TableSpec s;
+  {
+    const int words = (int)(sizeof(TableSpec) / 4);
+    const uint32_t* src = reinterpret_cast<const uint32_t*>(specs + si);
+    uint32_t* dst = reinterpret_cast<uint32_t*>(&s);
+    for (int i = threadIdx.x; i < words; i += blockDim.x) dst[i] = src[i];
+  }
+  __syncthreads();
+  const int64_t total = min(s.rows * s.row, (int64_t)(blockIdx.x - s.block0 + 1) * kBuildChunk);
   __shared__ int32_t sdig[kMaxDigits][256];       // per-thread digits (dynamic index)
   const bool small = total < 0x7FFFFFFF && s.row < 0x7FFFFFFF;
-  for (int64_t e = (blockIdx.x - s.block0) * 1024 + threadIdx.x; e < total; e += blockDim.x) {
+  for (int64_t e = (blockIdx.x - s.block0) * kBuildChunk + threadIdx.x; e < total; e += blockDim.x) {
     int64_t r, c;
     if (small) {
       r = (uint32_t)e / (uint32_t)s.row;
@@ -674,9 +714,9 @@ __device__ __forceinline__ void load4(const V* p, V* out) {
 //     whose intra cost equals B_p*[v];
 //  4. outputs in the caller's (unpruned) layout: A[u][v_orig], I[u][v_orig].
 // --------------------------------------------------------------------------
-template <typename V>
-__device__ void argmin_pair(const ArgminParams& ap, const int pair, unsigned char* smem_raw) {
-  constexpr int NT = 256;
+template <typename V, int NT>
+__device__ void argmin_pair(const ArgminParams& ap, const int pair, unsigned char* smem_raw,
+                            const V* pre_tabs = nullptr, const int64_t* hb_pre = nullptr) {
   const int tid = threadIdx.x;
   // descriptor pieces used inside loops -> shared memory (one global read each)
   __shared__ Term s_terms[kMaxTerms];
@@ -688,8 +728,14 @@ __device__ void argmin_pair(const ArgminParams& ap, const int pair, unsigned cha
   const EvalSpec& e = ap.e;
   const FoldParams& f = ap.f;
   for (int i = tid; i < e.nterm; i += NT) s_terms[i] = e.term[i];
-  for (int i = tid; i < f.nq; i += NT) s_q[i] = f.q[i];
+  __shared__ uint32_t s_qstr[kMaxCross], s_qrad[kMaxCross];   // consumer digit of each cross term
+  for (int i = tid; i < f.nq; i += NT) {
+    s_q[i] = f.q[i];
+    s_qstr[i] = (uint32_t)f.pre_stride[f.q[i].a];
+    s_qrad[i] = (uint32_t)e.radix[f.q[i].a];
+  }
   for (int i = tid; i < e.K; i += NT) s_rad[i] = e.radix[i];
+  TTRACE(2, 20);
   if (tid == 0) {
     s_misc[0] = f.nchunks; s_misc[1] = f.nhb; s_misc[2] = f.G; s_misc[3] = f.W;
     s_misc[4] = f.p_lo; s_misc[5] = f.Do; s_misc[6] = (int64_t)(uintptr_t)f.chunkmin;
@@ -705,28 +751,36 @@ __device__ void argmin_pair(const ArgminParams& ap, const int pair, unsigned cha
   const V* vals = static_cast<const V*>(f.vals);
   const int K = e.K, P = e.P, o = e.o, nterm = e.nterm, nq = f.nq;
   uint16_t* sd = reinterpret_cast<uint16_t*>(smem_raw);        // [K][NT] digits
-  V* tabs = reinterpret_cast<V*>(smem_raw + (((size_t)K * NT * 2 + 15) & ~(size_t)15));   // W/R tables
+  const V* tabs = pre_tabs;                                     // W/R tables (staged by the caller)
+  if (!pre_tabs) {
+  V* st = reinterpret_cast<V*>(smem_raw + (((size_t)K * NT * 2 + 15) & ~(size_t)15));
+  tabs = st;
   for (int i0 = tid; i0 < e.tab_n; i0 += NT * 8) {   // 8 loads in flight per thread
     V t8[8];
 #pragma unroll
     for (int k = 0; k < 8; ++k) t8[k] = i0 + k * NT < e.tab_n ? vals[e.tab_lo + i0 + k * NT] : (V)0;
 #pragma unroll
     for (int k = 0; k < 8; ++k)
-      if (i0 + k * NT < e.tab_n) tabs[i0 + k * NT] = t8[k];
+      if (i0 + k * NT < e.tab_n) st[i0 + k * NT] = t8[k];
+  }
   }
   const int u = pair / Do, v = pair - (pair / Do) * Do;
+  TTRACE(2, 21);
   const int64_t outi = (int64_t)u * ap.Do_orig + ap.vmap[v];
   // 1. the bucket minimum is the (merged) A computed by amin_kernel
-  const uint64_t Ag = ap.A_glob[outi];
+  const uint64_t Ag = __ldcg(ap.A_glob + outi);    // L2: written by other CTAs in the fused tail
   if (Ag == kInf64) {
     if (tid == 0) { ap.A_out[outi] = kInf64; ap.I_out[outi] = kInf64; }
     return;
   }
   const V best = (V)Ag;
-  // 2. chunks of this rank attaining it (none: this rank holds no candidate)
-  constexpr int LIST = 4 * NT;
+  // 2. chunks of this rank attaining it (none: this rank holds no candidate);
+  //    the fused tail's bucket-minimum pass already found the least attaining
+  //    h-block (hb_pre) -- then steps 1-2 are skipped
+  const int64_t hb_known = hb_pre ? __ldcg(hb_pre + pair) : -1;
+  constexpr int LIST = 4 * NT > 1024 ? 1024 : 4 * NT;
   __shared__ int64_t s_list[LIST];
-  for (int64_t c0 = (int64_t)tid * 4; c0 < nchunks; c0 += NT * 4) {
+  for (int64_t c0 = (int64_t)tid * 4; hb_known < 0 && c0 < nchunks; c0 += NT * 4) {
     V x[4];
 #pragma unroll
     for (int q = 0; q < 4; ++q) x[q] = c0 + q < nchunks ? cm[c0 + q] : VT<V>::CAP;
@@ -738,7 +792,8 @@ __device__ void argmin_pair(const ArgminParams& ap, const int pair, unsigned cha
       }
   }
   __syncthreads();
-  const int cnt_all = s_cnt;
+  const int cnt_all = hb_known >= 0 ? 1 : s_cnt;
+  TTRACE(2, 22);
   if (cnt_all == 0) {                               // possible only with world > 1
     if (tid == 0) { ap.A_out[outi] = kInf64; ap.I_out[outi] = kInf64; }
     return;
@@ -747,9 +802,10 @@ __device__ void argmin_pair(const ArgminParams& ap, const int pair, unsigned cha
   // order and every attaining chunk holds an attaining row: p* lies in the
   // chunks of the least attaining h-block
   __shared__ long long s_hbmin;
-  if (tid == 0) s_hbmin = 0x7FFFFFFFFFFFFFFFLL;
+  if (tid == 0) s_hbmin = hb_known >= 0 ? hb_known : 0x7FFFFFFFFFFFFFFFLL;
   __syncthreads();
-  if (cnt_all <= LIST) {
+  if (hb_known >= 0) {
+  } else if (cnt_all <= LIST) {
     for (int li = tid; li < cnt_all; li += NT) atomicMin(&s_hbmin, (long long)(s_list[li] % nhb));
   } else {
     for (int64_t c = tid; c < nchunks; c += NT)
@@ -757,6 +813,7 @@ __device__ void argmin_pair(const ArgminParams& ap, const int pair, unsigned cha
   }
   __syncthreads();
   const int64_t hbmin = s_hbmin;
+  TTRACE(2, 23);
   // rows of the chunks (l, hbmin), l < W, attaining the minimum
   __shared__ int32_t s_ls[NT];
   __shared__ int s_nl;
@@ -771,23 +828,43 @@ __device__ void argmin_pair(const ArgminParams& ap, const int pair, unsigned cha
   const int nl = min(s_nl, NT);                       // W > NT with > NT hits: rare, see below
   const bool all_l = s_nl > NT;
   const int64_t CH = f.CH;
-  for (int64_t w = tid; w < (all_l ? W : (int64_t)nl) * CH; w += NT) {
-    const int64_t li = w / CH, i = w - li * CH;
+  const int64_t nrow = (all_l ? W : (int64_t)nl) * CH;
+  const bool narrow_ix = nrow < 0x7FFFFFFF && p_lo + (hbmin + 1) * CH * W < 0x7FFFFFFF;
+#pragma unroll 2
+  for (int64_t w = tid; w < nrow; w += NT) {
+    int64_t li, i;
+    if (narrow_ix) {
+      li = (uint32_t)w / (uint32_t)CH;
+      i = (uint32_t)w - (uint32_t)li * (uint32_t)CH;
+    } else {
+      li = w / CH;
+      i = w - li * CH;
+    }
     const int64_t l = all_l ? li : s_ls[li];
     const int64_t hh = hbmin * CH + i;
     if (hh >= Gh) continue;
     if (all_l && cm[l * nhb + hbmin] != best) continue;
     const int64_t plr = hh * W + l;
     const int64_t pg = p_lo + plr;
+    const V b = Bp[plr * Do + v];
     V x = 0;
-    for (int qi = 0; qi < nq; ++qi) {
-      const Term q = s_q[qi];
-      x = VT<V>::sat(x, vals[q.off + (int64_t)u * q.db + prefix_digit(pg, q.a, P, s_rad)]);
+    if (narrow_ix) {                                 // 32-bit digit extraction by stride
+      const uint32_t pq = (uint32_t)pg;
+      for (int qi = 0; qi < nq; ++qi) {
+        const uint32_t d = (pq / s_qstr[qi]) % s_qrad[qi];
+        x = VT<V>::sat(x, vals[s_q[qi].off + (int64_t)u * s_q[qi].db + d]);
+      }
+    } else {
+      for (int qi = 0; qi < nq; ++qi) {
+        const Term q = s_q[qi];
+        x = VT<V>::sat(x, vals[q.off + (int64_t)u * q.db + prefix_digit(pg, q.a, P, s_rad)]);
+      }
     }
-    if (VT<V>::sat(x, Bp[plr * Do + v]) == best) atomicMin(&s_first, (unsigned long long)plr);
+    if (VT<V>::sat(x, b) == best) atomicMin(&s_first, (unsigned long long)plr);
   }
   __syncthreads();
   const int64_t pl = (int64_t)s_first;
+  TTRACE(2, 24);
   __syncthreads();
   if (tid == 0) s_first = ~0ull;
   const uint64_t target = (uint64_t)Bp[pl * Do + v];
@@ -803,6 +880,7 @@ __device__ void argmin_pair(const ArgminParams& ap, const int pair, unsigned cha
   // 3. least suffix (canonical order, s_o = v if o is a suffix digit) whose
   //    intra cost equals B_p*[v]
   const int64_t per = (nrest + NT - 1) / NT;
+  TTRACE(2, 25);
   const int64_t lo = (int64_t)tid * per;
   const int64_t hi = min(nrest, lo + per);
   if (lo < hi) {
@@ -858,7 +936,7 @@ __global__ void __launch_bounds__(256) argmin_kernel(const ArgminParams* __restr
     const ArgminEntry en = list[it];
     const ArgminParams& ap = aps[en.slot];
     if (ap.wide != wide) continue;                  // uniform per CTA
-    argmin_pair<V>(ap, en.pair, smem_raw);
+    argmin_pair<V, 256>(ap, en.pair, smem_raw);
     __syncthreads();
   }
 }
@@ -972,9 +1050,15 @@ __device__ __forceinline__ uint64_t warp_row_min(const uint64_t* row, const uint
 // goff[N] (rows of all instances) read from the parameter block's table
 __device__ __forceinline__ int64_t goff_n_of(const ChainParams& cp) { return cp.goff[cp.N]; }
 
+// part: kChainWhole = the kernel's cp.mode; inside the fused tail kernel (one
+// CTA, shared memory kept between the calls) kChainFusedEdges = mode 1 with the
+// A matrices read by plain loads (they were written by other CTAs of the same
+// launch) and no I staging, kChainFusedBacktrack = mode 2 with A, G and the
+// metadata still in shared memory from the first call and I loaded now.
+constexpr int kChainWhole = 0, kChainFusedEdges = 1, kChainFusedBacktrack = 2;
+
 template <bool SM>
-__global__ void __launch_bounds__(1024) chain_kernel(const ChainParams cp) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
+__device__ void chain_run(const ChainParams& cp, unsigned char* smem_raw, const int part) {
   const int tid = threadIdx.x, nth = blockDim.x;
   const int N = cp.N;
   uint64_t* sA = reinterpret_cast<uint64_t*>(smem_raw);
@@ -992,9 +1076,12 @@ __global__ void __launch_bounds__(1024) chain_kernel(const ChainParams cp) {
   uint64_t* G = SM ? sG : cp.G;
   uint64_t* Pw = SM ? sP : cp.powers;
   const int64_t* goff = SM ? sgoff : cp.goff;
-  if constexpr (SM) {
+  if (SM && part == kChainFusedBacktrack) {
+    for (int64_t e = tid; e < cp.mat_elems; e += nth) sI[e] = __ldcg(cp.baseI + e);   // other CTAs' writes
+    __syncthreads();
+  } else if constexpr (SM) {
     __shared__ __align__(8) uint64_t cbar;
-    const bool tma = (cp.mat_elems & 1) == 0;          // 16-byte multiples
+    const bool tma = part == kChainWhole && (cp.mat_elems & 1) == 0;   // 16-byte multiples
     if (tma) {
       if (tid == 0) {
         mbar_init(&cbar, 1);
@@ -1005,8 +1092,8 @@ __global__ void __launch_bounds__(1024) chain_kernel(const ChainParams cp) {
       }
     } else {
       for (int64_t e = tid; e < cp.mat_elems; e += nth) {
-        sA[e] = cp.baseA[e];
-        if (cp.backtrack) sI[e] = cp.baseI[e];
+        sA[e] = __ldcg(cp.baseA + e);
+        if (cp.backtrack && part == kChainWhole) sI[e] = cp.baseI[e];
       }
     }
     for (int i = tid; i < N + 2; i += nth) sgoff[i] = cp.goff[i];
@@ -1017,6 +1104,7 @@ __global__ void __launch_bounds__(1024) chain_kernel(const ChainParams cp) {
     if (tma) mbar_wait(&cbar, 0);
     __syncthreads();
   }
+  TTRACE(0, 1);
   auto rows_of = [&](int n) { return SM ? sinst[n].y : cp.inst[n].rows; };
   auto cols_of = [&](int n) { return SM ? sinst[n].z : cp.inst[n].cols; };
   auto mat_of = [&](int n) { return SM ? sinst[n].x : cp.inst[n].mat; };
@@ -1024,13 +1112,14 @@ __global__ void __launch_bounds__(1024) chain_kernel(const ChainParams cp) {
   auto matI = [&](int n) -> const uint64_t* { return SM ? sI + smoff[sinst[n].x] : cp.inst[n].I; };
   const int lastc = cols_of(N - 1);
   if (cp.mode == 2) {                               // suffix vectors already computed
-    if constexpr (SM)
+    if (SM && part != kChainFusedBacktrack)
       for (int64_t e2 = tid; e2 < goff[N + 1]; e2 += nth) G[e2] = cp.G[e2];
     __syncthreads();
   } else {
     for (int v = tid; v < lastc; v += nth) G[goff[N] + v] = cp.terminal ? cp.terminal[v] : 0;
     __syncthreads();
     for (int r = cp.nruns - 1; r >= 0; --r) {
+      TTRACE(0, 2 + min(cp.nruns - 1 - r, 7));
       const ChainRun run = cp.runs[r];
       const uint64_t* M = matA(run.first);
       const int R = rows_of(run.first), Cc = cols_of(run.first);
@@ -1076,6 +1165,7 @@ __global__ void __launch_bounds__(1024) chain_kernel(const ChainParams cp) {
     }
     if constexpr (SM)
       for (int64_t e2 = tid; e2 < goff[N + 1]; e2 += nth) cp.G[e2] = G[e2];
+    TTRACE(0, 10);
   }
   if (cp.mode == 1 && SM && cp.smax <= 32) {
     // optimal edges reachable from u_1 = 0, for <= 32 states per instance:
@@ -1129,6 +1219,7 @@ __global__ void __launch_bounds__(1024) chain_kernel(const ChainParams cp) {
     }
     __syncthreads();
     if (tid == 0) *cp.edge_count = s_cnt2;
+    TTRACE(0, 12);
     return;
   }
   if (cp.mode == 1) {
@@ -1186,6 +1277,7 @@ __global__ void __launch_bounds__(1024) chain_kernel(const ChainParams cp) {
     return;
   }
   if (!cp.backtrack) return;
+  TTRACE(0, 13);
   // forward greedy: at each instance the optimal successor with the least
   // combination index.  SM mode: the successor of every (n, u) is tabulated in
   // parallel first, then the walk from u_1 = 0 is a chain of shared loads.
@@ -1244,6 +1336,7 @@ __global__ void __launch_bounds__(1024) chain_kernel(const ChainParams cp) {
       }
     }
     __syncthreads();
+    TTRACE(0, 14);
     if (tid == 0) *cp.total = s_status ? kInf64 : G[0];
     if (s_status == 0)
       for (int n = tid; n < N; n += nth) {
@@ -1290,6 +1383,7 @@ __global__ void __launch_bounds__(1024) chain_kernel(const ChainParams cp) {
     }
   }
   __syncthreads();
+  TTRACE(0, 15);
   if (tid == 0) *cp.status = s_status;
   if (s_status != 0) return;
   __syncthreads();
@@ -1304,7 +1398,596 @@ __global__ void __launch_bounds__(1024) chain_kernel(const ChainParams cp) {
     }
     cp.digits[w] = dval;
   }
+  TTRACE(0, 16);
   __syncthreads();
+}
+
+template <bool SM>
+__global__ void __launch_bounds__(1024) chain_kernel(const ChainParams cp) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  chain_run<SM>(cp, smem_raw, kChainWhole);
+}
+
+// --------------------------------------------------------------------------
+// Fused tail: the chain on CTA 0 for state counts <= 32 (every layer graph of
+// the configs).  Values by repeated squaring + doubling in
+// the "big" encoding (INF -> 2^63 - 1, so an add never wraps and needs no INF
+// test; results >= 2^63 - 1 are INF); optimal-successor masks of every (n, u)
+// by warp ballots in parallel; reachability from u_1 = 0 as a bit walk; the
+// reachable optimal edges -> the argmin list.  The backtrack picks, per
+// reachable (n, u), the optimal successor with the least combination index.
+// --------------------------------------------------------------------------
+constexpr uint64_t kBigC = (1ull << 63) - 1;
+__device__ __forceinline__ uint64_t big_of(uint64_t x) { return x == kInf64 ? kBigC : x; }
+__device__ __forceinline__ uint64_t inf_of(uint64_t x) { return x >= kBigC ? kInf64 : x; }
+
+struct FusedChainSmem {
+  uint64_t *A, *G, *P;
+  int64_t *goff, *moff;
+  int4* inst;                   // (mat, rows, cols, K)
+  uint32_t *om, *rmask, *ebits;
+  int8_t* nxt;
+  int32_t* vseq;
+};
+
+__device__ __forceinline__ FusedChainSmem fused_chain_smem(const TailParams& tp, unsigned char* smem) {
+  const ChainParams& cp = tp.cp;
+  // goff[N] / goff[N + 1] are read from global here (metadata staged below)
+  const FusedChainLayout L(cp.mat_elems, cp.goff[cp.N + 1], cp.goff[cp.N], cp.N, cp.nmat, tp.levels, tp.smax);
+  FusedChainSmem s;
+  s.A = reinterpret_cast<uint64_t*>(smem + L.sA);
+  s.G = reinterpret_cast<uint64_t*>(smem + L.sG);
+  s.P = reinterpret_cast<uint64_t*>(smem + L.sP);
+  s.goff = reinterpret_cast<int64_t*>(smem + L.sgoff);
+  s.moff = reinterpret_cast<int64_t*>(smem + L.smoff);
+  s.inst = reinterpret_cast<int4*>(smem + L.sinst);
+  s.om = reinterpret_cast<uint32_t*>(smem + L.om);
+  s.rmask = reinterpret_cast<uint32_t*>(smem + L.rmask);
+  s.ebits = reinterpret_cast<uint32_t*>(smem + L.ebits);
+  s.nxt = reinterpret_cast<int8_t*>(smem + L.nxt);
+  s.vseq = reinterpret_cast<int32_t*>(smem + L.vseq);
+  return s;
+}
+
+// metadata only (independent of this launch's A): staged before the first barrier
+__device__ void fused_chain_meta(const TailParams& tp, const FusedChainSmem& s) {
+  const ChainParams& cp = tp.cp;
+  const int tid = threadIdx.x, nth = blockDim.x, N = cp.N;
+  for (int i = tid; i < N + 2; i += nth) s.goff[i] = cp.goff[i];
+  for (int i = tid; i < cp.nmat; i += nth) s.moff[i] = cp.moff[i];
+  for (int i = tid; i < N; i += nth) s.inst[i] = make_int4(cp.inst[i].mat, cp.inst[i].rows, cp.inst[i].cols, cp.inst[i].K);
+  for (int64_t i = tid; i < (cp.mat_elems + 31) / 32; i += nth) s.ebits[i] = 0;
+}
+
+// G_{e-1}[u] = min_v M[u][v] + G_e[v] for one instance (warp per row, lanes = v)
+__device__ __forceinline__ void fused_matvec(const uint64_t* M, int R, int Cc, const uint64_t* g, uint64_t* out) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int u = warp; u < R; u += (int)(blockDim.x >> 5)) {
+    uint64_t x = kBigC;
+    if (lane < Cc) x = big_of(M[u * Cc + lane]) + big_of(g[lane]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const uint64_t y = __shfl_xor_sync(0xffffffffu, x, o);
+      x = y < x ? y : x;
+    }
+    if (lane == 0) out[u] = inf_of(x);
+  }
+}
+
+__device__ void fused_chain_values(const TailParams& tp, const FusedChainSmem& s) {
+  const ChainParams& cp = tp.cp;
+  const int tid = threadIdx.x, nth = blockDim.x, N = cp.N;
+  for (int64_t e = tid; e < cp.mat_elems; e += nth) s.A[e] = __ldcg(cp.baseA + e);   // other CTAs' writes
+  const int lastc = s.inst[N - 1].z;
+  for (int v = tid; v < lastc; v += nth) s.G[s.goff[N] + v] = 0;                      // terminal 0 (Q8)
+  __syncthreads();
+  TTRACE(0, 40);
+  for (int r = cp.nruns - 1; r >= 0; --r) {
+    const ChainRun run = cp.runs[r];
+    TTRACE(0, 41 + min(cp.nruns - 1 - r, 3));
+    const int4 in = s.inst[run.first];
+    const uint64_t* M = s.A + s.moff[in.x];
+    const int R = in.y, Cc = in.z;
+    const int e = run.first + run.len;               // G_e known (1-based instance e)
+    if (run.len == 1) {
+      fused_matvec(M, R, Cc, s.G + s.goff[e], s.G + s.goff[e - 1]);
+      __syncthreads();
+      continue;
+    }
+    const int S = R;                                 // square (host: runs need rows == cols)
+    int levels = 0;
+    while ((1 << (levels + 1)) <= run.len) ++levels;
+    const int SS = S * S;
+    for (int c = tid; c < SS; c += nth) s.P[c] = big_of(M[c]);
+    __syncthreads();
+    for (int j = 1; j <= levels; ++j) {              // repeated squaring: P_j = P_{j-1} (x) P_{j-1}
+      const uint64_t* Pa = s.P + (int64_t)(j - 1) * SS;
+      uint64_t* Pc = s.P + (int64_t)j * SS;
+      for (int c = tid; c < SS; c += nth) {
+        const int i = c / S, k2 = c - i * S;
+        uint64_t b0 = kBigC, b1 = kBigC;
+        int k = 0;
+        for (; k + 2 <= S; k += 2) {
+          const uint64_t x0 = Pa[i * S + k] + Pa[k * S + k2];
+          const uint64_t x1 = Pa[i * S + k + 1] + Pa[(k + 1) * S + k2];
+          b0 = x0 < b0 ? x0 : b0;
+          b1 = x1 < b1 ? x1 : b1;
+        }
+        if (k < S) { const uint64_t x0 = Pa[i * S + k] + Pa[k * S + k2]; b0 = x0 < b0 ? x0 : b0; }
+        b0 = b1 < b0 ? b1 : b0;
+        Pc[c] = b0 < kBigC ? b0 : kBigC;
+      }
+      __syncthreads();
+    }
+    TTRACE(0, 45);
+    for (int j = 0; j <= levels; ++j) {              // doubling: G_{e-k} = P_j (x) G_{e-k+2^j}
+      const uint64_t* Pj = s.P + (int64_t)j * SS;
+      const int k_lo = 1 << j, k_hi = min(1 << (j + 1), run.len + 1);
+      const int work = (k_hi - k_lo) * S;
+      for (int w = tid; w < work; w += nth) {
+        const int k = k_lo + w / S, u = w - (w / S) * S;
+        const uint64_t* g = s.G + s.goff[e - k + (1 << j)];
+        const uint64_t* row = Pj + u * S;
+        uint64_t b0 = kBigC, b1 = kBigC;
+        int v = 0;
+        for (; v + 2 <= S; v += 2) {
+          const uint64_t x0 = row[v] + big_of(g[v]);
+          const uint64_t x1 = row[v + 1] + big_of(g[v + 1]);
+          b0 = x0 < b0 ? x0 : b0;
+          b1 = x1 < b1 ? x1 : b1;
+        }
+        if (v < S) { const uint64_t x0 = row[v] + big_of(g[v]); b0 = x0 < b0 ? x0 : b0; }
+        b0 = b1 < b0 ? b1 : b0;
+        s.G[s.goff[e - k] + u] = inf_of(b0);
+      }
+      __syncthreads();
+    }
+  }
+  TTRACE(0, 46);
+  for (int64_t e2 = tid; e2 < s.goff[N + 1]; e2 += nth) cp.G[e2] = s.G[e2];
+}
+
+// u64 minimum over the warp: two 32-bit CREDUX.MIN (high words, then the low
+// words of the lanes holding the least high word)
+__device__ __forceinline__ uint64_t warp_min_u64(uint64_t x) {
+  const uint32_t hi = (uint32_t)(x >> 32), lo = (uint32_t)x;
+  const uint32_t hm = __reduce_min_sync(0xffffffffu, hi);
+  const uint32_t lm = __reduce_min_sync(0xffffffffu, hi == hm ? lo : 0xFFFFFFFFu);
+  return ((uint64_t)hm << 32) | lm;
+}
+
+// Sequential backward recurrence G_n(u) = min_v A_n[u][v] + G_{n+1}(v) (the
+// textbook DP) with the optimal-successor mask of every (n, u) from
+// the same reduction (lanes v attaining the minimum): one warp per row, the
+// rows of the current matrix kept in registers across a run of identical
+// transitions, one CTA barrier per instance.  On one SM with <= 32 states this
+// is cheaper than repeated squaring + doubling (S^3 log L vs S^2 L work, both
+// latency-bound): measured in DESIGN.md §5.
+__device__ void fused_chain_values_seq(const TailParams& tp, const FusedChainSmem& s) {
+  constexpr int NW = kTailThreads / 32;
+  constexpr int RPW = (32 + NW - 1) / NW;              // rows per warp (<= 32 rows)
+  const ChainParams& cp = tp.cp;
+  const int tid = threadIdx.x, nth = blockDim.x, N = cp.N;
+  const int warp = tid >> 5, lane = tid & 31;
+  for (int64_t e = tid; e < cp.mat_elems; e += nth) s.A[e] = __ldcg(cp.baseA + e);   // other CTAs' writes
+  const int lastc = s.inst[N - 1].z;
+  for (int v = tid; v < lastc; v += nth) s.G[s.goff[N] + v] = 0;                      // terminal 0 (Q8)
+  __syncthreads();
+  TTRACE(0, 40);
+  int cur = -1;
+  uint64_t a[RPW];
+  for (int n = N - 1; n >= 0; --n) {
+    const int4 in = s.inst[n];
+    if (in.x != cur) {
+      const uint64_t* M = s.A + s.moff[in.x];
+#pragma unroll
+      for (int r = 0; r < RPW; ++r) {
+        const int u = warp + r * NW;
+        a[r] = (u < in.y && lane < in.z) ? big_of(M[u * in.z + lane]) : kBigC;
+      }
+      cur = in.x;
+    }
+    const int64_t g0 = s.goff[n];
+    const uint64_t gv = lane < in.z ? big_of(s.G[s.goff[n + 1] + lane]) : kBigC;
+#pragma unroll
+    for (int r = 0; r < RPW; ++r) {
+      const int u = warp + r * NW;
+      if (u < in.y) {
+        const uint64_t x = a[r] + gv;                  // <= 2^64 - 2: no wrap
+        const uint64_t m = warp_min_u64(x);
+        const uint32_t mask = __ballot_sync(0xffffffffu, x == m && m < kBigC);
+        if (lane == 0) {
+          s.G[g0 + u] = inf_of(m);
+          s.om[g0 + u] = mask;
+        }
+      }
+    }
+    __syncthreads();
+  }
+  TTRACE(0, 46);
+  for (int64_t e2 = tid; e2 < s.goff[N + 1]; e2 += nth) cp.G[e2] = s.G[e2];
+}
+
+// optimal-successor masks of every (n, u), reachability from u_1 = 0, and the
+// reachable optimal edges (deduplicated per distinct matrix) -> argmin list
+__device__ void fused_chain_edges(const TailParams& tp, const FusedChainSmem& s, bool have_om) {
+  const ChainParams& cp = tp.cp;
+  const int tid = threadIdx.x, nth = blockDim.x, N = cp.N;
+  const int warp = tid >> 5, lane = tid & 31, nw = nth >> 5;
+  __shared__ int s_ecnt;
+  if (tid == 0) s_ecnt = 0;
+  for (int n = have_om ? N : warp; n < N; n += nw) {  // warp per instance, lanes = v
+    const int4 in = s.inst[n];
+    const int64_t g0 = s.goff[n];
+    const uint64_t gv = lane < in.z ? s.G[s.goff[n + 1] + lane] : kInf64;
+    const uint64_t* Am = s.A + s.moff[in.x];
+    for (int u = 0; u < in.y; ++u) {
+      const uint64_t target = s.G[g0 + u];
+      const uint64_t a = lane < in.z ? Am[u * in.z + lane] : kInf64;
+      const uint32_t m = __ballot_sync(0xffffffffu, target != kInf64 && a != kInf64 && gv != kInf64 &&
+                                                        a + gv == target);
+      if (lane == 0) s.om[g0 + u] = m;
+    }
+  }
+  __syncthreads();
+  TTRACE(0, 47);
+  if (tid == 0) {
+    uint32_t r = s.G[0] == kInf64 ? 0u : 1u;
+    for (int n = 0; n < N; ++n) {
+      s.rmask[n] = r;
+      uint32_t nx = 0, rr = r;
+      const int64_t g0 = s.goff[n];
+      while (rr) {
+        const int u = __ffs(rr) - 1;
+        rr &= rr - 1;
+        nx |= s.om[g0 + u];
+      }
+      r = nx;
+    }
+  }
+  __syncthreads();
+  TTRACE(0, 48);
+  for (int64_t w = tid; w < (int64_t)N * 32; w += nth) {   // (instance, lane = u)
+    const int n = (int)(w >> 5), u = (int)(w & 31);
+    if (!((s.rmask[n] >> u) & 1u)) continue;
+    const int4 in = s.inst[n];
+    const int64_t fo = s.moff[in.x];
+    uint32_t m = s.om[s.goff[n] + u];
+    while (m) {
+      const int v = __ffs(m) - 1;
+      m &= m - 1;
+      const int64_t bit = fo + (int64_t)u * in.z + v;
+      if (!(atomicOr(&s.ebits[bit >> 5], 1u << (bit & 31)) & (1u << (bit & 31))))
+        cp.edge_list[atomicAdd(&s_ecnt, 1)] = ArgminEntry{in.x, u * in.z + v};
+    }
+  }
+  __syncthreads();
+  if (tid == 0) *cp.edge_count = s_ecnt;
+}
+
+// forward greedy: per reachable (n, u) the optimal successor with the least
+// combination index (I of the listed buckets, written by the argmin CTAs),
+// then the walk from u_1 = 0, the plan outputs and the digit decode
+__device__ void fused_backtrack(const TailParams& tp, const FusedChainSmem& s) {
+  const ChainParams& cp = tp.cp;
+  const int tid = threadIdx.x, nth = blockDim.x, N = cp.N;
+  __shared__ int s_stat;
+  for (int64_t w = tid; w < (int64_t)N * 32; w += nth) {
+    const int n = (int)(w >> 5), u = (int)(w & 31);
+    if (!((s.rmask[n] >> u) & 1u)) continue;
+    const int4 in = s.inst[n];
+    const uint64_t* I = cp.baseI + s.moff[in.x] + (int64_t)u * in.z;
+    uint32_t m = s.om[s.goff[n] + u];
+    uint64_t bi = kInf64;
+    int bv = -1;
+    while (m) {
+      const int v = __ffs(m) - 1;
+      m &= m - 1;
+      const uint64_t ix = __ldcg(I + v);             // other CTAs' writes
+      if (bv < 0 || ix < bi) { bi = ix; bv = v; }
+    }
+    s.nxt[s.goff[n] + u] = (int8_t)bv;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    int st = 0;
+    if (s.G[0] == kInf64) {
+      st = 3;
+    } else {
+      int u = 0;
+      for (int n = 0; n < N; ++n) {
+        const int v = s.nxt[s.goff[n] + u];
+        if (v < 0) { st = 3; break; }
+        s.vseq[n] = (u << 16) | v;
+        u = v;
+      }
+    }
+    s_stat = st;
+    *cp.total = st ? kInf64 : s.G[0];
+    *cp.status = st;
+  }
+  __syncthreads();
+  if (s_stat != 0) return;
+  for (int n = tid; n < N; n += nth) {
+    const int u = s.vseq[n] >> 16, v = s.vseq[n] & 0xFFFF;
+    const int4 in = s.inst[n];
+    const int64_t at = s.moff[in.x] + (int64_t)u * in.z + v;
+    cp.seg_index[n] = __ldcg(cp.baseI + at);
+    cp.seg_ns[n] = s.A[at];
+  }
+  __syncthreads();
+  for (int64_t w = tid; w < (int64_t)N * cp.kmax; w += nth) {
+    const int n = (int)(w / cp.kmax), j = (int)(w % cp.kmax);
+    const int4 in = s.inst[n];
+    int32_t dval = -1;
+    if (j < in.w) {
+      const int ro = cp.inst[n].radix_off;
+      uint64_t stride = 1;
+      for (int d = in.w - 1; d > j; --d) stride *= (uint64_t)cp.radix_blob[ro + d];
+      dval = (int32_t)((cp.seg_index[n] / stride) % (uint64_t)cp.radix_blob[ro + j]);
+    }
+    cp.digits[w] = dval;
+  }
+}
+
+// --------------------------------------------------------------------------
+// Fused tail (world 1).  One cooperative launch replaces bucket-minima,
+// chain mode 1, edge conversion, argmin and chain mode 2 (and the fills and
+// memsets between them): the steps are latency-bound and each separate launch
+// cost a few microseconds of fixed overhead.
+//   phase 1 (all CTAs): A[u][v] = min over the chunk minima for every bucket
+//            of every transition in the caller's layout (INF for pruned
+//            strategies), I = NOIDX;
+//   grid barrier;
+//   chain = 1: CTA 0 suffix vectors + reachable optimal edges (shared memory);
+//            grid barrier; CTAs 1.. least index of the listed buckets; CTA 0
+//            waits for them and runs the forward greedy + digit decode;
+//   chain = 0: every CTA takes buckets of the full list (segment tables).
+// Grid barrier: arrival counter + generation word; co-residency is
+// guaranteed by the cooperative launch.  The kernel leaves sync[] zero.
+// --------------------------------------------------------------------------
+__device__ __forceinline__ void tail_grid_sync(unsigned int* bar, unsigned int nblocks, unsigned int& gen) {
+  __syncthreads();
+  ++gen;
+  if (threadIdx.x == 0) {
+    __threadfence();
+    const unsigned int arrived = atomicAdd(bar, 1u) + 1u;
+    if (arrived == nblocks * gen) {
+      atomicExch(bar + 1, gen);
+    } else {
+      while (*reinterpret_cast<volatile unsigned int*>(bar + 1) < gen) __nanosleep(32);
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+__device__ __forceinline__ uint64_t tail_timer() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+// min over one bucket's chunk minima: 16-byte loads, several in flight per
+// lane (the loop is latency-bound otherwise), then a butterfly min
+template <typename V>
+__device__ __forceinline__ uint64_t bucket_min(const ArgminParams& ap, int pair, int lane) {
+  const V* cm = static_cast<const V*>(ap.f.chunkmin) + (int64_t)pair * ap.f.nchunks;
+  const int64_t n = ap.f.nchunks;
+  constexpr int VN = Vec4<V>::N;
+  V b[4] = {VT<V>::CAP, VT<V>::CAP, VT<V>::CAP, VT<V>::CAP};
+  int64_t done = 0;
+  if ((reinterpret_cast<uintptr_t>(cm) & 15) == 0) {
+    const int64_t nv = n / VN;
+    const typename Vec4<V>::T* cv = reinterpret_cast<const typename Vec4<V>::T*>(cm);
+#pragma unroll 4
+    for (int64_t i = lane; i < nv; i += 32) {
+      V x[VN];
+      load_vec<V>(reinterpret_cast<const V*>(cv + i), x);
+#pragma unroll
+      for (int q = 0; q < VN; ++q) b[q] = VT<V>::mn(b[q], x[q]);
+    }
+    done = nv * VN;
+  }
+#pragma unroll 4
+  for (int64_t c = done + lane; c < n; c += 32) b[0] = VT<V>::mn(b[0], cm[c]);
+  V best = VT<V>::mn(VT<V>::mn(b[0], b[1]), VT<V>::mn(b[2], b[3]));
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) best = VT<V>::mn(best, (V)__shfl_xor_sync(0xffffffffu, best, o));
+  return best >= VT<V>::CAP ? kInf64 : (uint64_t)best;
+}
+
+template <typename V>
+__device__ __forceinline__ void tail_argmin(const ArgminParams& ap, int pair, unsigned char* smem, const void* tabs) {
+  argmin_pair<V, kTailThreads>(ap, pair, smem, static_cast<const V*>(tabs), sizeof(V) == 4 ? ap.pstar : nullptr);
+}
+
+// narrow buckets: the minimum and the least h-block of a chunk attaining it,
+// as one min over the keys (value << 32 | hb) -- chunk c = l * nhb + hb
+__device__ __forceinline__ uint64_t bucket_min_hb(const ArgminParams& ap, int pair, int lane, int64_t* hb_out) {
+  const uint32_t* cm = static_cast<const uint32_t*>(ap.f.chunkmin) + (int64_t)pair * ap.f.nchunks;
+  const uint32_t n = (uint32_t)ap.f.nchunks, nhb = (uint32_t)ap.f.nhb;
+  uint64_t k0 = ~0ull, k1 = ~0ull;
+  uint32_t c = (uint32_t)lane;
+#pragma unroll 4
+  for (; c + 32 < n; c += 64) {
+    const uint32_t x0 = cm[c], x1 = cm[c + 32];
+    const uint64_t y0 = ((uint64_t)x0 << 32) | (c % nhb), y1 = ((uint64_t)x1 << 32) | ((c + 32) % nhb);
+    k0 = y0 < k0 ? y0 : k0;
+    k1 = y1 < k1 ? y1 : k1;
+  }
+  if (c < n) {
+    const uint64_t y0 = ((uint64_t)cm[c] << 32) | (c % nhb);
+    k0 = y0 < k0 ? y0 : k0;
+  }
+  k0 = k1 < k0 ? k1 : k0;
+  k0 = warp_min_u64(k0);
+  const uint32_t best = (uint32_t)(k0 >> 32);
+  *hb_out = best >= kCap32 ? -1 : (int64_t)(k0 & 0xFFFFFFFFu);
+  return best >= kCap32 ? kInf64 : (uint64_t)best;
+}
+
+// worker CTAs: copies of every slot's argmin descriptor and W/R tables in
+// shared memory (done while CTA 0 runs the chain, off the critical path)
+__device__ void tail_stage_argmin(const TailParams& tp, unsigned char* smem) {
+  const int tid = threadIdx.x, nth = blockDim.x;
+  ArgminParams* desc = reinterpret_cast<ArgminParams*>(smem + tp.arg_desc_off);
+  {
+    const int words = (int)(sizeof(ArgminParams) / 4) * tp.nslot;
+    const uint32_t* src = reinterpret_cast<const uint32_t*>(tp.aps);
+    uint32_t* dst = reinterpret_cast<uint32_t*>(desc);
+    for (int i = tid; i < words; i += nth) dst[i] = src[i];
+  }
+  for (int q = 0; q < tp.nslot; ++q) {
+    const ArgminParams& ap = tp.aps[q];
+    if (ap.f.nchunks == 0) continue;
+    const int n = ap.e.tab_n;
+    if (ap.wide) {
+      const uint64_t* v = static_cast<const uint64_t*>(ap.f.vals) + ap.e.tab_lo;
+      uint64_t* d = reinterpret_cast<uint64_t*>(smem + tp.arg_tab_off[q]);
+      for (int i = tid; i < n; i += nth) d[i] = v[i];
+    } else {
+      const uint32_t* v = static_cast<const uint32_t*>(ap.f.vals) + ap.e.tab_lo;
+      uint32_t* d = reinterpret_cast<uint32_t*>(smem + tp.arg_tab_off[q]);
+      for (int i = tid; i < n; i += nth) d[i] = v[i];
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kTailThreads, 1) tail_kernel(const TailParams tp) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int tid = threadIdx.x, lane = tid & 31;
+  const unsigned int G = gridDim.x;
+  unsigned int gen = 0;
+  const bool ts = tp.phase_ts != nullptr && blockIdx.x == 0 && tid == 0;
+  if (ts) tp.phase_ts[0] = tail_timer();
+  TTRACE(0, 30);
+  FusedChainSmem cs{};
+  if (tp.chain && blockIdx.x == 0) {
+    cs = fused_chain_smem(tp, smem_raw);
+    fused_chain_meta(tp, cs);                       // independent of this launch's A
+  }
+  // ---- phase 1: bucket minima (warp per caller-layout bucket), I = NOIDX
+  {
+    const int64_t total = tp.orig_off[tp.nslot];
+    const int64_t nw = (int64_t)G * (blockDim.x >> 5);
+    for (int64_t w = (int64_t)blockIdx.x * (blockDim.x >> 5) + (tid >> 5); w < total; w += nw) {
+      int s = 0;
+      while (w >= tp.orig_off[s + 1]) ++s;
+      const ArgminParams& ap = tp.aps[s];
+      const int po = (int)(w - tp.orig_off[s]);
+      const int u = po / ap.Do_orig, vo = po - u * ap.Do_orig;
+      const int vc = ap.f.nchunks > 0 ? ap.vinv[vo] : -1;   // empty types: no maps
+      uint64_t a = kInf64;
+      if (vc >= 0) {
+        const int pair = u * ap.f.Do + vc;
+        if (ap.wide) {
+          a = bucket_min<uint64_t>(ap, pair, lane);
+        } else {
+          int64_t hb;
+          a = bucket_min_hb(ap, pair, lane, &hb);
+          if (lane == 0) ap.pstar[pair] = hb;
+        }
+      }
+      if (lane == 0) {
+        ap.A_out[po] = a;
+        ap.I_out[po] = kInf64;
+      }
+    }
+  }
+  if (!tp.chain) {
+    tail_stage_argmin(tp, smem_raw);
+  }
+  tail_grid_sync(tp.sync, G, gen);
+  if (ts) tp.phase_ts[1] = tail_timer();
+  TTRACE(0, 31);
+  if (tp.chain) {
+    if (blockIdx.x == 0) {
+      if (tp.squaring) fused_chain_values(tp, cs);
+      else fused_chain_values_seq(tp, cs);
+      TTRACE(0, 10);
+      fused_chain_edges(tp, cs, !tp.squaring);
+      TTRACE(0, 12);
+    } else {
+      tail_stage_argmin(tp, smem_raw);
+    }
+    tail_grid_sync(tp.sync, G, gen);
+    if (ts) tp.phase_ts[2] = tail_timer();
+    TTRACE(0, 32);
+    TTRACE(1, 33);
+    if (blockIdx.x > 0) {
+#ifdef CFP_TAIL_TRACE
+      uint64_t t_w0;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_w0));
+#endif
+      const ArgminParams* desc = reinterpret_cast<const ArgminParams*>(smem_raw + tp.arg_desc_off);
+      const int n = __ldcg(tp.cp.edge_count);
+      for (int it = (int)blockIdx.x - 1; it < n; it += (int)G - 1) {
+        const long long raw = __ldcg(reinterpret_cast<const long long*>(tp.cp.edge_list) + it);   // CTA 0's writes
+        const ArgminEntry en{(int32_t)(raw & 0xFFFFFFFFll), (int32_t)(raw >> 32)};
+        const ArgminParams& ap = desc[en.slot];
+        const int u = en.pair / ap.Do_orig, vo = en.pair - u * ap.Do_orig;
+        const int vc = ap.vinv[vo];
+        const int pair = vc < 0 ? 0 : u * ap.f.Do + vc;     // pruned columns are INF: never optimal
+        const void* tabs = smem_raw + tp.arg_tab_off[en.slot];
+        if (ap.wide) tail_argmin<uint64_t>(ap, pair, smem_raw, tabs);
+        else tail_argmin<uint32_t>(ap, pair, smem_raw, tabs);
+        __syncthreads();
+      }
+      __syncthreads();
+      TTRACE(1, 36);
+#ifdef CFP_TAIL_TRACE
+      if (tid == 0 && blockIdx.x < 256) {
+        uint64_t t_w1;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_w1));
+        g_trace_cta[blockIdx.x] = t_w1 - t_w0;
+      }
+#endif
+      if (tid == 0) {
+        __threadfence();
+        atomicAdd(tp.sync + 2, 1u);
+      }
+      return;
+    }
+    if (tid == 0) {
+      while (*reinterpret_cast<volatile unsigned int*>(tp.sync + 2) < G - 1) __nanosleep(32);
+      __threadfence();
+    }
+    __syncthreads();
+    if (ts) tp.phase_ts[3] = tail_timer();
+    TTRACE(0, 34);
+    fused_backtrack(tp, cs);
+    __syncthreads();
+    if (tid == 0) {                                 // every other CTA is past its last barrier
+      tp.sync[0] = 0u;
+      tp.sync[1] = 0u;
+      tp.sync[2] = 0u;
+      if (ts) tp.phase_ts[4] = tail_timer();
+    }
+    TTRACE(0, 35);
+    return;
+  }
+  const ArgminParams* desc = reinterpret_cast<const ArgminParams*>(smem_raw + tp.arg_desc_off);
+  const int64_t npairs = tp.pair_off[tp.nslot];
+  for (int64_t it = blockIdx.x; it < npairs; it += G) {
+    int s = 0;
+    while (it >= tp.pair_off[s + 1]) ++s;
+    const ArgminParams& ap = desc[s];
+    const int pair = (int)(it - tp.pair_off[s]);
+    const void* tabs = smem_raw + tp.arg_tab_off[s];
+    if (ap.wide) tail_argmin<uint64_t>(ap, pair, smem_raw, tabs);
+    else tail_argmin<uint32_t>(ap, pair, smem_raw, tabs);
+    __syncthreads();
+  }
+  __syncthreads();
+  if (tid == 0) {
+    __threadfence();
+    if (atomicAdd(tp.sync + 2, 1u) == G - 1) {      // last CTA: everyone is past the barriers
+      tp.sync[0] = 0u;
+      tp.sync[1] = 0u;
+      tp.sync[2] = 0u;
+    }
+  }
 }
 
 // --------------------------------------------------------------------------
@@ -1359,7 +2042,7 @@ cudaError_t launch_build_tables(const TableSpec* specs, int nspecs, int64_t max_
                                 V* out, cudaStream_t st) {
   if (nspecs == 0) return cudaSuccess;
   // max_entries carries the total CTA count (sum of the tables' nblocks)
-  build_table_kernel<V><<<(unsigned)max_entries, 256, 0, st>>>(specs, vals, out);
+  build_table_kernel<V><<<(unsigned)max_entries, 256, 0, st>>>(specs, nspecs, vals, out);
   CFP_LAUNCH_CHECK();
   return cudaSuccess;
 }
@@ -1472,6 +2155,33 @@ cudaError_t launch_chain(const ChainParams& cp, cudaStream_t st) {
 }
 
 
+
+// co-resident CTAs of the tail kernel for a dynamic shared-memory size (cooperative launch bound)
+cudaError_t tail_max_blocks(size_t smem, int* per_sm) {
+  cudaError_t e = cudaFuncSetAttribute(tail_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  e = cudaFuncSetAttribute(tail_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+  if (e != cudaSuccess) return e;
+  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(per_sm, tail_kernel, kTailThreads, smem);
+}
+
+// one cooperative launch (grid <= co-resident CTAs, checked by the host)
+cudaError_t launch_tail(const TailParams& tp, int grid, size_t smem, cudaStream_t st) {
+  cudaError_t e = cudaFuncSetAttribute(tail_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  e = cudaFuncSetAttribute(tail_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+  if (e != cudaSuccess) return e;
+  void* args[] = {const_cast<TailParams*>(&tp)};
+  return cudaLaunchCooperativeKernel((void*)tail_kernel, dim3((unsigned)grid), dim3(kTailThreads), args, smem, st);
+}
+
+#ifdef CFP_TAIL_TRACE
+extern "C" int cfp_debug_trace(uint64_t* out64) {
+  int e = (int)cudaMemcpyFromSymbol(out64, g_trace, 64 * sizeof(uint64_t));
+  if (e) return e;
+  return (int)cudaMemcpyFromSymbol(out64 + 64, g_trace_cta, 256 * sizeof(uint64_t));
+}
+#endif
 
 cudaError_t launch_intpipe(int op, int blocks, int iters, uint32_t* out, cudaStream_t st) {
   if (op == 0) intpipe_kernel<0><<<blocks, 1024, 0, st>>>(out, iters, 7u);

@@ -568,3 +568,77 @@ def test_plan_reuse_alternating_configs(ctx, oracle_lib):
              G.make_config("C2", 1, "random"), G.make_config("C2", 0, "shaped")]
     for q in probs:
         _search_or_infeasible(ctx, O, q)
+
+
+# ---------------------------------------------------------------- fused tail
+# World 1 runs bucket minima, chain, argmin and backtrack as one cooperative
+# launch; CFP_FUSED_TAIL=0 keeps the separate launches.  Both must agree with
+# the oracle (and each other) bit for bit.
+
+
+@pytest.fixture(scope="module")
+def ctx_split():
+    import os
+    from paper_2504_00598_b200 import build as B
+    B.build()
+    from paper_2504_00598_b200 import cfp
+    old = os.environ.get("CFP_FUSED_TAIL")
+    os.environ["CFP_FUSED_TAIL"] = "0"
+    try:
+        c = cfp.Context(device=0)
+    finally:
+        if old is None:
+            del os.environ["CFP_FUSED_TAIL"]
+        else:
+            os.environ["CFP_FUSED_TAIL"] = old
+    yield c
+    c.close()
+
+
+@pytest.mark.parametrize("mode", MODES)
+def test_split_tail_corpus_search(ctx_split, oracle_lib, mode):
+    for seed in range(40):
+        p = G.tiny_random(seed * 11 + 3 + MODES.index(mode), mode=mode, max_plans=None, max_n=6)
+        _search_or_infeasible(ctx_split, oracle_lib, p)
+
+
+@pytest.mark.parametrize("seed", range(10))
+def test_split_tail_segment_tables(ctx_split, oracle_lib, seed):
+    O = oracle_lib
+    p = G.tiny_random(9100 + seed, mode=MODES[seed % 3], max_plans=None, max_n=3, max_k=5, max_d=5)
+    for tr_id, tr in enumerate(p.transitions):
+        A0, I0 = O.segment_table(p, tr_id)
+        A, I = ctx_split.segment_costs(p.types[tr.type], tr, p.d_in(tr_id))
+        assert np.array_equal(A, A0) and np.array_equal(I, I0), (seed, tr_id)
+
+
+@pytest.mark.parametrize("cfg", ["C1", "C2", "C3", "C5"])
+def test_fused_tail_taken_and_equal_split(ctx, ctx_split, cfg):
+    """The bench configurations take the fused tail (one launch after the
+    enumeration), and it returns the split path's plan byte for byte."""
+    p = G.make_config(cfg, seed=0, dist="shaped")
+    prep = ctx.prepare(p)
+    info = prep.info()
+    assert info.fused_tail and info.tail_grid >= 2
+    prep.execute()
+    a = prep.fetch()
+    prep.close()
+    b = ctx_split.search_plan(p)
+    assert a.total_ns == b.total_ns
+    assert np.array_equal(a.seg_index, b.seg_index) and np.array_equal(a.seg_ns, b.seg_ns)
+    assert np.array_equal(a.digits, b.digits)
+
+
+def test_fused_tail_repeated_executes(ctx, oracle_lib):
+    """The grid barrier words are left zero by every launch: many executes in
+    a row (and phase timing on) keep returning the oracle's plan."""
+    p = G.make_config("C2", seed=1, dist="ties")
+    want = oracle_lib.search_plan(p)
+    prep = ctx.prepare(p)
+    prep.time_kernels(2)
+    for _ in range(25):
+        prep.execute()
+        ph = prep.phase_ms()
+        assert all(v >= 0 for v in ph.values())
+    _assert_plan(prep.fetch(), want, "C2 repeated")
+    prep.close()
