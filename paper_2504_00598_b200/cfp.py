@@ -14,6 +14,7 @@ from __future__ import annotations
 
 import ctypes as C
 import os
+import weakref
 from dataclasses import dataclass
 from typing import Dict, List, Optional, Sequence, Tuple
 
@@ -197,6 +198,7 @@ def _a(a: Optional[np.ndarray]) -> Optional[int]:
 class _Marshal:
     def __init__(self):
         self.keep = []
+        self.concat = []        # concatenated edge / cross tables, in marshalling order
 
     def arr(self, a, dtype):
         if not (isinstance(a, np.ndarray) and a.dtype == dtype and a.flags.c_contiguous):
@@ -213,6 +215,8 @@ class _Marshal:
         dst = self.arr([_e(e)[1] for e in edges] or [0], np.int32)
         tab = self.arr(np.concatenate([np.asarray(_e(e)[2], np.uint32).ravel() for e in edges])
                        if edges else np.zeros(1, np.uint32), np.uint32)
+        if edges:
+            self.concat.append(tab)
         return cfp_segment_type(len(radix), _a(radix), _a(comp), _a(comm), len(edges), _a(src),
                                 _a(dst), _a(tab), int(ty.out_block))
 
@@ -221,16 +225,94 @@ class _Marshal:
         dst = self.arr([_x(x)[0] for x in xs] or [0], np.int32)
         tab = self.arr(np.concatenate([np.asarray(_x(x)[1], np.uint32).ravel() for x in xs])
                        if xs else np.zeros(1, np.uint32), np.uint32)
+        if xs:
+            self.concat.append(tab)
         return cfp_transition(int(tr.pred_type), int(tr.type), len(xs), _a(dst), _a(tab))
 
     def problem(self, prob) -> cfp_problem:
+        cached = _cached_problem(prob)
+        if cached is not None:
+            self.keep.append(cached[1])
+            return cached[0]
         types = (cfp_segment_type * len(prob.types))(*[self.segment_type(t) for t in prob.types])
         trans = (cfp_transition * len(prob.transitions))(*[self.transition(t) for t in prob.transitions])
         self.keep += [types, trans]
         mesh = self.arr(list(prob.mesh) or [1], np.int32)
         inst = self.arr(prob.instances, np.int32)
-        return cfp_problem(CFP_ABI_VERSION, cfp_mesh(len(prob.mesh), _p(mesh, C.c_int32)),
-                           len(prob.types), types, len(prob.transitions), trans, len(inst), _a(inst))
+        struct = cfp_problem(CFP_ABI_VERSION, cfp_mesh(len(prob.mesh), _p(mesh, C.c_int32)),
+                             len(prob.types), types, len(prob.transitions), trans, len(inst), _a(inst))
+        _cache_problem(prob, self, struct)
+        return struct
+
+
+# Marshalled problems are cached on the problem object: a repeated call with the
+# same array objects (shapes, dtypes, contiguity unchanged) reuses the ctypes
+# structs; the concatenated edge / cross tables are refilled from the current
+# arrays on every call (np.concatenate(out=...)), and every other pointer is
+# the caller's own array, so in-place value changes are always seen.
+def _sig(prob):
+    """Identity / shape signature of every array the marshalled struct refers to."""
+    s = [len(prob.types), len(prob.transitions), id(prob.instances), prob.instances.shape, tuple(prob.mesh)]
+    for t in prob.types:
+        s += [id(t.radix), id(t.comp_ns), id(t.comm_ns), t.comp_ns.shape, t.out_block, len(t.edges)]
+        s += [id(e.table) if hasattr(e, "table") else id(e[2]) for e in t.edges]
+    for tr in prob.transitions:
+        s += [tr.pred_type, tr.type, len(tr.in_edges)]
+        s += [id(x.table) if hasattr(x, "table") else id(x[1]) for x in tr.in_edges]
+    return tuple(s)
+
+
+_MCACHE = {}        # id(problem) -> (weakref, entry); entries die with their problem
+
+
+def _cached_problem(prob):
+    hit = _MCACHE.get(id(prob))
+    if hit is None or hit[0]() is not prob:
+        return None
+    c = hit[1]
+    if c[0] != _sig(prob):
+        return None
+    _, struct, keep, views, buf = c
+    if views:
+        np.concatenate(views, out=buf)    # current values of every edge / cross table
+    return struct, keep
+
+
+def _cache_problem(prob, m: "_Marshal", struct):
+    """Remember the marshalled struct (called after a fresh marshal): all
+    concatenated tables move into one buffer refilled by a single concatenate."""
+    srcs = [[_e(e)[2] for e in t.edges] for t in prob.types if t.edges]
+    srcs += [[_x(x)[1] for x in tr.in_edges] for tr in prob.transitions if tr.in_edges]
+    if len(srcs) != len(m.concat):
+        return
+    # the cache may only point at arrays it keeps alive and that are the caller's own
+    for t in prob.types:
+        for a in (t.radix, t.comp_ns, t.comm_ns):
+            if a is not None and not any(a is k for k in m.keep):
+                return                  # converted copy: a later in-place change would be missed
+    if not any(prob.instances is k for k in m.keep):
+        return
+    views = []
+    for group in srcs:
+        for a in group:
+            if not (isinstance(a, np.ndarray) and a.dtype == np.uint32 and a.flags.c_contiguous):
+                return
+            views.append(a.reshape(-1))
+    buf = np.concatenate(views) if views else np.zeros(1, np.uint32)
+    # re-point the structs at slices of the shared buffer
+    off = 0
+    slots = [(struct.types[i], "edge_ns") for i, t in enumerate(prob.types) if t.edges]
+    slots += [(struct.transitions[i], "in_ns") for i, tr in enumerate(prob.transitions) if tr.in_edges]
+    base = buf.__array_interface__["data"][0]
+    for (obj, field), cat in zip(slots, m.concat):
+        setattr(obj, field, base + off * 4)
+        off += cat.size
+    try:
+        ref = weakref.ref(prob)
+        weakref.finalize(prob, _MCACHE.pop, id(prob), None)
+    except TypeError:           # objects without weak references: no cache
+        return
+    _MCACHE[id(prob)] = (ref, (_sig(prob), struct, list(m.keep) + [buf], views, buf))
 
 
 def _mem_model(m: "_Marshal", prob, quantum: int, mem_limit: int) -> cfp_mem_model:

@@ -99,6 +99,8 @@ struct cfp_ctx {
   // side streams for concurrent per-type enumerations (fork/join by events):
   // the types are independent until the bucket reduction, and running them
   // side by side packs their CTAs into the same waves (no per-launch tail)
+  void* pinned = nullptr;           // pinned host staging (value uploads, plan downloads)
+  size_t pinned_bytes = 0;
   static constexpr int kLanes = 3;
   cudaStream_t lane[kLanes] = {};
   cudaEvent_t fork = nullptr, join[kLanes] = {};
@@ -175,6 +177,19 @@ extern "C" cfp_status cfp_ctx_create(cfp_ctx** out, const cfp_ctx_opts* opts) {
   return CFP_OK;
 }
 
+// grow the ctx's pinned staging buffer to at least `bytes` (the previous
+// call's copies have completed: every user of it synchronises)
+static cfp_status ctx_pinned(cfp_ctx* c, size_t bytes) {
+  if (c->pinned_bytes >= bytes) return CFP_OK;
+  if (c->pinned) CUDA_TRY(cudaFreeHost(c->pinned));
+  c->pinned = nullptr;
+  c->pinned_bytes = 0;
+  const size_t nb = std::max<size_t>(bytes, 64 * 1024);
+  CUDA_TRY(cudaMallocHost(&c->pinned, nb));
+  c->pinned_bytes = nb;
+  return CFP_OK;
+}
+
 extern "C" cfp_status cfp_ctx_nccl_info(cfp_ctx* c, int32_t* nranks, int32_t* version) {
   if (!c || !nranks || !version) return fail(CFP_EINVAL, "null argument");
   *nranks = 0;
@@ -198,6 +213,7 @@ extern "C" void cfp_ctx_destroy(cfp_ctx* c) {
     if (c->join[i]) cudaEventDestroy(c->join[i]);
   }
   if (c->fork) cudaEventDestroy(c->fork);
+  if (c->pinned) cudaFreeHost(c->pinned);
   if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
   delete c;
 }
@@ -369,6 +385,7 @@ struct cfp_prepared {
   // host-side copies for diagnostics
   std::vector<int> inst_rows, inst_cols;
   // timing
+  size_t plan_bytes = 0;          // plan buffer: total, seg_index, seg_ns, digits (status word after it)
   int timing = 0;                 // 1: events around a0 / enumeration / whole; 2: + every phase
   cudaEvent_t ev[7] = {};         // 0 start, 1 a0 done, 2 enumeration done, 3 end,
                                   // 4 bucket minima (+ all-reduce), 5 chain, 6 argmin (+ merge)
@@ -1476,8 +1493,9 @@ static cfp_status prepare_impl(cfp_ctx* ctx, const cfp_problem* p, bool do_chain
     CUDA_TRY(P->radix_blob.alloc(radix_blob.size() * 4));
     CUDA_TRY(cudaMemcpyAsync(P->radix_blob.p, radix_blob.data(), radix_blob.size() * 4, cudaMemcpyHostToDevice, st));
     // plan: total, seg_index[N], seg_ns[N], digits[N*kmax], status
-    CUDA_TRY(P->plan.alloc(8 + (size_t)N * 16 + (size_t)N * kmax * 4 + 16));
-    CUDA_TRY(P->status.alloc(16 + 64 * 8));
+    // plan: total, seg_index[N], seg_ns[N], digits[N*kmax], then the status word
+    P->plan_bytes = 8 + (size_t)N * 16 + (size_t)N * kmax * 4;
+    CUDA_TRY(P->plan.alloc(P->plan_bytes + 16));
     ChainParams& cp = P->cp;
     cp.N = N;
     cp.nruns = P->nruns;
@@ -1496,7 +1514,7 @@ static cfp_status prepare_impl(cfp_ctx* ctx, const cfp_problem* p, bool do_chain
     cp.digits = reinterpret_cast<int32_t*>(pl + 8 + (size_t)N * 16);
     cp.kmax = kmax;
     cp.radix_blob = P->radix_blob.as<int32_t>();
-    cp.status = P->status.as<int32_t>();
+    cp.status = reinterpret_cast<int32_t*>(pl + P->plan_bytes);
     {
       std::vector<ChainInst> mats(P->trans.size());
       int lv = 0, smax = 1;
@@ -1723,7 +1741,7 @@ static cfp_status execute_impl(cfp_ctx* ctx, cfp_prepared* P) {
   const bool edges = P->do_chain && P->use_edges;
   if (edges) {
     // a3: suffix vectors + the optimal edges reachable from the chain start
-    CUDA_TRY(cudaMemsetAsync(P->status.p, 0, 4, st));
+    CUDA_TRY(cudaMemsetAsync(P->cp.status, 0, 4, st));
     CUDA_TRY(cudaMemsetAsync(count, 0, 4, st));
     CUDA_TRY(cudaMemsetAsync(P->merge_keys.p, 0, (size_t)ai * 4, st));
     CUDA_TRY(cudaMemsetAsync(P->reach.p, 0, (size_t)P->reach_bytes, st));
@@ -1746,7 +1764,7 @@ static cfp_status execute_impl(cfp_ctx* ctx, cfp_prepared* P) {
   CUDA_TRY(phase(6));
   // a4 (+ a3 when the edge list is not used)
   if (P->do_chain) {
-    if (!edges) CUDA_TRY(cudaMemsetAsync(P->status.p, 0, 4, st));
+    if (!edges) CUDA_TRY(cudaMemsetAsync(P->cp.status, 0, 4, st));
     ChainParams c2 = P->cp;
     c2.mode = edges ? 2 : 0;
     CUDA_TRY(launch_chain(c2, st));
@@ -1798,11 +1816,14 @@ static cfp_status merge_ranks(cfp_prepared* P, cudaStream_t st) {
 static cfp_status fetch_impl(cfp_ctx* ctx, cfp_prepared* P, cfp_plan* out) {
   cudaStream_t st = ctx->stream;
   const int N = P->N;
-  int32_t status = 0;
-  CUDA_TRY(cudaMemcpyAsync(&status, P->status.p, 4, cudaMemcpyDeviceToHost, st));
-  std::vector<char> buf(8 + (size_t)N * 16 + (size_t)N * P->kmax * 4);
-  CUDA_TRY(cudaMemcpyAsync(buf.data(), P->plan.p, buf.size(), cudaMemcpyDeviceToHost, st));
+  // plan + status word in one copy, through the ctx's pinned staging buffer
+  const size_t nb = P->plan_bytes + 4;
+  TRY(ctx_pinned(ctx, nb));
+  CUDA_TRY(cudaMemcpyAsync(ctx->pinned, P->plan.p, nb, cudaMemcpyDeviceToHost, st));
   CUDA_TRY(cudaStreamSynchronize(st));
+  const char* buf = static_cast<const char*>(ctx->pinned);
+  int32_t status = 0;
+  memcpy(&status, buf + P->plan_bytes, 4);
   if (status == 4) return fail(CFP_ETOOBIG, "chain scratch too small");
   if (status == 3) {
     // diagnostic: forward reachability over finite entries of A_n
@@ -1829,11 +1850,11 @@ static cfp_status fetch_impl(cfp_ctx* ctx, cfp_prepared* P, cfp_plan* out) {
   }
   if (!out) return CFP_OK;
   if (out->kmax < P->kmax) return fail(CFP_EINVAL, "plan.kmax smaller than the largest K");
-  memcpy(&out->total_ns, buf.data(), 8);
-  if (out->seg_index) memcpy(out->seg_index, buf.data() + 8, (size_t)N * 8);
-  if (out->seg_ns) memcpy(out->seg_ns, buf.data() + 8 + (size_t)N * 8, (size_t)N * 8);
+  memcpy(&out->total_ns, buf, 8);
+  if (out->seg_index) memcpy(out->seg_index, buf + 8, (size_t)N * 8);
+  if (out->seg_ns) memcpy(out->seg_ns, buf + 8 + (size_t)N * 8, (size_t)N * 8);
   if (out->digits) {
-    const int32_t* d = reinterpret_cast<const int32_t*>(buf.data() + 8 + (size_t)N * 16);
+    const int32_t* d = reinterpret_cast<const int32_t*>(buf + 8 + (size_t)N * 16);
     for (int n = 0; n < N; ++n)
       for (int j = 0; j < out->kmax; ++j)
         out->digits[(int64_t)n * out->kmax + j] = j < P->kmax ? d[(int64_t)n * P->kmax + j] : -1;
@@ -1873,8 +1894,10 @@ extern "C" cfp_status cfp_search_plan(cfp_ctx* ctx, const cfp_problem* p, cfp_pl
       CUDA_TRY(cudaSetDevice(ctx->device));
       g_alloc_stream = ctx->stream;
       cfp_prepared* P = ctx->cached;
-      CUDA_TRY(cudaMemcpyAsync(P->raw.p, model.b.raw.data(), model.b.raw.size() * 4, cudaMemcpyHostToDevice,
-                               ctx->stream));
+      const size_t nb = model.b.raw.size() * 4;      // this call's values, via pinned staging
+      TRY(ctx_pinned(ctx, nb));
+      memcpy(ctx->pinned, model.b.raw.data(), nb);
+      CUDA_TRY(cudaMemcpyAsync(P->raw.p, ctx->pinned, nb, cudaMemcpyHostToDevice, ctx->stream));
       TRY(execute_impl(ctx, P));
       return fetch_impl(ctx, P, out);
     }

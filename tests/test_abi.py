@@ -116,3 +116,32 @@ def test_profile_space_errors(cfp):
     with pytest.raises(cfp.CfpError) as ei:
         cfp.profile_space(p)
     assert ei.value.status == cfp.CFP_EINVAL
+
+
+def test_marshal_cache_refills_values_in_place():
+    """The binding caches a problem's marshalled structs; the edge / cross
+    tables it hands to the C-ABI must follow in-place value changes and a
+    replaced table object must invalidate the cache (no GPU needed)."""
+    import copy
+    import ctypes as C
+    import numpy as np
+    from paper_2504_00598_b200 import cfp
+    from synth import make_config
+    p = copy.deepcopy(make_config("C3", 0, "shaped"))
+    cfp._Marshal().problem(p)
+    t = p.types[2]
+    off = sum(e.table.size for e in t.edges[:3])
+    t.edges[3].table.flat[5] += 7
+    s = cfp._Marshal().problem(p)
+    assert C.cast(s.types[2].edge_ns, C.POINTER(C.c_uint32))[off + 5] == int(t.edges[3].table.flat[5])
+    x = p.transitions[2].in_edges[1]
+    x.table.flat[3] += 9
+    s = cfp._Marshal().problem(p)
+    off2 = p.transitions[2].in_edges[0].table.size
+    assert C.cast(s.transitions[2].in_ns, C.POINTER(C.c_uint32))[off2 + 3] == int(x.table.flat[3])
+    new = x.table.copy()
+    new.flat[0] += 1
+    x.table = new                                  # a new object: the cache must not be used
+    s = cfp._Marshal().problem(p)
+    assert C.cast(s.transitions[2].in_ns, C.POINTER(C.c_uint32))[off2] == int(new.flat[0])
+    assert copy.deepcopy(p) is not None            # the cache does not ride on the object

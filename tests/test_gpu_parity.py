@@ -642,3 +642,54 @@ def test_fused_tail_repeated_executes(ctx, oracle_lib):
         assert all(v >= 0 for v in ph.values())
     _assert_plan(prep.fetch(), want, "C2 repeated")
     prep.close()
+
+
+@pytest.fixture(scope="module")
+def ctx_sq():
+    import os
+    from paper_2504_00598_b200 import build as B
+    B.build()
+    from paper_2504_00598_b200 import cfp
+    old = os.environ.get("CFP_TAIL_SQUARING")
+    os.environ["CFP_TAIL_SQUARING"] = "1"
+    try:
+        c = cfp.Context(device=0)
+    finally:
+        if old is None:
+            del os.environ["CFP_TAIL_SQUARING"]
+        else:
+            os.environ["CFP_TAIL_SQUARING"] = old
+    yield c
+    c.close()
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_fused_squaring_long_runs(ctx_sq, oracle_lib, seed):
+    """The fused tail's repeated squaring + doubling variant (CFP_TAIL_SQUARING=1)."""
+    p = G.tiny_random(8300 + seed, mode=MODES[seed % 3], max_plans=None, max_n=40, max_types=2, max_run=37)
+    _search_or_infeasible(ctx_sq, oracle_lib, p)
+
+
+@pytest.mark.parametrize("cfg", ["C2", "C3", "C5"])
+def test_fused_squaring_configs(ctx, ctx_sq, cfg):
+    p = G.make_config(cfg, seed=0, dist="shaped")
+    a, b = ctx.search_plan(p), ctx_sq.search_plan(p)
+    assert a.total_ns == b.total_ns and np.array_equal(a.seg_index, b.seg_index)
+    assert np.array_equal(a.seg_ns, b.seg_ns) and np.array_equal(a.digits, b.digits)
+
+
+def test_marshal_cache_sees_in_place_changes(ctx, oracle_lib):
+    """search_plan on the same problem object after in-place value changes:
+    the cached marshalling refills its tables, so the plan follows the values."""
+    import copy
+    p = copy.deepcopy(G.make_config("C2", seed=2, dist="random"))
+    _assert_plan(ctx.search_plan(p), oracle_lib.search_plan(p), "C2 before")
+    rng = np.random.default_rng(0)
+    for t in p.types:
+        t.comp_ns[:] = rng.integers(0, 1 << 20, t.comp_ns.shape, dtype=np.uint32)
+        for e in t.edges:
+            e.table[...] = rng.integers(0, 1 << 20, e.table.shape, dtype=np.uint32)
+    for tr in p.transitions:
+        for x in tr.in_edges:
+            x.table[...] = rng.integers(0, 1 << 20, x.table.shape, dtype=np.uint32)
+    _assert_plan(ctx.search_plan(p), oracle_lib.search_plan(p), "C2 after in-place change")
