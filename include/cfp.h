@@ -205,8 +205,20 @@ typedef struct {
   int32_t fused_tail;          /* 1: bucket minima + chain + argmin + backtrack run as one
                                   cooperative launch (world 1); 0: separate launches */
   int32_t tail_grid;           /* CTAs of that launch */
+  int32_t o_mode[CFP_MAX_BLOCKS];   /* per type: output block in the register group (0), the M
+                                       loop (1) or the prefix (2) of the enumeration schedule */
+  int32_t full_a[CFP_MAX_BLOCKS];   /* per type: 1 = the fully unrolled A-loop kernel variant runs */
 } cfp_prepared_info;
 cfp_status cfp_prepared_query(const cfp_prepared* prep, cfp_prepared_info* info);
+/* Segment tables of one transition through a prepared search's own schedule
+ * and kernels (the enumeration variant the search runs; parity tests at full
+ * size): re-executes the enumeration, then the least-index argmin of every
+ * bucket instead of the chain.  Outputs as cfp_segment_costs: caller-allocated
+ * host [d_in][D_o] cost and index (Eq. 3).  A transition
+ * merged with an identical earlier one (same cross tables) returns that one's
+ * tables.  EINVAL: the transition is not used by the instance list. */
+cfp_status cfp_prepared_tables(cfp_ctx* ctx, cfp_prepared* prep, int32_t transition,
+                               uint64_t* cost_out, uint64_t* index_out);
 /* Record CUDA events on the ctx stream during the next cfp_execute calls
  * (bench instrumentation).  on = 0: off; 1: events at the start, after a0
  * staging, after the enumeration (all side lanes joined) and at the end --

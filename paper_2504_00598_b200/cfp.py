@@ -90,13 +90,13 @@ class cfp_prepared_info(C.Structure):
                 ("num_types", C.c_int32), ("num_transitions", C.c_int32), ("wide_types", C.c_int32),
                 ("kernel_launches", C.c_int32), ("prefix_len", C.c_int32 * 32),
                 ("nb", C.c_int32 * 32), ("na", C.c_int32 * 32), ("fused_tail", C.c_int32),
-                ("tail_grid", C.c_int32)]
+                ("tail_grid", C.c_int32), ("o_mode", C.c_int32 * 32), ("full_a", C.c_int32 * 32)]
 
 
 EXPORTS = ["cfp_ctx_create", "cfp_ctx_destroy", "cfp_last_error", "cfp_nccl_unique_id",
            "cfp_segment_costs", "cfp_minplus_chain", "cfp_search_plan", "cfp_minplus_product",
            "cfp_prepare", "cfp_execute", "cfp_fetch_plan", "cfp_prepared_free",
-           "cfp_ctx_nccl_info", "cfp_prepared_query", "cfp_prepared_time_kernels", "cfp_prepared_kernel_ms", "cfp_prepared_phase_ms",
+           "cfp_ctx_nccl_info", "cfp_prepared_tables", "cfp_prepared_query", "cfp_prepared_time_kernels", "cfp_prepared_kernel_ms", "cfp_prepared_phase_ms",
            "cfp_shard_range", "cfp_pack_keys", "cfp_unpack_keys", "cfp_intpipe_bench",
            "cfp_minplus_bench", "cfp_search_plan_mem", "cfp_segment_costs_mem", "cfp_mem_prepare",
            "cfp_mem_execute", "cfp_mem_fetch_plan", "cfp_mem_free", "cfp_mem_time_kernels",
@@ -141,6 +141,7 @@ def lib() -> C.CDLL:
     L.cfp_prepared_kernel_ms.argtypes = [vp, P(C.c_double), P(C.c_double)]
     L.cfp_prepared_phase_ms.argtypes = [vp, P(C.c_double)]
     L.cfp_ctx_nccl_info.argtypes = [vp, P(C.c_int32), P(C.c_int32)]
+    L.cfp_prepared_tables.argtypes = [vp, vp, C.c_int32, P(C.c_uint64), P(C.c_uint64)]
     L.cfp_shard_range.argtypes = [C.c_int64, C.c_int64, C.c_int32, C.c_int32, P(C.c_int64), P(C.c_int64)]
     L.cfp_pack_keys.argtypes = [C.c_int64, P(C.c_uint64), P(C.c_uint64), C.c_int32, P(C.c_uint64)]
     L.cfp_unpack_keys.argtypes = [C.c_int64, P(C.c_uint64), C.c_int32, P(C.c_uint64), P(C.c_uint64)]
@@ -376,6 +377,8 @@ class PreparedInfo:
     schedule: List[Tuple[int, int, int, int]]   # per type (prefix_len, NB, VG, na)
     fused_tail: bool = False
     tail_grid: int = 0
+    o_mode: Tuple[int, ...] = ()      # per type: output block in B (0), M (1), prefix (2)
+    full_a: Tuple[int, ...] = ()      # per type: 1 = fully unrolled A-loop enumeration kernel
 
 
 class Context:
@@ -606,7 +609,16 @@ class Prepared:
         _check(lib().cfp_prepared_query(self._h, C.byref(i)))
         sched = [(i.prefix_len[t], i.nb[t] // 100, i.nb[t] % 100, i.na[t]) for t in range(i.num_types)]
         return PreparedInfo(i.combos, i.combos_local, i.evals, i.num_types, i.num_transitions,
-                            i.wide_types, i.kernel_launches, sched, bool(i.fused_tail), i.tail_grid)
+                            i.wide_types, i.kernel_launches, sched, bool(i.fused_tail), i.tail_grid,
+                            tuple(i.o_mode[t] for t in range(i.num_types)),
+                            tuple(i.full_a[t] for t in range(i.num_types)))
+
+    def tables(self, transition: int, d_in: int, d_out: int) -> Tuple[np.ndarray, np.ndarray]:
+        """(A, I) of one transition through this prepared search's schedule and kernels."""
+        A = np.empty((d_in, d_out), np.uint64)
+        I = np.empty((d_in, d_out), np.uint64)
+        _check(lib().cfp_prepared_tables(self.ctx._h, self._h, transition, _p(A, C.c_uint64), _p(I, C.c_uint64)))
+        return A, I
 
     def time_kernels(self, on=True):
         """0 off, 1 (True): events around a0 / enumeration / whole path, 2: + every phase."""

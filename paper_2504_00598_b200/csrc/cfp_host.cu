@@ -90,6 +90,9 @@ struct cfp_ctx {
   bool plan_cache = true;           // CFP_PLAN_CACHE=0: no structure-keyed reuse in cfp_search_plan
   bool fused_tail = true;           // CFP_FUSED_TAIL=0: separate launches after the enumeration (A/B, tests)
   bool tail_squaring = false;       // CFP_TAIL_SQUARING=1: fused chain by repeated squaring (A/B, tests)
+  int force_nb = 0;                 // CFP_ENUM_NB: register group size of the enumeration (tuning, tests)
+  bool force_o_m = false;           // CFP_ENUM_O_IN_M=1: output block in the M loop (tests)
+  int force_p = 0;                  // CFP_ENUM_P: prefix length of the enumeration schedule (tests)
   cfp_prepared* cached = nullptr;   // last cfp_search_plan's prepared plan (device buffers, schedule)
   std::vector<int64_t> cached_key;  //   and its structural key (plan_key)
   bool mem_chain_fused = true;      // CFP_MEM_CHAIN_FUSED=0: one launch per DP step (A/B tests)
@@ -144,6 +147,9 @@ extern "C" cfp_status cfp_ctx_create(cfp_ctx** out, const cfp_ctx_opts* opts) {
   if (const char* pc = getenv("CFP_PLAN_CACHE")) c->plan_cache = atoi(pc) != 0;
   if (const char* ft = getenv("CFP_FUSED_TAIL")) c->fused_tail = atoi(ft) != 0;
   if (const char* sq = getenv("CFP_TAIL_SQUARING")) c->tail_squaring = atoi(sq) != 0;
+  if (const char* nb = getenv("CFP_ENUM_NB")) c->force_nb = atoi(nb);
+  if (const char* om = getenv("CFP_ENUM_O_IN_M")) c->force_o_m = atoi(om) != 0;
+  if (const char* fp = getenv("CFP_ENUM_P")) c->force_p = atoi(fp);
   if (const char* ms = getenv("CFP_ENUM_MSPLIT_MIN_M")) c->msplit_min_m = std::max(2LL, atoll(ms));
   if (opts && opts->cuda_stream) {
     c->stream = (cudaStream_t)opts->cuda_stream;
@@ -358,6 +364,7 @@ struct cfp_prepared {
   std::vector<TypeExec> types;
   std::vector<TransExec> trans;
   std::vector<int> inst;
+  std::vector<int> canon;                   // dedup: transition -> canonical identical transition
   // device memory
   DevBuf raw, maps, vals32, vals64, jobs32, jobs64, specs32, specs64, mtab, bp, scratch,
       outAI, chain_inst, chain_runs, chain_mats, chain_moff, chain_G, chain_goff, chain_pow, plan, radix_blob, status,
@@ -369,7 +376,7 @@ struct cfp_prepared {
   DevBuf epi, aps, pair_off, locAI, edges, reach;
   // fused tail (world 1): one cooperative launch after the enumeration
   bool fused_tail = false;
-  int tail_grid = 0;
+  int tail_grid = 0, tail_per_sm = 1;
   size_t tail_smem = 0;
   TailParams tp{};
   DevBuf orig_off, tail_sync, phase_ts;
@@ -465,16 +472,19 @@ double schedule_cost(const HostType& t, int P, const std::vector<int>& role, int
 }
 
 Schedule plan_schedule(const HostType& t, const std::vector<int>& fold_digits, int ntrans_in,
-                       int sms, int din_max) {
+                       int sms, int din_max, int force_nb, bool force_o_m, int force_p) {
   const auto& r = t.radix_c;
   int Pmin = 0;
   for (int d : fold_digits) Pmin = std::max(Pmin, d + 1);
   Schedule best;
-  static const int force_nb = getenv("CFP_ENUM_NB") ? atoi(getenv("CFP_ENUM_NB")) : 0;
+  // force_nb (CFP_ENUM_NB): register group size override; force_o_m
+  // (CFP_ENUM_O_IN_M=1): only schedules with the output block in the M loop
+  // -- tuning / test overrides read at ctx creation
   int64_t nP = prod(r, 0, Pmin);
   for (int P = Pmin; P <= t.K; ++P) {
     if (P > Pmin) nP *= r[P - 1];
     if (nP > (int64_t)1 << 26) break;
+    if (force_p > 0 && P != std::max(force_p, Pmin)) continue;   // CFP_ENUM_P (tests)
     const int S = t.K - P;
     std::vector<int> role(t.K, 0);
     // enumerate roles of suffix digits (base-3 counter over M/A/B); cap size
@@ -492,6 +502,7 @@ Schedule plan_schedule(const HostType& t, const std::vector<int>& fold_digits, i
       }
       if (S > 9 && (na_d > 2 || nb_d > 2)) continue;
       if (role[t.o] == 2) continue;                    // o never in A
+      if (force_o_m && t.o >= P && role[t.o] != 1) continue;
       bool ok = true;
       for (int e = 0; e < t.E && ok; ++e) {
         int a = t.esrc[e], b = t.edst[e];
@@ -688,8 +699,8 @@ static cfp_status validate_and_model(const cfp_problem* p, std::vector<HostType>
 // tables (A, I): instances of the later one are pointed at the first, and the
 // later one is marked unused (not folded).  C3/C5: L1 -> L and L -> L carry
 // the same reshard profiles.
-static void dedup_transitions(const std::vector<HostType>& T, std::vector<HostTrans>& X, const Builder& b,
-                              std::vector<int>& inst) {
+static std::vector<int> dedup_transitions(const std::vector<HostType>& T, std::vector<HostTrans>& X,
+                                          const Builder& b, std::vector<int>& inst) {
   auto out_keep = [&](int pred) {
     return pred < 0 ? std::vector<int>{0} : T[pred].keep[T[pred].o];
   };
@@ -714,6 +725,7 @@ static void dedup_transitions(const std::vector<HostType>& T, std::vector<HostTr
   for (int& t : inst) t = canon[t];
   for (int x = 0; x < (int)X.size(); ++x)
     if (canon[x] != x) X[x].used = false;
+  return canon;
 }
 
 // Precision of a type: narrow (uint32) iff the sum of the finite maxima of
@@ -897,12 +909,13 @@ struct HostModel {
   std::vector<HostTrans> X;
   Builder b;
   std::vector<int> inst;
+  std::vector<int> canon;       // transition -> the identical transition whose tables it shares
 };
 
 static cfp_status build_model(cfp_ctx* ctx, const cfp_problem* p, bool do_chain, HostModel& m) {
   TRY(validate_and_model(p, m.T, m.X, m.b, do_chain));
   m.inst.assign(p->inst_transition, p->inst_transition + p->num_instances);
-  if (ctx->dedup) dedup_transitions(m.T, m.X, m.b, m.inst);
+  if (ctx->dedup) m.canon = dedup_transitions(m.T, m.X, m.b, m.inst);
   return CFP_OK;
 }
 
@@ -925,6 +938,7 @@ static cfp_status prepare_impl(cfp_ctx* ctx, const cfp_problem* p, bool do_chain
   P->do_chain = do_chain;
   P->N = p->num_instances;
   P->inst = pre->inst;
+  P->canon = pre->canon;
   const int world = ctx->world, rank = ctx->rank;
 
   TRY(check_chain_overflow(T, X, P->inst));
@@ -1028,7 +1042,8 @@ static cfp_status prepare_impl(cfp_ctx* ctx, const cfp_problem* p, bool do_chain
       for (int j : X[x].xdst) fold.push_back(j);
       din_max = std::max(din_max, X[x].Din);
     }
-    Schedule sc = plan_schedule(t, fold, (int)te.trans.size(), ctx->sms, din_max);
+    Schedule sc = plan_schedule(t, fold, (int)te.trans.size(), ctx->sms, din_max, ctx->force_nb, ctx->force_o_m,
+                                ctx->force_p);
     if (sc.cost >= 1e299) return fail(CFP_ETOOBIG, "no enumeration schedule for type " + std::to_string(te.id));
     te.P = sc.P;
     te.role = sc.role;
@@ -1610,6 +1625,7 @@ static cfp_status prepare_impl(cfp_ctx* ctx, const cfp_problem* p, bool do_chain
       int64_t g = do_chain ? std::max<int64_t>(8, (warps + wpc - 1) / wpc + 1) : std::max<int64_t>(1, P->npairs);
       g = std::max<int64_t>(2, std::min<int64_t>(g, (int64_t)ctx->sms * per_sm));
       P->tail_grid = (int)g;
+      P->tail_per_sm = per_sm;
       P->tail_smem = smem;
       P->fused_tail = true;
     }
@@ -1646,7 +1662,10 @@ static cfp_status run_type_kernels(cfp_prepared* P, TypeExec& te, cudaStream_t s
 
 static cfp_status merge_ranks(cfp_prepared* P, cudaStream_t st);
 
-static cfp_status execute_impl(cfp_ctx* ctx, cfp_prepared* P) {
+// all_tables: every bucket's least index (as cfp_segment_costs) instead of the
+// chain + backtrack -- cfp_prepared_tables reads the tables of the exact
+// schedule / kernels a search runs
+static cfp_status execute_impl(cfp_ctx* ctx, cfp_prepared* P, bool all_tables = false) {
   CUDA_TRY(cudaSetDevice(ctx->device));
   cudaStream_t st = ctx->stream;
   P->launches = 0;
@@ -1707,7 +1726,13 @@ static cfp_status execute_impl(cfp_ctx* ctx, cfp_prepared* P) {
   if (P->fused_tail) {
     TailParams tp = P->tp;
     tp.phase_ts = P->timing >= 2 ? P->phase_ts.as<uint64_t>() : nullptr;
-    CUDA_TRY(launch_tail(tp, P->tail_grid, P->tail_smem, st));
+    int grid = P->tail_grid;
+    if (all_tables && tp.chain) {
+      tp.chain = 0;
+      tp.phase_ts = nullptr;
+      grid = (int)std::max<int64_t>(2, std::min<int64_t>(P->npairs, (int64_t)ctx->sms * P->tail_per_sm));
+    }
+    CUDA_TRY(launch_tail(tp, grid, P->tail_smem, st));
     P->launches++;
     CUDA_TRY(phase(4));
     CUDA_TRY(phase(5));
@@ -1738,7 +1763,7 @@ static cfp_status execute_impl(cfp_ctx* ctx, cfp_prepared* P) {
   CUDA_TRY(phase(4));
   ArgminEntry* list = P->edges.as<ArgminEntry>();
   int32_t* count = reinterpret_cast<int32_t*>(P->edges.as<char>() + (size_t)(ai + 1) * sizeof(ArgminEntry));
-  const bool edges = P->do_chain && P->use_edges;
+  const bool edges = P->do_chain && P->use_edges && !all_tables;
   if (edges) {
     // a3: suffix vectors + the optimal edges reachable from the chain start
     CUDA_TRY(cudaMemsetAsync(P->cp.status, 0, 4, st));
@@ -1763,7 +1788,7 @@ static cfp_status execute_impl(cfp_ctx* ctx, cfp_prepared* P) {
   if (ctx->sharded) TRY(merge_ranks(P, st));
   CUDA_TRY(phase(6));
   // a4 (+ a3 when the edge list is not used)
-  if (P->do_chain) {
+  if (P->do_chain && !all_tables) {
     if (!edges) CUDA_TRY(cudaMemsetAsync(P->cp.status, 0, 4, st));
     ChainParams c2 = P->cp;
     c2.mode = edges ? 2 : 0;
@@ -1921,6 +1946,24 @@ extern "C" cfp_status cfp_search_plan(cfp_ctx* ctx, const cfp_problem* p, cfp_pl
   return CFP_OK;
 }
 
+extern "C" cfp_status cfp_prepared_tables(cfp_ctx* ctx, cfp_prepared* P, int32_t transition, uint64_t* cost_out,
+                                          uint64_t* index_out) {
+  if (!ctx || !P || !cost_out || !index_out) return fail(CFP_EINVAL, "null argument");
+  const TransExec* tx = nullptr;
+  if (transition >= 0 && transition < (int)P->canon.size()) transition = P->canon[transition];
+  for (const TransExec& t : P->trans) if (t.id == transition) tx = &t;
+  if (!tx) return fail(CFP_EINVAL, "transition " + std::to_string(transition) +
+                                       " is not used by the instance list (or was merged with an identical one)");
+  TRY(execute_impl(ctx, P, true));
+  const int64_t n = (int64_t)tx->Din * tx->Do_orig;
+  CUDA_TRY(cudaMemcpyAsync(cost_out, P->outAI.as<uint64_t>() + tx->out_off, n * 8, cudaMemcpyDeviceToHost,
+                           ctx->stream));
+  CUDA_TRY(cudaMemcpyAsync(index_out, P->outAI.as<uint64_t>() + P->ai + tx->out_off, n * 8,
+                           cudaMemcpyDeviceToHost, ctx->stream));
+  CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+  return CFP_OK;
+}
+
 extern "C" cfp_status cfp_prepared_query(const cfp_prepared* P, cfp_prepared_info* info) {
   if (!P || !info) return fail(CFP_EINVAL, "null argument");
   memset(info, 0, sizeof(*info));
@@ -1937,6 +1980,11 @@ extern "C" cfp_status cfp_prepared_query(const cfp_prepared* P, cfp_prepared_inf
     info->prefix_len[i] = P->types[i].P;
     info->nb[i] = P->types[i].NB * 100 + P->types[i].ep.VG;
     info->na[i] = P->types[i].ep.na;
+    const EnumParams& e = P->types[i].ep;
+    info->o_mode[i] = e.o_mode;
+    info->full_a[i] = (!P->types[i].wide && e.MS == 1 && e.staged && e.ymerge && e.na == P->types[i].NB &&
+                       (P->types[i].NB == 23 || P->types[i].NB == 24) && !e.no_full_a &&
+                       e.na_pad >= (P->types[i].NB + 3) / 4 * 4) ? 1 : 0;
   }
   return CFP_OK;
 }

@@ -356,6 +356,38 @@ def make_config(cfg: str, seed: int = 0, dist: str = "shaped") -> Problem:
     return prob
 
 
+def midsize(cfg: str, keep, n_layers: int = 6, seed: int = 0, dist: str = "shaped") -> Problem:
+    """A config's graph with its layer types restricted to the blocks `keep`
+    (renumbered in order), for parity tests of the full-size kernels at a size
+    the oracle enumerates in seconds: the same radices (D = 24, or 23 feasible
+    with the (B,B) strategy infeasible at C4/C5), value tables, edges among the
+    kept blocks, cross tables of the kept consumer blocks and output block.
+    Pure slicing of the config's inputs."""
+    base = make_config(cfg, seed, dist)
+    keep = list(keep)
+    pos = {b: i for i, b in enumerate(keep)}
+
+    def cut(t: SegmentType) -> SegmentType:
+        o = t.offsets()
+        sl = lambda a: None if a is None else np.concatenate([a[o[j]:o[j + 1]] for j in keep])
+        edges = [Edge(pos[e.src], pos[e.dst], e.table) for e in t.edges if e.src in pos and e.dst in pos]
+        return SegmentType(radix=t.radix[keep].copy(), comp_ns=sl(t.comp_ns), comm_ns=sl(t.comm_ns),
+                           edges=edges, out_block=pos[t.out_block], name=t.name + "'", mem=sl(t.mem))
+
+    E, L1, L, H = base.types
+    types = [E, cut(L1), cut(L), H]
+    trs = []
+    for tr in base.transitions:
+        if tr.type in (1, 2):
+            xs = [CrossEdge(pos[x.dst], x.table) for x in tr.in_edges if x.dst in pos]
+        else:
+            xs = list(tr.in_edges)
+        trs.append(Transition(tr.pred_type, tr.type, xs, tr.name))
+    inst = [0, 1, 2] + [3] * (n_layers - 2) + [4]
+    return Problem(base.mesh, types, trs, np.array(inst, dtype=np.int32),
+                   f"{cfg}[{','.join(map(str, keep))}]x{n_layers}")
+
+
 # --------------------------------------------------------------------------
 # tiny random corpus (SURVEY §8(c))
 # --------------------------------------------------------------------------
