@@ -330,34 +330,44 @@ int orc_minplus(int32_t m, int32_t k, int32_t n, const uint64_t* A, const uint64
  * ------------------------------------------------------------------------- */
 static uint64_t ceil_div(uint64_t a, uint64_t b) { return a / b + (a % b != 0); }
 
-static uint64_t block_q(const orc_type* t, int32_t j, int32_t s, uint64_t quantum) {
+static uint64_t block_mem(const orc_type* t, int32_t j, int32_t s) {
   if (!t->mem) return 0;
   int64_t off = 0;
   for (int32_t q = 0; q < j; ++q) off += t->radix[q];
-  return ceil_div((uint64_t)t->mem[off + s], quantum);   /* R-M1: per-block ceiling */
+  return (uint64_t)t->mem[off + s];
 }
 
+/* m_n(i_n): the segment plan's peak memory, Eq. 4 restricted to one segment
+ * (the sum of its ParallelBlocks' profiled memories, reading R-M1). */
+uint64_t orc_mem_exact(const orc_type* t, const int32_t* s) {
+  uint64_t m = 0;
+  for (int32_t j = 0; j < t->K; ++j) m += block_mem(t, j, s[j]);
+  return m;
+}
+
+/* "we quantize the memory usage of each parallelism plan": the
+ * plan's quanta q = ceil(m_n(i_n) / quantum) (ceiling; R-M1). */
 uint64_t orc_mem_q(const orc_type* t, const int32_t* s, uint64_t quantum) {
-  uint64_t q = 0;                                         /* Eq. 4 within a segment */
-  for (int32_t j = 0; j < t->K; ++j) q += block_q(t, j, s[j], quantum);
-  return q;
+  return ceil_div(orc_mem_exact(t, s), quantum);
 }
 
+/* [qlo, qhi] of a type: the ceilings of the smallest and largest plan memory
+ * over ALL strategies (R-M3; ceil is monotone, so every plan lies inside). */
 int orc_mem_range(const orc_type* t, uint64_t quantum, int64_t* qlo, int64_t* qhi) {
   if (quantum == 0) return ORC_EINVAL;
-  int64_t lo = 0, hi = 0;
+  uint64_t lo = 0, hi = 0;
   for (int32_t j = 0; j < t->K; ++j) {
     uint64_t mn = ORC_INF64, mx = 0;
     for (int32_t s = 0; s < t->radix[j]; ++s) {
-      uint64_t q = block_q(t, j, s, quantum);
-      if (q < mn) mn = q;
-      if (q > mx) mx = q;
+      uint64_t m = block_mem(t, j, s);
+      if (m < mn) mn = m;
+      if (m > mx) mx = m;
     }
-    lo += (int64_t)mn;
-    hi += (int64_t)mx;
+    lo += mn;
+    hi += mx;
   }
-  *qlo = lo;
-  *qhi = hi;
+  *qlo = (int64_t)ceil_div(lo, quantum);
+  *qhi = (int64_t)ceil_div(hi, quantum);
   return ORC_OK;
 }
 

@@ -113,9 +113,11 @@ int orc_search_plan(const orc_problem* p, int nthreads, uint64_t* total,
 int orc_minplus(int32_t m, int32_t k, int32_t n, const uint64_t* A, const uint64_t* B,
                 uint64_t* C, uint64_t* argk);
 /* ---- memory-constrained search (NEXT-1) ---- */
-/* qlo/qhi of a type: sum_j min/max_s ceil(m_j[s] / quantum). */
+/* qlo/qhi of a type: ceil(sum_j min_s m_j[s] / quantum), ceil(sum_j max_s m_j[s] / quantum). */
 int orc_mem_range(const orc_type* t, uint64_t quantum, int64_t* qlo, int64_t* qhi);
-/* q(s) = sum_j ceil(m_j[s_j] / quantum). */
+/* m(s) = sum_j m_j[s_j]: the segment plan's memory (Eq. 4 within a segment). */
+uint64_t orc_mem_exact(const orc_type* t, const int32_t* s);
+/* q(s) = ceil(m(s) / quantum): each plan's memory quantised. */
 uint64_t orc_mem_q(const orc_type* t, const int32_t* s, uint64_t quantum);
 /* Am, Im: [D_in][D_o][qhi - qlo + 1]. */
 int orc_segment_table_mem(const orc_problem* p, int32_t tr, uint64_t quantum,

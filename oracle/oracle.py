@@ -458,8 +458,9 @@ def search_plan_mem(prob: Problem, quantum: int, mem_limit: int, nthreads: int =
 
 
 def py_mem_q(ty, s: Sequence[int], quantum: int) -> int:
-    """q(s) = sum_j ceil(m_j[s_j] / quantum) (pure Python, independent of the C code)."""
-    return sum(-(-int(ty.mem_of(j)[s[j]]) // quantum) for j in range(ty.K))
+    """q(s) = ceil(sum_j m_j[s_j] / quantum): the segment plan's memory
+    quantised as a whole, P:628 (pure Python, independent of the C code)."""
+    return -(-sum(int(ty.mem_of(j)[s[j]]) for j in range(ty.K)) // quantum)
 
 
 def py_mem_exact(ty, s: Sequence[int]) -> int:
@@ -468,7 +469,7 @@ def py_mem_exact(ty, s: Sequence[int]) -> int:
 
 def brute_force_mem(prob: Problem, quantum: int, mem_limit: int, limit: int = 10 ** 6) -> Dict:
     """All global plans in lexicographic order; feasible iff
-    sum_n q_n <= floor(mem_limit / quantum) (Eq. 4 with per-block ceilings);
+    sum_n q_n <= floor(mem_limit / quantum), q_n = ceil(m_n(i_n) / quantum) (Eq. 4, P:628);
     minimal Eq. 3 total, lexicographically smallest tuple."""
     Qmax = mem_limit // quantum
     spaces = []
@@ -515,9 +516,9 @@ def brute_force_mem(prob: Problem, quantum: int, mem_limit: int, limit: int = 10
 def brute_force_table_mem(prob: Problem, tr: int, quantum: int):
     """Am/Im of one transition by direct enumeration in Python (tiny only)."""
     ty = prob.types[prob.transitions[tr].type]
-    qs = [[-(-int(x) // quantum) for x in ty.mem_of(j)] for j in range(ty.K)]
-    qlo = sum(min(q) for q in qs)
-    qhi = sum(max(q) for q in qs)
+    lo = sum(min(int(x) for x in ty.mem_of(j)) for j in range(ty.K))
+    hi = sum(max(int(x) for x in ty.mem_of(j)) for j in range(ty.K))
+    qlo, qhi = -(-lo // quantum), -(-hi // quantum)
     din, dout = prob.d_in(tr), prob.d_out(tr)
     A = np.full((din, dout, qhi - qlo + 1), INF64, dtype=np.uint64)
     I = np.full_like(A, NOIDX)

@@ -36,7 +36,7 @@ def _search(p, quantum, limit):
         return dict(total=None)
 
 
-@pytest.mark.parametrize("name", ["m1", "m2"])
+@pytest.mark.parametrize("name", ["m1", "m2", "m3", "m4"])
 def test_golden_mixed_plans(oracle_lib, name):
     d = load(name)
     p = problem_from(d["problem"])
@@ -56,6 +56,22 @@ def test_mem_range_by_hand(oracle_lib):
     assert O.mem_range(p, 0, 2) == (2, 3)
     assert O.mem_range(p, 0, 4) == (1, 2)
     assert O.mem_range(p, 0, 7) == (1, 1)
+    # M3: plan memories 2..10 quantised per plan: ceil(2/4) = 1,
+    # ceil(10/4) = 3 -- per-block ceilings would give (2, 4)
+    p = problem_from(load("m3")["problem"])
+    assert O.mem_range(p, 0, 4) == (1, 3)
+    assert O.mem_range(p, 0, 1) == (2, 10)
+
+
+def test_m3_table_by_hand(oracle_lib):
+    """M3's table at quantum 4: bucket (u=0, v=s1, q): plan 0 (v 0, q 1, T 20),
+    plan 1 (v 1, q 2, T 14), plan 2 (v 0, q 2, T 14), plan 3 (v 1, q 3, T 8)."""
+    p = problem_from(load("m3")["problem"])
+    A, I, qlo = O.segment_table_mem(p, 0, 4)
+    INF = O.INF64
+    assert qlo == 1 and A.shape == (1, 2, 3)
+    assert A[0].tolist() == [[20, 14, INF], [INF, 14, 8]]
+    assert I[0].tolist() == [[0, 2, INF], [INF, 1, 3]]
 
 
 @pytest.mark.parametrize("seed", range(60))
