@@ -277,9 +277,13 @@ struct TailParams {
 // suffix digit.  For ctx value c and suffix combination sigma the host
 // tabulates T[c][sigma] = every Eq. 3 term touching a suffix digit; K0[p] =
 // every term inside the prefix.  Cost of combination (p, sigma) =
-// K0[p] + T[ctx(p)][sigma].  Buckets: output layout v and quantised memory
-// q = qP(p) + qS(sigma); suffix classes cls = vslot * RQs + (qS - qS_lo),
-// vslot = s_o when o is a suffix digit, else 0 (v then comes from the prefix).
+// K0[p] + T[ctx(p)][sigma].  Buckets: output layout v and quantised plan
+// memory q = ceil((mP(p) + mS(sigma)) / quantum) (each plan's memory is
+// quantised).  Prefixes are grouped by exact mP; for group g the suffix class
+// is cls = vslot * RQs + rs, rs = q - q0(g), q0(g) = ceil((mP_g + mS_min) /
+// quantum), vslot = s_o when o is a suffix digit, else 0 (v then comes from
+// the prefix).  Suffixes sorted by (vslot, mS): every class of a group is one
+// contiguous run of that order.
 // ---------------------------------------------------------------------------
 constexpr int kMemFoldRows = 64;     // rows staged per fold step
 constexpr int kMemFoldCols = 128;    // columns (classes) per fold CTA
@@ -306,9 +310,10 @@ struct MemEnumParams {
   int32_t Wc;                        // classes per prefix row
   int32_t Tlen;                      // padded sorted row length (multiple of 4)
   int64_t nP;
-  const void* Ts;                    // [nC][Tlen] class-sorted, each class padded with CAP
-  const int32_t* cstart;             // [Wc + 1]
-  const int4* etiles;                // (pos_start, count, ctx, 0)
+  const void* Ts;                    // [nC][Tlen] suffixes sorted by (vslot, exact memory), CAP padded
+  const int2* runs;                  // [ngroups][Wc] class runs [start, end) of the sorted row
+  const int4* ctiles;                // CTA: (first warp tile, warp tiles <= 8, ctx, 0)
+  const int4* wtiles;                // warp: (pos_start, count <= 32 * NPF, prefix group, 0)
   const int32_t* perm;
   const void* K0;                    // [nP] natural prefix order
   void* B;                           // [Wc/4][nP][4] out: K0[p] + min over the class
@@ -356,7 +361,12 @@ struct MemArgSlot {                  // one transition (argmin side)
   const void* chunk;
   const void* K0;
   const void* Tc;                    // [nC][nS] canonical suffix order
-  const int32_t* sinfo;              // [nS] class of each suffix combination
+  const int32_t* svs;                // [nS] output slot of each suffix combination
+  const uint64_t* sms;               // [nS] its exact memory mS
+  const int32_t* gP;                 // [nP] prefix group (natural prefix order)
+  const uint64_t* gmem;              // [ngroups] group memory mP_g
+  const int32_t* gq0;                // [ngroups] q0(g)
+  uint64_t quantum;
   int64_t nS;
   const uint64_t* Am;
   uint64_t* Im;                      // [Din][Do][nq]

@@ -84,57 +84,78 @@ __device__ __forceinline__ int64_t mem_ctx(const MemPrefixMap& m, int64_t p) {
 }
 
 // --------------------------------------------------------------------------
-// Enumeration.  CTA = one enumeration tile (<= kMemNPF * 256 positions of one
-// ctx value c); thread = kMemNPF positions.  T[c] (class-sorted, padded with
-// CAP) is staged in shared memory; every combination of a class is one
-// VIADDMNMX per prefix: acc_i = min(K0[p_i] + T[c][e], acc_i).  B[cls][pos]
-// stores are coalesced (consecutive lanes, consecutive positions).
+// Enumeration.  CTA = up to 8 warp tiles of one ctx value c; warp tile = up to
+// 32 * NPF consecutive prefix positions of one prefix-memory group g (so one
+// set of suffix class runs); lane = NPF positions.  T[c] (suffixes sorted by
+// (output slot, exact memory), CAP padded) is staged in shared memory; every
+// combination of a class run is one VIADDMNMX per prefix:
+// acc_i = min(K0[p_i] + T[c][e], acc_i).  The runs start anywhere in the row:
+// a scalar head up to the next 16-byte boundary, 16-byte loads (warp-uniform
+// addresses: broadcasts), a scalar tail.  B[cls][pos] stores are coalesced.
 // --------------------------------------------------------------------------
 template <typename V, int NPF>
 __global__ void __launch_bounds__(256) mem_enum_kernel(const MemEnumParams p) {
   using M = MT<V>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   V* ts = reinterpret_cast<V*>(smem_raw);
-  int32_t* cs = reinterpret_cast<int32_t*>(ts + p.Tlen);
-  const int4 et = p.etiles[blockIdx.x];
-  const V* src = static_cast<const V*>(p.Ts) + (int64_t)et.z * p.Tlen;
+  const int4 ct = p.ctiles[blockIdx.x];
+  const V* src = static_cast<const V*>(p.Ts) + (int64_t)ct.z * p.Tlen;
   for (int e = threadIdx.x * 4; e < p.Tlen; e += 256 * 4) {
     V t[4];
     M::load4(src + e, t);
 #pragma unroll
     for (int q = 0; q < 4; ++q) ts[e + q] = t[q];
   }
-  for (int e = threadIdx.x; e <= p.Wc; e += 256) cs[e] = p.cstart[e];
   __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (warp >= ct.y) return;                          // no barrier below
+  const int4 wt = p.wtiles[ct.x + warp];
   int64_t pos[NPF];
   V k0[NPF];
   bool live[NPF];
 #pragma unroll
   for (int i = 0; i < NPF; ++i) {
-    const int r = i * 256 + threadIdx.x;
-    live[i] = r < et.y;
-    pos[i] = (int64_t)et.x + r;
+    const int r = i * 32 + lane;
+    live[i] = r < wt.y;
+    pos[i] = (int64_t)wt.x + r;
     k0[i] = live[i] ? static_cast<const V*>(p.K0)[p.perm[pos[i]]] : M::CAP;
   }
+  const int2* rg = p.runs + (int64_t)wt.z * p.Wc;
   V* B = static_cast<V*>(p.B);
-  for (int cls = 0; cls < p.Wc; ++cls) {
-    const int s0 = cs[cls], s1 = cs[cls + 1];
-    V acc[NPF];
+  for (int c0 = 0; c0 < p.Wc; c0 += 32) {
+    const int2 myrun = c0 + lane < p.Wc ? rg[c0 + lane] : make_int2(0, 0);   // one coalesced load per 32 classes
+    const int nc = min(32, p.Wc - c0);
+    for (int ci = 0; ci < nc; ++ci) {
+      const int s0 = __shfl_sync(0xffffffffu, myrun.x, ci), s1 = __shfl_sync(0xffffffffu, myrun.y, ci);
+      V acc[NPF];
 #pragma unroll
-    for (int i = 0; i < NPF; ++i) acc[i] = M::CAP;
+      for (int i = 0; i < NPF; ++i) acc[i] = M::CAP;
+      const int a0 = min((s0 + 3) & ~3, s1), a1 = max(a0, s1 & ~3);
+      for (int e = s0; e < a0; ++e) {                  // head
+        const V t = ts[e];
+#pragma unroll
+        for (int i = 0; i < NPF; ++i) acc[i] = M::addmin(k0[i], t, acc[i]);
+      }
 #pragma unroll 2
-    for (int e = s0; e < s1; e += 4) {
-      V t[4];
-      M::load4(ts + e, t);
+      for (int e = a0; e < a1; e += 4) {               // 16-byte body
+        V t[4];
+        M::load4(ts + e, t);
 #pragma unroll
-      for (int q = 0; q < 4; ++q)
+        for (int q = 0; q < 4; ++q)
 #pragma unroll
-        for (int i = 0; i < NPF; ++i) acc[i] = M::addmin(k0[i], t[q], acc[i]);
+          for (int i = 0; i < NPF; ++i) acc[i] = M::addmin(k0[i], t[q], acc[i]);
+      }
+      for (int e = a1; e < s1; ++e) {                  // tail
+        const V t = ts[e];
+#pragma unroll
+        for (int i = 0; i < NPF; ++i) acc[i] = M::addmin(k0[i], t, acc[i]);
+      }
+      const int cls = c0 + ci;
+      V* row = B + (int64_t)(cls >> 2) * p.nP * 4 + (cls & 3);     // B[cls/4][pos][cls%4]
+#pragma unroll
+      for (int i = 0; i < NPF; ++i)
+        if (live[i]) row[pos[i] * 4] = acc[i];
     }
-    V* row = B + (int64_t)(cls >> 2) * p.nP * 4 + (cls & 3);     // B[cls/4][pos][cls%4]
-#pragma unroll
-    for (int i = 0; i < NPF; ++i)
-      if (live[i]) row[pos[i] * 4] = acc[i];
   }
 }
 
@@ -649,11 +670,20 @@ __global__ void __launch_bounds__(256) mem_argmin_kernel(const MemArgSlot* __res
     V xs = 0;                                        // X_{p*}[u]
     for (int j = 0; j < S.nqx; ++j)
       xs = M::sat(xs, vals[S.q_off[j] + (int64_t)mem_digit(S.pm, pstar, S.q_pos[j]) * S.DinP + u]);
-    // the least suffix of p* whose cost K0[p*] + T[c][s] = A - X_{p*}[u]
+    // the least suffix of p* in class (vslot, rs) -- plan memory
+    // ceil((mP_g + mS) / quantum) = q0(g) + rs -- whose cost
+    // K0[p*] + T[c][s] = A - X_{p*}[u]
     const V rel = target - xs - static_cast<const V*>(S.K0)[pstar];
     const V* T = static_cast<const V*>(S.Tc) + c * S.nS;
+    const int g = S.gP[pstar];
+    const uint64_t mPg = S.gmem[g];
+    const int64_t qwant = (int64_t)S.gq0[g] + rs;
+    (void)cls;
     for (int64_t s = tid; s < S.nS; s += 256)
-      if (S.sinfo[s] == cls && T[s] == rel) atomicMin(&s_sig, (unsigned long long)s);
+      if (S.svs[s] == vslot && T[s] == rel) {
+        const uint64_t m = mPg + S.sms[s];
+        if ((int64_t)(m / S.quantum + (m % S.quantum != 0)) == qwant) atomicMin(&s_sig, (unsigned long long)s);
+      }
     __syncthreads();
     if (tid == 0) S.Im[cell] = s_sig == ~0ull ? kInf64 : (uint64_t)pstar * (uint64_t)S.nS + s_sig;
     __syncthreads();
@@ -704,7 +734,7 @@ __global__ void mem_greedy_kernel(const MemChainParams cp, const int32_t* succ) 
 // ---------------------------------------------------------------- launchers
 template <typename V>
 cudaError_t launch_mem_enum(const MemEnumParams& p, int64_t ntiles, int npf, cudaStream_t st) {
-  const size_t smem = (size_t)p.Tlen * sizeof(V) + (size_t)(p.Wc + 1) * 4 + 16;
+  const size_t smem = (size_t)p.Tlen * sizeof(V) + 16;
   if (ntiles <= 0) return cudaSuccess;
   auto go = [&](auto kern) -> cudaError_t {
     if (smem > 48 * 1024) {

@@ -2,7 +2,9 @@
 the C-ABI (cfp_search_plan_mem, cfp_segment_costs_mem) vs the CPU oracle,
 bit-exact: integer ns costs, integer quanta, least-index tie-break.
 
-Cases: the hand-worked golden examples M1/M2; memory-bucketed
+Cases: the hand-worked golden examples M1/M2 and M3/M4 (P:628:
+each plan's memory quantised as a whole -- answers that differ from a
+per-block ceiling); memory-bucketed
 segment tables of random tiny problems (ragged digit splits, INF entries,
 narrow and wide paths, o inside and outside the prefix); full searches with a
 limit drawn between the smallest and largest plan memory (binding or
@@ -63,7 +65,7 @@ def _compare(ctx, O, p, quantum, limit, name=""):
     return got
 
 
-@pytest.mark.parametrize("name", ["m1", "m2"])
+@pytest.mark.parametrize("name", ["m1", "m2", "m3", "m4"])
 def test_golden_mem(ctx, oracle_lib, name):
     d = load(name)
     p = problem_from(d["problem"])
@@ -175,3 +177,26 @@ def test_c3_mem_full_size_sampled(ctx, oracle_lib):
     _, q, ix, cost = O.reconstruct_mem(mats, idxs, qlos, Qmax, Gs)
     assert ix.tolist() == got.seg_index.tolist()
     assert cost.tolist() == got.seg_ns.tolist() and q.tolist() == got.seg_q.tolist()
+
+
+@pytest.mark.parametrize("cfg,keep", [("C3", [3, 4, 5, 6]), ("C5", [3, 4, 5, 6])])
+def test_midsize_mem_tables_every_bucket(ctx, oracle_lib, cfg, keep):
+    """Mid-size cuts of the bench graphs with their memory tables: many prefix
+    memory groups and suffix memories per class, so the per-plan class runs
+    start and end anywhere in the sorted suffix row; every (u, v, q) bucket of
+    every transition vs the oracle, then the search."""
+    O = oracle_lib
+    from synth.generators import midsize
+    p = midsize(cfg, keep, n_layers=5)
+    lo, hi = _qtotals(O, p, 1)                       # exact chain memory range
+    m = O.Marshalled(p)
+    top = max(O.mem_range(p, p.transitions[int(t)].type, 1, m)[1] for t in p.instances)
+    for quantum in (max(1, top // 300), max(1, top // 40)):   # ~300 / ~40 levels per segment
+        for tr in sorted({int(t) for t in p.instances}):
+            A, I, qlo = O.segment_table_mem(p, tr, quantum, m=m)
+            Ag, Ig, qlog = ctx.segment_costs_mem(p.types[p.transitions[tr].type], quantum, p.transitions[tr], p.d_in(tr))
+            assert qlog == qlo and np.array_equal(Ag, A) and np.array_equal(Ig, I), (cfg, quantum, tr)
+        qlo_t, qhi_t = _qtotals(O, p, quantum)
+        for frac in (0.3, 0.7):
+            limit = int((qlo_t + frac * (qhi_t - qlo_t)) * quantum)
+            _compare(ctx, O, p, quantum, limit, f"{cfg} midsize q{quantum} {frac}")
