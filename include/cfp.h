@@ -236,12 +236,15 @@ cfp_status cfp_prepared_phase_ms(cfp_prepared* prep, double* ms /* [6] */);
  * The paper's DP carries a memory constraint: Eq. 4 sums the profiled
  * peak memory of the chosen strategies, and the search keeps plans whose
  * memory fits the device.  Reading R-M1
- * (DESIGN.md): memory is profiled per ParallelBlock strategy, m_j[s], and
- * quantised per block with a ceiling, q_j[s] = ceil(m_j[s] / quantum), so the
- * quantised sum never under-estimates (never falsely feasible).
- *   segment table  Am[u][v][q - qlo] = min_{s: s_o = v, sum_j q_j[s_j] = q} C(u,s)
+ * (DESIGN.md): memory is profiled per ParallelBlock strategy, m_j[s]; a
+ * segment plan's memory is their sum m(s) = sum_j m_j[s_j] (Eq. 4 within the
+ * segment), and "we quantize the memory usage of each parallelism plan"
+ * (P:628): q(s) = ceil(m(s) / quantum) -- a ceiling, so the quantised
+ * total never under-estimates (never falsely feasible).
+ *   segment table  Am[u][v][q - qlo] = min_{s: s_o = v, q(s) = q} C(u,s)
  *                  Im = least big-endian index attaining it (CFP_NOIDX if none),
- *                  qlo/qhi = sum_j min/max_s q_j[s] over ALL strategies;
+ *                  qlo/qhi = ceil(sum_j min_s m_j[s] / quantum) and
+ *                  ceil(sum_j max_s m_j[s] / quantum) over ALL strategies;
  *   chain          states (u, c), c = quantised memory used so far,
  *                  G_N(v, c) = 0 for c <= Qmax = floor(mem_limit / quantum),
  *                  G_{n-1}(u, c) = min_{v, q: c + q <= Qmax} Am_n[u][v][q] + G_n(v, c + q),
@@ -249,8 +252,9 @@ cfp_status cfp_prepared_phase_ms(cfp_prepared* prep, double* ms /* [6] */);
  *   plan           forward greedy from (0, 0), least combination index among
  *                  the optimal successors (v, q) -- the canonical plan.
  * Same conventions as above (host memory, caller-allocated outputs, status
- * codes).  Single-GPU: world > 1 gives CFP_EINVAL.  Limits: Qmax < 65536 and
- * per-block q_j < 2^20 (else CFP_ETOOBIG). */
+ * codes).  Single-GPU: world > 1 gives CFP_EINVAL.  Limits (else CFP_ETOOBIG):
+ * Qmax < 65536, qhi - qlo < 65536 per segment, D_o x (qhi - qlo + 1) of a
+ * segment fits the DP's shared-memory row (coarser quantum otherwise). */
 typedef struct {
   uint64_t quantum;                 /* >= 1, unit of m_j (e.g. KiB) */
   uint64_t mem_limit;               /* per-device limit in the same unit */
