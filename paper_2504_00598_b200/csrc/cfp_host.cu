@@ -90,10 +90,12 @@ struct cfp_ctx {
   bool plan_cache = true;           // CFP_PLAN_CACHE=0: no structure-keyed reuse in cfp_search_plan
   bool fused_tail = true;           // CFP_FUSED_TAIL=0: separate launches after the enumeration (A/B, tests)
   bool tail_squaring = false;       // CFP_TAIL_SQUARING=1: fused chain by repeated squaring (A/B, tests)
+  bool k0_inline = false;           // CFP_K0_INLINE=1: K0 in the enumeration prologue (measured slower)
   int force_nb = 0;                 // CFP_ENUM_NB: register group size of the enumeration (tuning, tests)
   bool force_o_m = false;           // CFP_ENUM_O_IN_M=1: output block in the M loop (tests)
   int force_p = 0;                  // CFP_ENUM_P: prefix length of the enumeration schedule (tests)
   cfp_prepared* cached = nullptr;   // last cfp_search_plan's prepared plan (device buffers, schedule)
+  struct cfp_mem_prepared* mem_cached = nullptr;   // last cfp_search_plan_mem's prepared search
   std::vector<int64_t> cached_key;  //   and its structural key (plan_key)
   bool mem_chain_fused = true;      // CFP_MEM_CHAIN_FUSED=0: one launch per DP step (A/B tests)
   bool dedup = true;                // CFP_DEDUP=0: fold identical transitions separately (A/B tests)
@@ -147,6 +149,7 @@ extern "C" cfp_status cfp_ctx_create(cfp_ctx** out, const cfp_ctx_opts* opts) {
   if (const char* pc = getenv("CFP_PLAN_CACHE")) c->plan_cache = atoi(pc) != 0;
   if (const char* ft = getenv("CFP_FUSED_TAIL")) c->fused_tail = atoi(ft) != 0;
   if (const char* sq = getenv("CFP_TAIL_SQUARING")) c->tail_squaring = atoi(sq) != 0;
+  if (const char* k0 = getenv("CFP_K0_INLINE")) c->k0_inline = atoi(k0) != 0;
   if (const char* nb = getenv("CFP_ENUM_NB")) c->force_nb = atoi(nb);
   if (const char* om = getenv("CFP_ENUM_O_IN_M")) c->force_o_m = atoi(om) != 0;
   if (const char* fp = getenv("CFP_ENUM_P")) c->force_p = atoi(fp);
@@ -213,6 +216,7 @@ extern "C" void cfp_ctx_destroy(cfp_ctx* c) {
   if (!c) return;
   cudaSetDevice(c->device);
   if (c->cached) cfp_prepared_free(c->cached);     // frees on c->stream: before the streams go
+  if (c->mem_cached) cfp_mem_free(c->mem_cached);
   if (c->comm) ncclCommDestroy(c->comm);
   for (int i = 0; i < cfp_ctx::kLanes; ++i) {
     if (c->lane[i]) cudaStreamDestroy(c->lane[i]);
@@ -1119,11 +1123,21 @@ static cfp_status prepare_impl(cfp_ctx* ctx, const cfp_problem* p, bool do_chain
     te.xt_off = place(sx);
     te.yt_off = place(sy);
     te.zt_off = place(sz);
-    te.k0_off = place(sk);
     auto& specs = te.wide ? P->hspecs64 : P->hspecs32;
-    specs.push_back(sx); specs.push_back(sy); specs.push_back(sz); specs.push_back(sk);
+    specs.push_back(sx); specs.push_back(sy); specs.push_back(sz);
     // thread mapping
     EnumParams& ep = te.ep;
+    // K0 (terms inside the prefix): computed in the enumeration prologue when
+    // the term list is short (every config), else a derived table
+    if (sk.nterm <= 12 && ctx->k0_inline) {
+      ep.nk0 = sk.nterm;
+      for (int q = 0; q < sk.nterm; ++q) ep.k0t[q] = sk.term[q];
+      te.k0_off = -1;
+    } else {
+      ep.nk0 = -1;
+      te.k0_off = place(sk);
+      specs.push_back(sk);
+    }
     ep.P = Pp;
     for (int i = 0; i < Pp; ++i) ep.pre_radix[i] = r[i];
     int lmin = Pp;
@@ -1390,7 +1404,7 @@ static cfp_status prepare_impl(cfp_ctx* ctx, const cfp_problem* p, bool do_chain
     ep.XT = vals + (base + te.xt_off) * vb;
     ep.YT = vals + (base + te.yt_off) * vb;
     ep.ZT = vals + (base + te.zt_off) * vb;
-    ep.K0 = vals + (base + te.k0_off) * vb;
+    ep.K0 = te.k0_off < 0 ? nullptr : vals + (base + te.k0_off) * vb;
     ep.mtab = P->mtab.as<int4>() + te.mtab_off;
     ep.Bp = (char*)P->bp.p + te.bp_off;
     for (int x : te.trans) {

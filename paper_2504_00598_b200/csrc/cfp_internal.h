@@ -92,6 +92,11 @@ struct EnumParams {
   int64_t xspan, yspan, zspan;  // slice lengths (staged)
   // device pointers (element type = the path's value type)
   const void* XT; const void* YT; const void* ZT; const void* K0;
+  // K0[p] computed by the enumeration thread itself from the compact W/R
+  // tables (nk0 >= 0: terms over prefix positions, offsets into `vals`) --
+  // no K0 table to build in a0; nk0 = -1: read the K0 table
+  int32_t nk0;
+  Term k0t[12];
   const int4* mtab;             // [nM] (x, y, z, v_o)
   void* Bp;                     // [G*W][Do] local canonical prefixes
   // epilogue fold of the cross-segment terms (one chunk = one CTA's prefixes)
@@ -305,6 +310,30 @@ struct MemPrefixMap {
 // value resp. a (ctx, class) group.  B is class-quad-major: B[cls/4][pos][cls%4]
 // (coalesced enumeration stores, 16-byte fold loads).
 constexpr int kMemFoldTile = 512;
+
+// a0 of the memory-constrained search: the per-prefix K0 and the per-ctx
+// suffix tables (canonical Tc and the (slot, memory)-sorted Ts) summed on the
+// device from the raw input values (every execute; the host keeps only the
+// structure).  One job = one table of one type.
+struct MemValTerm {
+  int32_t kind;                      // 0 unary block a: raw comp (+ comm) ; 1 pair R[d_a][d_b]
+  int32_t a, b;                      // block ids
+  int32_t db;                        // pair: row length (radix of b)
+  int64_t off, off2;                 // raw offsets: comp / table; comm (< 0: none)
+};
+struct MemValJob {
+  int32_t kind;                      // 0: K0[p] over the prefix; 1: Tc[c][sigma]; 2: Ts[c][i], sigma = order[i]
+  int32_t P, K;                      // prefix length, blocks
+  int32_t radix[kMaxDigits];         // original radices of the blocks
+  int32_t nctx, ctx_pos[kMaxDigits]; // ctx blocks (canonical order)
+  int32_t nterm;
+  MemValTerm term[48];
+  int64_t n;                         // entries
+  int64_t nS, Tlen;                  // suffix combinations, sorted row length
+  const int32_t* order;              // kind 2: [nS] sigma of sorted position i
+  void* out;
+  int64_t block0;                    // first CTA of this job in the launch
+};
 
 struct MemEnumParams {
   int32_t Wc;                        // classes per prefix row

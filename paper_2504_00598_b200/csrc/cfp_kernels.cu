@@ -354,6 +354,30 @@ __global__ void __launch_bounds__(kBlock, 4) enum_kernel(const EnumParams p) {
       if (d == p.o_pre) od = dig;
     }
   }
+  // K0[p]: every Eq. 3 term inside the prefix, from the compact W/R tables
+  // (issued before the staging wait below, so its loads overlap the TMA)
+  V k0 = T::CAP;
+  if (live) {
+    if (p.nk0 >= 0) {
+      const V* vals0 = static_cast<const V*>(p.vals);
+      k0 = 0;
+      const bool n32 = pg < 0x7FFFFFFF;
+      for (int t = 0; t < p.nk0; ++t) {
+        const Term tm = p.k0t[t];
+        const int da = n32 ? (int)(((uint32_t)pg / (uint32_t)p.pre_stride[tm.a]) % (uint32_t)p.pre_radix[tm.a])
+                           : (int)((pg / p.pre_stride[tm.a]) % p.pre_radix[tm.a]);
+        int64_t at = tm.off + da;
+        if (tm.kind == 1) {
+          const int db = n32 ? (int)(((uint32_t)pg / (uint32_t)p.pre_stride[tm.b]) % (uint32_t)p.pre_radix[tm.b])
+                             : (int)((pg / p.pre_stride[tm.b]) % p.pre_radix[tm.b]);
+          at = tm.off + (int64_t)da * tm.db + db;
+        }
+        k0 = T::sat(k0, vals0[at]);
+      }
+    } else {
+      k0 = static_cast<const V*>(p.K0)[pg];
+    }
+  }
   const V* XT = static_cast<const V*>(p.XT);
   const V* YT = static_cast<const V*>(p.YT);
   const V* ZT = static_cast<const V*>(p.ZT);
@@ -414,7 +438,6 @@ __global__ void __launch_bounds__(kBlock, 4) enum_kernel(const EnumParams p) {
   if (live) {
     if (p.init_row)
       for (int v = 0; v < p.Do; ++v) Bp[v] = T::CAP;
-    const V k0 = static_cast<const V*>(p.K0)[pg];
     // MS = 2: warps of half 0 take m in [0, mh), warps of half 1 [mh, nM)
     const int nM = (int)p.nM;                      // host: nM < 2^31 (mtab rows)
     const int mh = MSPLIT == 2 ? (nM + 1) / 2 : nM;

@@ -84,6 +84,66 @@ __device__ __forceinline__ int64_t mem_ctx(const MemPrefixMap& m, int64_t p) {
 }
 
 // --------------------------------------------------------------------------
+// a0: K0 / Tc / Ts of every type from the raw input values (saturating uint64
+// sums, INF absorbing, clamped to the path's CAP).  Grid-stride over the jobs'
+// entries; a CTA belongs to one job (block0 ranges).
+// --------------------------------------------------------------------------
+template <typename V>
+__global__ void __launch_bounds__(256) mem_values_kernel(const MemValJob* __restrict__ jobs, int njobs,
+                                                         const uint32_t* __restrict__ raw) {
+  __shared__ int s_j;
+  if (threadIdx.x == 0) {
+    int j = 0;
+    while (j + 1 < njobs && (int64_t)blockIdx.x >= jobs[j + 1].block0) ++j;
+    s_j = j;
+  }
+  __syncthreads();
+  const MemValJob& J = jobs[s_j];
+  const int64_t nblk = (s_j + 1 < njobs ? jobs[s_j + 1].block0 : (int64_t)gridDim.x) - J.block0;
+  V* out = static_cast<V*>(J.out);
+  for (int64_t e = (blockIdx.x - J.block0) * (int64_t)blockDim.x + threadIdx.x; e < J.n;
+       e += nblk * blockDim.x) {
+    int dig[kMaxDigits];
+    uint64_t acc = 0;
+    bool pad = false;
+    if (J.kind == 0) {                                   // prefix p, natural order
+      int64_t q = e;
+      for (int d = J.P - 1; d >= 0; --d) { dig[d] = (int)(q % J.radix[d]); q /= J.radix[d]; }
+    } else {
+      const int64_t row = J.kind == 1 ? J.nS : J.Tlen;
+      int64_t c = e / row, i = e - c * row;
+      if (J.kind == 2) {
+        if (i >= J.nS) pad = true;
+        else i = J.order[i];
+      }
+      for (int d = J.K - 1; d >= J.P; --d) { dig[d] = (int)(i % J.radix[d]); i /= J.radix[d]; }
+      for (int t = J.nctx - 1; t >= 0; --t) {
+        const int b = J.ctx_pos[t];
+        dig[b] = (int)(c % J.radix[b]);
+        c /= J.radix[b];
+      }
+    }
+    if (!pad) {
+      for (int t = 0; t < J.nterm && acc != kInf64; ++t) {
+        const MemValTerm tm = J.term[t];
+        uint64_t x;
+        if (tm.kind == 0) {
+          const uint32_t pc = raw[tm.off + dig[tm.a]];
+          const uint32_t cc = tm.off2 >= 0 ? raw[tm.off2 + dig[tm.a]] : 0u;
+          x = (pc == 0xFFFFFFFFu || cc == 0xFFFFFFFFu) ? kInf64 : (uint64_t)pc + cc;
+        } else {
+          const uint32_t r = raw[tm.off + (int64_t)dig[tm.a] * tm.db + dig[tm.b]];
+          x = r == 0xFFFFFFFFu ? kInf64 : (uint64_t)r;
+        }
+        acc = x == kInf64 ? kInf64 : acc + x;
+      }
+    }
+    const uint64_t cap = MT<V>::CAP;
+    out[e] = (V)((pad || acc >= cap) ? cap : acc);
+  }
+}
+
+// --------------------------------------------------------------------------
 // Enumeration.  CTA = up to 8 warp tiles of one ctx value c; warp tile = up to
 // 32 * NPF consecutive prefix positions of one prefix-memory group g (so one
 // set of suffix class runs); lane = NPF positions.  T[c] (suffixes sorted by
@@ -749,6 +809,13 @@ cudaError_t launch_mem_enum(const MemEnumParams& p, int64_t ntiles, int npf, cud
   return go(mem_enum_kernel<V, 1>);
 }
 template <typename V>
+cudaError_t launch_mem_values(const MemValJob* jobs, int njobs, int64_t nblocks, const uint32_t* raw,
+                              cudaStream_t st) {
+  if (njobs <= 0 || nblocks <= 0) return cudaSuccess;
+  mem_values_kernel<V><<<(unsigned)nblocks, 256, 0, st>>>(jobs, njobs, raw);
+  return cudaGetLastError();
+}
+template <typename V>
 cudaError_t launch_mem_fold(const MemFoldParams& p, int64_t ntiles, cudaStream_t st) {
   if (ntiles <= 0) return cudaSuccess;
   const int64_t xthreads = p.nP * (p.DinP / 4);
@@ -832,6 +899,8 @@ cudaError_t launch_mem_greedy(const MemChainParams& cp, const int32_t* succ, cud
   return cudaGetLastError();
 }
 
+template cudaError_t launch_mem_values<uint32_t>(const MemValJob*, int, int64_t, const uint32_t*, cudaStream_t);
+template cudaError_t launch_mem_values<uint64_t>(const MemValJob*, int, int64_t, const uint32_t*, cudaStream_t);
 template cudaError_t launch_mem_enum<uint32_t>(const MemEnumParams&, int64_t, int, cudaStream_t);
 template cudaError_t launch_mem_enum<uint64_t>(const MemEnumParams&, int64_t, int, cudaStream_t);
 template cudaError_t launch_mem_fold<uint32_t>(const MemFoldParams&, int64_t, cudaStream_t);

@@ -200,3 +200,26 @@ def test_midsize_mem_tables_every_bucket(ctx, oracle_lib, cfg, keep):
         for frac in (0.3, 0.7):
             limit = int((qlo_t + frac * (qhi_t - qlo_t)) * quantum)
             _compare(ctx, O, p, quantum, limit, f"{cfg} midsize q{quantum} {frac}")
+
+
+def test_mem_plan_reuse_alternating(ctx, oracle_lib):
+    """cfp_search_plan_mem keeps the last prepared search: calls with the same
+    structure / memory profile / quantum / limit but new cost values reuse it
+    (values re-uploaded, K0 / T rebuilt on the device), anything else
+    re-prepares; every answer matches the oracle."""
+    import copy
+    O = oracle_lib
+    from synth.memcfg import mem_workload
+    base, quantum, limit = mem_workload("C2", 0, "shaped")
+    other, quantum1, limit1 = mem_workload("C1", 0, "shaped")
+    variants = []
+    for k in range(3):
+        q = copy.deepcopy(base)
+        rng = np.random.default_rng(k)
+        for t in q.types:
+            t.comp_ns[:] = rng.integers(0, 1 << 20, t.comp_ns.shape, dtype=np.uint32)
+        variants.append(q)
+    for p, q, lim in [(variants[0], quantum, limit), (variants[1], quantum, limit), (other, quantum1, limit1),
+                      (variants[2], quantum, limit), (variants[2], quantum, limit + quantum * 7),
+                      (variants[0], quantum, limit)]:
+        _compare(ctx, O, p, q, lim, "reuse")

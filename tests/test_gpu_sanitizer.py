@@ -1,0 +1,42 @@
+"""compute-sanitizer over every CUDA path (SURVEY §5 race / failure detection).
+
+memcheck (out-of-bounds and misaligned device accesses, API errors), racecheck (shared-memory hazards: the enumeration's staged
+tables and fold stripes, the fused tail's chain and argmin scratch), synccheck
+(barriers in divergent code: the tail kernel's early-exit warps, the grid
+barriers' __syncthreads) on tests/sanitize_driver.py, which runs the plain
+search (fused and split tails, the squaring variant), segment tables,
+min-plus chains, the memory-constrained search, dense tables and the
+profiling budget on tiny inputs and checks every answer against the oracle.
+The sanitizer's report is written to gpurun_out/sanitizer_<tool>_<path>.log.
+"""
+import os
+import shutil
+import subprocess
+import sys
+
+import pytest
+
+pytestmark = [pytest.mark.gpu, pytest.mark.slow]
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _sanitizer():
+    for c in (shutil.which("compute-sanitizer"), "/usr/local/cuda/bin/compute-sanitizer"):
+        if c and os.path.exists(c):
+            return c
+    pytest.fail("compute-sanitizer not found")
+
+
+@pytest.mark.parametrize("path", ["plain", "mem", "dense", "budget"])
+@pytest.mark.parametrize("tool", ["memcheck", "racecheck", "synccheck"])
+def test_compute_sanitizer_clean(tool, path):
+    cmd = [_sanitizer(), "--tool", tool, "--error-exitcode", "97", "--print-limit", "50"]
+    cmd += [sys.executable, os.path.join(ROOT, "tests", "sanitize_driver.py"), path]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=1500, cwd=ROOT)
+    out = r.stdout + r.stderr
+    os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
+    with open(os.path.join(ROOT, "gpurun_out", f"sanitizer_{tool}_{path}.log"), "w") as f:
+        f.write(" ".join(cmd) + "\n" + out)
+    assert r.returncode == 0, out[-3000:]
+    assert f"{path}: ok" in out
+    assert "ERROR SUMMARY: 0 errors" in out, out[-3000:]
