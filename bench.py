@@ -393,14 +393,20 @@ def run_cfp(args, prob, rank, world, local_rank):
             traffic = json.load(fh)["traffic_bytes_per_launch"]["enum_kernel"]
     except Exception:
         pass
+    # N2 (min,+) product microbenchmark (S in {256 .. 8192},
+    # u32 / u64, with and without the least-k argmin), part of every default
+    # run on rank 0 (~2 s); --no-minplus skips it
     minplus = None
-    if args.minplus and rank == 0:
+    if not args.no_minplus and rank == 0:
         minplus = []
         for S in (256, 1024, 4096, 8192):
             for wide in (False, True):
-                ms, ops = ctx.minplus_bench(S, wide=wide, iters=3 if S < 8192 else 1)
-                minplus.append({"S": S, "dtype": "u64" if wide else "u32", "ms": ms,
-                                "addmin_per_s": ops, "frac_of_alu_peak": ops / (peak * 1e9)})
+                for argk in (False, True):
+                    if argk and S > 4096:
+                        continue
+                    ms, ops = ctx.minplus_bench(S, wide=wide, iters=3 if S < 8192 else 1, argk=argk)
+                    minplus.append({"S": S, "dtype": "u64" if wide else "u32", "argk": argk, "ms": ms,
+                                    "addmin_per_s": ops, "frac_of_alu_peak": ops / (peak * 1e9)})
     out = None
     if rank == 0:
         out = {
@@ -447,6 +453,13 @@ def run_cfp(args, prob, rank, world, local_rank):
         }
         if minplus is not None:
             out["minplus_microbench"] = minplus
+            best = max((r for r in minplus if r["dtype"] == "u32" and not r["argk"]), key=lambda r: r["addmin_per_s"])
+            out["minplus_roofline"] = {
+                "bound": "alu", "kernel": "minplus_tiled_kernel<u32>", "S": best["S"],
+                "achieved": best["addmin_per_s"] / 1e9, "peak": peak, "unit": "Gop/s",
+                "frac": best["addmin_per_s"] / (peak * 1e9),
+                "note": "one fused add+min (VIADDMNMX.U32) per (i, j, k), S^3 per product; u64 add+min is "
+                        "6 SASS instructions (IADD3, IADD3.X, 2 ISETP, 2 SEL), bound ~1/6 of this peak"}
         if world > 1:
             nr, nv = ctx.nccl_info()
             out["nccl"] = {"nranks": nr, "version": nv,
@@ -767,7 +780,7 @@ def main():
     ap.add_argument("--dist", default="shaped")
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--minplus", action="store_true", help="also run the (min,+) product microbenchmark")
+    ap.add_argument("--no-minplus", action="store_true", help="skip the (min,+) product microbenchmark")
     ap.add_argument("--mem", action="store_true", help="memory-constrained search (NEXT-1) instead")
     ap.add_argument("--dense", action="store_true", help="dense per-plan tables (NEXT-2) instead")
     ap.add_argument("--budget", action="store_true", help="dynamic profiling budget (NEXT-3) instead")

@@ -26,6 +26,7 @@
 #include <vector>
 
 #include "../../include/cfp.h"
+#include <nvtx3/nvToolsExt.h>   // header-only NVTX v3: ranges for nsys / ncu timelines (no-ops untraced)
 #include "cfp_internal.h"
 
 namespace cfp {
@@ -50,6 +51,13 @@ cudaError_t launch_matvec_batch(const uint64_t*, int, int, const uint64_t*, cons
 }  // namespace cfp
 
 using namespace cfp;
+
+// NVTX range for the duration of a scope (host-side phases of prepare /
+// execute / fetch; a profiler attaches the GPU work enqueued inside)
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
 
 // ---------------------------------------------------------------- errors
 static thread_local std::string g_err;
@@ -925,6 +933,7 @@ static cfp_status build_model(cfp_ctx* ctx, const cfp_problem* p, bool do_chain,
 
 static cfp_status prepare_impl(cfp_ctx* ctx, const cfp_problem* p, bool do_chain,
                                cfp_prepared** out, HostModel* pre = nullptr) {
+  NvtxRange nv("cfp_prepare");
   PrepTimer tm;
   *out = nullptr;
   g_alloc_stream = ctx->stream;
@@ -1681,6 +1690,7 @@ static cfp_status merge_ranks(cfp_prepared* P, cudaStream_t st);
 // schedule / kernels a search runs
 static cfp_status execute_impl(cfp_ctx* ctx, cfp_prepared* P, bool all_tables = false) {
   CUDA_TRY(cudaSetDevice(ctx->device));
+  NvtxRange nv("cfp_execute");
   cudaStream_t st = ctx->stream;
   P->launches = 0;
   if (P->timing) {
@@ -1853,6 +1863,7 @@ static cfp_status merge_ranks(cfp_prepared* P, cudaStream_t st) {
 
 // ---------------------------------------------------------------- fetch
 static cfp_status fetch_impl(cfp_ctx* ctx, cfp_prepared* P, cfp_plan* out) {
+  NvtxRange nv("cfp_fetch_plan");
   cudaStream_t st = ctx->stream;
   const int N = P->N;
   // plan + status word in one copy, through the ctx's pinned staging buffer
@@ -1921,6 +1932,7 @@ extern "C" cfp_status cfp_fetch_plan(cfp_ctx* ctx, cfp_prepared* prep, cfp_plan*
 extern "C" cfp_status cfp_search_plan(cfp_ctx* ctx, const cfp_problem* p, cfp_plan* out) {
   if (!ctx || !p || !out) return fail(CFP_EINVAL, "null argument");
   if (ctx->sim) return fail(CFP_EINVAL, "shard simulation ctx (world > 1 without nccl_unique_id): tables only");
+  NvtxRange nv("cfp_search_plan");
   std::vector<int64_t> key;
   HostModel model;
   TRY(build_model(ctx, p, true, model));

@@ -32,6 +32,15 @@ namespace cfp {
 #ifdef CFP_TAIL_TRACE
 __device__ uint64_t g_trace[64];
 __device__ uint64_t g_trace_cta[256];
+__device__ uint64_t g_enum_trace[4096 * 8];     // per CTA of one enum launch: phase marks
+#define ETRACE(i)                                                                              \
+  do {                                                                                         \
+    if (threadIdx.x == 0 && p.ntau > 0 && blockIdx.x < 4096) {                                 \
+      uint64_t t_;                                                                             \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                                   \
+      g_enum_trace[blockIdx.x * 8 + (i)] = t_;                                                 \
+    }                                                                                          \
+  } while (0)
 #define TTRACE(cta, i)                                                                      \
   do {                                                                                     \
     if (threadIdx.x == 0 && blockIdx.x == (cta)) {                                         \
@@ -42,6 +51,7 @@ __device__ uint64_t g_trace_cta[256];
   } while (0)
 #else
 #define TTRACE(cta, i) do { } while (0)
+#define ETRACE(i) do { } while (0)
 #endif
 
 template <typename V> struct VT;
@@ -316,6 +326,7 @@ __global__ void __launch_bounds__(kBlock, 4) enum_kernel(const EnumParams p) {
   constexpr int VN = Vec4<V>::N;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int tid = threadIdx.x;
+  ETRACE(0);
   constexpr int CH = kBlock / MSPLIT;                       // prefixes per CTA (= p.CH)
   const int slot = MSPLIT == 2 ? (tid & (CH - 1)) : tid;    // this thread's prefix slot
   const int half = MSPLIT == 2 ? tid / CH : 0;              // its share of the M values
@@ -382,6 +393,7 @@ __global__ void __launch_bounds__(kBlock, 4) enum_kernel(const EnumParams p) {
   const V* YT = static_cast<const V*>(p.YT);
   const V* ZT = static_cast<const V*>(p.ZT);
   const int4* MT = p.mtab;
+  ETRACE(1);
   if constexpr (STAGED) {
     V* xs = reinterpret_cast<V*>(smem_raw);
     V* ys = xs + p.xspan;
@@ -413,8 +425,10 @@ __global__ void __launch_bounds__(kBlock, 4) enum_kernel(const EnumParams p) {
       for (int64_t e = tid; e < p.nM; e += kBlock) ms[e] = MT[e];
     }
     for (int64_t e = tid; e < p.zspan; e += kBlock) zs[e] = ZT[sz + e];
+    ETRACE(2);
     if (tma && tid == 0) mbar_wait(&sbar, 0);       // the barrier below releases everyone after it
     __syncthreads();
+    ETRACE(3);
     XT = xs; YT = ys; ZT = zs; MT = ms;
     sx = sy = sz = 0;
     if constexpr (MERGED) {
@@ -430,6 +444,7 @@ __global__ void __launch_bounds__(kBlock, 4) enum_kernel(const EnumParams p) {
       YT = ym;
     }
   }
+  ETRACE(4);
   V* Bp = static_cast<V*>(p.Bp) + row * p.Do;
   V acc[NB];
 #pragma unroll
@@ -522,6 +537,7 @@ __global__ void __launch_bounds__(kBlock, 4) enum_kernel(const EnumParams p) {
       Bp[od] = r;
     }
   }
+  ETRACE(5);
   const bool simple = p.o_mode == 0 && p.o_bstride == 1 && p.o_bradix == p.nb;
   const int v_lo = simple ? ybase : 0;
   const int v_cnt = simple ? min(NB, p.nb - ybase) : p.Do;
@@ -702,6 +718,7 @@ __global__ void __launch_bounds__(kBlock, 4) enum_kernel(const EnumParams p) {
       __syncthreads();
     }
   }
+  ETRACE(6);
 }
 
 // --------------------------------------------------------------------------
@@ -1124,7 +1141,7 @@ __device__ void chain_run(const ChainParams& cp, unsigned char* smem_raw, const 
     for (int i = tid; i < N; i += nth) sinst[i] = make_int4(cp.inst[i].mat, cp.inst[i].rows, cp.inst[i].cols, 0);
     if (cp.mode == 1)
       for (int64_t i = tid; i < (cp.mat_elems + 31) / 32; i += nth) ebits[i] = 0;
-    if (tma) mbar_wait(&cbar, 0);
+    if (tma && tid == 0) mbar_wait(&cbar, 0);      // only the initialising thread polls; the barrier below releases the rest
     __syncthreads();
   }
   TTRACE(0, 1);
@@ -2202,7 +2219,9 @@ cudaError_t launch_tail(const TailParams& tp, int grid, size_t smem, cudaStream_
 extern "C" int cfp_debug_trace(uint64_t* out64) {
   int e = (int)cudaMemcpyFromSymbol(out64, g_trace, 64 * sizeof(uint64_t));
   if (e) return e;
-  return (int)cudaMemcpyFromSymbol(out64 + 64, g_trace_cta, 256 * sizeof(uint64_t));
+  e = (int)cudaMemcpyFromSymbol(out64 + 64, g_trace_cta, 256 * sizeof(uint64_t));
+  if (e) return e;
+  return (int)cudaMemcpyFromSymbol(out64 + 320, g_enum_trace, 4096 * 8 * sizeof(uint64_t));
 }
 #endif
 

@@ -54,7 +54,7 @@ __device__ __forceinline__ void lds4(const V* p, V* o) {
 }
 
 template <typename V, bool ARGK>
-__global__ void __launch_bounds__(256) minplus_tiled_kernel(int m, int k, int n, const V* __restrict__ A,
+__global__ void __launch_bounds__(256, sizeof(V) == 4 ? 2 : 1) minplus_tiled_kernel(int m, int k, int n, const V* __restrict__ A,
                                                             const V* __restrict__ B, V* __restrict__ C,
                                                             uint32_t* __restrict__ argk) {
   using O = Ops<V>;

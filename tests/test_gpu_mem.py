@@ -223,3 +223,15 @@ def test_mem_plan_reuse_alternating(ctx, oracle_lib):
                       (variants[2], quantum, limit), (variants[2], quantum, limit + quantum * 7),
                       (variants[0], quantum, limit)]:
         _compare(ctx, O, p, q, lim, "reuse")
+
+
+def test_mem_infeasible_diagnostic_names_least_memory_plan(ctx, oracle_lib):
+    """EINFEASIBLE carries the least-memory plan's memory and quanta."""
+    from golden_util import load, problem_from
+    cfp = _cfp()
+    p = problem_from(load("m4")["problem"])
+    with pytest.raises(cfp.CfpError) as ei:
+        ctx.search_plan_mem(p, 4, 7)            # M4: each of the 2 segments needs >= 1 quantum, Qmax = 1
+    assert ei.value.status == cfp.CFP_EINFEASIBLE
+    msg = str(ei.value)
+    assert "least-memory plan (0,0) (0,0)" in msg and "needs 4 memory units = 2 quanta" in msg and "Qmax = 1" in msg, msg
