@@ -291,7 +291,8 @@ struct TailParams {
 // contiguous run of that order.
 // ---------------------------------------------------------------------------
 constexpr int kMemFoldRows = 64;     // rows staged per fold step
-constexpr int kMemFoldCols = 128;    // columns (classes) per fold CTA
+constexpr int kMemFoldStage = 128;   // fold rows per stage x sizeof(V) (32 u32 rows, 16 u64 rows)
+constexpr int kMemFoldQuads = 48;    // class quads per fold CTA at most (smem, copies per thread)
 constexpr int kMemNPF = 4;           // prefixes per enumeration thread
 
 struct MemPrefixMap {

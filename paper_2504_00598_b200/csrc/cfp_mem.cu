@@ -266,36 +266,59 @@ __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_gr
 template <typename V>
 __global__ void __launch_bounds__(256) mem_fold_kernel(const MemFoldParams p) {
   using M = MT<V>;
-  constexpr int R = sizeof(V) == 4 ? 32 : 16;       // rows per stage (static smem < 48 KB)
-  constexpr int FC = kMemFoldCols;
+  constexpr int R = kMemFoldStage / (int)sizeof(V);   // rows per stage
   constexpr int VPU = 16 / sizeof(V);               // elements per 16-byte copy
-  __shared__ __align__(16) V Xs[2][R][32];
-  __shared__ __align__(16) V Bs[2][R][FC + 4];      // +4: conflict-free row stores
+  extern __shared__ __align__(16) unsigned char fsm[];
   const int fc = p.fc;
+  const int FP = fc + 4;                            // Bs row pitch (+4: conflict-free row stores)
+  V* Xs = reinterpret_cast<V*>(fsm);                // [2][R][32]
+  V* Bs = Xs + 2 * R * 32;                          // [2][R][FP]
   const int4 tile = p.tiles[blockIdx.x];
   const int col0 = blockIdx.y * fc;
   const int ncols = min(fc, p.Wc - col0);
-  const int tid = threadIdx.x;
+  const int tid = threadIdx.x, nth = blockDim.x;
   const int ncq = (ncols + 3) >> 2;                 // class quads of this block
   const int tu = tid / ncq, tc = tid - tu * ncq;    // thread = (u quad, class quad)
   const V* B = static_cast<const V*>(p.B);
   const V* X = static_cast<const V*>(p.X);
   V* out = static_cast<V*>(p.chunk) + (int64_t)blockIdx.x * p.Din * p.Wc;
   const int nchunk = (tile.y + R - 1) / R;
+  // this thread's 16-byte copies of a full stage, (row, column unit) pairs
+  // computed once (the per-stage index math was a quarter of the kernel's
+  // instructions); a short last stage skips rows >= its row count
+  constexpr int MAXB = (kMemFoldStage / 4) * kMemFoldQuads * 2 / 256 + 1;   // >= R x (16-byte units per row) / threads
+  int brow[MAXB], bcol[MAXB];
+  const int nbq = ncq * (4 / VPU);                  // 16-byte units per B row
+  int nbc = 0;
+  const bool pre = R * nbq <= MAXB * nth;          // else (few threads, wide block) index per copy
+#pragma unroll
+  for (int i = 0; i < MAXB; ++i) {                  // fully unrolled: brow / bcol stay in registers
+    const int e = tid + i * nth;
+    brow[i] = pre && e < R * nbq ? e % R : R;       // R = no copy
+    bcol[i] = e / R;
+  }
+  (void)nbc;
   for (int ub = 0; ub < p.Din; ub += 32) {          // input states in blocks of 32
     const int ucnt = min(32, p.DinP - ub);
     const int xu = ucnt / VPU;                      // 16-byte units per X row
     auto issue = [&](int st, int c) {
       const int64_t pos0 = (int64_t)tile.x + (int64_t)c * R;
       const int nr = min(R, tile.y - c * R);
-      for (int e = tid; e < nr * xu; e += blockDim.x) {
+      for (int e = tid; e < nr * xu; e += nth) {
         const int r = e / xu, k = e - r * xu;
-        cp_async16(&Xs[st][r][k * VPU], X + (pos0 + r) * p.DinP + ub + k * VPU);
+        cp_async16(Xs + (st * R + r) * 32 + k * VPU, X + (pos0 + r) * p.DinP + ub + k * VPU);
       }
-      for (int e = tid; e < nr * ncq * (4 / VPU); e += blockDim.x) {   // lanes over positions (coalesced)
+#pragma unroll
+      for (int i = 0; i < MAXB; ++i) {
+        if (brow[i] >= nr) continue;
+        const int cq = bcol[i] / (4 / VPU), h = bcol[i] - cq * (4 / VPU);
+        cp_async16(Bs + (st * R + brow[i]) * FP + cq * 4 + h * VPU,
+                   B + ((int64_t)(col0 / 4 + cq) * p.nP + pos0 + brow[i]) * 4 + h * VPU);
+      }
+      for (int e = tid; !pre && e < nr * nbq; e += nth) {
         const int r = e % nr, q = e / nr;
         const int cq = q / (4 / VPU), h = q - cq * (4 / VPU);
-        cp_async16(&Bs[st][r][cq * 4 + h * VPU], B + ((int64_t)(col0 / 4 + cq) * p.nP + pos0 + r) * 4 + h * VPU);
+        cp_async16(Bs + (st * R + r) * FP + cq * 4 + h * VPU, B + ((int64_t)(col0 / 4 + cq) * p.nP + pos0 + r) * 4 + h * VPU);
       }
       cp_async_commit();
     };
@@ -316,11 +339,13 @@ __global__ void __launch_bounds__(256) mem_fold_kernel(const MemFoldParams p) {
       const int st = c & 1;
       const int nr = min(R, tile.y - c * R);
       if (tu < 8 && tu * 4 < ucnt) {
+        const V* xr = Xs + st * R * 32 + tu * 4;
+        const V* br = Bs + st * R * FP + tc * 4;
 #pragma unroll 4
         for (int r = 0; r < nr; ++r) {
           V x[4], y[4];
-          M::load4(&Xs[st][r][tu * 4], x);
-          M::load4(&Bs[st][r][tc * 4], y);
+          M::load4(xr + r * 32, x);
+          M::load4(br + r * FP, y);
 #pragma unroll
           for (int i = 0; i < 4; ++i)
 #pragma unroll
@@ -826,7 +851,13 @@ cudaError_t launch_mem_fold(const MemFoldParams& p, int64_t ntiles, cudaStream_t
   // when D_in < 32 (C3: 6 x 30 -> 192 instead of 256 with 76 idle)
   const int ntu = std::min(8, (std::min(32, p.DinP) + 3) / 4);
   const int nthr = std::min(256, (ntu * ((p.fc + 3) / 4) + 31) / 32 * 32);
-  mem_fold_kernel<V><<<dim3((unsigned)ntiles, (unsigned)p.ncolblk), nthr, 0, st>>>(p);
+  constexpr int R = kMemFoldStage / (int)sizeof(V);
+  const size_t smem = (size_t)2 * R * 32 * sizeof(V) + (size_t)2 * R * (p.fc + 4) * sizeof(V);
+  if (smem > 48 * 1024) {
+    e = cudaFuncSetAttribute(mem_fold_kernel<V>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+  }
+  mem_fold_kernel<V><<<dim3((unsigned)ntiles, (unsigned)p.ncolblk), nthr, smem, st>>>(p);
   return cudaGetLastError();
 }
 template <typename V>
