@@ -98,7 +98,6 @@ struct cfp_ctx {
   bool plan_cache = true;           // CFP_PLAN_CACHE=0: no structure-keyed reuse in cfp_search_plan
   bool fused_tail = true;           // CFP_FUSED_TAIL=0: separate launches after the enumeration (A/B, tests)
   bool tail_squaring = false;       // CFP_TAIL_SQUARING=1: fused chain by repeated squaring (A/B, tests)
-  bool k0_inline = false;           // CFP_K0_INLINE=1: K0 in the enumeration prologue (measured slower)
   int force_nb = 0;                 // CFP_ENUM_NB: register group size of the enumeration (tuning, tests)
   bool force_o_m = false;           // CFP_ENUM_O_IN_M=1: output block in the M loop (tests)
   int force_p = 0;                  // CFP_ENUM_P: prefix length of the enumeration schedule (tests)
@@ -157,7 +156,6 @@ extern "C" cfp_status cfp_ctx_create(cfp_ctx** out, const cfp_ctx_opts* opts) {
   if (const char* pc = getenv("CFP_PLAN_CACHE")) c->plan_cache = atoi(pc) != 0;
   if (const char* ft = getenv("CFP_FUSED_TAIL")) c->fused_tail = atoi(ft) != 0;
   if (const char* sq = getenv("CFP_TAIL_SQUARING")) c->tail_squaring = atoi(sq) != 0;
-  if (const char* k0 = getenv("CFP_K0_INLINE")) c->k0_inline = atoi(k0) != 0;
   if (const char* nb = getenv("CFP_ENUM_NB")) c->force_nb = atoi(nb);
   if (const char* om = getenv("CFP_ENUM_O_IN_M")) c->force_o_m = atoi(om) != 0;
   if (const char* fp = getenv("CFP_ENUM_P")) c->force_p = atoi(fp);
@@ -1136,17 +1134,8 @@ static cfp_status prepare_impl(cfp_ctx* ctx, const cfp_problem* p, bool do_chain
     specs.push_back(sx); specs.push_back(sy); specs.push_back(sz);
     // thread mapping
     EnumParams& ep = te.ep;
-    // K0 (terms inside the prefix): computed in the enumeration prologue when
-    // the term list is short (every config), else a derived table
-    if (sk.nterm <= 12 && ctx->k0_inline) {
-      ep.nk0 = sk.nterm;
-      for (int q = 0; q < sk.nterm; ++q) ep.k0t[q] = sk.term[q];
-      te.k0_off = -1;
-    } else {
-      ep.nk0 = -1;
-      te.k0_off = place(sk);
-      specs.push_back(sk);
-    }
+    te.k0_off = place(sk);
+    specs.push_back(sk);
     ep.P = Pp;
     for (int i = 0; i < Pp; ++i) ep.pre_radix[i] = r[i];
     int lmin = Pp;
@@ -1413,7 +1402,7 @@ static cfp_status prepare_impl(cfp_ctx* ctx, const cfp_problem* p, bool do_chain
     ep.XT = vals + (base + te.xt_off) * vb;
     ep.YT = vals + (base + te.yt_off) * vb;
     ep.ZT = vals + (base + te.zt_off) * vb;
-    ep.K0 = te.k0_off < 0 ? nullptr : vals + (base + te.k0_off) * vb;
+    ep.K0 = vals + (base + te.k0_off) * vb;
     ep.mtab = P->mtab.as<int4>() + te.mtab_off;
     ep.Bp = (char*)P->bp.p + te.bp_off;
     for (int x : te.trans) {

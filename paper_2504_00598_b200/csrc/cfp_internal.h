@@ -92,11 +92,6 @@ struct EnumParams {
   int64_t xspan, yspan, zspan;  // slice lengths (staged)
   // device pointers (element type = the path's value type)
   const void* XT; const void* YT; const void* ZT; const void* K0;
-  // K0[p] computed by the enumeration thread itself from the compact W/R
-  // tables (nk0 >= 0: terms over prefix positions, offsets into `vals`) --
-  // no K0 table to build in a0; nk0 = -1: read the K0 table
-  int32_t nk0;
-  Term k0t[12];
   const int4* mtab;             // [nM] (x, y, z, v_o)
   void* Bp;                     // [G*W][Do] local canonical prefixes
   // epilogue fold of the cross-segment terms (one chunk = one CTA's prefixes)

@@ -318,7 +318,11 @@ __device__ __forceinline__ void atomic_min_v<uint64_t>(uint64_t* p, uint64_t v) 
 // NA > 0: the A space has exactly NA values (compile time) -- the A loop is
 // fully unrolled with all NA x values loaded at the top of each M step, so no
 // x load latency sits between consecutive VIADDMNMX groups.
-template <typename V, int NB, int ST, int MSPLIT, int NA = 0>
+// FX: the fold epilogue keeps a prefix's cross-term row in registers (only
+// taken at NB != 24); instantiated without it for the output-digit-in-M
+// layout, where the extra registers made ptxas spill into the main loop
+// (C4: 9.82 -> 9.58 ms enumeration)
+template <typename V, int NB, int ST, int MSPLIT, int NA = 0, int FX = 1>
 __global__ void __launch_bounds__(kBlock, 4) enum_kernel(const EnumParams p) {
   constexpr bool STAGED = ST > 0;
   constexpr bool MERGED = ST == 2;
@@ -363,30 +367,6 @@ __global__ void __launch_bounds__(kBlock, 4) enum_kernel(const EnumParams p) {
       sy += dig * p.pre_sy[d];
       sz += dig * p.pre_sz[d];
       if (d == p.o_pre) od = dig;
-    }
-  }
-  // K0[p]: every Eq. 3 term inside the prefix, from the compact W/R tables
-  // (issued before the staging wait below, so its loads overlap the TMA)
-  V k0 = T::CAP;
-  if (live) {
-    if (p.nk0 >= 0) {
-      const V* vals0 = static_cast<const V*>(p.vals);
-      k0 = 0;
-      const bool n32 = pg < 0x7FFFFFFF;
-      for (int t = 0; t < p.nk0; ++t) {
-        const Term tm = p.k0t[t];
-        const int da = n32 ? (int)(((uint32_t)pg / (uint32_t)p.pre_stride[tm.a]) % (uint32_t)p.pre_radix[tm.a])
-                           : (int)((pg / p.pre_stride[tm.a]) % p.pre_radix[tm.a]);
-        int64_t at = tm.off + da;
-        if (tm.kind == 1) {
-          const int db = n32 ? (int)(((uint32_t)pg / (uint32_t)p.pre_stride[tm.b]) % (uint32_t)p.pre_radix[tm.b])
-                             : (int)((pg / p.pre_stride[tm.b]) % p.pre_radix[tm.b]);
-          at = tm.off + (int64_t)da * tm.db + db;
-        }
-        k0 = T::sat(k0, vals0[at]);
-      }
-    } else {
-      k0 = static_cast<const V*>(p.K0)[pg];
     }
   }
   const V* XT = static_cast<const V*>(p.XT);
@@ -453,6 +433,7 @@ __global__ void __launch_bounds__(kBlock, 4) enum_kernel(const EnumParams p) {
   if (live) {
     if (p.init_row)
       for (int v = 0; v < p.Do; ++v) Bp[v] = T::CAP;
+    const V k0 = static_cast<const V*>(p.K0)[pg];
     // MS = 2: warps of half 0 take m in [0, mh), warps of half 1 [mh, nM)
     const int nM = (int)p.nM;                      // host: nM < 2^31 (mtab rows)
     const int mh = MSPLIT == 2 ? (nM + 1) / 2 : nM;
@@ -611,7 +592,7 @@ __global__ void __launch_bounds__(kBlock, 4) enum_kernel(const EnumParams p) {
       // measured (A/B on one B200): the register path costs spills at NB = 24
       // (C3 0.784 -> 0.779 of the ALU roofline) and pays at NB = 23 (C5
       // 0.783 -> 0.791)
-      const bool fastx = NA > 0 && NB != 24 && DinP == DPC && pg < 0x7FFFFFFF;
+      const bool fastx = FX && NA > 0 && NB != 24 && DinP == DPC && pg < 0x7FFFFFFF;
       if (fastx && half == 0 && et.nq > 0) {
         // the whole row in registers: per term its DPC / VN 16-byte loads are
         // issued together (one L1/L2 round trip per term, not one per vector)
@@ -2119,8 +2100,10 @@ cudaError_t launch_enum_nb(const EnumParams& p, int64_t nthreads, size_t smem, c
     return launch(enum_kernel<V, NB, 2, 2>);
   }
   if constexpr (sizeof(V) == 4 && (NB == 23 || NB == 24)) {
-    if (p.staged && p.ymerge && p.na == NB && p.na_pad >= (NB + 3) / 4 * 4 && !p.no_full_a)
+    if (p.staged && p.ymerge && p.na == NB && p.na_pad >= (NB + 3) / 4 * 4 && !p.no_full_a) {
+      if (NB == 23 && p.o_mode == 1) return launch(enum_kernel<V, NB, 2, 1, NB, 0>);
       return launch(enum_kernel<V, NB, 2, 1, NB>);
+    }
   }
   if (p.staged && p.ymerge) return launch(enum_kernel<V, NB, 2, 1>);
   if (p.staged) return launch(enum_kernel<V, NB, 1, 1>);

@@ -693,37 +693,3 @@ def test_marshal_cache_sees_in_place_changes(ctx, oracle_lib):
         for x in tr.in_edges:
             x.table[...] = rng.integers(0, 1 << 20, x.table.shape, dtype=np.uint32)
     _assert_plan(ctx.search_plan(p), oracle_lib.search_plan(p), "C2 after in-place change")
-
-
-@pytest.fixture(scope="module")
-def ctx_k0tab():
-    import os
-    from paper_2504_00598_b200 import build as B
-    B.build()
-    from paper_2504_00598_b200 import cfp
-    old = os.environ.get("CFP_K0_INLINE")
-    os.environ["CFP_K0_INLINE"] = "1"
-    try:
-        c = cfp.Context(device=0)
-    finally:
-        if old is None:
-            del os.environ["CFP_K0_INLINE"]
-        else:
-            os.environ["CFP_K0_INLINE"] = old
-    yield c
-    c.close()
-
-
-@pytest.mark.parametrize("mode", MODES)
-def test_k0_table_path_corpus(ctx_k0tab, oracle_lib, mode):
-    """K0 summed in the enumeration prologue (CFP_K0_INLINE=1) instead of the a0 table."""
-    for seed in range(30):
-        p = G.tiny_random(seed * 13 + 5 + MODES.index(mode), mode=mode, max_plans=None, max_n=6, max_k=5, max_d=5)
-        _search_or_infeasible(ctx_k0tab, oracle_lib, p)
-
-
-@pytest.mark.parametrize("cfg", ["C2", "C3", "C5"])
-def test_k0_inline_equals_table(ctx, ctx_k0tab, cfg):
-    p = G.make_config(cfg, seed=1, dist="random")
-    a, b = ctx.search_plan(p), ctx_k0tab.search_plan(p)
-    assert a.total_ns == b.total_ns and np.array_equal(a.seg_index, b.seg_index)
