@@ -117,6 +117,26 @@ def plan_bytes(prob) -> int:
     return 8 + N * 16 + N * kmax * 4 + 4
 
 
+def ncu_traffic(name, kernel):
+    """DRAM bytes (read + write) of one launch of `kernel` from a committed
+    `ncu --set full` summary (profiles/<name>.json, profiles/summarize_ncu.py);
+    None when absent."""
+    try:
+        with open(os.path.join(ROOT, "profiles", name + ".json")) as fh:
+            ks = json.load(fh)["kernels"]
+    except Exception:
+        return None
+    units = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+    for k, v in ks.items():
+        if kernel in k:
+            tot = 0.0
+            for m in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+                val, unit = v.get(m, ["0", "byte"])
+                tot += float(val) * units.get(unit, 1)
+            return tot
+    return None
+
+
 def perturbed(prob):
     """A copy of `prob` with the same structure (shapes, INF pattern, per-block
     maxima) and different values: every finite compute entry that is not its
@@ -387,12 +407,7 @@ def run_cfp(args, prob, rank, world, local_rank):
     peak = alu_peak_gops(1965.0)
     # N5 microbenchmark (measured ALU lane-op rate of VIADDMNMX.U32 on this GPU)
     ip_ops, ip_ms = ctx.intpipe_bench(0, 4000)
-    traffic = None
-    try:
-        with open(os.path.join(ROOT, "profiles", "r01_ncu_enum_v11.json")) as fh:
-            traffic = json.load(fh)["traffic_bytes_per_launch"]["enum_kernel"]
-    except Exception:
-        pass
+    traffic = ncu_traffic("r02_ncu_enum_v7", "enum_kernel")
     # N2 (min,+) product microbenchmark (S in {256 .. 8192},
     # u32 / u64, with and without the least-k argmin), part of every default
     # run on rank 0 (~2 s); --no-minplus skips it
@@ -443,7 +458,7 @@ def run_cfp(args, prob, rank, world, local_rank):
                                  "peak = 64 lane-ops/clk/SM x 148 SMs x 1965 MHz (derived, DESIGN.md); "
                                  "achieved = combos / device time of the enumeration phase (all enum "
                                  "launches incl. the cross-term fold epilogue); traffic = DRAM bytes per "
-                                 "enum launch from ncu (profiles/r01_ncu_enum_v11.json), algorithmic bytes ~0"},
+                                 "enum launch from ncu (profiles/r02_ncu_enum_v7.json), algorithmic bytes ~0"},
             "intpipe_measured": {"op": "VIADDMNMX.U32", "lane_ops_per_s": ip_ops,
                                  "lane_ops_per_clk_per_sm": ip_ops / (SMS * 1e6 * (clocks["sm_mhz"] or 1965.0)),
                                  "frac_of_derived_peak": ip_ops / (peak * 1e9)},
@@ -551,9 +566,10 @@ def run_cfp_mem(args, rank, world, local_rank):
                 plan_bytes(prob) + 8 * len(prob.instances)},
         "gpu_launches": launches,
         "roofline": {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "Gop/s",
-                     "frac": achieved / peak, "traffic": None,
+                     "frac": achieved / peak, "traffic": ncu_traffic("r02_ncu_memenum_v8", "mem_enum_kernel"),
                      "note": "enumeration kernels: one VIADDMNMX.U32 per strategy combination "
-                             "(K0[p] + T[ctx][sigma] into its (layout, memory) class)"},
+                             "(K0[p] + T[ctx][sigma] into its (layout, memory) class); traffic: DRAM bytes "
+                             "of one layer-type launch (profiles/r02_ncu_memenum_v8.json)"},
         "fold_roofline": {"bound": "alu", "achieved": fold_ops / (f_ms * 1e-3) / 1e9, "peak": peak,
                           "unit": "Gop/s", "frac": fold_ops / (f_ms * 1e-3) / 1e9 / peak,
                           "addmins_per_step": fold_ops},
@@ -643,8 +659,9 @@ def run_cfp_dense(args, rank, world, local_rank):
                 "note": "tables are device-resident inputs (tens of GB); e2e covers the search call"},
         "gpu_launches": launches,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": None,
+                     "frac": achieved / peak, "traffic": ncu_traffic("r02_ncu_dense_v8", "dense_rows"),
                      "note": f"dense_rows_kernel: 4 B read per combination (algorithmic) / stream time; "
+                             f"traffic: DRAM bytes of one layer-type launch (profiles/r02_ncu_dense_v8.json); "
                              f"peak: {peak_src}"},
         "clocks": clocks, "plan_total_ns": plan.total_ns,
     }
@@ -707,12 +724,7 @@ def run_cfp_budget(args, rank, world, local_rank):
     peak, peak_src = hbm_peak_gbs()
     achieved = ns[big] * 4 / (kb * 1e-3) / 1e9
     pruned = sum(r["pruned"] for r in ref.values())
-    traffic = None
-    try:
-        with open(os.path.join(ROOT, "profiles", "r01_ncu_budget.json")) as fh:
-            traffic = json.load(fh)["traffic_bytes_per_launch"]["budget_kernel"]
-    except Exception:
-        pass
+    traffic = ncu_traffic("r02_ncu_budget_v8", "budget_kernel")
     out = {
         "metric": "budgeted profiling tasks screened/sec (dense per-plan tables, NEXT-3)",
         "value": tasks / (ms * 1e-3), "unit": "tasks/s", "n_gpus": 1, "steps": args.steps,
@@ -732,7 +744,7 @@ def run_cfp_budget(args, rank, world, local_rank):
                      "frac": achieved / peak, "traffic": traffic,
                      "note": f"budget_kernel on the largest type ({ns[big]} tasks): 4 B read per task "
                              f"(algorithmic, {ns[big] * 4} B per launch) / device time of the call; "
-                             f"traffic = DRAM bytes of that launch (profiles/r01_ncu_budget.json); "
+                             f"traffic = DRAM bytes of that launch (profiles/r02_ncu_budget_v8.json); "
                              f"peak: {peak_src}"},
         "clocks": clocks,
     }

@@ -9,8 +9,9 @@
 //    pruned  = W[i] finite, best_i finite, W[i] > thr_i  (== W*den > best*num)
 //    spent  += pruned ? thr_i : (W[i] finite ? W[i] : 0)
 //
-// HBM sees each task once: a persistent grid takes 32768-task slices (128 KB)
-// in index order from a ticket counter; pass 1 streams the slice from HBM for
+// HBM sees each task once (up to the pass-2 L2 misses below): a persistent
+// grid takes kBudSlice-task slices (49152 tasks = 192 KB) in index order from
+// a ticket counter; pass 1 streams the slice from HBM for
 // its minimum (published at once), a decoupled look-back over the earlier
 // slices' status words (aggregate published before the look-back, inclusive
 // prefix after it) gives the minimum of everything before the slice, and pass
@@ -79,10 +80,11 @@ __device__ __forceinline__ void budget_load(const BudgetParams& p, uint64_t tbas
 // (16 loads of 16 bytes in flight per thread in pass 1; pass 2 prefetches
 // the next tile):
 // pass 1 streams it from HBM for its minimum (published at once for the
-// look-back of later slices), pass 2 re-reads it -- still L2-resident: the
-// slices in flight total <= grid x 128 KB -- for the per-task decisions.
-// HBM sees each task once; the ticket, look-back and barriers are paid per
-// 128 KB instead of per tile.
+// look-back of later slices), pass 2 re-reads it -- mostly L2-resident: the
+// slices in flight total <= grid x kBudSlice x 4 B (444 CTAs x 192 KB =
+// 85 MB of the 126 MB L2; ncu: 22.3 GB of DRAM reads for an 18.35 GB table,
+// i.e. ~18 % of the pass-2 re-reads miss, profiles/r02_ncu_budget_v8.json).
+// The ticket, look-back and barriers are paid per slice instead of per tile.
 __global__ void __launch_bounds__(kBudThreads, 3) budget_kernel(const BudgetParams p) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   constexpr unsigned FULL = 0xFFFFFFFFu;
