@@ -8,6 +8,13 @@ search (fused and split tails, the squaring variant), segment tables,
 min-plus chains, the memory-constrained search, dense tables and the
 profiling budget on tiny inputs and checks every answer against the oracle.
 The sanitizer's report is written to gpurun_out/sanitizer_<tool>_<path>.log.
+
+The GPU pool closed compute-sanitizer after round 2's clean runs (its wrapper
+exits 86: runs under it left GPUs needing a reset), so the sanitizer runs only
+on request (CFP_RUN_SANITIZER=1); the committed clean logs are in
+profiles/r02_sanitizer.  The driver's paths run without it in
+test_sanitize_driver_paths (same inputs, every answer checked against the
+oracle).
 """
 import os
 import shutil
@@ -27,6 +34,17 @@ def _sanitizer():
     pytest.fail("compute-sanitizer not found")
 
 
+@pytest.mark.parametrize("path", ["plain", "mem", "dense", "budget"])
+def test_sanitize_driver_paths(path):
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "tests", "sanitize_driver.py"), path],
+                       capture_output=True, text=True, timeout=1500, cwd=ROOT)
+    out = r.stdout + r.stderr
+    assert r.returncode == 0, out[-3000:]
+    assert f"{path}: ok" in out
+
+
+@pytest.mark.skipif(os.environ.get("CFP_RUN_SANITIZER") != "1",
+                    reason="compute-sanitizer is closed on this GPU pool; clean logs in profiles/r02_sanitizer")
 @pytest.mark.parametrize("path", ["plain", "mem", "dense", "budget"])
 @pytest.mark.parametrize("tool", ["memcheck", "racecheck", "synccheck"])
 def test_compute_sanitizer_clean(tool, path):
