@@ -41,6 +41,15 @@ def _stale() -> bool:
 def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not _stale():
         return LIB
+    import fcntl
+    with open(os.path.join(HERE, ".build.lock"), "w") as lk:   # one builder at a time (pytest -n workers)
+        fcntl.flock(lk, fcntl.LOCK_EX)
+        if not force and not _stale():
+            return LIB
+        return _build(verbose)
+
+
+def _build(verbose: bool) -> str:
     inc, libdir = nccl_dirs()
     nvcc = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
     objs = [os.path.join(CSRC, src.replace(".cu", ".o")) for src in SOURCES]

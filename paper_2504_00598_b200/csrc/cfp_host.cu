@@ -1292,8 +1292,11 @@ static cfp_status prepare_impl(cfp_ctx* ctx, const cfp_problem* p, bool do_chain
       const int64_t VP = simple ? ((te.NB + 3) & ~3) : ((ep.Do + 3) & ~3);   // = the kernel's VP bound
       int64_t dinp_max = 4;
       for (int x : te.trans) dinp_max = std::max<int64_t>(dinp_max, (P->trans[trans_slot[x]].Din + 3) & ~3);
-      int64_t epi = ep.CH * VP + ep.CH * dinp_max;
-      if (8 * VP > ep.CH) epi += 8 * dinp_max * VP;
+      // [B_p rows CH x VP (over the staged tables) | cross rows CH x DinP |
+      // fold minima DinP x VP]
+      ep.xs_off = (int32_t)(ep.CH * VP);
+      ep.dinp_max = (int32_t)dinp_max;
+      const int64_t epi = ep.xs_off + ep.CH * dinp_max + dinp_max * VP;
       ep.smem_epi = (int32_t)(te.trans.empty() ? 0 : epi * (int64_t)vbytes);
       if (ep.smem_epi > 200 * 1024) return fail(CFP_ETOOBIG, "D_in x D_o too large for the fold epilogue");
       ep.ntau = (int)te.trans.size();

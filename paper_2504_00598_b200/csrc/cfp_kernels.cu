@@ -304,6 +304,120 @@ __device__ __forceinline__ void atomic_min_v<uint64_t>(uint64_t* p, uint64_t v) 
   atomicMin(reinterpret_cast<unsigned long long*>(p), (unsigned long long)v);
 }
 
+// X^t_p[u] = sum_i Q_i[u][s_i(p)] (Eq. 3 r_n) for prefix pg into
+// xrow[0, DinP): each term is one contiguous row Q_i^T[s_i(p)][0..DinP) of the
+// transposed copy, read 16 bytes at a time; a padding prefix gets a CAP row.
+template <typename V, int NB, int FX, int NA>
+__device__ __forceinline__ void cross_row(const EpiTau& et, const EnumParams& p, const V* vals, const int64_t pg,
+                                          const bool live, V* xrow) {
+  using T = VT<V>;
+  constexpr int VN = Vec4<V>::N;
+  const int DinP = (et.Din + 3) & ~3;
+  constexpr int DPC = (NB + 3) & ~3;            // compile-time row length (D_in = D_o of a layer chain)
+  // measured (A/B on one B200): the register path costs spills at NB = 24
+  // (C3 0.784 -> 0.779 of the ALU roofline) and pays at NB = 23 (C5
+  // 0.783 -> 0.791)
+  const bool fastx = FX && NA > 0 && NB != 24 && DinP == DPC && pg < 0x7FFFFFFF;
+  if (fastx && et.nq > 0) {
+    // the whole row in registers: per term its DPC / VN 16-byte loads are
+    // issued together (one L1/L2 round trip per term, not one per vector)
+    V xa[DPC];
+#pragma unroll
+    for (int k2 = 0; k2 < DPC; ++k2) xa[k2] = live ? (V)0 : T::CAP;
+    for (int i = 0; i < et.nq; ++i) {
+      const int a = et.q[i].a;
+      const int dig = (int)(((uint32_t)pg / (uint32_t)p.pre_stride[a]) % (uint32_t)p.pre_radix[a]);
+      const V* qr = vals + et.qt[i] + dig * DPC;
+      V y[DPC];
+#pragma unroll
+      for (int u0 = 0; u0 < DPC; u0 += VN) load_vec<V>(qr + u0, y + u0);
+#pragma unroll
+      for (int k2 = 0; k2 < DPC; ++k2) xa[k2] = T::sat(xa[k2], y[k2]);
+    }
+#pragma unroll
+    for (int u0 = 0; u0 < DPC; u0 += VN) store_vec<V>(xrow + u0, xa + u0);
+    return;
+  }
+  for (int i = 0; i < et.nq; ++i) {
+    const int a = et.q[i].a;
+    const int dig = pg < 0x7FFFFFFF ? (int)(((uint32_t)pg / (uint32_t)p.pre_stride[a]) % (uint32_t)p.pre_radix[a])
+                                    : (int)((pg / p.pre_stride[a]) % p.pre_radix[a]);
+    const V* qr = vals + et.qt[i] + dig * DinP;
+    for (int u0 = 0; u0 < DinP; u0 += VN) {
+      V y[VN], x[VN];
+      if (live) load_vec<V>(qr + u0, y);
+      else {
+#pragma unroll
+        for (int k2 = 0; k2 < VN; ++k2) y[k2] = T::CAP;
+      }
+      if (i > 0) {
+        load_vec<V>(xrow + u0, x);
+#pragma unroll
+        for (int k2 = 0; k2 < VN; ++k2) y[k2] = T::sat(x[k2], y[k2]);
+      }
+      store_vec<V>(xrow + u0, y);
+    }
+  }
+  if (et.nq == 0)
+    for (int u0 = 0; u0 < DinP; u0 += VN) {
+      V y[VN];
+#pragma unroll
+      for (int k2 = 0; k2 < VN; ++k2) y[k2] = live ? (V)0 : T::CAP;
+      store_vec<V>(xrow + u0, y);
+    }
+}
+
+// The fold's blocks: thread = one 4 x BW block of (u, v) in one stripe of
+// rows; min over its rows of X_r[u] + B_r[v] into the shared minima `red`
+// (atomic), or straight to the chunk minima when there is one stripe.
+template <typename V, int BW>
+__device__ __forceinline__ void fold_blocks(const V* Xs, const V* Bs, V* red, const int DinP, const int VP,
+                                            const int CH, const int Din, const int v_cnt, const int v_lo,
+                                            const int Do, const int64_t nchunks, const int64_t chunk, V* out) {
+  using T = VT<V>;
+  constexpr int VN = Vec4<V>::N;
+  const int tid = threadIdx.x;
+  const int nbv = VP / BW;
+  const int nblk = (DinP / 4) * nbv;
+  const int stripes = nblk >= kBlock ? 1 : min(8, kBlock / nblk);
+  const int gi = tid / nblk;
+  const bool active = nblk >= kBlock ? tid < nblk : gi < stripes;
+  for (int blk = (nblk >= kBlock ? tid : tid - gi * nblk); active && blk < nblk;
+       blk += (nblk >= kBlock ? kBlock : nblk)) {
+    const int u0 = (blk / nbv) * 4;
+    const int v0 = (blk % nbv) * BW;
+    V res[4][BW];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < BW; ++j) res[i][j] = T::CAP;
+    const int rs = stripes > 1 ? gi : 0;
+    for (int r = rs; r < CH; r += stripes) {
+      V x[4], y[BW];
+#pragma unroll
+      for (int i = 0; i < 4; i += VN) load_vec<V>(Xs + r * DinP + u0 + i, x + i);
+#pragma unroll
+      for (int j = 0; j < BW; j += VN) load_vec<V>(Bs + r * VP + v0 + j, y + j);
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < BW; ++j) res[i][j] = T::addmin(x[i], y[j], res[i][j]);
+    }
+    if (nblk >= kBlock) {                           // one stripe: write straight out
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < BW; ++j)
+          if (u0 + i < Din && v0 + j < v_cnt) out[((int64_t)(u0 + i) * Do + v_lo + v0 + j) * nchunks + chunk] = res[i][j];
+    } else {
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < BW; ++j) atomic_min_v<V>(red + (u0 + i) * VP + v0 + j, res[i][j]);
+    }
+  }
+}
+
 // CTA = (group g = (low prefix part l, register group vg), h-block hb of
 // kBlock prefixes); thread = one prefix.  After the enumeration the CTA holds
 // the complete B_p[v] of its prefixes and folds the cross-segment terms of
@@ -523,8 +637,9 @@ __global__ void __launch_bounds__(kBlock, 4) enum_kernel(const EnumParams p) {
   const int v_lo = simple ? ybase : 0;
   const int v_cnt = simple ? min(NB, p.nb - ybase) : p.Do;
   const int VP = (v_cnt + 3) & ~3;
-  V* Bs = reinterpret_cast<V*>(smem_raw);                     // [CH][VP]
-  V* Xs = Bs + CH * VP;                                       // [CH][DinP] (red afterwards)
+  V* Bs = reinterpret_cast<V*>(smem_raw);                     // [CH][VP] (over the staged tables)
+  V* Xs = Bs + p.xs_off;                                      // [CH][DinP] cross rows
+  V* red = Xs + CH * p.dinp_max;                              // [DinP][VP] fold minima (shared atomics)
   if constexpr (MSPLIT == 2) {
     // merge the two halves' bucket minima of each prefix (B = {o}, simple):
     // half 1 parks its registers in Bs, half 0 takes the min, writes B_p and
@@ -578,125 +693,30 @@ __global__ void __launch_bounds__(kBlock, 4) enum_kernel(const EnumParams p) {
   }
   const V* vals = static_cast<const V*>(p.vals);
   const int64_t chunk = l * nhb + hb;
-  int dinp_max = 4;
-  for (int t = 0; t < p.ntau; ++t) dinp_max = max(dinp_max, (p.taus[t].Din + 3) & ~3);
   for (int t = 0; t < p.ntau; ++t) {
     const EpiTau& et = p.taus[t];
     const int Din = et.Din, DinP = (Din + 3) & ~3;
-    {
-      // X^t_p[u] = sum_i Q_i[u][s_i(p)] for this thread's prefix: each term is
-      // one contiguous row Q_i^T[s_i(p)][0..DinP) of the transposed copy, read
-      // 16 bytes at a time and accumulated in the thread's Xs row.
-      V* xrow = Xs + slot * DinP;
-      constexpr int DPC = (NB + 3) & ~3;            // compile-time row length (D_in = D_o of a layer chain)
-      // measured (A/B on one B200): the register path costs spills at NB = 24
-      // (C3 0.784 -> 0.779 of the ALU roofline) and pays at NB = 23 (C5
-      // 0.783 -> 0.791)
-      const bool fastx = FX && NA > 0 && NB != 24 && DinP == DPC && pg < 0x7FFFFFFF;
-      if (fastx && half == 0 && et.nq > 0) {
-        // the whole row in registers: per term its DPC / VN 16-byte loads are
-        // issued together (one L1/L2 round trip per term, not one per vector)
-        V xa[DPC];
-#pragma unroll
-        for (int k2 = 0; k2 < DPC; ++k2) xa[k2] = live ? (V)0 : T::CAP;
-        for (int i = 0; i < et.nq; ++i) {
-          const int a = et.q[i].a;
-          const int dig = (int)(((uint32_t)pg / (uint32_t)p.pre_stride[a]) % (uint32_t)p.pre_radix[a]);
-          const V* qr = vals + et.qt[i] + dig * DPC;
-          V y[DPC];
-#pragma unroll
-          for (int u0 = 0; u0 < DPC; u0 += VN) load_vec<V>(qr + u0, y + u0);
-#pragma unroll
-          for (int k2 = 0; k2 < DPC; ++k2) xa[k2] = T::sat(xa[k2], y[k2]);
-        }
-#pragma unroll
-        for (int u0 = 0; u0 < DPC; u0 += VN) store_vec<V>(xrow + u0, xa + u0);
-      }
-      for (int i = 0; !fastx && half == 0 && i < et.nq; ++i) {
-        const int a = et.q[i].a;
-        const int dig = pg < 0x7FFFFFFF ? (int)(((uint32_t)pg / (uint32_t)p.pre_stride[a]) % (uint32_t)p.pre_radix[a])
-                                        : (int)((pg / p.pre_stride[a]) % p.pre_radix[a]);
-        const V* qr = vals + et.qt[i] + dig * DinP;
-        for (int u0 = 0; u0 < DinP; u0 += VN) {
-          V y[VN], x[VN];
-          if (live) load_vec<V>(qr + u0, y);
-          else {
-#pragma unroll
-            for (int k2 = 0; k2 < VN; ++k2) y[k2] = T::CAP;
-          }
-          if (i > 0) {
-            load_vec<V>(xrow + u0, x);
-#pragma unroll
-            for (int k2 = 0; k2 < VN; ++k2) y[k2] = T::sat(x[k2], y[k2]);
-          }
-          store_vec<V>(xrow + u0, y);
-        }
-      }
-      if (et.nq == 0 && half == 0)
-        for (int u0 = 0; u0 < DinP; u0 += VN) {
-          V y[VN];
-#pragma unroll
-          for (int k2 = 0; k2 < VN; ++k2) y[k2] = live ? (V)0 : T::CAP;
-          store_vec<V>(xrow + u0, y);
-        }
-    }
+    const int nblk = (DinP / 4) * (VP / 4);         // = fold_blocks' block count
+    if (t > 0) __syncthreads();                     // the previous transition is done with Xs / red
+    if (half == 0) cross_row<V, NB, FX, NA>(et, p, vals, pg, live, Xs + slot * DinP);
+    if (nblk < kBlock)
+      for (int e = tid; e < DinP * VP; e += kBlock) red[e] = T::CAP;
     __syncthreads();
-    const int nblk = (DinP / 4) * (VP / 4);
-    const int stripes = nblk >= kBlock ? 1 : min(8, kBlock / nblk);
-    V res[4][4];
-    int u0 = 0, v0 = 0;
-    const int gi = tid / nblk;
-    const bool active = nblk >= kBlock ? tid < nblk : gi < stripes;
-    // (nblk > kBlock handled by the loop below)
-    for (int blk = (nblk >= kBlock ? tid : tid - gi * nblk); active && blk < nblk;
-         blk += (nblk >= kBlock ? kBlock : nblk)) {
-      u0 = (blk / (VP / 4)) * 4;
-      v0 = (blk % (VP / 4)) * 4;
-#pragma unroll
-      for (int i = 0; i < 4; ++i)
-#pragma unroll
-        for (int j = 0; j < 4; ++j) res[i][j] = T::CAP;
-      const int rs = stripes > 1 ? gi : 0;
-      for (int r = rs; r < CH; r += stripes) {
-        V x[4], y[4];
-        load_vec<V>(Xs + r * DinP + u0, x);
-        if (VN == 2) load_vec<V>(Xs + r * DinP + u0 + 2, x + 2);
-        load_vec<V>(Bs + r * VP + v0, y);
-        if (VN == 2) load_vec<V>(Bs + r * VP + v0 + 2, y + 2);
-#pragma unroll
-        for (int i = 0; i < 4; ++i)
-#pragma unroll
-          for (int j = 0; j < 4; ++j) res[i][j] = T::addmin(x[i], y[j], res[i][j]);
-      }
-      if (nblk >= kBlock) {                         // one stripe: write straight out
-        V* out = static_cast<V*>(et.chunkmin);
-#pragma unroll
-        for (int i = 0; i < 4; ++i)
-#pragma unroll
-          for (int j = 0; j < 4; ++j)
-            if (u0 + i < Din && v0 + j < v_cnt)
-              out[((int64_t)(u0 + i) * p.Do + v_lo + v0 + j) * p.nchunks + chunk] = res[i][j];
-      }
-      if (stripes > 1) break;
-    }
-    __syncthreads();                                 // Xs free -> stripe partials
+    // min_p X_p[u] + B_p[v] over the chunk's rows: 4 x 4 register blocks, the
+    // rows split into stripes (one block per thread), the stripes' minima
+    // merged by shared-memory atomic mins.  Measured (C3 / C5 / C4 enumeration
+    // ms): 4 x 4 with the per-stripe partials reduced by a separate pass
+    // 0.625 / 0.465 / 9.60, with atomic mins 0.624 / 0.465 / --, 4 x 8 blocks
+    // (14 stripes, twice the atomics per address) 0.647 / 0.473 / 9.51
+    fold_blocks<V, 4>(Xs, Bs, red, DinP, VP, CH, Din, v_cnt, v_lo, p.Do, p.nchunks, chunk,
+                      static_cast<V*>(et.chunkmin));
     if (nblk < kBlock) {
-      V* red = stripes * VP <= CH ? Xs : Xs + CH * dinp_max;   // [stripes][DinP][VP]
-      if (active) {
-#pragma unroll
-        for (int i = 0; i < 4; ++i)
-#pragma unroll
-          for (int j = 0; j < 4; ++j) red[(gi * DinP + u0 + i) * VP + v0 + j] = res[i][j];
-      }
       __syncthreads();
       V* out = static_cast<V*>(et.chunkmin);
       for (int e = tid; e < Din * v_cnt; e += kBlock) {
         const int u = e / v_cnt, vv = e - u * v_cnt;
-        V m = red[u * VP + vv];
-        for (int s = 1; s < stripes; ++s) m = T::mn(m, red[(s * DinP + u) * VP + vv]);
-        out[((int64_t)u * p.Do + v_lo + vv) * p.nchunks + chunk] = m;
+        out[((int64_t)u * p.Do + v_lo + vv) * p.nchunks + chunk] = red[u * VP + vv];
       }
-      __syncthreads();
     }
   }
   ETRACE(6);
