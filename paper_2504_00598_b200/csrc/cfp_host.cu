@@ -1927,11 +1927,15 @@ extern "C" cfp_status cfp_search_plan(cfp_ctx* ctx, const cfp_problem* p, cfp_pl
   NvtxRange nv("cfp_search_plan");
   std::vector<int64_t> key;
   HostModel model;
+  static const bool dbg = getenv("CFP_DEBUG_E2E") != nullptr;
+  PrepTimer tm;
   TRY(build_model(ctx, p, true, model));
+  if (dbg) tm.mark("build_model");
   if (ctx->plan_cache) {
     // the same structure as the last call: reuse its prepared plan (schedule,
     // device buffers, chain setup) and upload only this call's values
     key = plan_key(p, model.T, model.X, model.inst, model.b);
+    if (dbg) tm.mark("plan_key");
     if (ctx->cached && key == ctx->cached_key) {
       TRY(check_chain_overflow(model.T, model.X, model.inst));
       CUDA_TRY(cudaSetDevice(ctx->device));
@@ -1941,8 +1945,12 @@ extern "C" cfp_status cfp_search_plan(cfp_ctx* ctx, const cfp_problem* p, cfp_pl
       TRY(ctx_pinned(ctx, nb));
       memcpy(ctx->pinned, model.b.raw.data(), nb);
       CUDA_TRY(cudaMemcpyAsync(P->raw.p, ctx->pinned, nb, cudaMemcpyHostToDevice, ctx->stream));
+      if (dbg) tm.mark("h2d_submit");
       TRY(execute_impl(ctx, P));
-      return fetch_impl(ctx, P, out);
+      if (dbg) tm.mark("execute_submit");
+      cfp_status st = fetch_impl(ctx, P, out);
+      if (dbg) tm.mark("fetch");
+      return st;
     }
   }
   // structure changed: release the previous plan's device buffers first, so a
