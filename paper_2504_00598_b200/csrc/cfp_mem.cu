@@ -23,6 +23,7 @@
 
 #include <algorithm>
 #include <cstdint>
+#include <cstdlib>
 
 #include "cfp_internal.h"
 
@@ -362,6 +363,113 @@ __global__ void __launch_bounds__(256) mem_fold_kernel(const MemFoldParams p) {
         if (tu < 8 && u < p.Din && cl < col0 + ncols && tu * 4 + i < ucnt) out[(int64_t)u * p.Wc + cl] = res[i][j];
       }
   }
+}
+
+// --------------------------------------------------------------------------
+// Fold of one transition, 32-bit path.  CTA = (tile of <= kMemFoldTile
+// positions, block of fc classes); thread = U input states x 4 classes:
+// per row U/4 X loads (warp broadcasts: a warp spans <= 2 state groups) and
+// one 16-byte B load feed 4U fused add+mins (C3: U = 12, 48 per 4 loads --
+// the 4 x 4 kernel above needs 2 loads per 16).  Rows arrive by cp.async in
+// a 3-stage shared-memory ring.
+// --------------------------------------------------------------------------
+constexpr int kFoldUR = 16;      // rows per stage (3 x 16 rows of C3: 56 KB, 4 CTAs per SM)
+constexpr int kFoldUS = 3;       // stages (2: C3 0.622 ms, C5 1.321 ms; 3: 0.630, 1.144)
+template <int U>
+__global__ void __launch_bounds__(256) mem_fold_u_kernel(const MemFoldParams p) {
+  using M = MT<uint32_t>;
+  constexpr int R = kFoldUR, NS = kFoldUS;
+  extern __shared__ __align__(16) unsigned char fsm[];
+  const int fc = p.fc, FP = fc + 4, XP = p.DinP;
+  uint32_t* Xs = reinterpret_cast<uint32_t*>(fsm);  // [NS][R][XP]
+  uint32_t* Bs = Xs + NS * R * XP;                  // [NS][R][FP]
+  const int4 tile = p.tiles[blockIdx.x];
+  const int col0 = blockIdx.y * fc;
+  const int ncols = min(fc, p.Wc - col0);
+  const int tid = threadIdx.x, nth = blockDim.x;
+  const int ncq = (ncols + 3) >> 2;
+  const int ngu = (p.DinP + U - 1) / U;
+  const int tg = tid / ncq, tc = tid - tg * ncq;    // thread = (state group, class quad)
+  const bool act = tg < ngu;
+  const uint32_t* B = static_cast<const uint32_t*>(p.B);
+  const uint32_t* X = static_cast<const uint32_t*>(p.X);
+  const int nchunk = (tile.y + R - 1) / R;
+  const int xu = XP / 4;
+  // this thread's X copies of a stage, (row, 16-byte unit) fixed over the
+  // stages (index math once, not per copy); B copies are (quad, row) =
+  // (e / R, e % R) with R a power of two
+  constexpr int MAXX = 2;
+  int xr_[MAXX], xk_[MAXX];
+#pragma unroll
+  for (int i = 0; i < MAXX; ++i) {
+    const int e = tid + i * nth;
+    xr_[i] = e < R * xu ? e / xu : R;               // R = no copy
+    xk_[i] = e - (e / xu) * xu;
+  }
+  const bool xfew = R * xu <= MAXX * nth;
+  const int64_t bq_stride = (int64_t)p.nP * 4;
+  const uint32_t* Bc = B + (int64_t)(col0 / 4) * bq_stride;
+  auto issue = [&](int st, int c) {
+    if (c < nchunk) {
+      const int64_t pos0 = (int64_t)tile.x + (int64_t)c * R;
+      const int nr = min(R, tile.y - c * R);
+      if (xfew) {
+#pragma unroll
+        for (int i = 0; i < MAXX; ++i)
+          if (xr_[i] < nr) cp_async16(Xs + (st * R + xr_[i]) * XP + xk_[i] * 4, X + (pos0 + xr_[i]) * XP + xk_[i] * 4);
+      } else {
+        for (int e = tid; e < nr * xu; e += nth) {
+          const int r = e / xu, k = e - r * xu;
+          cp_async16(Xs + (st * R + r) * XP + k * 4, X + (pos0 + r) * XP + k * 4);
+        }
+      }
+      const uint32_t* Bp0 = Bc + pos0 * 4;
+      for (int e = tid; e < R * ncq; e += nth) {
+        const int q = e / R, r = e % R;             // consecutive threads: consecutive positions
+        if (r < nr) cp_async16(Bs + (st * R + r) * FP + q * 4, Bp0 + q * bq_stride + r * 4);
+      }
+    }
+    cp_async_commit();                              // (an empty group past the last chunk)
+  };
+  uint32_t res[U][4];
+#pragma unroll
+  for (int i = 0; i < U; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) res[i][j] = M::CAP;
+#pragma unroll
+  for (int s = 0; s < NS - 1; ++s) issue(s, s);
+  for (int c = 0; c < nchunk; ++c) {
+    issue((c + NS - 1) % NS, c + NS - 1);
+    cp_async_wait<NS - 1>();
+    __syncthreads();
+    const int st = c % NS;
+    const int nr = min(R, tile.y - c * R);
+    if (act) {
+      const uint32_t* xr = Xs + st * R * XP + tg * U;
+      const uint32_t* br = Bs + st * R * FP + tc * 4;
+#pragma unroll 2
+      for (int r = 0; r < nr; ++r) {
+        uint32_t x[U], y[4];
+#pragma unroll
+        for (int i = 0; i < U; i += 4) M::load4(xr + r * XP + i, x + i);
+        M::load4(br + r * FP, y);
+#pragma unroll
+        for (int i = 0; i < U; ++i)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) res[i][j] = M::addmin(x[i], y[j], res[i][j]);
+      }
+    }
+    __syncthreads();                                 // stage st is refilled by a later issue
+  }
+  if (!act) return;
+  uint32_t* out = static_cast<uint32_t*>(p.chunk) + (int64_t)blockIdx.x * p.Din * p.Wc;
+#pragma unroll
+  for (int i = 0; i < U; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int u = tg * U + i, cl = col0 + tc * 4 + j;
+      if (u < p.Din && cl < col0 + ncols) out[(int64_t)u * p.Wc + cl] = res[i][j];
+    }
 }
 
 // --------------------------------------------------------------------------
@@ -847,6 +955,31 @@ cudaError_t launch_mem_fold(const MemFoldParams& p, int64_t ntiles, cudaStream_t
   mem_xrows_kernel<V><<<(unsigned)std::min<int64_t>(148 * 16, (xthreads + 255) / 256), 256, 0, st>>>(p);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
+  if (sizeof(V) == 4 && !getenv("CFP_MEM_FOLD4") && p.DinP <= 48) {
+    // U states x 4 classes per thread (U = 12 / 8 / 4 dividing D_in padded);
+    // column blocks so that (state groups) x (class quads) <= 256 threads
+    const int U = p.DinP % 12 == 0 ? 12 : p.DinP % 8 == 0 ? 8 : 4;
+    const int ngu = p.DinP / U;
+    // <= 64 KB of stages per CTA
+    const int fcmax = (int)(64 * 1024 / (kFoldUS * kFoldUR * sizeof(uint32_t))) - p.DinP - 4;
+    const int ncq = (p.Wc + 3) / 4, qmax = std::max(1, std::min(256 / ngu, fcmax / 4));
+    // (a column-block / CTAs-per-SM choice for whole waves was measured
+    // slower on both C3 and C5 and dropped)
+    MemFoldParams q = p;
+    q.ncolblk = (ncq + qmax - 1) / qmax;
+    q.fc = ((ncq + q.ncolblk - 1) / q.ncolblk) * 4;
+    const int nthr = (ngu * (q.fc / 4) + 31) / 32 * 32;
+    const size_t smem = (size_t)kFoldUS * kFoldUR * (p.DinP + q.fc + 4) * sizeof(uint32_t);
+    auto go = [&](auto kern) -> cudaError_t {
+      cudaError_t e2 = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (e2 != cudaSuccess) return e2;
+      kern<<<dim3((unsigned)ntiles, (unsigned)q.ncolblk), nthr, smem, st>>>(q);
+      return cudaGetLastError();
+    };
+    if (U == 12) return go(mem_fold_u_kernel<12>);
+    if (U == 8) return go(mem_fold_u_kernel<8>);
+    return go(mem_fold_u_kernel<4>);
+  }
   // threads = (u quads of one 32-state block) x (class quads): no idle threads
   // when D_in < 32 (C3: 6 x 30 -> 192 instead of 256 with 76 idle)
   const int ntu = std::min(8, (std::min(32, p.DinP) + 3) / 4);
