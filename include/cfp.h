@@ -380,8 +380,10 @@ cfp_status cfp_unpack_keys(int64_t n, const uint64_t* keys, int32_t idx_bits,
                            uint64_t* cost, uint64_t* idx);
 
 /* ---- N5 integer-pipe microbenchmark (roofline denominator) --------------
- * op 0: VIADDMNMX.U32 (fused add+min), op 1: IADD3, op 2: 64-bit add+min.
- * Reports lane-ops/s and the elapsed ms of one launch. */
+ * op 0: VIADDMNMX.U32 (fused add+min), op 1: IADD3, op 2: 64-bit add+min,
+ * op 3: the enumeration's two-pipe group (VIADDMNMX + two FMA-pipe IMAD adds
+ * + VIMNMX3: three add+mins in four instructions over the ALU and FMA pipes).
+ * Reports lane-ops/s (op 3: add+mins/s) and the elapsed ms of one launch. */
 cfp_status cfp_intpipe_bench(cfp_ctx* ctx, int32_t op, int32_t iters, double* ops_per_s,
                              double* ms);
 

@@ -106,6 +106,8 @@ struct cfp_ctx {
   std::vector<int64_t> cached_key;  //   and its structural key (plan_key)
   bool mem_chain_fused = true;      // CFP_MEM_CHAIN_FUSED=0: one launch per DP step (A/B tests)
   bool dedup = true;                // CFP_DEDUP=0: fold identical transitions separately (A/B tests)
+  int enum_mix = 3;                 // CFP_ENUM_MIX: full-A loop (B = {o}) on two pipes in groups of 3 or 4
+                                    // A values; 0 = ALU pipe only (A/B, tests)
   bool no_full_a = false;           // CFP_ENUM_FULL_A=0: runtime-length A loop only (A/B tests)
   int64_t msplit_min_m = 128;       // M split when nM >= this (CFP_ENUM_MSPLIT_MIN_M; tests force 2)
   // side streams for concurrent per-type enumerations (fork/join by events):
@@ -151,6 +153,7 @@ extern "C" cfp_status cfp_ctx_create(cfp_ctx** out, const cfp_ctx_opts* opts) {
                                std::to_string(prop.major) + std::to_string(prop.minor));
   c->sms = prop.multiProcessorCount;
   if (const char* fa = getenv("CFP_ENUM_FULL_A")) c->no_full_a = atoi(fa) == 0;
+  if (const char* mx = getenv("CFP_ENUM_MIX")) c->enum_mix = atoi(mx) == 4 ? 4 : atoi(mx) == 0 ? 0 : 3;
   if (const char* dd = getenv("CFP_DEDUP")) c->dedup = atoi(dd) != 0;
   if (const char* mf = getenv("CFP_MEM_CHAIN_FUSED")) c->mem_chain_fused = atoi(mf) != 0;
   if (const char* pc = getenv("CFP_PLAN_CACHE")) c->plan_cache = atoi(pc) != 0;
@@ -1227,6 +1230,9 @@ static cfp_status prepare_impl(cfp_ctx* ctx, const cfp_problem* p, bool do_chain
     ep.MS = (!ep.init_row && ep.o_mode == 0 && nM >= ctx->msplit_min_m && ep.staged && ep.ymerge) ? 2 : 1;
     ep.CH = kBlock / ep.MS;
     ep.no_full_a = ctx->no_full_a ? 1 : 0;
+    ep.one = 1;
+    ep.mix = 0;
+    if (ctx->enum_mix && ep.o_mode == 0) ep.mix = (int32_t)ctx->enum_mix;
     ep.Gpad = (ep.G + ep.CH - 1) / ep.CH * ep.CH;
     te.smem = ep.staged ? smem : 0;
     te.nthreads = ep.Gpad * ep.W * ep.VG * ep.MS;
@@ -2379,7 +2385,7 @@ extern "C" cfp_status cfp_minplus_bench(cfp_ctx* ctx, int32_t S, int32_t wide, i
 }
 
 extern "C" cfp_status cfp_intpipe_bench(cfp_ctx* ctx, int32_t op, int32_t iters, double* ops_per_s, double* ms) {
-  if (!ctx || op < 0 || op > 2 || iters < 1) return fail(CFP_EINVAL, "bad intpipe arguments");
+  if (!ctx || op < 0 || op > 3 || iters < 1) return fail(CFP_EINVAL, "bad intpipe arguments");
   g_alloc_stream = ctx->stream;
   CUDA_TRY(cudaSetDevice(ctx->device));
   cudaStream_t st = ctx->stream;
@@ -2398,7 +2404,8 @@ extern "C" cfp_status cfp_intpipe_bench(cfp_ctx* ctx, int32_t op, int32_t iters,
   CUDA_TRY(cudaEventElapsedTime(&t, e0, e1));
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
-  const double ops = (double)blocks * 1024 * iters * 64;
+  // op 3: 2 * blocks CTAs x 256 threads x 576 add+mins per step
+  const double ops = op == 3 ? (double)blocks * 2 * 256 * iters * 576 : (double)blocks * 1024 * iters * 64;
   if (ops_per_s) *ops_per_s = ops / (t * 1e-3);
   if (ms) *ms = t;
   return CFP_OK;

@@ -101,6 +101,8 @@ struct EnumParams {
   const void* vals;             // value blob (compact Q tables)
   int64_t nchunks;              // W * (Gpad / CH)
   int32_t smem_epi;             // bytes of the epilogue region
+  int32_t one;                  // 1 (the FMA-pipe adds' multiplier, opaque to the compiler)
+  int32_t mix;                  // 1: full-A loop on two pipes (ALU + FMA), 0: VIADDMNMX only
   int32_t xs_off;               // elements from the region start to the cross rows Xs
   int32_t dinp_max;             // largest padded D_in of the incoming transitions
 };

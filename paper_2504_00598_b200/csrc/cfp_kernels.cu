@@ -78,6 +78,14 @@ template <> struct VT<uint64_t> {
   static __device__ __forceinline__ uint64_t mn(uint64_t a, uint64_t b) { return a < b ? a : b; }
 };
 
+// x * one + y as an IMAD on the FMA pipe (one = 1 at run time, so ptxas can
+// neither fold it to an ALU IADD3 nor to a VIADDMNMX)
+__device__ __forceinline__ uint32_t mad_fma(uint32_t x, uint32_t one, uint32_t y) {
+  uint32_t r;
+  asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(r) : "r"(x), "r"(one), "r"(y));
+  return r;
+}
+
 // --------------------------------------------------------------------------
 // TMA 1-D bulk copies (cp.async.bulk, SASS UBLKCP) with mbarrier completion.
 // --------------------------------------------------------------------------
@@ -436,7 +444,7 @@ __device__ __forceinline__ void fold_blocks(const V* Xs, const V* Bs, V* red, co
 // taken at NB != 24); instantiated without it for the output-digit-in-M
 // layout, where the extra registers made ptxas spill into the main loop
 // (C4: 9.82 -> 9.58 ms enumeration)
-template <typename V, int NB, int ST, int MSPLIT, int NA = 0, int FX = 1>
+template <typename V, int NB, int ST, int MSPLIT, int NA = 0, int FX = 1, int MX = 0>
 __global__ void __launch_bounds__(kBlock, 4) enum_kernel(const EnumParams p) {
   constexpr bool STAGED = ST > 0;
   constexpr bool MERGED = ST == 2;
@@ -540,6 +548,7 @@ __global__ void __launch_bounds__(kBlock, 4) enum_kernel(const EnumParams p) {
   }
   ETRACE(4);
   V* Bp = static_cast<V*>(p.Bp) + row * p.Do;
+  const uint32_t one = (uint32_t)p.one;            // 1, opaque to the compiler (keeps IMAD an FMA-pipe add)
   V acc[NB];
 #pragma unroll
   for (int j = 0; j < NB; ++j) acc[j] = T::CAP;
@@ -574,10 +583,38 @@ __global__ void __launch_bounds__(kBlock, 4) enum_kernel(const EnumParams p) {
         V x[NAV];
 #pragma unroll
         for (int a = 0; a < NAV; a += VN) load_vec<V>(xr + a, x + a);
+        if constexpr (MX && sizeof(V) == 4) {
+          // two pipes: of every three A values, one combination is a
+          // VIADDMNMX (ALU pipe) and two are adds on the FMA pipe (IMAD with a
+          // runtime 1) folded in by one three-way min (VIMNMX3, ALU pipe):
+          // 4 instructions, 2 per pipe, per 3 combinations instead of 3 ALU
+          // instructions (exact: every sum <= 2 CAP < 2^32)
+          // MX = A values per group: MX - 2 VIADDMNMX + one FMA-pipe pair
 #pragma unroll
-        for (int a = 0; a < NA; ++a)
+          for (int j0 = 0; j0 < NB; j0 += 4)
 #pragma unroll
-          for (int j = 0; j < NB; ++j) acc[j] = T::addmin(x[a], y[j], acc[j]);
+            for (int a = 0; a < NA; a += MX)
+#pragma unroll
+              for (int q = 0; q < 4; ++q) {
+                const int j = j0 + q;
+                if (j < NB) {
+                  V t = acc[j];
+#pragma unroll
+                  for (int b = 0; b < MX - 2; ++b)
+                    if (a + b < NA) t = T::addmin(x[a + b], y[j], t);
+                  if (a + MX - 1 < NA)
+                    t = __vimin3_u32(t, mad_fma(x[a + MX - 2], one, y[j]), mad_fma(x[a + MX - 1], one, y[j]));
+                  else if (a + MX - 2 < NA)
+                    t = T::addmin(x[a + MX - 2], y[j], t);
+                  acc[j] = t;
+                }
+              }
+        } else {
+#pragma unroll
+          for (int a = 0; a < NA; ++a)
+#pragma unroll
+            for (int j = 0; j < NB; ++j) acc[j] = T::addmin(x[a], y[j], acc[j]);
+        }
       }
       const int na_v = NA > 0 ? 0 : p.na & ~(VN - 1);
 #pragma unroll 2
@@ -2066,6 +2103,45 @@ __global__ void __launch_bounds__(1024) intpipe_kernel(uint32_t* out, int iters,
   if (s == 0x12345678u) out[threadIdx.x] = s;
 }
 
+// N5 op 3: the enumeration's full-A step on two pipes, as in enum_kernel
+// (24 accumulators, the step's 24 x values in registers, y rows streamed from
+// shared memory 4 at a time; per 3 combinations one VIADDMNMX, two FMA-pipe
+// IMAD adds and one VIMNMX3), 4 CTAs x 256 threads per SM.  576 add+mins per
+// step.
+__global__ void __launch_bounds__(256, 4) intpipe_mix_kernel(uint32_t* out, int iters, uint32_t one) {
+  __shared__ __align__(16) uint32_t xs[64 * 24];
+  __shared__ __align__(16) uint32_t ys[64 * 24];
+  for (int i = threadIdx.x; i < 64 * 24; i += 256) {
+    xs[i] = (i * 2654435761u) & 0x3FFFFFFFu;
+    ys[i] = (i * 40503u + 17u) & 0x3FFFFFFFu;
+  }
+  __syncthreads();
+  uint32_t acc[24];
+#pragma unroll
+  for (int j = 0; j < 24; ++j) acc[j] = 0x7FFFFFFFu - threadIdx.x - j;
+  for (int it = 0; it < iters; ++it) {
+    const int m = it & 63;
+    uint32_t x[24];
+#pragma unroll
+    for (int a = 0; a < 24; a += 4) load_vec<uint32_t>(xs + m * 24 + a, x + a);
+#pragma unroll
+    for (int j0 = 0; j0 < 24; j0 += 4) {
+      uint32_t y[4];
+      load_vec<uint32_t>(ys + m * 24 + j0, y);
+#pragma unroll
+      for (int a = 0; a < 24; a += 3)
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          acc[j0 + q] = __vimin3_u32(__viaddmin_u32(x[a], y[q], acc[j0 + q]), mad_fma(x[a + 1], one, y[q]),
+                                     mad_fma(x[a + 2], one, y[q]));
+    }
+  }
+  uint32_t s = 0;
+#pragma unroll
+  for (int j = 0; j < 24; ++j) s ^= acc[j];
+  if (s == 0x12345678u) out[threadIdx.x] = s;
+}
+
 // ===================== launchers (called from cfp_host.cu) =================
 #define CFP_LAUNCH_CHECK() do { cudaError_t e_ = cudaGetLastError(); if (e_ != cudaSuccess) return e_; } while (0)
 
@@ -2121,6 +2197,8 @@ cudaError_t launch_enum_nb(const EnumParams& p, int64_t nthreads, size_t smem, c
   }
   if constexpr (sizeof(V) == 4 && (NB == 23 || NB == 24)) {
     if (p.staged && p.ymerge && p.na == NB && p.na_pad >= (NB + 3) / 4 * 4 && !p.no_full_a) {
+      if (p.mix == 3) return launch(enum_kernel<V, NB, 2, 1, NB, 1, 3>);
+      if (p.mix == 4) return launch(enum_kernel<V, NB, 2, 1, NB, 1, 4>);
       if (NB == 23 && p.o_mode == 1) return launch(enum_kernel<V, NB, 2, 1, NB, 0>);
       return launch(enum_kernel<V, NB, 2, 1, NB>);
     }
@@ -2231,6 +2309,7 @@ extern "C" int cfp_debug_trace(uint64_t* out64) {
 cudaError_t launch_intpipe(int op, int blocks, int iters, uint32_t* out, cudaStream_t st) {
   if (op == 0) intpipe_kernel<0><<<blocks, 1024, 0, st>>>(out, iters, 7u);
   else if (op == 1) intpipe_kernel<1><<<blocks, 1024, 0, st>>>(out, iters, 7u);
+  else if (op == 3) intpipe_mix_kernel<<<blocks * 2, 256, 0, st>>>(out, iters, 1u);   // 4 x 256 per SM
   else intpipe_kernel<2><<<blocks, 1024, 0, st>>>(out, iters, 7u);
   CFP_LAUNCH_CHECK();
   return cudaSuccess;
