@@ -346,6 +346,7 @@ struct MemEnumParams {
   const int32_t* perm;
   const void* K0;                    // [nP] natural prefix order
   void* B;                           // [Wc/4][nP][4] out: K0[p] + min over the class
+  uint32_t one;                      // 1 (the FMA-pipe adds' multiplier, opaque to the compiler)
 };
 
 struct MemFoldParams {

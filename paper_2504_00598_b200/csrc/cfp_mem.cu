@@ -55,6 +55,14 @@ template <> struct MT<uint64_t> {
   }
 };
 
+// x * one + y on the FMA pipe (one = 1 at run time: ptxas keeps the IMAD)
+__device__ __forceinline__ uint32_t mem_mad(uint32_t x, uint32_t one, uint32_t y) {
+  uint32_t r;
+  asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(r) : "r"(x), "r"(one), "r"(y));
+  return r;
+}
+__device__ __forceinline__ uint64_t mem_mad(uint64_t x, uint32_t, uint64_t y) { return x + y; }
+
 // Natural prefix index from (ctx value, other-digit value).
 __device__ __forceinline__ int64_t mem_prefix(const MemPrefixMap& m, int64_t c, int64_t n) {
   int64_t p = 0;
@@ -201,10 +209,21 @@ __global__ void __launch_bounds__(256) mem_enum_kernel(const MemEnumParams p) {
       for (int e = a0; e < a1; e += 4) {               // 16-byte body
         V t[4];
         M::load4(ts + e, t);
+        if constexpr (sizeof(V) == 4) {
+          // two pipes (as enum_kernel's loop): per 4 combinations two
+          // VIADDMNMX (ALU) and two FMA-pipe IMAD adds folded by one VIMNMX3
 #pragma unroll
-        for (int q = 0; q < 4; ++q)
+          for (int i = 0; i < NPF; ++i) {
+            V a = M::addmin(k0[i], t[0], acc[i]);
+            a = M::addmin(k0[i], t[1], a);
+            acc[i] = __vimin3_u32(a, mem_mad(k0[i], p.one, t[2]), mem_mad(k0[i], p.one, t[3]));
+          }
+        } else {
 #pragma unroll
-          for (int i = 0; i < NPF; ++i) acc[i] = M::addmin(k0[i], t[q], acc[i]);
+          for (int q = 0; q < 4; ++q)
+#pragma unroll
+            for (int i = 0; i < NPF; ++i) acc[i] = M::addmin(k0[i], t[q], acc[i]);
+        }
       }
       for (int e = a1; e < s1; ++e) {                  // tail
         const V t = ts[e];
