@@ -415,7 +415,7 @@ def run_cfp(args, prob, rank, world, local_rank):
     ip_ops, ip_ms = ctx.intpipe_bench(0, 4000)
     ip3_ops, _ = ctx.intpipe_bench(3, 4000)
     peak = max(peak_alu, ip3_ops / 1e9)
-    traffic = ncu_traffic("r02_ncu_enum_v7", "enum_kernel")
+    traffic = ncu_traffic("r02_ncu_enum_v9", "enum_kernel<unsigned int, 24")
     # N2 (min,+) product microbenchmark (S in {256 .. 8192},
     # u32 / u64, with and without the least-k argmin), part of every default
     # run on rank 0 (~2 s); --no-minplus skips it
@@ -469,7 +469,7 @@ def run_cfp(args, prob, rank, world, local_rank):
                                  "SMs x 1965 MHz, whichever is higher (DESIGN.md); achieved = combos / "
                                  "device time of the enumeration phase (all enum launches incl. the "
                                  "cross-term fold epilogue); traffic = DRAM bytes per enum launch from "
-                                 "ncu, algorithmic bytes ~0"},
+                                 "ncu (profiles/r02_ncu_enum_v9.json), algorithmic bytes ~0"},
             "intpipe_measured": {"op": "VIADDMNMX.U32", "lane_ops_per_s": ip_ops,
                                  "lane_ops_per_clk_per_sm": ip_ops / (SMS * 1e6 * (clocks["sm_mhz"] or 1965.0)),
                                  "frac_of_derived_peak": ip_ops / (peak_alu * 1e9),
@@ -583,12 +583,12 @@ def run_cfp_mem(args, rank, world, local_rank):
                 plan_bytes(prob) + 8 * len(prob.instances)},
         "gpu_launches": launches,
         "roofline": {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "Gop/s",
-                     "frac": achieved / peak, "traffic": ncu_traffic("r02_ncu_memenum_v8", "mem_enum_kernel"),
+                     "frac": achieved / peak, "traffic": ncu_traffic("r02_ncu_mem_v9", "mem_enum_kernel<unsigned int, 4>"),
                      "frac_of_alu_only_peak": achieved / peak_alu,
                      "note": "enumeration kernels: one fused add+min per strategy combination "
                              "(K0[p] + T[ctx][sigma] into its (layout, memory) class), the 16-byte body on "
                              "two pipes; peak = max(N5 op-3 two-pipe rate, 64 VIADDMNMX/clk/SM); traffic: "
-                             "DRAM bytes of one layer-type launch (profiles/r02_ncu_memenum_v8.json)"},
+                             "DRAM bytes of one layer-type launch (profiles/r02_ncu_mem_v9.json)"},
         "fold_roofline": {"bound": "alu", "achieved": fold_ops / (f_ms * 1e-3) / 1e9, "peak": peak_alu,
                           "unit": "Gop/s", "frac": fold_ops / (f_ms * 1e-3) / 1e9 / peak_alu,
                           "addmins_per_step": fold_ops},
