@@ -106,6 +106,8 @@ struct cfp_ctx {
   std::vector<int64_t> cached_key;  //   and its structural key (plan_key)
   bool mem_chain_fused = true;      // CFP_MEM_CHAIN_FUSED=0: one launch per DP step (A/B tests)
   bool dedup = true;                // CFP_DEDUP=0: fold identical transitions separately (A/B tests)
+  std::vector<uint32_t> raw_pool;   // host value blob reused across cfp_search_plan calls (its
+                                    // pages stay mapped: a fresh 70 KB+ blob page-faulted every call)
   int enum_mix = 3;                 // CFP_ENUM_MIX: full-A loop (B = {o}) on two pipes in groups of 3 or 4
                                     // A values; 0 = ALU pipe only (A/B, tests)
   bool no_full_a = false;           // CFP_ENUM_FULL_A=0: runtime-length A loop only (A/B tests)
@@ -577,6 +579,26 @@ struct Builder {
 
 }  // namespace
 
+// largest finite (!= CFP_INF32) entry of t[0, n), 0 if none: 8 independent
+// lanes, so the host compiler vectorises it (a serial max chain was most of a
+// reused-plan call's host model time)
+static inline uint32_t max_finite(const uint32_t* t, int64_t n) {
+  uint32_t m[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  int64_t q = 0;
+  for (; q + 8 <= n; q += 8)
+    for (int k = 0; k < 8; ++k) {
+      const uint32_t v = t[q + k] == CFP_INF32 ? 0u : t[q + k];
+      m[k] = m[k] > v ? m[k] : v;
+    }
+  uint32_t r = 0;
+  for (int k = 0; k < 8; ++k) r = r > m[k] ? r : m[k];
+  for (; q < n; ++q) {
+    const uint32_t v = t[q] == CFP_INF32 ? 0u : t[q];
+    r = r > v ? r : v;
+  }
+  return r;
+}
+
 static cfp_status validate_and_model(const cfp_problem* p, std::vector<HostType>& T,
                                      std::vector<HostTrans>& X, Builder& b, bool chain) {
   if (!p) return fail(CFP_EINVAL, "null problem");
@@ -630,6 +652,7 @@ static cfp_status validate_and_model(const cfp_problem* p, std::vector<HostType>
     h.wmax.assign(h.K, 0);
     off = 0;
     for (int j = 0; j < h.K; ++j) {
+      h.keep[j].reserve(h.radix[j]);
       for (int q = 0; q < h.radix[j]; ++q) {
         uint32_t pc = s.comp_ns[off + q], cc = s.comm_ns ? s.comm_ns[off + q] : 0;
         if (pc == CFP_INF32 || cc == CFP_INF32) continue;
@@ -644,11 +667,20 @@ static cfp_status validate_and_model(const cfp_problem* p, std::vector<HostType>
     for (int e = 0; e < h.E; ++e) {
       int a = h.esrc[e], c = h.edst[e];
       uint64_t m = 0;
-      for (int x : h.keep[a])
-        for (int y : h.keep[c]) {
-          uint32_t v = s.edge_ns[eoff + (int64_t)x * h.radix[c] + y];
-          if (v != CFP_INF32) m = std::max<uint64_t>(m, v);
-        }
+      if ((int)h.keep[a].size() == h.radix[a] && (int)h.keep[c].size() == h.radix[c]) {
+        // every strategy feasible: one branch-free pass over the table (INF -> 0)
+        const uint32_t* t = s.edge_ns + eoff;
+        const int64_t n = (int64_t)h.radix[a] * h.radix[c];
+        uint32_t mm = 0;
+        mm = max_finite(t, n);
+        m = mm;
+      } else {
+        for (int x : h.keep[a])
+          for (int y : h.keep[c]) {
+            uint32_t v = s.edge_ns[eoff + (int64_t)x * h.radix[c] + y];
+            if (v != CFP_INF32) m = std::max<uint64_t>(m, v);
+          }
+      }
       h.emax.push_back(m);
       eoff += (int64_t)h.radix[a] * h.radix[c];
     }
@@ -677,11 +709,18 @@ static cfp_status validate_and_model(const cfp_problem* p, std::vector<HostType>
       int64_t n = (int64_t)h.Din * ty.radix[j];
       h.x_off.push_back(b.put_raw(s.in_ns + off, n));
       uint64_t m = 0;
-      for (int u = 0; u < h.Din; ++u)
-        for (int y : ty.keep[j]) {
-          uint32_t v = s.in_ns[off + (int64_t)u * ty.radix[j] + y];
-          if (v != CFP_INF32) m = std::max<uint64_t>(m, v);
-        }
+      if ((int)ty.keep[j].size() == ty.radix[j]) {
+        const uint32_t* t = s.in_ns + off;
+        uint32_t mm = 0;
+        mm = max_finite(t, n);
+        m = mm;
+      } else {
+        for (int u = 0; u < h.Din; ++u)
+          for (int y : ty.keep[j]) {
+            uint32_t v = s.in_ns[off + (int64_t)u * ty.radix[j] + y];
+            if (v != CFP_INF32) m = std::max<uint64_t>(m, v);
+          }
+      }
       h.xmax.push_back(m);
       off += n;
     }
@@ -1933,6 +1972,12 @@ extern "C" cfp_status cfp_search_plan(cfp_ctx* ctx, const cfp_problem* p, cfp_pl
   NvtxRange nv("cfp_search_plan");
   std::vector<int64_t> key;
   HostModel model;
+  model.b.raw.swap(ctx->raw_pool);
+  model.b.raw.clear();
+  struct PoolBack {
+    cfp_ctx* c; Builder& b;
+    ~PoolBack() { c->raw_pool.swap(b.raw); }
+  } pool_back{ctx, model.b};
   static const bool dbg = getenv("CFP_DEBUG_E2E") != nullptr;
   PrepTimer tm;
   TRY(build_model(ctx, p, true, model));
@@ -2419,3 +2464,4 @@ extern "C" cfp_status cfp_intpipe_bench(cfp_ctx* ctx, int32_t op, int32_t iters,
 
 // profiling space and dynamic profiling budget (NEXT-3)
 #include "cfp_profile_host.inc"
+
