@@ -108,6 +108,7 @@ struct cfp_ctx {
   bool dedup = true;                // CFP_DEDUP=0: fold identical transitions separately (A/B tests)
   std::vector<uint32_t> raw_pool;   // host value blob reused across cfp_search_plan calls (its
                                     // pages stay mapped: a fresh 70 KB+ blob page-faulted every call)
+  bool no_ym_inplace = false;       // CFP_YM_INPLACE=0: merged Y' rows in their own region (A/B)
   int enum_mix = 3;                 // CFP_ENUM_MIX: full-A loop (B = {o}) on two pipes in groups of 3 or 4
                                     // A values; 0 = ALU pipe only (A/B, tests)
   bool no_full_a = false;           // CFP_ENUM_FULL_A=0: runtime-length A loop only (A/B tests)
@@ -155,6 +156,7 @@ extern "C" cfp_status cfp_ctx_create(cfp_ctx** out, const cfp_ctx_opts* opts) {
                                std::to_string(prop.major) + std::to_string(prop.minor));
   c->sms = prop.multiProcessorCount;
   if (const char* fa = getenv("CFP_ENUM_FULL_A")) c->no_full_a = atoi(fa) == 0;
+  if (const char* yi = getenv("CFP_YM_INPLACE")) c->no_ym_inplace = atoi(yi) == 0;
   if (const char* mx = getenv("CFP_ENUM_MIX")) c->enum_mix = atoi(mx) == 4 ? 4 : atoi(mx) == 0 ? 0 : 3;
   if (const char* dd = getenv("CFP_DEDUP")) c->dedup = atoi(dd) != 0;
   if (const char* mf = getenv("CFP_MEM_CHAIN_FUSED")) c->mem_chain_fused = atoi(mf) != 0;
@@ -1256,9 +1258,15 @@ static cfp_status prepare_impl(cfp_ctx* ctx, const cfp_problem* p, bool do_chain
     size_t smem = (size_t)(ep.xspan + ep.yspan + ((ep.zspan + 3) & ~3LL)) * vbytes + (size_t)nM * 16;
     ep.staged = smem <= 160 * 1024;
     {
-      const size_t ymb = (size_t)nM * ep.nb_pad * vbytes;   // merged Y'[m][j] rows
+      // merged Y'[m][j] = Y + Z rows: in place when the slice's Y rows are
+      // exactly the M values in order (Y depends on every M digit: C3, C4),
+      // else a second region
+      bool inplace = ep.yspan == nM * ep.nb_pad;
+      for (int64_t m = 0; inplace && m < nM; ++m) inplace = mtab_all[te.mtab_off + m].y == m * ep.nb_pad;
+      const size_t ymb = inplace ? 0 : (size_t)nM * ep.nb_pad * vbytes;
       ep.ymerge = ep.staged && ymb <= 64 * 1024 && smem + ymb <= 160 * 1024;
-      if (ep.ymerge) smem += ymb;
+      ep.ym_inplace = ep.ymerge && inplace && !ctx->no_ym_inplace;
+      if (ep.ymerge && !ep.ym_inplace) smem += (size_t)nM * ep.nb_pad * vbytes;
     }
     ep.init_row = ep.o_mode != 0 || !(ep.o_bstride == 1 && ep.o_bradix == ep.nb);
     // M split (B = {o}): two threads per prefix halve the work unit, so the
@@ -1271,7 +1279,7 @@ static cfp_status prepare_impl(cfp_ctx* ctx, const cfp_problem* p, bool do_chain
     ep.no_full_a = ctx->no_full_a ? 1 : 0;
     ep.one = 1;
     ep.mix = 0;
-    if (ctx->enum_mix && ep.o_mode == 0) ep.mix = (int32_t)ctx->enum_mix;
+    if (ctx->enum_mix && ep.o_mode == 0) ep.mix = (int32_t)ctx->enum_mix;   // C4's o-in-M loop: measured slower
     ep.Gpad = (ep.G + ep.CH - 1) / ep.CH * ep.CH;
     te.smem = ep.staged ? smem : 0;
     te.nthreads = ep.Gpad * ep.W * ep.VG * ep.MS;

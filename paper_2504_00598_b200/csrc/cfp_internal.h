@@ -88,6 +88,7 @@ struct EnumParams {
   int32_t Do;                   // compact output radix
   int32_t staged;               // 1: tables sliced into shared memory per CTA
   int32_t ymerge;               // 1 (staged only): Z folded into per-m Y rows in smem
+  int32_t ym_inplace;           // 1: ... in place (the slice's Y rows are the M values in order)
   int32_t init_row;             // 1: B_p row must be pre-filled with CAP
   int64_t xspan, yspan, zspan;  // slice lengths (staged)
   // device pointers (element type = the path's value type)

@@ -534,16 +534,22 @@ __global__ void __launch_bounds__(kBlock, 4) enum_kernel(const EnumParams p) {
     XT = xs; YT = ys; ZT = zs; MT = ms;
     sx = sy = sz = 0;
     if constexpr (MERGED) {
-      V* ym = reinterpret_cast<V*>(ms + p.nM);
       const int n = (int)(p.nM * p.nb_pad);           // staged: fits shared memory
       const uint32_t nbp = (uint32_t)p.nb_pad;
-      for (int e = tid; e < n; e += kBlock) {
-        const int m = (int)((uint32_t)e / nbp);
-        const int4 mt = ms[m];
-        ym[e] = T::sat(ys[mt.y + (e - m * (int)nbp)], zs[mt.z]);
+      if (p.ym_inplace) {                             // Y row m is the slice's row m: Y' over Y
+        for (int e = tid; e < n; e += kBlock) ys[e] = T::sat(ys[e], zs[ms[(uint32_t)e / nbp].z]);
+        __syncthreads();
+        YT = ys;
+      } else {
+        V* ym = reinterpret_cast<V*>(ms + p.nM);
+        for (int e = tid; e < n; e += kBlock) {
+          const int m = (int)((uint32_t)e / nbp);
+          const int4 mt = ms[m];
+          ym[e] = T::sat(ys[mt.y + (e - m * (int)nbp)], zs[mt.z]);
+        }
+        __syncthreads();
+        YT = ym;
       }
-      __syncthreads();
-      YT = ym;
     }
   }
   ETRACE(4);
