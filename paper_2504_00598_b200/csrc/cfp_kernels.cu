@@ -2,7 +2,8 @@
 //
 // Hot path and where each step lives:
 //   a0 stage:      compact_kernel (prune + p+c), build_table_kernel (X/Y/Z/K0)
-//   a1 enumerate:  enum_kernel -- one VIADDMNMX per strategy combination; its
+//   a1 enumerate:  enum_kernel -- one fused add+min per strategy combination
+//                  (VIADDMNMX, or for 2 of 3 an FMA-pipe IMAD + VIMNMX3); its
 //                  epilogue folds the cross-segment terms of every incoming
 //                  transition into per-CTA chunk minima
 //   a1 reduce:     amin_kernel -- A[u][v] = min over chunk minima
