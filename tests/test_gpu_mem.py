@@ -179,12 +179,15 @@ def test_c3_mem_full_size_sampled(ctx, oracle_lib):
     assert cost.tolist() == got.seg_ns.tolist() and q.tolist() == got.seg_q.tolist()
 
 
+@pytest.mark.parametrize("fold", ["u", "4x4"])     # mem_fold_u_kernel (default) / the 4 x 4 fold
 @pytest.mark.parametrize("cfg,keep", [("C3", [3, 4, 5, 6]), ("C5", [3, 4, 5, 6])])
-def test_midsize_mem_tables_every_bucket(ctx, oracle_lib, cfg, keep):
+def test_midsize_mem_tables_every_bucket(ctx, oracle_lib, cfg, keep, fold, monkeypatch):
     """Mid-size cuts of the bench graphs with their memory tables: many prefix
     memory groups and suffix memories per class, so the per-plan class runs
     start and end anywhere in the sorted suffix row; every (u, v, q) bucket of
     every transition vs the oracle, then the search."""
+    if fold == "4x4":
+        monkeypatch.setenv("CFP_MEM_FOLD4", "1")      # read at each fold launch
     O = oracle_lib
     from synth.generators import midsize
     p = midsize(cfg, keep, n_layers=5)
