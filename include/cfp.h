@@ -307,8 +307,20 @@ cfp_status cfp_segment_costs_mem(cfp_ctx* ctx, const cfp_segment_type* t, const 
  * W arguments are DEVICE pointers (the tables are tens of GB; the caller
  * allocates them on ctx's device and keeps them resident), 16-byte aligned
  * for the vector path; the types' comp/comm/edge tables are ignored (comp_ns
- * must still be non-NULL for validation).  Single GPU (world > 1: EINVAL);
- * output block with <= 64 strategies (else ETOOBIG). */
+ * must still be non-NULL for validation); output block with <= 64
+ * strategies (else ETOOBIG).
+ * world > 1 (C4's two 313 GB tables fit only on 8 GPUs): every rank holds the
+ * rows of a contiguous range of block 0's strategies -- combination indices
+ * [first, first + count) of cfp_dense_shard -- and W points at the first of
+ * them; each rank streams its rows, its least indices are global, and the
+ * buckets are merged as the plain path's (NCCL MIN all-reduce of A, then of
+ * the least index among the ranks attaining it); the chain is replicated.  A
+ * shard-simulation ctx (world > 1 without nccl_unique_id) answers
+ * cfp_segment_costs_dense with the rank-local tables only. */
+/* This rank's share of a type's dense table: combination indices
+ * [*first, *first + *count) (a block-0 strategy range, cfp_shard_range over
+ * D_0; count may be 0).  EINVAL: null or malformed type. */
+cfp_status cfp_dense_shard(cfp_ctx* ctx, const cfp_segment_type* t, int64_t* first, int64_t* count);
 /* Synthetic tables: W[e] = splitmix64 stream of (e ^ base), 24-bit ns,
  * CFP_INF32 when the low 12 bits are zero (synth.generators.dense_table). */
 cfp_status cfp_dense_fill(cfp_ctx* ctx, uint32_t* W_dev, uint64_t n, uint64_t base);

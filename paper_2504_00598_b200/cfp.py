@@ -100,7 +100,7 @@ EXPORTS = ["cfp_ctx_create", "cfp_ctx_destroy", "cfp_last_error", "cfp_nccl_uniq
            "cfp_shard_range", "cfp_pack_keys", "cfp_unpack_keys", "cfp_intpipe_bench",
            "cfp_minplus_bench", "cfp_search_plan_mem", "cfp_segment_costs_mem", "cfp_mem_prepare",
            "cfp_mem_execute", "cfp_mem_fetch_plan", "cfp_mem_free", "cfp_mem_time_kernels",
-           "cfp_mem_kernel_ms", "cfp_mem_fold_ops", "cfp_dense_fill", "cfp_search_plan_dense",
+           "cfp_mem_kernel_ms", "cfp_mem_fold_ops", "cfp_dense_fill", "cfp_dense_shard", "cfp_search_plan_dense",
            "cfp_segment_costs_dense", "cfp_dense_prepare", "cfp_dense_execute", "cfp_dense_fetch_plan",
            "cfp_dense_free", "cfp_dense_time_kernels", "cfp_dense_kernel_ms", "cfp_profile_space",
            "cfp_profile_budget"]
@@ -163,6 +163,7 @@ def lib() -> C.CDLL:
                                     P(C.c_int32)]
     L.cfp_mem_fold_ops.argtypes = [vp, P(C.c_double)]
     L.cfp_dense_fill.argtypes = [vp, vp, C.c_uint64, C.c_uint64]
+    L.cfp_dense_shard.argtypes = [vp, P(cfp_segment_type), P(C.c_int64), P(C.c_int64)]
     L.cfp_search_plan_dense.argtypes = [vp, P(cfp_problem), P(vp), P(cfp_plan)]
     L.cfp_segment_costs_dense.argtypes = [vp, P(cfp_segment_type), vp, P(cfp_transition), C.c_int32,
                                           P(C.c_uint64), P(C.c_uint64)]
@@ -525,6 +526,15 @@ class Context:
     # -- dense per-plan tables (NEXT-2); W arguments are device pointers (int)
     def dense_fill(self, w_ptr: int, n: int, base: int):
         _check(lib().cfp_dense_fill(self._h, C.c_void_p(w_ptr), n, base))
+
+    def dense_shard(self, seg_type) -> Tuple[int, int]:
+        """(first, count): the combination indices of seg_type's dense table
+        this rank holds (world > 1; (0, prod D) at world 1)."""
+        m = _Marshal()
+        t = m.segment_type(seg_type)
+        first, count = C.c_int64(), C.c_int64()
+        _check(lib().cfp_dense_shard(self._h, C.byref(t), C.byref(first), C.byref(count)))
+        return first.value, count.value
 
     def search_plan_dense(self, prob, w_ptrs: Sequence[Optional[int]]) -> Plan:
         m = _Marshal()

@@ -137,7 +137,7 @@ __global__ void __launch_bounds__(256) dense_fold_kernel(const DenseSlotParams s
   for (int ub = 0; ub < s.Din; ub += 32) {
     const int uc = min(32, s.Din - ub);
     for (int r = tid; r < rows; r += 256) {          // digits once per row, then every u
-      const int64_t p = p0 + r;
+      const int64_t p = s.p_lo + p0 + r;             // global prefix (digits)
       int64_t base[kMaxCross];
       for (int i = 0; i < s.nq; ++i)
         base[i] = s.q_off[i] + (int64_t)((p / s.q_stride[i]) % s.q_radix[i]);
@@ -154,7 +154,7 @@ __global__ void __launch_bounds__(256) dense_fold_kernel(const DenseSlotParams s
       const int r = e / s.nVs, v = e % s.nVs;
       Bs[r * s.nVs + v] = s.B[(p0 + r) * s.nVs + v];
     }
-    for (int r = tid; r < rows; r += 256) vps[r] = dense_vp(s, p0 + r);
+    for (int r = tid; r < rows; r += 256) vps[r] = dense_vp(s, s.p_lo + p0 + r);
     __syncthreads();
     for (int e = tid; e < uc * s.Do; e += 256) {
       const int u = e / s.Do, v = e % s.Do;
@@ -221,9 +221,9 @@ __global__ void __launch_bounds__(256) dense_argmin_kernel(const DenseSlotParams
     const int64_t p0 = (int64_t)s_c * kDenseChunk;
     const int rows = s.nP - p0 < kDenseChunk ? (int)(s.nP - p0) : kDenseChunk;
     for (int r = tid; r < rows; r += 256) {
-      const int64_t p = p0 + r;
-      if (s.nVs == 1 && dense_vp(s, p) != v) continue;
-      const uint64_t x = dense_x(s, p, u);
+      const int64_t p = p0 + r;                      // local row; digits of the global prefix
+      if (s.nVs == 1 && dense_vp(s, s.p_lo + p) != v) continue;
+      const uint64_t x = dense_x(s, s.p_lo + p, u);
       const uint32_t b = s.B[p * s.nVs + (s.nVs == 1 ? 0 : v)];
       if (x != kInf64 && b != 0xFFFFFFFFu && x + b == A) atomicMin(&s_p, (unsigned long long)p);
     }
@@ -234,7 +234,7 @@ __global__ void __launch_bounds__(256) dense_argmin_kernel(const DenseSlotParams
     for (int64_t j = tid; j < s.nS; j += 256)
       if (row[j] == b && (s.nVs == 1 || (int)(j % s.Do) == v)) atomicMin(&s_s, (unsigned long long)j);
     __syncthreads();
-    if (tid == 0) s.I[cell] = (uint64_t)ps * (uint64_t)s.nS + s_s;
+    if (tid == 0) s.I[cell] = (uint64_t)(s.p_lo + ps) * (uint64_t)s.nS + s_s;
     __syncthreads();
   }
 }
@@ -331,9 +331,11 @@ cudaError_t launch_dense_fold(const DenseSlotParams& s, cudaStream_t st) {
     cudaError_t e = cudaFuncSetAttribute(dense_fold_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
   }
-  dense_fold_kernel<<<(unsigned)s.nchunks, 256, smem, st>>>(s);
-  cudaError_t e = cudaGetLastError();
-  if (e != cudaSuccess) return e;
+  if (s.nchunks > 0) {                               // (an empty shard: A = INF from the minima below)
+    dense_fold_kernel<<<(unsigned)s.nchunks, 256, smem, st>>>(s);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+  }
   const int64_t tot = (int64_t)s.Din * s.Do;
   dense_amin_kernel<<<(unsigned)((tot * 32 + 255) / 256), 256, 0, st>>>(s);
   return cudaGetLastError();

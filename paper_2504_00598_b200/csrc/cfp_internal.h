@@ -457,6 +457,7 @@ struct DenseRowParams {
 struct DenseSlotParams {             // one transition
   const uint32_t* W;
   int64_t nP, nS;
+  int64_t p_lo;                      // global prefix row of local row 0 (rank's shard; 0 at world 1)
   int32_t Din, Do, nVs;
   int64_t o_stride;                  // output digit's stride in the prefix index (nVs == 1)
   int32_t nq;

@@ -149,3 +149,70 @@ def test_dense_c3_full_size(ctx, oracle_lib):
     assert [int(x) for x in rec[1]] == got.seg_index.tolist()
     del bufs
     torch.cuda.empty_cache()
+
+
+# ---------------------------------------------------------------- world > 1
+# Every rank holds the rows of a block-0 strategy range (cfp_dense_shard) and
+# answers with rank-local (A, least global index); the lexicographic (cost,
+# index) min over the ranks -- what the NCCL merge computes -- must equal the
+# single-GPU tables.  Shard simulation: world > 1 contexts without a
+# communicator on one GPU.
+
+
+def _merge(parts):
+    A, I = parts[0][0].copy(), parts[0][1].copy()
+    for a, i in parts[1:]:
+        take = (a < A) | ((a == A) & (i < I))
+        A, I = np.where(take, a, A), np.where(take, i, I)
+    return A, I
+
+
+def _dense_shards(cfp, ty, W, tr, din, world):
+    d = _dev(W)
+    parts, covered = [], 0
+    for r in range(world):
+        c = cfp.Context(device=0, world=world, rank=r)
+        first, count = c.dense_shard(ty)
+        assert first == covered                          # contiguous, in rank order
+        covered += count
+        parts.append(c.segment_costs_dense(ty, d.data_ptr() + 4 * first, tr, din))
+        c.close()
+    assert covered == len(W)
+    return _merge(parts)
+
+
+@pytest.mark.parametrize("seed", range(16))
+def test_dense_shard_simulation_random(ctx, seed):
+    from paper_2504_00598_b200 import cfp
+    p = G.tiny_random(7300 + seed, max_k=4, max_d=6)
+    Ws = _tables(p, seed, inf_every=7 if seed % 3 == 1 else 0)
+    for tr in sorted({int(t) for t in p.instances}):
+        t = p.transitions[tr].type
+        d = _dev(Ws[t])
+        A1, I1 = ctx.segment_costs_dense(p.types[t], d.data_ptr(), p.transitions[tr], p.d_in(tr))
+        for world in (2, 3, 8):
+            A, I = _dense_shards(cfp, p.types[t], Ws[t], p.transitions[tr], p.d_in(tr), world)
+            assert np.array_equal(A, A1) and np.array_equal(I, I1), (seed, tr, world)
+
+
+def test_dense_shard_simulation_c2(ctx):
+    from paper_2504_00598_b200 import cfp
+    p = G.make_config("C2", 0, "shaped")
+    Ws = _tables(p, 5)
+    for tr in sorted({int(t) for t in p.instances}):
+        t = p.transitions[tr].type
+        d = _dev(Ws[t])
+        A1, I1 = ctx.segment_costs_dense(p.types[t], d.data_ptr(), p.transitions[tr], p.d_in(tr))
+        A, I = _dense_shards(cfp, p.types[t], Ws[t], p.transitions[tr], p.d_in(tr), 4)
+        assert np.array_equal(A, A1) and np.array_equal(I, I1), tr
+
+
+def test_dense_shard_simulation_search_refused(ctx):
+    from paper_2504_00598_b200 import cfp
+    p = G.tiny_random(7301, max_k=3, max_d=4)
+    Ws = _tables(p, 1)
+    ds = [_dev(w) for w in Ws]
+    c = cfp.Context(device=0, world=2, rank=0)
+    with pytest.raises(cfp.CfpError):
+        c.search_plan_dense(p, [d.data_ptr() for d in ds])
+    c.close()
