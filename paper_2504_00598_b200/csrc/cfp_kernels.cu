@@ -616,6 +616,17 @@ __global__ void __launch_bounds__(kBlock, 4) enum_kernel(const EnumParams p) {
                   acc[j] = t;
                 }
               }
+        } else if constexpr (FX == 0) {
+          // FX = 0: the bucket-digit-in-M instantiation (C4, launched for
+          // o_mode 1 only): the accumulators start every M step at
+          // CAP, so the first A value's add+min takes CAP as its third operand
+          // (an immediate) instead of NB register resets after each flush
+#pragma unroll
+          for (int j = 0; j < NB; ++j) acc[j] = T::addmin(x[0], y[j], T::CAP);
+#pragma unroll
+          for (int a = 1; a < NA; ++a)
+#pragma unroll
+            for (int j = 0; j < NB; ++j) acc[j] = T::addmin(x[a], y[j], acc[j]);
         } else {
 #pragma unroll
           for (int a = 0; a < NA; ++a)
@@ -644,8 +655,9 @@ __global__ void __launch_bounds__(kBlock, 4) enum_kernel(const EnumParams p) {
         for (int j = 1; j < NB; ++j) r = T::mn(r, acc[j]);
         if constexpr (MERGED) r = T::sat(r, k0);
         Bp[mt.w] = T::mn(Bp[mt.w], r);
+        if constexpr (!(NA > 0 && MX == 0 && FX == 0))  // that loop restarts from CAP itself
 #pragma unroll
-        for (int j = 0; j < NB; ++j) acc[j] = T::CAP;
+          for (int j = 0; j < NB; ++j) acc[j] = T::CAP;
       }
     }
     if constexpr (MERGED) {
