@@ -216,3 +216,34 @@ def test_dense_shard_simulation_search_refused(ctx):
     with pytest.raises(cfp.CfpError):
         c.search_plan_dense(p, [d.data_ptr() for d in ds])
     c.close()
+
+
+@pytest.fixture(scope="module")
+def ctx_nccl():
+    from paper_2504_00598_b200 import cfp
+    c = cfp.Context(device=0, world=1, rank=0, nccl_unique_id=cfp.nccl_unique_id())
+    yield c
+    c.close()
+
+
+@pytest.mark.parametrize("seed", range(10))
+def test_dense_nccl_one_rank(ctx_nccl, oracle_lib, seed):
+    """The world > 1 merge code (NCCL MIN of A, masked MIN of the least
+    indices) on a 1-rank communicator: tables and plans == the oracle."""
+    O = oracle_lib
+    p = G.tiny_random(7400 + seed, max_k=4, max_d=5)
+    Ws = _tables(p, seed)
+    m = O.Marshalled(p)
+    for tr in sorted({int(t) for t in p.instances}):
+        t = p.transitions[tr].type
+        A, I = O.dense_segment_table(p, tr, Ws[t], m=m)
+        d = _dev(Ws[t])
+        Ag, Ig = ctx_nccl.segment_costs_dense(p.types[t], d.data_ptr(), p.transitions[tr], p.d_in(tr))
+        assert np.array_equal(Ag, A) and np.array_equal(Ig, I), (seed, tr)
+    devs = [_dev(w) for w in Ws]
+    try:
+        want = O.dense_search_plan(p, Ws)
+    except O.OracleError:
+        return
+    got = ctx_nccl.search_plan_dense(p, [d.data_ptr() for d in devs])
+    assert got.total_ns == want["total"] and got.seg_index.tolist() == want["seg_index"].tolist()
