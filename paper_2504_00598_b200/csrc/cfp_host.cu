@@ -1279,7 +1279,7 @@ static cfp_status prepare_impl(cfp_ctx* ctx, const cfp_problem* p, bool do_chain
     ep.no_full_a = ctx->no_full_a ? 1 : 0;
     ep.one = 1;
     ep.mix = 0;
-    if (ctx->enum_mix && ep.o_mode == 0) ep.mix = (int32_t)ctx->enum_mix;   // C4's o-in-M loop: measured slower
+    if (ctx->enum_mix) ep.mix = (int32_t)ctx->enum_mix;
     ep.Gpad = (ep.G + ep.CH - 1) / ep.CH * ep.CH;
     te.smem = ep.staged ? smem : 0;
     te.nthreads = ep.Gpad * ep.W * ep.VG * ep.MS;

@@ -605,7 +605,8 @@ __global__ void __launch_bounds__(kBlock, 4) enum_kernel(const EnumParams p) {
               for (int q = 0; q < 4; ++q) {
                 const int j = j0 + q;
                 if (j < NB) {
-                  V t = acc[j];
+                  // FX = 0 (bucket digit in M): every M step starts from CAP
+                  V t = (FX == 0 && a == 0) ? T::CAP : acc[j];
 #pragma unroll
                   for (int b = 0; b < MX - 2; ++b)
                     if (a + b < NA) t = T::addmin(x[a + b], y[j], t);
@@ -655,7 +656,7 @@ __global__ void __launch_bounds__(kBlock, 4) enum_kernel(const EnumParams p) {
         for (int j = 1; j < NB; ++j) r = T::mn(r, acc[j]);
         if constexpr (MERGED) r = T::sat(r, k0);
         Bp[mt.w] = T::mn(Bp[mt.w], r);
-        if constexpr (!(NA > 0 && MX == 0 && FX == 0))  // that loop restarts from CAP itself
+        if constexpr (!(NA > 0 && FX == 0))             // those loops restart from CAP themselves
 #pragma unroll
           for (int j = 0; j < NB; ++j) acc[j] = T::CAP;
       }
@@ -2216,6 +2217,7 @@ cudaError_t launch_enum_nb(const EnumParams& p, int64_t nthreads, size_t smem, c
   }
   if constexpr (sizeof(V) == 4 && (NB == 23 || NB == 24)) {
     if (p.staged && p.ymerge && p.na == NB && p.na_pad >= (NB + 3) / 4 * 4 && !p.no_full_a) {
+      if (p.mix == 3 && NB == 23 && p.o_mode == 1) return launch(enum_kernel<V, NB, 2, 1, NB, 0, 3>);
       if (p.mix == 3) return launch(enum_kernel<V, NB, 2, 1, NB, 1, 3>);
       if (p.mix == 4) return launch(enum_kernel<V, NB, 2, 1, NB, 1, 4>);
       if (NB == 23 && p.o_mode == 1) return launch(enum_kernel<V, NB, 2, 1, NB, 0>);
